@@ -1,0 +1,1156 @@
+// paracycle_b200 C ABI implementation (see include/paracycle_b200.h).
+//
+// Host-side orchestration of the PTL-cycled parabolic advance:
+//   pc_cycle  == ptl.cycle_operator: one F+argmax pass, the
+//   Eq. 5 pair kernel, ONE 64-byte device->host read per cycle, then either
+//   s fused STS stage kernels (RKL2/RKG2) or a device-driven Jacobi-PCG solve.
+// Integer decisions (s, coefficient tables, remaining-time bookkeeping) are
+// computed here with the same expressions as oracle/schemes.py and
+// oracle/ptl.py (host code compiled with -ffp-contract=off).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/paracycle_b200.h"
+#include "kernels.cuh"
+#include "nccl_shim.h"
+
+using namespace pc;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static thread_local int64_t g_info = 0;
+
+static int fail(int code, const std::string& msg, int64_t info = 0) {
+  g_err = msg;
+  g_info = info;
+  return code;
+}
+#define CUDA_TRY(x)                                                                       \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(PC_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+#define TRY(x)                 \
+  do {                         \
+    int r_ = (x);              \
+    if (r_ != PC_OK) return r_; \
+  } while (0)
+
+// ------------------------------------------------------------------ objects
+struct Stats {
+  double stage_ms = 0.0;
+  int64_t stage_launches = 0;
+  int64_t launches = 0;
+};
+
+struct pc_ctx {
+  int device = 0;
+  int nranks = 1, rank = 0;
+  cudaStream_t s = nullptr;
+  ncclComm_t comm = nullptr;
+  int max_blocks = 148 * 16;
+  // reduction scratch
+  double* red_v = nullptr;
+  double* red_v2 = nullptr;
+  long long* red_i = nullptr;
+  unsigned int* counter = nullptr;
+  ArgRes* res = nullptr;
+  PcgDev* pcg = nullptr;
+  int* bad = nullptr;
+  unsigned long long* minbits = nullptr;
+  double* maxout = nullptr;
+  // pinned host mirrors
+  ArgRes* h_res = nullptr;
+  PcgDev* h_pcg = nullptr;
+  int* h_bad = nullptr;
+  unsigned long long* h_minbits = nullptr;
+  double* h_maxout = nullptr;
+  // staging for AoS conversion
+  double* staging = nullptr;
+  size_t staging_bytes = 0;
+  // workspace pool of single-component buffers
+  std::vector<std::pair<size_t, double*>> pool;
+  Stats st;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+};
+
+struct pc_grid {
+  pc_ctx* ctx;
+  GridDev g;
+  double* tables = nullptr;
+  int64_t shape[3];
+  size_t comp_elems;  // (n0 + 2) * plane
+};
+
+struct pc_field {
+  pc_grid* grid;
+  int ncomp;
+  double* buf[3];  // allocation base (ghost plane -1)
+  double* base(int q) const { return buf[q] + grid->g.plane; }
+};
+
+enum { K_SCALAR = 0, K_ALIGNED = 1 };
+
+struct pc_op {
+  pc_grid* grid;
+  int kind;
+  int ncomp;
+  ScalarOp so{};
+  AlignedOp ao{};
+  double* cbuf = nullptr;   // aligned conductivity (component-sized buffer)
+  double* dbuf = nullptr;   // Jacobi diagonal -J_ii
+  double* kfc = nullptr;    // kappa0 * f_c(r) per axis-0 row (n0 + 2)
+  double Tfloor = 1e-10;
+  double lam_max = 0.0;
+  double dt_euler = INFINITY;
+  bool frozen = false;
+};
+
+// ------------------------------------------------------------------ helpers
+static int grid_blocks(pc_ctx* c, int64_t n) {
+  int64_t b = (n + kThreads - 1) / kThreads;
+  if (b < 1) b = 1;
+  return (int)std::min<int64_t>(b, c->max_blocks);
+}
+
+static double* pool_get(pc_ctx* c, size_t elems) {
+  for (size_t q = 0; q < c->pool.size(); ++q) {
+    if (c->pool[q].first == elems) {
+      double* p = c->pool[q].second;
+      c->pool.erase(c->pool.begin() + q);
+      return p;
+    }
+  }
+  double* p = nullptr;
+  if (cudaMalloc(&p, elems * sizeof(double)) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(p, 0, elems * sizeof(double), c->s);
+  return p;
+}
+static void pool_put(pc_ctx* c, size_t elems, double* p) {
+  if (p) c->pool.push_back({elems, p});
+}
+
+static CFld cfld(const pc_field* f) {
+  CFld r{{nullptr, nullptr, nullptr}};
+  for (int q = 0; q < f->ncomp; ++q) r.p[q] = f->base(q);
+  for (int q = f->ncomp; q < 3; ++q) r.p[q] = r.p[0];
+  return r;
+}
+static Fld fld(pc_field* f) {
+  Fld r{{nullptr, nullptr, nullptr}};
+  for (int q = 0; q < f->ncomp; ++q) r.p[q] = f->base(q);
+  for (int q = f->ncomp; q < 3; ++q) r.p[q] = r.p[0];
+  return r;
+}
+// a set of ncomp pool buffers viewed as a field
+struct Work {
+  pc_ctx* c;
+  size_t elems;
+  int ncomp;
+  int64_t plane;
+  double* b[3] = {nullptr, nullptr, nullptr};
+  double* base(int q) const { return b[q] + plane; }
+  CFld cf() const {
+    CFld r{{base(0), ncomp > 1 ? base(1) : base(0), ncomp > 2 ? base(2) : base(0)}};
+    return r;
+  }
+  Fld f() const {
+    Fld r{{base(0), ncomp > 1 ? base(1) : base(0), ncomp > 2 ? base(2) : base(0)}};
+    return r;
+  }
+};
+static int work_get(pc_grid* g, int ncomp, Work& w) {
+  w.c = g->ctx;
+  w.elems = g->comp_elems;
+  w.ncomp = ncomp;
+  w.plane = g->g.plane;
+  for (int q = 0; q < ncomp; ++q) {
+    w.b[q] = pool_get(g->ctx, w.elems);
+    if (!w.b[q]) return fail(PC_E_CUDA, "workspace allocation failed (out of device memory?)");
+  }
+  return PC_OK;
+}
+static void work_put(Work& w) {
+  for (int q = 0; q < w.ncomp; ++q) {
+    pool_put(w.c, w.elems, w.b[q]);
+    w.b[q] = nullptr;
+  }
+}
+// swap the storage of a field with a work set (pointer rotation, no copy)
+static void swap_storage(pc_field* f, Work& w) {
+  for (int q = 0; q < f->ncomp; ++q) std::swap(f->buf[q], w.b[q]);
+}
+
+static int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(PC_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return PC_OK;
+}
+
+// ------------------------------------------------------------------ NCCL
+static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp) {
+  if (c->nranks <= 1) return PC_OK;
+  nccl::Api* A = nccl::api();
+  if (!A) return fail(PC_E_NCCL, "NCCL not available");
+  const size_t pl = (size_t)g->g.plane;
+  const int n0 = g->g.n0;
+  int lo = g->g.ghost_lo0 ? (c->rank - 1 + c->nranks) % c->nranks : -1;
+  int hi = g->g.ghost_hi0 ? (c->rank + 1) % c->nranks : -1;
+  if (A->groupStart() != 0) return fail(PC_E_NCCL, "ncclGroupStart");
+  for (int q = 0; q < ncomp; ++q) {
+    double* base = bufs[q] + pl;  // interior plane 0
+    if (lo >= 0) {
+      A->send(base, pl, nccl::kDouble, lo, c->comm, c->s);
+      A->recv(base - pl, pl, nccl::kDouble, lo, c->comm, c->s);
+    }
+    if (hi >= 0) {
+      A->send(base + (size_t)(n0 - 1) * pl, pl, nccl::kDouble, hi, c->comm, c->s);
+      A->recv(base + (size_t)n0 * pl, pl, nccl::kDouble, hi, c->comm, c->s);
+    }
+  }
+  if (A->groupEnd() != 0) return fail(PC_E_NCCL, "ncclGroupEnd");
+  return PC_OK;
+}
+static int halo_field(pc_field* f) {
+  double* b[3] = {f->buf[0], f->buf[1], f->buf[2]};
+  return halo_exchange(f->grid->ctx, f->grid, b, f->ncomp);
+}
+static int halo_work(pc_grid* g, Work& w) {
+  double* b[3] = {w.b[0], w.b[1], w.b[2]};
+  return halo_exchange(g->ctx, g, b, w.ncomp);
+}
+static int allreduce_d(pc_ctx* c, double* dptr, size_t n, int op) {
+  if (c->nranks <= 1) return PC_OK;
+  nccl::Api* A = nccl::api();
+  if (!A || A->allReduce(dptr, dptr, n, nccl::kDouble, op, c->comm, c->s) != 0)
+    return fail(PC_E_NCCL, "ncclAllReduce");
+  return PC_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+// (entry points get C linkage from the extern "C" declarations in the header)
+
+const char* pc_last_error(void) { return g_err.c_str(); }
+int64_t pc_last_error_info(void) { return g_info; }
+int pc_version(void) { return 1; }
+
+int pc_nccl_unique_id(void* out128) {
+  nccl::Api* A = nccl::api();
+  if (!A) return fail(PC_E_NCCL, "NCCL library not found");
+  if (A->getUniqueId(out128) != 0) return fail(PC_E_NCCL, "ncclGetUniqueId");
+  return PC_OK;
+}
+
+int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return fail(PC_E_INVALID, "bad context arguments");
+  CUDA_TRY(cudaSetDevice(device));
+  pc_ctx* c = new pc_ctx();
+  c->device = device;
+  c->nranks = nranks;
+  c->rank = rank;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  c->max_blocks = sms * 16;
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+  CUDA_TRY(cudaMalloc(&c->red_v, sizeof(double) * c->max_blocks));
+  CUDA_TRY(cudaMalloc(&c->red_v2, sizeof(double) * c->max_blocks));
+  CUDA_TRY(cudaMalloc(&c->red_i, sizeof(long long) * c->max_blocks));
+  CUDA_TRY(cudaMalloc(&c->counter, sizeof(unsigned int) * 4));
+  CUDA_TRY(cudaMemset(c->counter, 0, sizeof(unsigned int) * 4));
+  CUDA_TRY(cudaMalloc(&c->res, sizeof(ArgRes)));
+  CUDA_TRY(cudaMalloc(&c->pcg, sizeof(PcgDev)));
+  CUDA_TRY(cudaMalloc(&c->bad, sizeof(int)));
+  CUDA_TRY(cudaMalloc(&c->minbits, sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&c->maxout, sizeof(double)));
+  CUDA_TRY(cudaMallocHost(&c->h_res, sizeof(ArgRes)));
+  CUDA_TRY(cudaMallocHost(&c->h_pcg, sizeof(PcgDev)));
+  CUDA_TRY(cudaMallocHost(&c->h_bad, sizeof(int)));
+  CUDA_TRY(cudaMallocHost(&c->h_minbits, sizeof(unsigned long long)));
+  CUDA_TRY(cudaMallocHost(&c->h_maxout, sizeof(double)));
+  if (nranks > 1) {
+    nccl::Api* A = nccl::api();
+    if (!A) {
+      delete c;
+      return fail(PC_E_NCCL, "NCCL library not found (needed for nranks > 1)");
+    }
+    if (!nccl_uid) return fail(PC_E_INVALID, "nranks > 1 needs an ncclUniqueId");
+    if (A->commInitRank(&c->comm, nranks, nccl_uid, rank) != 0) return fail(PC_E_NCCL, "ncclCommInitRank");
+  }
+  *out = c;
+  return PC_OK;
+}
+
+int pc_ctx_destroy(pc_ctx* c) {
+  if (!c) return PC_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->s);
+  for (auto& p : c->pool) cudaFree(p.second);
+  for (auto& e : c->ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (c->comm) {
+    nccl::Api* A = nccl::api();
+    if (A) A->commDestroy(c->comm);
+  }
+  cudaFree(c->red_v);
+  cudaFree(c->red_v2);
+  cudaFree(c->red_i);
+  cudaFree(c->counter);
+  cudaFree(c->res);
+  cudaFree(c->pcg);
+  cudaFree(c->bad);
+  cudaFree(c->minbits);
+  cudaFree(c->maxout);
+  cudaFree(c->staging);
+  cudaFreeHost(c->h_res);
+  cudaFreeHost(c->h_pcg);
+  cudaFreeHost(c->h_bad);
+  cudaFreeHost(c->h_minbits);
+  cudaFreeHost(c->h_maxout);
+  cudaStreamDestroy(c->s);
+  delete c;
+  return PC_OK;
+}
+
+int pc_ctx_sync(pc_ctx* c) {
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  return PC_OK;
+}
+
+int pc_ctx_enable_timing(pc_ctx* c, int on) {
+  c->timing = on != 0;
+  return PC_OK;
+}
+int pc_ctx_reset_stats(pc_ctx* c) {
+  c->st = Stats();
+  return PC_OK;
+}
+static void flush_events(pc_ctx* c) {
+  for (auto& e : c->ev) {
+    float ms = 0.f;
+    cudaEventSynchronize(e.second);
+    cudaEventElapsedTime(&ms, e.first, e.second);
+    c->st.stage_ms += ms;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c->ev.clear();
+}
+int pc_ctx_stats(pc_ctx* c, double* stage_ms, int64_t* stage_launches, int64_t* launches_total) {
+  cudaStreamSynchronize(c->s);
+  flush_events(c);
+  if (stage_ms) *stage_ms = c->st.stage_ms;
+  if (stage_launches) *stage_launches = c->st.stage_launches;
+  if (launches_total) *launches_total = c->st.launches;
+  return PC_OK;
+}
+
+// table layout (paper_2403_01004_b200/geometry.py TABLE_ORDER)
+static void table_sizes(const int64_t shape[3], int64_t& A, int64_t& K, int64_t& J) {
+  A = (shape[0] + 2) * shape[1];
+  K = shape[2];
+  J = shape[1];
+}
+int64_t pc_grid_table_size(const int64_t shape[3]) {
+  int64_t A, K, J;
+  table_sizes(shape, A, K, J);
+  return 17 * A + 15 * K + 48 * J;
+}
+
+int pc_grid_create(pc_ctx* c, const int64_t shape[3], const int32_t* fl, const double* tables,
+                   int64_t ntables, pc_grid** out) {
+  if (!c || !shape || !fl || !tables || !out) return fail(PC_E_INVALID, "null argument");
+  for (int a = 0; a < 3; ++a)
+    if (shape[a] < 1) return fail(PC_E_INVALID, "grid shape must be positive");
+  if (ntables != pc_grid_table_size(shape)) return fail(PC_E_INVALID, "table size mismatch");
+  CUDA_TRY(cudaSetDevice(c->device));
+  pc_grid* g = new pc_grid();
+  g->ctx = c;
+  for (int a = 0; a < 3; ++a) g->shape[a] = shape[a];
+  GridDev& d = g->g;
+  d.n0 = (int)shape[0];
+  d.n1 = (int)shape[1];
+  d.n2 = (int)shape[2];
+  d.plane = shape[1] * shape[2];
+  d.N = shape[0] * d.plane;
+  d.per0 = fl[0];
+  d.per1 = fl[1];
+  d.per2 = fl[2];
+  d.pin_lo0 = fl[3];
+  d.pin_hi0 = fl[4];
+  d.pin_lo1 = fl[5];
+  d.pin_hi1 = fl[6];
+  d.pin_lo2 = fl[7];
+  d.pin_hi2 = fl[8];
+  d.ghost_lo0 = fl[9];
+  d.ghost_hi0 = fl[10];
+  d.n0g = fl[11];
+  d.i0g = fl[12];
+  d.spherical = fl[13];
+  g->comp_elems = (size_t)(shape[0] + 2) * (size_t)d.plane;
+  CUDA_TRY(cudaMalloc(&g->tables, sizeof(double) * ntables));
+  CUDA_TRY(cudaMemcpy(g->tables, tables, sizeof(double) * ntables, cudaMemcpyHostToDevice));
+  int64_t A, K, J;
+  table_sizes(shape, A, K, J);
+  const double* p = g->tables;
+  auto takeA = [&]() { const double* r = p + d.n1; p += A; return r; };  // skip ghost row -1
+  auto takeK = [&]() { const double* r = p; p += K; return r; };
+  for (int a = 0; a < 3; ++a) d.W2[a] = takeA();
+  for (int a = 0; a < 3; ++a) d.g1[a] = takeK();
+  d.iV2 = takeA();
+  d.igv = takeK();
+  for (int q = 0; q < 6; ++q) d.iL2[q] = takeA();
+  for (int q = 0; q < 6; ++q) d.iL1[q] = takeK();
+  for (int q = 0; q < 4; ++q) d.wo01[q] = takeA();
+  for (int q = 0; q < 2; ++q) d.wo2[q] = takeK();
+  d.iVal2 = takeA();
+  d.iValg = takeK();
+  for (int q = 0; q < 4; ++q) { d.M[q] = p; p += J * 9; }
+  for (int q = 0; q < 4; ++q) { d.Rabs[q] = p; p += J * 3; }
+  d.V2 = takeA();
+  d.gv = takeK();
+  d.Val2 = takeA();
+  d.Valg = takeK();
+  *out = g;
+  return PC_OK;
+}
+
+int pc_grid_destroy(pc_grid* g) {
+  if (!g) return PC_OK;
+  cudaFree(g->tables);
+  delete g;
+  return PC_OK;
+}
+
+int pc_field_create(pc_grid* g, int ncomp, pc_field** out) {
+  if (!g || !out || ncomp < 1 || ncomp > 3) return fail(PC_E_INVALID, "fields have 1..3 components");
+  pc_field* f = new pc_field();
+  f->grid = g;
+  f->ncomp = ncomp;
+  for (int q = 0; q < 3; ++q) f->buf[q] = nullptr;
+  for (int q = 0; q < ncomp; ++q) {
+    if (cudaMalloc(&f->buf[q], g->comp_elems * sizeof(double)) != cudaSuccess) {
+      for (int r = 0; r < q; ++r) cudaFree(f->buf[r]);
+      delete f;
+      return fail(PC_E_CUDA, "field allocation failed (out of device memory)");
+    }
+    cudaMemsetAsync(f->buf[q], 0, g->comp_elems * sizeof(double), g->ctx->s);
+  }
+  *out = f;
+  return PC_OK;
+}
+
+int pc_field_destroy(pc_field* f) {
+  if (!f) return PC_OK;
+  cudaStreamSynchronize(f->grid->ctx->s);
+  for (int q = 0; q < f->ncomp; ++q) cudaFree(f->buf[q]);
+  delete f;
+  return PC_OK;
+}
+
+static int ensure_staging(pc_ctx* c, size_t bytes) {
+  if (c->staging_bytes >= bytes) return PC_OK;
+  cudaStreamSynchronize(c->s);
+  cudaFree(c->staging);
+  c->staging = nullptr;
+  CUDA_TRY(cudaMalloc(&c->staging, bytes));
+  c->staging_bytes = bytes;
+  return PC_OK;
+}
+
+int pc_field_upload(pc_field* f, const double* host, int layout) {
+  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+  pc_grid* g = f->grid;
+  pc_ctx* c = g->ctx;
+  const size_t pl = (size_t)g->g.plane, n0 = (size_t)g->g.n0;
+  if (layout == PC_LAYOUT_SOA || f->ncomp == 1) {
+    for (int q = 0; q < f->ncomp; ++q)
+      CUDA_TRY(cudaMemcpyAsync(f->base(q), host + (size_t)q * n0 * pl, n0 * pl * sizeof(double),
+                               cudaMemcpyHostToDevice, c->s));
+  } else {
+    const size_t chunk_planes = std::max<size_t>(1, std::min<size_t>(n0, (256u << 20) / (pl * f->ncomp * 8)));
+    TRY(ensure_staging(c, chunk_planes * pl * f->ncomp * sizeof(double)));
+    for (size_t p0 = 0; p0 < n0; p0 += chunk_planes) {
+      size_t np = std::min(chunk_planes, n0 - p0);
+      CUDA_TRY(cudaMemcpyAsync(c->staging, host + p0 * pl * f->ncomp, np * pl * f->ncomp * sizeof(double),
+                               cudaMemcpyHostToDevice, c->s));
+      k_aos_to_soa<<<grid_blocks(c, (int64_t)(np * pl)), kThreads, 0, c->s>>>(g->g, f->ncomp, c->staging, fld(f),
+                                                                               (int)p0, (int)np);
+      c->st.launches++;
+      TRY(check_launch("k_aos_to_soa"));
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  return PC_OK;
+}
+
+int pc_field_download(const pc_field* f, double* host, int layout) {
+  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+  pc_grid* g = f->grid;
+  pc_ctx* c = g->ctx;
+  const size_t pl = (size_t)g->g.plane, n0 = (size_t)g->g.n0;
+  if (layout == PC_LAYOUT_SOA || f->ncomp == 1) {
+    for (int q = 0; q < f->ncomp; ++q)
+      CUDA_TRY(cudaMemcpyAsync(host + (size_t)q * n0 * pl, f->base(q), n0 * pl * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->s));
+  } else {
+    const size_t chunk_planes = std::max<size_t>(1, std::min<size_t>(n0, (256u << 20) / (pl * f->ncomp * 8)));
+    TRY(ensure_staging(c, chunk_planes * pl * f->ncomp * sizeof(double)));
+    for (size_t p0 = 0; p0 < n0; p0 += chunk_planes) {
+      size_t np = std::min(chunk_planes, n0 - p0);
+      k_soa_to_aos<<<grid_blocks(c, (int64_t)(np * pl)), kThreads, 0, c->s>>>(g->g, f->ncomp, cfld(f), c->staging,
+                                                                               (int)p0, (int)np);
+      c->st.launches++;
+      TRY(check_launch("k_soa_to_aos"));
+      CUDA_TRY(cudaMemcpyAsync(host + p0 * pl * f->ncomp, c->staging, np * pl * f->ncomp * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->s));
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  return PC_OK;
+}
+
+int pc_field_copy(pc_field* dst, const pc_field* src) {
+  if (!dst || !src || dst->ncomp != src->ncomp || dst->grid->comp_elems != src->grid->comp_elems)
+    return fail(PC_E_INVALID, "field copy: shape mismatch");
+  for (int q = 0; q < dst->ncomp; ++q)
+    CUDA_TRY(cudaMemcpyAsync(dst->buf[q], src->buf[q], dst->grid->comp_elems * sizeof(double),
+                             cudaMemcpyDeviceToDevice, dst->grid->ctx->s));
+  return PC_OK;
+}
+
+int pc_field_fill(pc_field* f, double v) {
+  pc_ctx* c = f->grid->ctx;
+  for (int q = 0; q < f->ncomp; ++q) {
+    k_fill<<<grid_blocks(c, (int64_t)f->grid->comp_elems), kThreads, 0, c->s>>>(f->buf[q],
+                                                                                 (int64_t)f->grid->comp_elems, v);
+    c->st.launches++;
+  }
+  return check_launch("k_fill");
+}
+
+int pc_field_exchange_halo(pc_field* f) { return halo_field(f); }
+
+int pc_host_register(void* p, size_t bytes) {
+  CUDA_TRY(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+  return PC_OK;
+}
+int pc_host_unregister(void* p) {
+  CUDA_TRY(cudaHostUnregister(p));
+  return PC_OK;
+}
+
+// ------------------------------------------------------------------ operators
+int pc_op_create_scalar(pc_grid* g, int ncomp, int vector_metric, double D_const, const pc_field* D,
+                        const pc_field* rho, pc_op** out) {
+  if (!g || !out || ncomp < 1 || ncomp > 3) return fail(PC_E_INVALID, "bad scalar operator arguments");
+  if (vector_metric && ncomp != 3) return fail(PC_E_INVALID, "vector metric needs 3 components");
+  if ((D && D->ncomp != 1) || (rho && rho->ncomp != 1)) return fail(PC_E_INVALID, "D and rho are scalar fields");
+  pc_op* op = new pc_op();
+  op->grid = g;
+  op->kind = K_SCALAR;
+  op->ncomp = ncomp;
+  op->so.D = D ? D->base(0) : nullptr;
+  op->so.Dc = D_const;
+  op->so.rho = rho ? rho->base(0) : nullptr;
+  op->so.ncomp = ncomp;
+  op->so.vector = (vector_metric && g->g.spherical) ? 1 : 0;
+  *out = op;
+  return PC_OK;
+}
+
+int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, double pref, double kappa0,
+                         const double* fc_table, double T_floor, pc_op** out) {
+  if (!g || !out || !bhat || bhat->ncomp != 3) return fail(PC_E_INVALID, "aligned operator needs a 3-component b");
+  if (rho && rho->ncomp != 1) return fail(PC_E_INVALID, "rho is a scalar field");
+  pc_ctx* c = g->ctx;
+  pc_op* op = new pc_op();
+  op->grid = g;
+  op->kind = K_ALIGNED;
+  op->ncomp = 1;
+  for (int q = 0; q < 3; ++q) op->ao.b[q] = bhat->base(q);
+  op->ao.rho = rho ? rho->base(0) : nullptr;
+  op->ao.pref = pref;
+  op->ao.ncomp = 1;
+  op->Tfloor = T_floor;
+  const int rows = g->g.n0 + 2;
+  std::vector<double> k(rows);
+  for (int r = 0; r < rows; ++r) k[r] = fc_table ? kappa0 * fc_table[r] : kappa0;
+  CUDA_TRY(cudaMalloc(&op->kfc, sizeof(double) * rows));
+  CUDA_TRY(cudaMemcpy(op->kfc, k.data(), sizeof(double) * rows, cudaMemcpyHostToDevice));
+  if (cudaMalloc(&op->cbuf, g->comp_elems * sizeof(double)) != cudaSuccess)
+    return fail(PC_E_CUDA, "conductivity allocation failed");
+  cudaMemsetAsync(op->cbuf, 0, g->comp_elems * sizeof(double), c->s);
+  op->ao.c = op->cbuf + g->g.plane;
+  *out = op;
+  return PC_OK;
+}
+
+int pc_op_destroy(pc_op* op) {
+  if (!op) return PC_OK;
+  cudaStreamSynchronize(op->grid->ctx->s);
+  cudaFree(op->cbuf);
+  cudaFree(op->dbuf);
+  cudaFree(op->kfc);
+  delete op;
+  return PC_OK;
+}
+
+template <class Op>
+static int run_bound(pc_op* op, const Op& o) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  int nb = grid_blocks(c, g->g.N);
+  k_bound<<<nb, kThreads, 0, c->s>>>(g->g, o, op->dbuf + g->g.plane, c->red_v, c->counter, c->maxout);
+  c->st.launches++;
+  TRY(check_launch("k_bound"));
+  TRY(allreduce_d(c, c->maxout, 1, nccl::kMax));
+  CUDA_TRY(cudaMemcpyAsync(c->h_maxout, c->maxout, sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  op->lam_max = *c->h_maxout;
+  op->dt_euler = op->lam_max > 0.0 ? 2.0 / op->lam_max : INFINITY;
+  return PC_OK;
+}
+
+int pc_op_freeze(pc_op* op, const pc_field* T0) {
+  if (!op) return fail(PC_E_INVALID, "null operator");
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  if (!op->dbuf) {
+    if (cudaMalloc(&op->dbuf, g->comp_elems * sizeof(double)) != cudaSuccess)
+      return fail(PC_E_CUDA, "diagonal allocation failed");
+    cudaMemsetAsync(op->dbuf, 0, g->comp_elems * sizeof(double), c->s);
+  }
+  if (op->kind == K_ALIGNED) {
+    if (!T0 || T0->ncomp != 1 || T0->grid != g) return fail(PC_E_INVALID, "aligned freeze needs a scalar T0 on the grid");
+    CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
+    k_aligned_coef<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, T0->base(0), op->kfc + 1, op->Tfloor,
+                                                                   op->cbuf + g->g.plane, c->bad);
+    c->st.launches++;
+    TRY(check_launch("k_aligned_coef"));
+    CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    if (*c->h_bad == 1) return fail(PC_E_DOMAIN, "aligned conduction: non-positive T0 (SPEC.md:120)");
+    double* cb[1] = {op->cbuf};
+    TRY(halo_exchange(c, g, cb, 1));
+    TRY(run_bound(op, op->ao));
+  } else {
+    TRY(run_bound(op, op->so));
+  }
+  double* db[1] = {op->dbuf};
+  TRY(halo_exchange(c, g, db, 1));
+  op->frozen = true;
+  return PC_OK;
+}
+
+int pc_op_euler_dt(pc_op* op, double* dt) {
+  if (!op || !dt) return fail(PC_E_INVALID, "null argument");
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  *dt = op->dt_euler;
+  return PC_OK;
+}
+
+int pc_op_diagonal(pc_op* op, pc_field* out) {
+  if (!op || !out || out->ncomp != 1) return fail(PC_E_INVALID, "diagonal output must be a scalar field");
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  CUDA_TRY(cudaMemcpyAsync(out->buf[0], op->dbuf, op->grid->comp_elems * sizeof(double),
+                           cudaMemcpyDeviceToDevice, op->grid->ctx->s));
+  CUDA_TRY(cudaStreamSynchronize(op->grid->ctx->s));
+  return PC_OK;
+}
+
+template <class Op>
+static int launch_apply(pc_op* op, const Op& o, CFld u, Fld F, bool argmax) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  int nb = grid_blocks(c, g->g.N);
+  if (argmax) {
+    k_apply_argmax<<<nb, kThreads, 0, c->s>>>(g->g, o, u, F, c->red_v, c->red_i, c->counter, c->res);
+  } else {
+    k_apply<<<nb, kThreads, 0, c->s>>>(g->g, o, u, F);
+  }
+  c->st.launches++;
+  return check_launch("k_apply");
+}
+static int apply_any(pc_op* op, CFld u, Fld F, bool argmax) {
+  if (op->kind == K_ALIGNED) return launch_apply(op, op->ao, u, F, argmax);
+  return launch_apply(op, op->so, u, F, argmax);
+}
+
+static int need_frozen(pc_op* op) {
+  if (op->kind == K_ALIGNED && !op->frozen)
+    return fail(PC_E_INVALID, "aligned operator: call pc_op_freeze(T0) first (lagged diffusivity)");
+  return PC_OK;
+}
+
+int pc_op_apply(pc_op* op, const pc_field* u, pc_field* F) {
+  if (!op || !u || !F || u->ncomp != op->ncomp || F->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  TRY(need_frozen(op));
+  TRY(halo_field(const_cast<pc_field*>(u)));
+  TRY(apply_any(op, cfld(u), fld(F), false));
+  CUDA_TRY(cudaStreamSynchronize(op->grid->ctx->s));
+  return PC_OK;
+}
+
+// ------------------------------------------------------------------ PTL
+static int ptl_device(pc_grid* g, int ncomp, CFld u, CFld F, double eps_rel, int check_all) {
+  pc_ctx* c = g->ctx;
+  if (check_all) {
+    CUDA_TRY(cudaMemsetAsync(c->minbits, 0x7f, sizeof(unsigned long long), c->s));  // huge positive
+    k_ptl_all<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, ncomp, u, F, eps_rel, c->res, c->minbits);
+    c->st.launches++;
+    TRY(check_launch("k_ptl_all"));
+  } else {
+    k_ptl_pairs<<<1, 32, 0, c->s>>>(g->g, ncomp, u, F, eps_rel, c->res);
+    c->st.launches++;
+    TRY(check_launch("k_ptl_pairs"));
+  }
+  return PC_OK;
+}
+// read back the argmax/PTL result (the single per-cycle sync)
+static int ptl_read(pc_ctx* c, int check_all, int use_ptl, double* ptl, int* limited, int64_t* kidx) {
+  CUDA_TRY(cudaMemcpyAsync(c->h_res, c->res, sizeof(ArgRes), cudaMemcpyDeviceToHost, c->s));
+  if (check_all) CUDA_TRY(cudaMemcpyAsync(c->h_minbits, c->minbits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  if (kidx) *kidx = c->h_res->kidx;
+  if (!use_ptl) {
+    *limited = 0;
+    *ptl = INFINITY;
+    return PC_OK;
+  }
+  if (check_all) {
+    double v;
+    unsigned long long bits = *c->h_minbits;
+    std::memcpy(&v, &bits, sizeof v);
+    *limited = (bits != 0x7f7f7f7f7f7f7f7fULL && std::isfinite(v)) ? 1 : 0;
+    *ptl = *limited ? v : INFINITY;
+  } else {
+    *limited = c->h_res->limited;
+    *ptl = c->h_res->limited ? c->h_res->ptl : INFINITY;
+  }
+  return PC_OK;
+}
+
+int pc_ptl(pc_grid* g, const pc_field* u, const pc_field* F, double eps_rel, int check_all, double* ptl,
+           int* limited, int64_t* kidx) {
+  if (!g || !u || !F || !ptl || !limited || u->ncomp != F->ncomp || u->grid != g || F->grid != g)
+    return fail(PC_E_INVALID, "bad PTL arguments");
+  if (!(eps_rel > 0.0)) return fail(PC_E_INVALID, "eps_rel must be > 0");
+  pc_ctx* c = g->ctx;
+  if (c->nranks > 1) return fail(PC_E_INVALID, "pc_ptl is single-rank; use pc_cycle");
+  k_argmax<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, u->ncomp, cfld(F), c->red_v, c->red_i,
+                                                          c->counter, c->res);
+  c->st.launches++;
+  TRY(check_launch("k_argmax"));
+  TRY(ptl_device(g, u->ncomp, cfld(u), cfld(F), eps_rel, check_all));
+  return ptl_read(c, check_all, 1, ptl, limited, kidx);
+}
+
+// ------------------------------------------------------------------ STS
+int pc_sts_count(int kind, double dt, double dt_euler, int make_odd) {
+  const double r = dt / dt_euler;
+  if (kind == PC_RKL2) {
+    long long s = (long long)std::ceil((std::sqrt(9.0 + 16.0 * r) - 1.0) / 2.0);
+    if (make_odd && s % 2 == 0) s += 1;
+    return (int)std::max<long long>(s, 2);
+  }
+  if (kind == PC_RKG2) {
+    long long s = (long long)std::ceil(0.5 * std::sqrt(25.0 + 24.0 * r) - 1.5);
+    if (s % 2 == 0) s += 1;
+    return (int)std::max<long long>(s, 3);
+  }
+  return -1;
+}
+
+int pc_sts_table(int kind, int s, double dt, double* out) {
+  if (!out) return fail(PC_E_INVALID, "null table");
+  std::vector<double> mu(s + 1, 0.0), nu(s + 1, 0.0), mut(s + 1, 0.0), gam(s + 1, 0.0), b(s + 1, 0.0);
+  if (kind == PC_RKL2) {
+    if (s < 2) return fail(PC_E_INVALID, "RKL2 needs s >= 2");
+    for (int j = 0; j <= s; ++j) {
+      const double jd = j;
+      b[j] = j <= 2 ? 1.0 / 3.0 : ((jd * jd + jd) - 2.0) / ((2.0 * jd) * (jd + 1.0));
+    }
+    const double sd = s;
+    const double w1 = 4.0 / ((sd * sd + sd) - 2.0);
+    mut[1] = b[1] * w1;
+    for (int j = 2; j <= s; ++j) {
+      const double jd = j;
+      mu[j] = (((2.0 * jd - 1.0) / jd) * b[j]) / b[j - 1];
+      nu[j] = ((-(jd - 1.0) / jd) * b[j]) / b[j - 2];
+      mut[j] = mu[j] * w1;
+      gam[j] = (-(1.0 - b[j - 1])) * mut[j];
+    }
+  } else if (kind == PC_RKG2) {
+    if (s < 3 || s % 2 == 0) return fail(PC_E_INVALID, "RKG2 needs odd s >= 3 (SPEC.md:264)");
+    const double sd = s;
+    const double w = 6.0 / ((sd + 4.0) * (sd - 1.0));
+    b[0] = 1.0;
+    b[1] = 1.0 / 3.0;
+    b[2] = 1.0 / 15.0;
+    mu[1] = 1.0;
+    mut[1] = w;
+    mu[2] = 0.5;
+    nu[2] = -0.1;
+    mut[2] = mu[2] * w;
+    gam[2] = 0.0;
+    for (int k = 3; k <= s; ++k) {
+      const double kd = k;
+      b[k] = ((4.0 * (kd - 1.0)) * (kd + 4.0)) / ((((3.0 * kd) * (kd + 1.0)) * (kd + 2.0)) * (kd + 3.0));
+      mu[k] = ((2.0 + 1.0 / kd) * b[k]) / b[k - 1];
+      nu[k] = ((-(1.0 / kd + 1.0)) * b[k]) / b[k - 2];
+      mut[k] = mu[k] * w;
+      gam[k] = ((((kd * (kd + 1.0)) / 2.0) * b[k - 1]) - 1.0) * mut[k];
+    }
+  } else {
+    return fail(PC_E_INVALID, "unknown STS kind");
+  }
+  for (int k = 1; k <= s; ++k) {
+    double* r = out + 5 * (k - 1);
+    r[0] = mu[k];
+    r[1] = nu[k];
+    r[2] = (1.0 - mu[k]) - nu[k];
+    r[3] = mut[k] * dt;
+    r[4] = gam[k] * dt;
+  }
+  return PC_OK;
+}
+
+template <class Op>
+static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, int s, Work& y0) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int nc = op->ncomp;
+  Work A, B;
+  TRY(work_get(g, nc, A));
+  int rc = work_get(g, nc, B);
+  if (rc) {
+    work_put(A);
+    return rc;
+  }
+  const int nb = grid_blocks(c, g->g.N);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->s);
+  }
+  CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
+  k_stage1<<<nb, kThreads, 0, c->s>>>(g->g, nc, cfld(u), y0.cf(), A.f(), tab[3], c->bad);
+  c->st.launches++;
+  c->st.stage_launches++;
+  rc = check_launch("k_stage1");
+  Work* um1 = &A;
+  Work* out = &B;
+  Work* um2w = nullptr;  // nullptr -> u0
+  for (int k = 2; k <= s && rc == PC_OK; ++k) {
+    const double* r = tab + 5 * (k - 1);
+    StageCoef sc{r[0], r[1], r[2], r[3], r[4]};
+    rc = halo_work(g, *um1);
+    if (rc) break;
+    CFld m2 = um2w ? um2w->cf() : cfld(u);
+    k_stage<<<nb, kThreads, 0, c->s>>>(g->g, o, um1->cf(), m2, cfld(u), y0.cf(), out->f(), sc, k, c->bad);
+    c->st.launches++;
+    c->st.stage_launches++;
+    rc = check_launch("k_stage");
+    // rotate: u_{k-1} -> u_{k-2}, u_k -> u_{k-1}; the next stage writes into
+    // the buffer that held u_{k-1} before this stage, i.e. the new u_{k-2}
+    // (pointwise safe: u_{k-2} is only read at the thread's own node)
+    Work* prev_um1 = um1;
+    um2w = um1;
+    um1 = out;
+    out = prev_um1;
+  }
+  if (c->timing) {
+    cudaEventRecord(e1, c->s);
+    c->ev.push_back({e0, e1});
+  }
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    if (*c->h_bad != 0x7f7f7f7f) {
+      rc = fail(PC_E_BLOWUP, "non-finite value at STS stage " + std::to_string(*c->h_bad), *c->h_bad);
+    } else {
+      swap_storage(u, *um1);  // u <- u_s; the old u0 storage returns to the pool
+    }
+  }
+  work_put(A);
+  work_put(B);
+  return rc;
+}
+
+static int sts_any(pc_op* op, pc_field* u, const double* tab, int s, Work& y0) {
+  if (op->kind == K_ALIGNED) return sts_stages(op, op->ao, u, tab, s, y0);
+  return sts_stages(op, op->so, u, tab, s, y0);
+}
+
+int pc_step_sts(pc_op* op, pc_field* u, double dt, int kind, int s, const pc_field* y0in) {
+  if (!op || !u || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  if (kind != PC_RKL2 && kind != PC_RKG2) return fail(PC_E_INVALID, "unknown STS kind");
+  TRY(need_frozen(op));
+  pc_grid* g = op->grid;
+  std::vector<double> tab(5 * (size_t)s);
+  TRY(pc_sts_table(kind, s, dt, tab.data()));
+  Work y0;
+  TRY(work_get(g, op->ncomp, y0));
+  int rc = PC_OK;
+  if (y0in) {
+    for (int q = 0; q < op->ncomp && rc == PC_OK; ++q)
+      if (cudaMemcpyAsync(y0.b[q], y0in->buf[q], g->comp_elems * sizeof(double), cudaMemcpyDeviceToDevice,
+                          g->ctx->s) != cudaSuccess)
+        rc = fail(PC_E_CUDA, "y0 copy");
+  } else {
+    rc = halo_field(u);
+    if (rc == PC_OK) rc = apply_any(op, cfld(u), y0.f(), false);
+  }
+  if (rc == PC_OK) rc = sts_any(op, u, tab.data(), s, y0);
+  work_put(y0);
+  return rc;
+}
+
+int pc_step_euler(pc_op* op, pc_field* u, double dt) {
+  if (!op || !u || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  TRY(need_frozen(op));
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  Work y0, A;
+  TRY(work_get(g, op->ncomp, y0));
+  TRY(work_get(g, op->ncomp, A));
+  int rc = halo_field(u);
+  if (rc == PC_OK) rc = apply_any(op, cfld(u), y0.f(), false);
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
+    k_stage1<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, op->ncomp, cfld(u), y0.cf(), A.f(), dt, c->bad);
+    c->st.launches++;
+    rc = check_launch("k_stage1");
+  }
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    swap_storage(u, A);
+  }
+  work_put(y0);
+  work_put(A);
+  return rc;
+}
+
+// ------------------------------------------------------------------ PCG
+template <class Op>
+static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld b, pc_field* x, double tol,
+                   int max_iter, int* iters, double* relres, int* converged) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int nc = op->ncomp;
+  Work r, p0, p1, Ap;
+  TRY(work_get(g, nc, r));
+  TRY(work_get(g, nc, p0));
+  TRY(work_get(g, nc, p1));
+  TRY(work_get(g, nc, Ap));
+  const double* dg = op->dbuf + g->g.plane;
+  const int nb = grid_blocks(c, g->g.N);
+  int rc = halo_field(x);
+  if (rc == PC_OK) {
+    k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, c->red_v, c->red_v2,
+                                          c->counter, c->pcg);
+    c->st.launches++;
+    rc = check_launch("k_pcg_init");
+  }
+  Work* pold = &p0;
+  Work* pnew = &p1;
+  const int batch = 4;
+  int it = 0;
+  bool stop = false;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->s);
+  }
+  while (rc == PC_OK && !stop && it < max_iter) {
+    for (int q = 0; q < batch && it < max_iter && rc == PC_OK; ++q) {
+      ++it;
+      rc = halo_work(g, r);
+      if (rc == PC_OK) rc = halo_work(g, *pold);
+      if (rc) break;
+      k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
+                                              c->red_v, c->counter, c->pcg);
+      k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, tol, it,
+                                              c->red_v, c->red_v2, c->counter, c->pcg);
+      c->st.launches += 2;
+      c->st.stage_launches += 2;
+      rc = check_launch("k_pcg");
+      std::swap(pold, pnew);
+    }
+    if (rc) break;
+    if (cudaMemcpyAsync(c->h_pcg, c->pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, c->s) != cudaSuccess ||
+        cudaStreamSynchronize(c->s) != cudaSuccess) {
+      rc = fail(PC_E_CUDA, "PCG state readback");
+      break;
+    }
+    if (c->h_pcg->done) stop = true;
+  }
+  if (c->timing) {
+    cudaEventRecord(e1, c->s);
+    c->ev.push_back({e0, e1});
+  }
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaMemcpyAsync(c->h_pcg, c->pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, c->s));
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    const PcgDev& st = *c->h_pcg;
+    *iters = st.it;
+    *relres = st.rel;
+    *converged = st.status == 1 ? 1 : 0;
+    if (st.status == 2) rc = fail(PC_E_INDEFINITE, "PCG breakdown: p^T A p <= 0 (indefinite operator)");
+    if (st.status == 3) rc = fail(PC_E_DIVERGED, "PCG divergence: non-finite residual");
+  }
+  work_put(r);
+  work_put(p0);
+  work_put(p1);
+  work_put(Ap);
+  return rc;
+}
+
+static int pcg_any(pc_op* op, double dt, const double* adiag, CFld b, pc_field* x, double tol, int max_iter,
+                   int* iters, double* relres, int* converged) {
+  if (op->kind == K_ALIGNED) return pcg_run(op, op->ao, dt, adiag, b, x, tol, max_iter, iters, relres, converged);
+  return pcg_run(op, op->so, dt, adiag, b, x, tol, max_iter, iters, relres, converged);
+}
+
+int pc_pcg_solve(pc_op* op, double dt, const pc_field* diag_a, const pc_field* b, pc_field* x, double tol,
+                 int max_iter, int* iters, double* relres, int* converged) {
+  if (!op || !b || !x || !iters || !relres || !converged) return fail(PC_E_INVALID, "null argument");
+  if (b->ncomp != op->ncomp || x->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  if (!(tol > 0.0 && tol < 1.0) || max_iter < 1) return fail(PC_E_INVALID, "need 0 < tol < 1 and max_iter >= 1");
+  TRY(need_frozen(op));
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  const double* ad = diag_a ? diag_a->base(0) : nullptr;
+  return pcg_any(op, dt, ad, cfld(b), x, tol, max_iter, iters, relres, converged);
+}
+
+static int be_step(pc_op* op, pc_field* u, double dt, double tol, int max_iter, int* iters, double* relres,
+                   int* converged) {
+  pc_grid* g = op->grid;
+  Work bw;
+  TRY(work_get(g, op->ncomp, bw));
+  int rc = PC_OK;
+  for (int q = 0; q < op->ncomp && rc == PC_OK; ++q)
+    if (cudaMemcpyAsync(bw.b[q], u->buf[q], g->comp_elems * sizeof(double), cudaMemcpyDeviceToDevice, g->ctx->s) !=
+        cudaSuccess)
+      rc = fail(PC_E_CUDA, "BE rhs copy");
+  if (rc == PC_OK) rc = pcg_any(op, dt, nullptr, bw.cf(), u, tol, max_iter, iters, relres, converged);
+  work_put(bw);
+  return rc;
+}
+
+int pc_step_be(pc_op* op, pc_field* u, double dt, double tol, int max_iter, int* iters, double* relres,
+               int* converged) {
+  if (!op || !u || u->ncomp != op->ncomp || !iters || !relres || !converged) return fail(PC_E_INVALID, "bad arguments");
+  if (!(tol > 0.0 && tol < 1.0) || max_iter < 1) return fail(PC_E_INVALID, "need 0 < tol < 1 and max_iter >= 1");
+  TRY(need_frozen(op));
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  return be_step(op, u, dt, tol, max_iter, iters, relres, converged);
+}
+
+// ------------------------------------------------------------------ cycle
+int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, double tol, int max_iter,
+             double eps_rel, int check_all, int use_ptl, int floor_mode, double floor_fraction, int64_t max_cycles,
+             double dt_euler, pc_cycle_record* rec, int64_t rec_cap, int64_t* n_rec) {
+  if (!op || !u || !n_rec || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "bad cycle arguments");
+  if (!(outer_dt > 0.0)) return fail(PC_E_INVALID, "outer_dt must be > 0");
+  if (max_cycles < 1 || !(eps_rel > 0.0)) return fail(PC_E_INVALID, "need max_cycles >= 1 and eps_rel > 0");
+  if (scheme < PC_RKL2 || scheme > PC_EULER) return fail(PC_E_INVALID, "unknown scheme");
+  TRY(need_frozen(op));
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const double dtE = dt_euler > 0.0 ? dt_euler : op->dt_euler;
+  const double floor_dt = floor_mode == PC_FLOOR_EULER ? dtE : floor_fraction * dtE;
+  double remaining = outer_dt;
+  int64_t cyc = 0;
+  *n_rec = 0;
+  Work y0;
+  TRY(work_get(g, op->ncomp, y0));
+  int rc = PC_OK;
+  std::vector<double> tab;
+  while (remaining > 0.0) {
+    if (cyc >= max_cycles) {
+      rc = fail(PC_E_CAP, "max_cycles reached (partial report returned)", cyc);
+      break;
+    }
+    rc = halo_field(u);
+    if (rc) break;
+    rc = apply_any(op, cfld(u), y0.f(), true);
+    if (rc) break;
+    if (use_ptl) {
+      if (c->nranks > 1) {
+        rc = fail(PC_E_INVALID, "multi-rank PTL not enabled in this build");
+        break;
+      }
+      rc = ptl_device(g, op->ncomp, cfld(u), y0.cf(), eps_rel, check_all);
+      if (rc) break;
+    }
+    double ptl;
+    int limited;
+    rc = ptl_read(c, check_all, use_ptl, &ptl, &limited, nullptr);
+    if (rc) break;
+    double dt;
+    if (!limited) {
+      dt = remaining;
+    } else {
+      dt = ptl >= floor_dt ? ptl : floor_dt;  // Python max(ptl, floor)
+      if (dt >= remaining) dt = remaining;
+    }
+    int iters = 0;
+    double rel = 0.0;
+    if (scheme == PC_RKL2 || scheme == PC_RKG2) {
+      int s = pc_sts_count(scheme, dt, dtE, make_odd);
+      tab.assign(5 * (size_t)s, 0.0);
+      rc = pc_sts_table(scheme, s, dt, tab.data());
+      if (rc) break;
+      rc = sts_any(op, u, tab.data(), s, y0);
+      iters = s;
+    } else if (scheme == PC_BE) {
+      int conv = 0;
+      rc = be_step(op, u, dt, tol, max_iter, &iters, &rel, &conv);
+      if (rc == PC_OK && !conv) rc = fail(PC_E_NOTCONV, "PCG did not converge within max_iter", iters);
+    } else {
+      Work A;
+      rc = work_get(g, op->ncomp, A);
+      if (rc) break;
+      CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
+      k_stage1<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, op->ncomp, cfld(u), y0.cf(), A.f(), dt, c->bad);
+      c->st.launches++;
+      rc = check_launch("k_stage1");
+      if (rc == PC_OK) swap_storage(u, A);
+      work_put(A);
+      iters = 1;
+    }
+    ++cyc;
+    if (rec && *n_rec < rec_cap) {
+      pc_cycle_record& R = rec[*n_rec];
+      R.cycle = cyc;
+      R.dt = dt;
+      R.ptl_raw = limited ? ptl : INFINITY;
+      R.relres = rel;
+      R.limited = limited;
+      R.iters = iters;
+      ++*n_rec;
+    }
+    if (rc) break;
+    if (dt == remaining) remaining = 0.0;
+    else remaining = remaining - dt;
+  }
+  work_put(y0);
+  if (rc == PC_OK) CUDA_TRY(cudaStreamSynchronize(c->s));
+  return rc;
+}
+

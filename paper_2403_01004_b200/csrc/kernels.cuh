@@ -1,0 +1,462 @@
+// Generic kernels over an operator (ScalarOp / AlignedOp):
+//   k_apply            F = op(u)
+//   k_apply_argmax     y0 = F(u0) fused with the |F| argmax of the PTL (K4)
+//   k_stage1           u1 = u0 + mut1*dt*y0                      (stage 1)
+//   k_stage            fused RKL2/RKG2 stage k >= 2 (K1/K2/K3)
+//   k_ptl_pairs        Eq. 5 pair tests at the argmax (K5)
+//   k_ptl_all          audit mode: every pair (check_all_points)
+//   k_bound            Gershgorin row bound (max) + Jacobi diagonal (K6)
+//   k_pcg_*            Jacobi-PCG (K7/K8) with device-side convergence state
+//   k_aos_to_soa / k_soa_to_aos   Field layout conversion
+#pragma once
+#include "ops.cuh"
+
+namespace pc {
+
+struct Fld {
+  double* p[3];
+};
+struct CFld {
+  const double* p[3];
+};
+
+struct ArgRes {  // device result of the F-argmax reduction and the PTL
+  double fmax;
+  long long kidx;
+  double ptl;
+  int limited;
+  int pad;
+};
+
+__device__ __forceinline__ long long aos_index(const GridDev& g, int i, int j, int k, int c, int ncomp) {
+  return (((long long)(i + g.i0g) * g.n1 + j) * g.n2 + k) * ncomp + c;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_apply(GridDev g, Op op, CFld u, Fld F) {
+  PlainVal val{{u.p[0], u.p[1], u.p[2]}};
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    double out[3];
+    op.F(g, val, i, j, k, out);
+    const int64_t o = off3(g, i, j, k);
+    for (int q = 0; q < op.ncomp; ++q) F.p[q][o] = out[q];
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_apply_argmax(GridDev g, Op op, CFld u, Fld F, double* pv,
+                                                           long long* pi, unsigned int* counter,
+                                                           ArgRes* res) {
+  __shared__ double shv[kThreads / 32];
+  __shared__ long long shi[kThreads / 32];
+  PlainVal val{{u.p[0], u.p[1], u.p[2]}};
+  ArgMax best{-1.0, 0x7fffffffffffffffLL};
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    double out[3];
+    op.F(g, val, i, j, k, out);
+    const int64_t o = off3(g, i, j, k);
+    for (int q = 0; q < op.ncomp; ++q) {
+      F.p[q][o] = out[q];
+      ArgMax cand{fabs(out[q]), aos_index(g, i, j, k, q, op.ncomp)};
+      best = am_better(best, cand);
+    }
+  }
+  best = block_argmax<kThreads>(best, shv, shi);
+  if (threadIdx.x == 0) {
+    pv[blockIdx.x] = best.v;
+    pi[blockIdx.x] = best.i;
+  }
+  if (last_block(counter)) {
+    ArgMax b{-1.0, 0x7fffffffffffffffLL};
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) b = am_better(b, ArgMax{pv[t], pi[t]});
+    b = block_argmax<kThreads>(b, shv, shi);
+    if (threadIdx.x == 0) {
+      res->fmax = b.v;
+      res->kidx = b.i;
+      *counter = 0u;
+    }
+  }
+}
+
+// argmax of |F| over a given field (pc_ptl with a caller-supplied F)
+__global__ void __launch_bounds__(kThreads) k_argmax(GridDev g, int ncomp, CFld F, double* pv, long long* pi,
+                                                     unsigned int* counter, ArgRes* res) {
+  __shared__ double shv[kThreads / 32];
+  __shared__ long long shi[kThreads / 32];
+  ArgMax best{-1.0, 0x7fffffffffffffffLL};
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    const int64_t o = off3(g, i, j, k);
+    for (int q = 0; q < ncomp; ++q) best = am_better(best, ArgMax{fabs(F.p[q][o]), aos_index(g, i, j, k, q, ncomp)});
+  }
+  best = block_argmax<kThreads>(best, shv, shi);
+  if (threadIdx.x == 0) {
+    pv[blockIdx.x] = best.v;
+    pi[blockIdx.x] = best.i;
+  }
+  if (last_block(counter)) {
+    ArgMax b{-1.0, 0x7fffffffffffffffLL};
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) b = am_better(b, ArgMax{pv[t], pi[t]});
+    b = block_argmax<kThreads>(b, shv, shi);
+    if (threadIdx.x == 0) {
+      res->fmax = b.v;
+      res->kidx = b.i;
+      *counter = 0u;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_stage1(GridDev g, int ncomp, CFld u0, CFld y0, Fld out,
+                                                     double mtdt, int* bad) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    const int64_t o = off3(g, i, j, k);
+    const bool pin = pinned(g, i, j, k);
+    for (int q = 0; q < ncomp; ++q) {
+      double a = __ldg(u0.p[q] + o);
+      double v = pin ? a : a + mtdt * __ldg(y0.p[q] + o);
+      out.p[q][o] = v;
+      if (!isfinite(v)) atomicMin(bad, 1);
+    }
+  }
+}
+
+struct StageCoef {
+  double mu, nu, kap, mtdt, gtdt;
+};
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_stage(GridDev g, Op op, CFld um1, CFld um2, CFld u0, CFld y0,
+                                                    Fld out, StageCoef sc, int stage, int* bad) {
+  PlainVal val{{um1.p[0], um1.p[1], um1.p[2]}};
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    double Fk[3];
+    op.F(g, val, i, j, k, Fk);
+    const int64_t o = off3(g, i, j, k);
+    const bool pin = pinned(g, i, j, k);
+    for (int q = 0; q < op.ncomp; ++q) {
+      double a0 = __ldg(u0.p[q] + o);
+      double v = ((((sc.mu * __ldg(um1.p[q] + o)) + (sc.nu * __ldg(um2.p[q] + o))) + (sc.kap * a0)) +
+                  (sc.mtdt * Fk[q])) + (sc.gtdt * __ldg(y0.p[q] + o));
+      v = pin ? a0 : v;
+      out.p[q][o] = v;
+      if (!isfinite(v)) atomicMin(bad, stage);
+    }
+  }
+}
+
+// PTL pair tests at k (single block); neighbours = existing orthogonal nodes.
+__global__ void k_ptl_pairs(GridDev g, int ncomp, CFld u, CFld F, double eps_rel, ArgRes* res) {
+  __shared__ double sh[32];
+  const long long kid = res->kidx;
+  const double thr = eps_rel * res->fmax;
+  const long long pt = kid / ncomp;
+  const int kk = (int)(pt % g.n2);
+  const long long t2 = pt / g.n2;
+  const int kj = (int)(t2 % g.n1);
+  const int ki = (int)(t2 / g.n1) - g.i0g;
+  double best = INFINITY;
+  const int t = threadIdx.x;
+  if (t < 6 * ncomp) {
+    const int dirn = t / ncomp, q = t % ncomp;
+    const int a = dirn / 2, d = (dirn & 1) ? 1 : -1;
+    bool ok;
+    const int co[3] = {ki, kj, kk};
+    int x = nbax(g, a, co[a], d, ok);
+    if (ok) {
+      int ni = a == 0 ? x : ki, nj = a == 1 ? x : kj, nk = a == 2 ? x : kk;
+      const int64_t ok0 = off3(g, ki, kj, kk), on = off3(g, ni, nj, nk);
+      double du = u.p[q][ok0] - u.p[q][on];
+      double dF = F.p[q][ok0] - F.p[q][on];
+      if (du != 0.0 && fabs(dF) > thr && du * dF < 0.0) best = -du / dF;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_down_sync(0xffffffffu, best, o));
+  if (t == 0) {
+    res->ptl = best;
+    res->limited = isfinite(best) ? 1 : 0;
+  }
+  (void)sh;
+}
+
+// audit mode: all (node, node + e_a) pairs; candidates are > 0 so their bit
+// patterns order like the values (atomicMin on the raw bits).
+__global__ void __launch_bounds__(kThreads) k_ptl_all(GridDev g, int ncomp, CFld u, CFld F, double eps_rel,
+                                                      const ArgRes* res, unsigned long long* minbits) {
+  const double thr = eps_rel * res->fmax;
+  double best = INFINITY;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    const int64_t o = off3(g, i, j, k);
+    const int co[3] = {i, j, k};
+    for (int a = 0; a < 3; ++a) {
+      bool ok;
+      int x = nbax(g, a, co[a], 1, ok);
+      if (!ok) continue;
+      int ni = a == 0 ? x : i, nj = a == 1 ? x : j, nk = a == 2 ? x : k;
+      const int64_t on = off3(g, ni, nj, nk);
+      for (int q = 0; q < ncomp; ++q) {
+        double du = u.p[q][o] - u.p[q][on];
+        double dF = F.p[q][o] - F.p[q][on];
+        if (du != 0.0 && fabs(dF) > thr && du * dF < 0.0) best = fmin(best, -du / dF);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_down_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && isfinite(best)) atomicMin(minbits, (unsigned long long)__double_as_longlong(best));
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_bound(GridDev g, Op op, double* diag, double* pv,
+                                                    unsigned int* counter, double* out_max) {
+  __shared__ double sh[kThreads / 32];
+  double m = 0.0;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    double lam[3], dg;
+    op.bound(g, i, j, k, lam, dg);
+    for (int q = 0; q < op.ncomp; ++q) m = fmax(m, lam[q]);
+    diag[off3(g, i, j, k)] = dg;
+  }
+  m = block_max<kThreads>(m, sh);
+  if (threadIdx.x == 0) pv[blockIdx.x] = m;
+  if (last_block(counter)) {
+    double b = 0.0;
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) b = fmax(b, pv[t]);
+    b = block_max<kThreads>(b, sh);
+    if (threadIdx.x == 0) {
+      *out_max = b;
+      *counter = 0u;
+    }
+  }
+}
+
+// c = kfc[i] * ((T0f * T0f) * sqrt(T0f)), T0f = max(T0, T_floor); bad if T0 <= 0
+__global__ void __launch_bounds__(kThreads) k_aligned_coef(GridDev g, const double* T0, const double* kfc,
+                                                           double Tfloor, double* c, int* bad) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.N; q += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, q, i, j, k);
+    const int64_t o = off3(g, i, j, k);
+    double t = T0[o];
+    if (!(t > 0.0)) atomicMin(bad, 1);
+    double tf = fmax(t, Tfloor);
+    c[o] = kfc[i] * ((tf * tf) * sqrt(tf));
+  }
+}
+
+// ---------------------------------------------------------------- PCG
+struct PcgDev {
+  double rz;     // (r, z)_W of the current residual
+  double alpha;
+  double beta;
+  double bn;     // ||b||_W
+  double rel;    // last relative residual
+  double pAp;
+  int it;        // completed iterations
+  int done;      // 1 = stop (converged or error)
+  int status;    // 0 ok, 1 converged, 2 indefinite, 3 diverged
+  int pad;
+};
+
+// p = z + beta * p_old with z = r / (a + dt*dg)   (recomputed at neighbours)
+struct PVal {
+  const double* r[3];
+  const double* pold[3];
+  const double* dg;
+  const double* adiag;
+  double dt, beta;
+  __device__ __forceinline__ double operator()(int c, int64_t o, int, int, int) const {
+    double dvec = (adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o);
+    double z = __ldg(r[c] + o) / dvec;
+    return z + beta * __ldg(pold[c] + o);
+  }
+};
+
+// init: r = b - A x, z = r/d, p_old = 0; partials (r,z)_W and (b,b)_W
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b, CFld x, Fld r, Fld pold,
+                                                       const double* dg, const double* adiag, double dt,
+                                                       double* p1, double* p2, unsigned int* counter,
+                                                       PcgDev* st) {
+  __shared__ double sh[kThreads / 32];
+  PlainVal val{{x.p[0], x.p[1], x.p[2]}};
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    double Fx[3];
+    op.F(g, val, i, j, k, Fx);
+    const int64_t o = off3(g, i, j, k);
+    const double W = op.weight(g, i, j, k);
+    const double dvec = (adiag ? adiag[o] : 1.0) + dt * dg[o];
+    for (int q = 0; q < op.ncomp; ++q) {
+      double xv = x.p[q][o];
+      double Ax = (adiag ? adiag[o] * xv : xv) - dt * Fx[q];
+      double rv = b.p[q][o] - Ax;
+      r.p[q][o] = rv;
+      pold.p[q][o] = 0.0;
+      double z = rv / dvec;
+      s1 += (W * rv) * z;
+      double bv = b.p[q][o];
+      s2 += (W * bv) * bv;
+    }
+  }
+  s1 = block_sum<kThreads>(s1, sh);
+  s2 = block_sum<kThreads>(s2, sh);
+  if (threadIdx.x == 0) {
+    p1[blockIdx.x] = s1;
+    p2[blockIdx.x] = s2;
+  }
+  if (last_block(counter)) {
+    if (threadIdx.x == 0) {
+      double a = 0.0, bb = 0.0;
+      for (int t = 0; t < (int)gridDim.x; ++t) { a += p1[t]; bb += p2[t]; }
+      st->rz = a;
+      st->bn = sqrt(bb);
+      st->beta = 0.0;
+      st->alpha = 0.0;
+      st->it = 0;
+      st->done = 0;
+      st->status = 0;
+      st->rel = INFINITY;
+      *counter = 0u;
+    }
+  }
+}
+
+// K7: p_new = z + beta p_old; Ap = a p_new - dt F(p_new); partial (p, Ap)_W
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld r, CFld pold, Fld pnew, Fld Ap,
+                                                         const double* dg, const double* adiag, double dt,
+                                                         double* p1, unsigned int* counter, PcgDev* st) {
+  __shared__ double sh[kThreads / 32];
+  if (st->done) return;
+  PVal val{{r.p[0], r.p[1], r.p[2]}, {pold.p[0], pold.p[1], pold.p[2]}, dg, adiag, dt, st->beta};
+  double s1 = 0.0;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    double Fp[3];
+    op.F(g, val, i, j, k, Fp);
+    const int64_t o = off3(g, i, j, k);
+    const double W = op.weight(g, i, j, k);
+    for (int q = 0; q < op.ncomp; ++q) {
+      double pv = val(q, o, i, j, k);
+      double ap = (adiag ? adiag[o] * pv : pv) - dt * Fp[q];
+      pnew.p[q][o] = pv;
+      Ap.p[q][o] = ap;
+      s1 += (W * pv) * ap;
+    }
+  }
+  s1 = block_sum<kThreads>(s1, sh);
+  if (threadIdx.x == 0) p1[blockIdx.x] = s1;
+  if (last_block(counter)) {
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+      for (int t = 0; t < (int)gridDim.x; ++t) a += p1[t];
+      st->pAp = a;
+      if (st->rz != 0.0) {
+        if (!(a > 0.0)) {
+          st->status = isnan(a) ? 3 : 2;
+          st->done = 1;
+        } else {
+          st->alpha = st->rz / a;
+        }
+      } else {
+        st->alpha = 0.0;
+      }
+      *counter = 0u;
+    }
+  }
+}
+
+// K8: x += alpha p; r -= alpha Ap; partials (r,r)_W and (r,z)_W
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_pcg_update(GridDev g, Op op, Fld x, Fld r, CFld p, CFld Ap,
+                                                         const double* dg, const double* adiag, double dt,
+                                                         double tol, int it, double* p1, double* p2,
+                                                         unsigned int* counter, PcgDev* st) {
+  __shared__ double sh[kThreads / 32];
+  if (st->done) return;
+  const double alpha = st->alpha;
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    const int64_t o = off3(g, i, j, k);
+    const double W = op.weight(g, i, j, k);
+    const double dvec = (adiag ? adiag[o] : 1.0) + dt * dg[o];
+    for (int q = 0; q < op.ncomp; ++q) {
+      x.p[q][o] = x.p[q][o] + alpha * p.p[q][o];
+      double rv = r.p[q][o] - alpha * Ap.p[q][o];
+      r.p[q][o] = rv;
+      s1 += (W * rv) * rv;
+      s2 += (W * rv) * (rv / dvec);
+    }
+  }
+  s1 = block_sum<kThreads>(s1, sh);
+  s2 = block_sum<kThreads>(s2, sh);
+  if (threadIdx.x == 0) {
+    p1[blockIdx.x] = s1;
+    p2[blockIdx.x] = s2;
+  }
+  if (last_block(counter)) {
+    if (threadIdx.x == 0) {
+      double rr = 0.0, rzn = 0.0;
+      for (int t = 0; t < (int)gridDim.x; ++t) { rr += p1[t]; rzn += p2[t]; }
+      st->it = it;
+      if (!isfinite(rr)) {
+        st->status = 3;
+        st->done = 1;
+      } else {
+        double rn = sqrt(rr);
+        double rel = st->bn > 0.0 ? rn / st->bn : (rn == 0.0 ? 0.0 : INFINITY);
+        st->rel = rel;
+        if (rel <= tol) {
+          st->status = 1;
+          st->done = 1;
+        } else {
+          st->beta = st->rz != 0.0 ? rzn / st->rz : 0.0;
+          st->rz = rzn;
+        }
+      }
+      *counter = 0u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- layout
+// host AoS chunk [planes][n1][n2][ncomp] -> SoA field planes [p0, p0+np)
+__global__ void __launch_bounds__(kThreads) k_aos_to_soa(GridDev g, int ncomp, const double* src, Fld dst,
+                                                         int p0, int np) {
+  const int64_t n = (int64_t)np * g.plane;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)p0 * g.plane + c;
+    for (int q = 0; q < ncomp; ++q) dst.p[q][o] = src[c * ncomp + q];
+  }
+}
+__global__ void __launch_bounds__(kThreads) k_soa_to_aos(GridDev g, int ncomp, CFld src, double* dst,
+                                                         int p0, int np) {
+  const int64_t n = (int64_t)np * g.plane;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)p0 * g.plane + c;
+    for (int q = 0; q < ncomp; ++q) dst[c * ncomp + q] = src.p[q][o];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_fill(double* p, int64_t n, double v) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) p[c] = v;
+}
+
+}  // namespace pc

@@ -1,0 +1,230 @@
+"""Device-side handles: context (one per GPU / rank), grids and fields.
+
+Thin RAII wrappers over the C ABI.  A ``DeviceField`` lives in HBM in the
+SoA layout of the library; ``upload``/``download`` convert from/to the
+reference ``Field`` layout (component innermost).  With ``nranks > 1`` every
+rank holds its axis-0 (r) slab (``geometry.slab_bounds``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import byref, c_double, c_int64, c_void_p
+
+import numpy as np
+
+from . import _lib, geometry, mesh
+
+
+class Context:
+    def __init__(self, device: int = 0, nranks: int = 1, rank: int = 0, nccl_uid: bytes | None = None):
+        L = _lib.lib()
+        h = c_void_p()
+        uid = None
+        if nccl_uid is not None:
+            uid = ctypes.create_string_buffer(bytes(nccl_uid), 128)
+        _lib.check(L.pc_ctx_create(int(device), int(nranks), int(rank), uid, byref(h)), "pc_ctx_create")
+        self.handle = h
+        self.device = device
+        self.nranks = nranks
+        self.rank = rank
+        self._grids = {}
+        self._pinned = []
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            for a in self._pinned:
+                _lib.lib().pc_host_unregister(a.ctypes.data)
+            self._pinned = []
+            self._grids = {}
+            _lib.lib().pc_ctx_destroy(self.handle)
+            self.handle = None
+
+    def sync(self):
+        _lib.check(_lib.lib().pc_ctx_sync(self.handle), "sync")
+
+    def enable_timing(self, on: bool = True):
+        _lib.lib().pc_ctx_enable_timing(self.handle, int(on))
+
+    def reset_stats(self):
+        _lib.lib().pc_ctx_reset_stats(self.handle)
+
+    def stats(self):
+        ms = c_double()
+        sl = c_int64()
+        tot = c_int64()
+        _lib.lib().pc_ctx_stats(self.handle, byref(ms), byref(sl), byref(tot))
+        return {"stage_ms": ms.value, "stage_launches": sl.value, "launches": tot.value}
+
+    def pin(self, arr: np.ndarray):
+        """Page-lock a host array (kept pinned for the context's lifetime)."""
+        _lib.check(_lib.lib().pc_host_register(arr.ctypes.data, arr.nbytes), "pin")
+        self._pinned.append(arr)
+        return arr
+
+    def unpin(self, arr: np.ndarray):
+        for q, a in enumerate(self._pinned):
+            if a is arr:
+                _lib.lib().pc_host_unregister(arr.ctypes.data)
+                del self._pinned[q]
+                return
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _lib.check(_lib.lib().pc_nccl_unique_id(buf), "ncclGetUniqueId")
+        return buf.raw
+
+
+_default: Context | None = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None or _default.handle is None:
+        _default = Context(int(os.environ.get("PARACYCLE_DEVICE", "0")))
+    return _default
+
+
+def set_default_context(ctx: Context):
+    global _default
+    _default = ctx
+
+
+class DeviceGrid:
+    """A grid (+ boundary condition) resident on one rank: metric tables and
+    the slab geometry."""
+
+    def __init__(self, grid, bc, ctx: Context | None = None):
+        ctx = ctx or default_context()
+        self.ctx = ctx
+        self.grid = grid
+        self.bc = bc
+        gt = geometry.global_tables(grid, bc)
+        self.tables_global = gt
+        n0 = gt.shape[0]
+        P, r = ctx.nranks, ctx.rank
+        if P > n0:
+            raise ValueError(f"{P} ranks but only {n0} axis-0 planes")
+        i0, n0l = geometry.slab_bounds(n0, P, r)
+        per0 = gt.periodic[0]
+        self.ghost_lo = P > 1 and (r > 0 or per0)
+        self.ghost_hi = P > 1 and (r < P - 1 or per0)
+        self.i0, self.n0_local = i0, n0l
+        self.global_shape = gt.shape
+        self.shape = (n0l, gt.shape[1], gt.shape[2])
+        tab = geometry.pack(gt, i0, n0l, self.ghost_lo, self.ghost_hi)
+        fl = geometry.flags(gt, i0, n0l, self.ghost_lo, self.ghost_hi)
+        shp = (c_int64 * 3)(*self.shape)
+        L = _lib.lib()
+        if L.pc_grid_table_size(shp) != tab.size:
+            raise RuntimeError("table layout mismatch between geometry.py and the library")
+        h = c_void_p()
+        _lib.check(L.pc_grid_create(ctx.handle, shp, fl.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                    _lib.dptr(tab), tab.size, byref(h)), "pc_grid_create")
+        self.handle = h
+        self.pinned = gt.pinned
+
+    @property
+    def ncells(self) -> int:
+        return int(np.prod(self.shape))
+
+    def local_slice(self, values: np.ndarray) -> np.ndarray:
+        """This rank's axis-0 slab of a global grid-shaped array."""
+        if self.ctx.nranks == 1:
+            return values
+        return values[self.i0:self.i0 + self.n0_local]
+
+    def __del__(self):
+        try:
+            if self.handle is not None and self.ctx.handle is not None:
+                _lib.lib().pc_grid_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def device_grid(grid, bc, ctx: Context | None = None) -> DeviceGrid:
+    ctx = ctx or default_context()
+    key = (id(grid), id(bc))
+    hit = ctx._grids.get(key)
+    if hit is not None and hit[0] is grid and hit[1] is bc:
+        return hit[2]
+    dg = DeviceGrid(grid, bc, ctx)
+    ctx._grids[key] = (grid, bc, dg)
+    return dg
+
+
+def _embed3(values: np.ndarray, dims: int) -> np.ndarray:
+    """(grid shape..., ncomp) -> (n0, n1, n2, ncomp) for 1-D/2-D grids."""
+    v = values
+    while v.ndim < 4:
+        v = v[..., None, :] if dims < 3 else v
+        dims += 1
+    return v
+
+
+class DeviceField:
+    def __init__(self, dgrid: DeviceGrid, ncomp: int = 1):
+        self.dgrid = dgrid
+        self.ncomp = int(ncomp)
+        h = c_void_p()
+        _lib.check(_lib.lib().pc_field_create(dgrid.handle, self.ncomp, byref(h)), "pc_field_create")
+        self.handle = h
+
+    @property
+    def shape(self):
+        return self.dgrid.shape
+
+    def upload(self, values: np.ndarray, layout: int = _lib.LAYOUT_AOS):
+        """values: local slab, (n0, n1, n2, ncomp) AoS (or (ncomp, n0, n1, n2) SoA)."""
+        a = np.ascontiguousarray(values, dtype=np.float64)
+        if a.size != self.ncomp * self.dgrid.ncells:
+            raise ValueError(f"upload: {a.size} values for {self.ncomp} x {self.dgrid.shape}")
+        _lib.check(_lib.lib().pc_field_upload(self.handle, _lib.dptr(a), layout), "upload")
+        return self
+
+    def download(self, out: np.ndarray | None = None, layout: int = _lib.LAYOUT_AOS) -> np.ndarray:
+        shape = tuple(self.dgrid.shape) + (self.ncomp,) if layout == _lib.LAYOUT_AOS else (self.ncomp,) + tuple(self.dgrid.shape)
+        if out is None:
+            out = np.empty(shape)
+        elif not (out.flags.c_contiguous and out.dtype == np.float64 and out.size == int(np.prod(shape))):
+            raise ValueError("download target must be a contiguous float64 array of the field size")
+        _lib.check(_lib.lib().pc_field_download(self.handle, _lib.dptr(out), layout), "download")
+        return out.reshape(shape)
+
+    def copy_from(self, other: "DeviceField"):
+        _lib.check(_lib.lib().pc_field_copy(self.handle, other.handle), "copy")
+        return self
+
+    def clone(self) -> "DeviceField":
+        f = DeviceField(self.dgrid, self.ncomp)
+        return f.copy_from(self)
+
+    def fill(self, v: float):
+        _lib.check(_lib.lib().pc_field_fill(self.handle, float(v)), "fill")
+        return self
+
+    def to_field(self) -> mesh.Field:
+        grid = self.dgrid.grid
+        vals = self.download()
+        return mesh.Field(grid, vals.reshape(tuple(grid.shape) + (self.ncomp,)))
+
+    @classmethod
+    def from_values(cls, dgrid: DeviceGrid, values: np.ndarray, ncomp: int | None = None) -> "DeviceField":
+        """values: global-grid-shaped (+ ncomp) AoS array; this rank's slab is uploaded."""
+        v = np.asarray(values, dtype=np.float64)
+        gshape = tuple(dgrid.grid.shape)
+        if v.shape == gshape:
+            v = v[..., None]
+        nc = v.shape[-1] if ncomp is None else ncomp
+        v = v.reshape(tuple(dgrid.global_shape) + (nc,))
+        f = cls(dgrid, nc)
+        f.upload(dgrid.local_slice(v))
+        return f
+
+    def __del__(self):
+        try:
+            if self.handle is not None and self.dgrid.ctx.handle is not None:
+                _lib.lib().pc_field_destroy(self.handle)
+        except Exception:
+            pass
