@@ -156,12 +156,15 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd,
              int floor_mode, double floor_fraction, int64_t max_cycles, double dt_euler,
              pc_cycle_record* rec, int64_t rec_cap, int64_t* n_rec);
 
-/* ---- instrumentation: device time (ms) and launches of the last pc_cycle,
- * and the per-kernel-class breakdown (class 0 = STS stages, 1 = F+argmax,
- * 2 = PCG, 3 = other). */
+/* ---- instrumentation (enabled by pc_ctx_enable_timing): device time of the
+ * fused STS stage kernels (k >= 2) and of the PCG iteration kernels, their
+ * launch count, and the total number of kernels this context launched. */
 int pc_ctx_stats(pc_ctx* ctx, double* stage_ms, int64_t* stage_launches, int64_t* launches_total);
 int pc_ctx_reset_stats(pc_ctx* ctx);
 int pc_ctx_enable_timing(pc_ctx* ctx, int on);
+/* CUDA events on the context stream: record mark id (0..15); elapsed ms */
+int pc_ctx_mark(pc_ctx* ctx, int id);
+int pc_ctx_elapsed(pc_ctx* ctx, int id0, int id1, double* ms);
 
 #ifdef __cplusplus
 }

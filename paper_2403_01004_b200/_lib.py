@@ -73,6 +73,8 @@ _SIGS = {
     "pc_ctx_stats": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int64), POINTER(c_int64)]),
     "pc_ctx_reset_stats": (c_int, [c_void_p]),
     "pc_ctx_enable_timing": (c_int, [c_void_p, c_int]),
+    "pc_ctx_mark": (c_int, [c_void_p, c_int]),
+    "pc_ctx_elapsed": (c_int, [c_void_p, c_int, c_int, POINTER(c_double)]),
 }
 
 EXPORTED = tuple(_SIGS)

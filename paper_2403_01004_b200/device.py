@@ -46,6 +46,15 @@ class Context:
     def enable_timing(self, on: bool = True):
         _lib.lib().pc_ctx_enable_timing(self.handle, int(on))
 
+    def mark(self, slot: int):
+        """Record a CUDA event on the library stream (device timing)."""
+        _lib.check(_lib.lib().pc_ctx_mark(self.handle, int(slot)), "mark")
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        v = c_double()
+        _lib.check(_lib.lib().pc_ctx_elapsed(self.handle, int(a), int(b), byref(v)), "elapsed")
+        return v.value
+
     def reset_stats(self):
         _lib.lib().pc_ctx_reset_stats(self.handle)
 

@@ -177,12 +177,25 @@ def split_advance(ops, state: dict, outer_dt: float, cfgs, *, outer_step: int = 
     Returns (state, [CycleReport per operator]).
     """
     refresh = refresh or {}
+    # host Fields go to the device once per outer step (uploaded on the grid of
+    # the first operator acting on them) and come back once at the end
+    host_names = {}
+    dev = dict(state)
+    for (name, op) in ops:
+        if name in dev and not isinstance(dev[name], device.DeviceField):
+            f = dev[name]
+            dop = op.device_op(f.grid, f.n_components)
+            dev[name] = device.DeviceField.from_values(dop.dgrid, f.values)
+            host_names[name] = True
     for q, (name, op) in enumerate(ops):
         if op.kind == "aligned":
-            src = state[refresh.get(q, name)]
+            src = dev.get(refresh.get(q, name), state.get(refresh.get(q, name)))
             op.freeze(src)
     reports = []
     for (name, op), (scheme, pcfg) in zip(ops, cfgs):
-        state[name], rep = cycle_operator(op, scheme, state[name], outer_dt, pcfg, outer_step=outer_step)
+        dev[name], rep = cycle_operator(op, scheme, dev[name], outer_dt, pcfg, outer_step=outer_step)
         reports.append(rep)
-    return state, reports
+    out = dict(state)
+    for name in dev:
+        out[name] = dev[name].to_field() if host_names.get(name) else dev[name]
+    return out, reports

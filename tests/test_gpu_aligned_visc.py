@@ -1,0 +1,81 @@
+"""Parity of the 19-point aligned (Spitzer) and the vector-viscosity paths
+(C3 / C4 / C2 recipes at reduced size) against the CPU oracle."""
+import numpy as np
+import pytest
+
+from helpers import oracle_aligned, oracle_scalar, soa
+from oracle import ptl as optl
+from paper_2403_01004_b200 import configs, operators, ptl, schemes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c3s():
+    return configs.c3(n=(24, 24, 48))
+
+
+def _aligned(w):
+    cfg = operators.AlignedConductionConfig(b_hat=w.fields["b"], m_p=3.0, k_B=1.0, bc=w.bc)
+    return operators.DiffusionOperator.aligned(cfg, operators.Field(w.grid, w.fields["T"]))
+
+
+def test_aligned_apply_and_bound_bitwise(gpu_ctx, c3s):
+    op = _aligned(c3s)
+    T = operators.Field(c3s.grid, c3s.fields["T"])
+    F = op.apply(T)
+    oop = oracle_aligned(c3s.grid, c3s.bc, c3s.fields["b"], c3s.fields["T"])
+    Fo = oop.apply(soa(c3s.fields["T"][..., None]))
+    assert np.array_equal(F.values[..., 0], Fo[0])
+    assert op.device_op(c3s.grid, 1).dt_euler == oop.euler_dt()
+    d = op.device_op(c3s.grid, 1).diagonal().download()[..., 0]
+    assert np.array_equal(d, oop.bound_and_diag()[1][0])
+
+
+def test_aligned_rkl2_ptl_parity(gpu_ctx, c3s):
+    op = _aligned(c3s)
+    dtE = op.device_op(c3s.grid, 1).dt_euler
+    T = operators.Field(c3s.grid, c3s.fields["T"])
+    out, rep = ptl.cycle_operator(op, schemes.SchemeConfig("rkl2"), T, 1e4 * dtE)
+    oop = oracle_aligned(c3s.grid, c3s.bc, c3s.fields["b"], c3s.fields["T"])
+    uo, repo = optl.cycle_operator(oop, optl.OracleScheme("rkl2"), soa(c3s.fields["T"][..., None]), 1e4 * dtE,
+                                   dt_euler=dtE)
+    assert [e.iters for e in rep.entries] == [r.iters for r in repo]
+    assert [e.dt for e in rep.entries] == [r.dt for r in repo]
+    assert np.array_equal(out.values[..., 0], uo[0])
+
+
+def test_aligned_be_pcg_parity(gpu_ctx, c3s):
+    op = _aligned(c3s)
+    dtE = op.device_op(c3s.grid, 1).dt_euler
+    T = operators.Field(c3s.grid, c3s.fields["T"])
+    out, rep = ptl.cycle_operator(op, schemes.SchemeConfig("backward_euler", tol=1e-9), T, 1e4 * dtE)
+    oop = oracle_aligned(c3s.grid, c3s.bc, c3s.fields["b"], c3s.fields["T"])
+    uo, repo = optl.cycle_operator(oop, optl.OracleScheme("backward_euler", tol=1e-9),
+                                   soa(c3s.fields["T"][..., None]), 1e4 * dtE, dt_euler=dtE)
+    assert len(rep.entries) == len(repo)
+    assert [e.iters for e in rep.entries] == [r.iters for r in repo]
+    a, b = out.values[..., 0], uo[0]
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-10
+
+
+@pytest.fixture(scope="module")
+def c2s():
+    return configs.c2(n=(20, 24, 48))
+
+
+def test_viscous_rkl2_ptl_parity(gpu_ctx, c2s):
+    cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=c2s.bc, vector_metric=True)
+    op = operators.DiffusionOperator.scalar(cfg, 3)
+    v = operators.Field(c2s.grid, c2s.fields["v"])
+    F = op.apply(v)
+    oop = oracle_scalar(c2s.grid, c2s.bc, ncomp=3, vector_metric=True)
+    Fo = oop.apply(soa(c2s.fields["v"]))
+    assert np.array_equal(np.moveaxis(F.values, -1, 0), Fo)
+    dtE = op.device_op(c2s.grid, 3).dt_euler
+    assert dtE == oop.euler_dt()
+    out, rep = ptl.cycle_operator(op, schemes.SchemeConfig("rkl2"), v, 2000 * dtE)
+    uo, repo = optl.cycle_operator(oop, optl.OracleScheme("rkl2"), soa(c2s.fields["v"]), 2000 * dtE, dt_euler=dtE)
+    assert [e.iters for e in rep.entries] == [r.iters for r in repo]
+    assert [e.dt for e in rep.entries] == [r.dt for r in repo]
+    assert np.array_equal(np.moveaxis(out.values, -1, 0), uo)
