@@ -28,6 +28,22 @@ class CycleRecord(ctypes.Structure):
 
 
 _lib = None
+_shutting_down = False
+
+
+def _mark_shutdown():
+    global _shutting_down
+    _shutting_down = True
+
+
+import atexit  # noqa: E402
+
+atexit.register(_mark_shutdown)
+
+
+def alive() -> bool:
+    """False once the interpreter is exiting (destructors must not call CUDA)."""
+    return _lib is not None and not _shutting_down
 
 _SIGS = {
     "pc_last_error": (ctypes.c_char_p, []),

@@ -18,7 +18,6 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libparacycle_b200.so")
 SOURCES = ["capi.cu"]
-HEADERS = ["common.cuh", "ops.cuh", "kernels.cuh", "nccl_shim.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -41,7 +40,7 @@ def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(HERE, "..", "include", "paracycle_b200.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 

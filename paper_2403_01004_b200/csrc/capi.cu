@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,7 +19,7 @@
 #include <vector>
 
 #include "../../include/paracycle_b200.h"
-#include "kernels.cuh"
+#include "march.cuh"
 #include "nccl_shim.h"
 
 using namespace pc;
@@ -57,6 +58,7 @@ struct pc_ctx {
   cudaStream_t s = nullptr;
   ncclComm_t comm = nullptr;
   int max_blocks = 148 * 16;
+  int max_red = 1 << 18;  // partial-sum slots (march grids are larger)
   // reduction scratch
   double* red_v = nullptr;
   double* red_v2 = nullptr;
@@ -262,9 +264,9 @@ int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   c->max_blocks = sms * 16;
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
-  CUDA_TRY(cudaMalloc(&c->red_v, sizeof(double) * c->max_blocks));
-  CUDA_TRY(cudaMalloc(&c->red_v2, sizeof(double) * c->max_blocks));
-  CUDA_TRY(cudaMalloc(&c->red_i, sizeof(long long) * c->max_blocks));
+  CUDA_TRY(cudaMalloc(&c->red_v, sizeof(double) * c->max_red));
+  CUDA_TRY(cudaMalloc(&c->red_v2, sizeof(double) * c->max_red));
+  CUDA_TRY(cudaMalloc(&c->red_i, sizeof(long long) * c->max_red));
   CUDA_TRY(cudaMalloc(&c->counter, sizeof(unsigned int) * 4));
   CUDA_TRY(cudaMemset(c->counter, 0, sizeof(unsigned int) * 4));
   CUDA_TRY(cudaMalloc(&c->res, sizeof(ArgRes)));
@@ -688,6 +690,28 @@ int pc_op_diagonal(pc_op* op, pc_field* out) {
   return PC_OK;
 }
 
+// r-chunk length of the marching aligned kernels
+static int march_R(const pc_grid* g) {
+  const int tiles = ((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + MTJ - 1) / MTJ);
+  int R = 32;
+  while (R > 4 && (int64_t)tiles * ((g->g.n0 + R - 1) / R) < 148 * 8) R /= 2;
+  return R;
+}
+static dim3 march_grid(const pc_grid* g, int R) {
+  return dim3((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + MTJ - 1) / MTJ, (g->g.n0 + R - 1) / R);
+}
+template <class Val, class Epi>
+static int launch_march(pc_op* op, const Val& val, const Epi& epi, const char* what) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int R = march_R(g);
+  dim3 grid = march_grid(g, R);
+  if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
+  k_aligned_march<Val, Epi><<<grid, dim3(MTK, MTJ), 0, c->s>>>(g->g, op->ao, val, epi, R);
+  c->st.launches++;
+  return check_launch(what);
+}
+
 template <class Op>
 static int launch_apply(pc_op* op, const Op& o, CFld u, Fld F, bool argmax) {
   pc_grid* g = op->grid;
@@ -702,7 +726,15 @@ static int launch_apply(pc_op* op, const Op& o, CFld u, Fld F, bool argmax) {
   return check_launch("k_apply");
 }
 static int apply_any(pc_op* op, CFld u, Fld F, bool argmax) {
-  if (op->kind == K_ALIGNED) return launch_apply(op, op->ao, u, F, argmax);
+  if (op->kind == K_ALIGNED) {
+    pc_ctx* c = op->grid->ctx;
+    PlainVal val{{u.p[0], u.p[1], u.p[2]}};
+    if (argmax) {
+      EpiArgmax e{F.p[0], c->red_v, c->red_i, c->counter, c->res, ArgMax{-1.0, 0x7fffffffffffffffLL}};
+      return launch_march(op, val, e, "k_aligned_march<argmax>");
+    }
+    return launch_march(op, val, EpiStore{F.p[0]}, "k_aligned_march<apply>");
+  }
   return launch_apply(op, op->so, u, F, argmax);
 }
 
@@ -877,10 +909,16 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     rc = halo_work(g, *um1);
     if (rc) break;
     CFld m2 = um2w ? um2w->cf() : cfld(u);
-    k_stage<<<nb, kThreads, 0, c->s>>>(g->g, o, um1->cf(), m2, cfld(u), y0.cf(), out->f(), sc, k, c->bad);
-    c->st.launches++;
+    if constexpr (std::is_same<Op, AlignedOp>::value) {
+      PlainVal val{{um1->base(0), um1->base(0), um1->base(0)}};
+      EpiStage e{m2.p[0], cfld(u).p[0], y0.base(0), out->base(0), sc, k, c->bad};
+      rc = launch_march(op, val, e, "k_aligned_march<stage>");
+    } else {
+      k_stage<<<nb, kThreads, 0, c->s>>>(g->g, o, um1->cf(), m2, cfld(u), y0.cf(), out->f(), sc, k, c->bad);
+      c->st.launches++;
+      rc = check_launch("k_stage");
+    }
     c->st.stage_launches++;
-    rc = check_launch("k_stage");
     // rotate: u_{k-1} -> u_{k-2}, u_k -> u_{k-1}; the next stage writes into
     // the buffer that held u_{k-1} before this stage, i.e. the new u_{k-2}
     // (pointwise safe: u_{k-2} is only read at the thread's own node)
@@ -999,8 +1037,16 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
       rc = halo_work(g, r);
       if (rc == PC_OK) rc = halo_work(g, *pold);
       if (rc) break;
-      k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
-                                              c->red_v, c->counter, c->pcg);
+      if constexpr (std::is_same<Op, AlignedOp>::value) {
+        // beta is read on the device inside PVal via the state pointer
+        PValDev val{r.base(0), pold->base(0), dg, adiag, dt, c->pcg, 0.0};
+        EpiMatvec e{pnew->base(0), Ap.base(0), adiag, dt, c->red_v, c->counter, c->pcg, op->ao, 0.0};
+        rc = launch_march(op, val, e, "k_aligned_march<matvec>");
+        c->st.launches--;  // counted below with the update kernel
+      } else {
+        k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
+                                                c->red_v, c->counter, c->pcg);
+      }
       k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, tol, it,
                                               c->red_v, c->red_v2, c->counter, c->pcg);
       c->st.launches += 2;

@@ -13,6 +13,8 @@ namespace pc {
 // value provider for a plain SoA field
 struct PlainVal {
   const double* p[3];
+  __device__ __forceinline__ bool skip() const { return false; }
+  __device__ __forceinline__ void init() {}
   __device__ __forceinline__ double operator()(int c, int64_t o, int, int, int) const {
     return __ldg(p[c] + o);
   }

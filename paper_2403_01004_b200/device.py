@@ -146,7 +146,7 @@ class DeviceGrid:
 
     def __del__(self):
         try:
-            if self.handle is not None and self.ctx.handle is not None:
+            if _lib.alive() and self.handle is not None and self.ctx.handle is not None:
                 _lib.lib().pc_grid_destroy(self.handle)
         except Exception:
             pass
@@ -233,7 +233,7 @@ class DeviceField:
 
     def __del__(self):
         try:
-            if self.handle is not None and self.dgrid.ctx.handle is not None:
+            if _lib.alive() and self.handle is not None and self.dgrid.ctx.handle is not None:
                 _lib.lib().pc_field_destroy(self.handle)
         except Exception:
             pass

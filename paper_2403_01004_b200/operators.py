@@ -271,7 +271,7 @@ class DeviceOperator:
 
     def __del__(self):
         try:
-            if self.handle is not None and self.ctx.handle is not None:
+            if _lib.alive() and self.handle is not None and self.ctx.handle is not None:
                 _lib.lib().pc_op_destroy(self.handle)
         except Exception:
             pass
