@@ -707,7 +707,13 @@ static int launch_march(pc_op* op, const Val& val, const Epi& epi, const char* w
   const int R = march_R(g);
   dim3 grid = march_grid(g, R);
   if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
-  k_aligned_march<Val, Epi><<<grid, dim3(MTK, MTJ), 0, c->s>>>(g->g, op->ao, val, epi, R);
+  static bool attr = false;  // one per template instantiation
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_aligned_march<Val, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(MarchSmem)));
+    attr = true;
+  }
+  k_aligned_march<Val, Epi><<<grid, dim3(MTK, MTJ), sizeof(MarchSmem), c->s>>>(g->g, op->ao, val, epi, R);
   c->st.launches++;
   return check_launch(what);
 }

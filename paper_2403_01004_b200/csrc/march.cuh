@@ -108,16 +108,41 @@ __device__ __forceinline__ void node_E(const NodeIn& n, int only_a, int only_s, 
   }
 }
 
-// gather the inputs of node (hj, hk) of the tile from shared memory
+// ---- async copy helpers (LDGSTS) -----------------------------------------
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+constexpr int NROWT = 11;  // per-(row, j) tables: iL2[6], wo01[4], iVal2
+constexpr int MSLOTS = 4;  // T ring: planes t-1, t, t+1 in use, t+2 in flight
+
 struct MarchSmem {
-  double T[3][MHP];
-  double b[3][MHP];
-  double c[MHP];
-  double E[2][4][MHP];  // E_{1,+}, E_{1,-}, E_{2,+}, E_{2,-} per plane parity
+  double T[MSLOTS][MHP];
+  double b[2][3][MHP];
+  double c[2][MHP];
+  double rowt[3][NROWT][MHJ];  // row tables for planes (p mod 3)
+  double E[2][4][MHP];         // E_{1,+}, E_{1,-}, E_{2,+}, E_{2,-} per plane parity
 };
 
-__device__ __forceinline__ void gather(const GridDev& g, const MarchSmem& S, int sm, int sc, int sp, int h, int row,
-                                       int jg, int kg, NodeIn& n) {
+// per-thread column constants (depend on k only)
+struct ColT {
+  double il1[6];
+  double w2[2];
+  double ivg;
+};
+__device__ __forceinline__ void load_col(const GridDev& g, int k, ColT& c) {
+#pragma unroll
+  for (int q = 0; q < 6; ++q) c.il1[q] = __ldg(g.iL1[q] + k);
+  c.w2[0] = __ldg(g.wo2[0] + k);
+  c.w2[1] = __ldg(g.wo2[1] + k);
+  c.ivg = __ldg(g.iValg + k);
+}
+
+__device__ __forceinline__ void gather(const MarchSmem& S, int sm, int sc, int sp, int bs, int rs, int h, int hj,
+                                       const ColT& col, NodeIn& n) {
   n.Tv = S.T[sc][h];
   n.Tn[0][0] = S.T[sp][h];
   n.Tn[0][1] = S.T[sm][h];
@@ -125,24 +150,24 @@ __device__ __forceinline__ void gather(const GridDev& g, const MarchSmem& S, int
   n.Tn[1][1] = S.T[sc][h >= MHK ? h - MHK : h];
   n.Tn[2][0] = S.T[sc][h + 1];
   n.Tn[2][1] = S.T[sc][h - 1];
-  n.b[0] = S.b[0][h];
-  n.b[1] = S.b[1][h];
-  n.b[2] = S.b[2][h];
-  n.c = S.c[h];
-  const int64_t r2 = row2(g, row, jg);
+  n.b[0] = S.b[bs][0][h];
+  n.b[1] = S.b[bs][1][h];
+  n.b[2] = S.b[bs][2][h];
+  n.c = S.c[bs][h];
 #pragma unroll
-  for (int q = 0; q < 6; ++q) n.il[q >> 1][q & 1] = __ldg(g.iL2[q] + r2) * __ldg(g.iL1[q] + kg);
+  for (int q = 0; q < 6; ++q) n.il[q >> 1][q & 1] = S.rowt[rs][q][hj] * col.il1[q];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) n.w01[q] = __ldg(g.wo01[q] + r2);
-  n.w2[0] = __ldg(g.wo2[0] + kg);
-  n.w2[1] = __ldg(g.wo2[1] + kg);
+  for (int q = 0; q < 4; ++q) n.w01[q] = S.rowt[rs][6 + q][hj];
+  n.w2[0] = col.w2[0];
+  n.w2[1] = col.w2[1];
 }
 
-// Epilogue contract: epi(g, node i, j, k, offset, F, uc) where uc is the
-// input value at the node (from shared memory); epi.finish(...) at the end.
+// Epilogue contract: epi.prefetch(o) early in the step, then
+// epi(g, i, j, k, o, F, uc) (uc = input value at the node), epi.finish(g).
 template <class Val, class Epi>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp op, Val val, Epi epi, int R) {
-  __shared__ MarchSmem S;
+  extern __shared__ __align__(16) unsigned char march_smem[];
+  MarchSmem& S = *reinterpret_cast<MarchSmem*>(march_smem);
   if (val.skip()) return;
   val.init();
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -153,113 +178,150 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   const bool inside = jg < g.n1 && kg < g.n2;
   const int hown = (ty + 1) * MHK + (tx + 1);
 
-  // stage one field plane (tile + halo) into shared memory
-  auto load_T = [&](int slot, int p) {
-    PlaneMap pm = plane_map(g, p);
-    for (int e = tid; e < MHP; e += MNT) {
-      const int hj = e / MHK, hk = e - hj * MHK;
-      bool oj, ok;
-      const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
-      S.T[slot][e] = val(0, off3(g, pm.mem, jj, kk), pm.mem, jj, kk);
-    }
+  // smem fill slots of this thread (tile + halo, wrapped / clamped in-plane)
+  int foff[2];  // in-plane offsets (plane < 2^31 elements)
+  bool fon[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int e = tid + q * MNT;
+    fon[q] = e < MHP;
+    const int hj = e / MHK, hk = e - hj * MHK;
+    bool oj, ok;
+    const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
+    foff[q] = jj * g.n2 + kk;
+  }
+  // row-table slot of this thread: tid < NROWT * MHJ
+  const bool rton = tid < NROWT * MHJ;
+  const int rtab = tid / MHJ, rhj = tid - (tid / MHJ) * MHJ;
+  bool rok;
+  const int rjj = map_j(g, j0 - 1 + rhj, rok);
+  const double* rbase = !rton ? nullptr : (rtab < 6 ? g.iL2[rtab] : (rtab < 10 ? g.wo01[rtab - 6] : g.iVal2));
+
+  bool ojo, oko;
+  const int jm = map_j(g, jg, ojo), km = map_k(g, kg, oko);
+  const bool own_ok = ojo && oko;
+  ColT col;
+  load_col(g, km, col);
+  const bool pin_jk = (g.pin_lo1 && jg == 0) || (g.pin_hi1 && jg == g.n1 - 1) || (g.pin_lo2 && kg == 0) ||
+                      (g.pin_hi2 && kg == g.n2 - 1);
+
+  // ring assignment: j-rings (tid < 2 MTK) and k-rings (next 2 MTJ threads)
+  int ra = -1, rs_ = 0, rhj_ = 0, rhk_ = 0;
+  if (tid < 2 * MTK) {
+    ra = 1;
+    rs_ = tid < MTK ? 0 : 1;
+    rhk_ = 1 + (tid % MTK);
+    rhj_ = rs_ == 0 ? 0 : MTJ + 1;
+  } else if (tid < 2 * MTK + 2 * MTJ) {
+    const int q = tid - 2 * MTK;
+    ra = 2;
+    rs_ = q < MTJ ? 0 : 1;
+    rhj_ = 1 + (q % MTJ);
+    rhk_ = rs_ == 0 ? 0 : MTK + 1;
+  }
+  bool rjo = false, rko = false;
+  const int rj = ra >= 0 ? map_j(g, j0 - 1 + rhj_, rjo) : 0;
+  const int rk = ra >= 0 ? map_k(g, k0 - 1 + rhk_, rko) : 0;
+  const bool ring_on = ra >= 0 && rjo && rko &&
+                       ((ra == 1) ? (k0 - 1 + rhk_ < g.n2) : (j0 - 1 + rhj_ < g.n1));
+  (void)rj;
+
+  auto issue_T = [&](int slot, int p) {
+    const PlaneMap pm = plane_map(g, p);
+    const int64_t base = (int64_t)pm.mem * g.plane;
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (fon[q]) val.stage(&S.T[slot][tid + q * MNT], base + foff[q], pm.mem);
   };
-  auto load_bc = [&](int p) {
-    PlaneMap pm = plane_map(g, p);
-    for (int e = tid; e < MHP; e += MNT) {
-      const int hj = e / MHK, hk = e - hj * MHK;
-      bool oj, ok;
-      const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
-      const int64_t o = off3(g, pm.mem, jj, kk);
-      S.b[0][e] = __ldg(op.b[0] + o);
-      S.b[1][e] = __ldg(op.b[1] + o);
-      S.b[2][e] = __ldg(op.b[2] + o);
-      S.c[e] = __ldg(op.c + o);
+  auto issue_bc = [&](int slot, int p) {
+    const PlaneMap pm = plane_map(g, p);
+    const int64_t base = (int64_t)pm.mem * g.plane;
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (fon[q]) {
+        const int e = tid + q * MNT;
+        cp_async8(&S.b[slot][0][e], op.b[0] + base + foff[q]);
+        cp_async8(&S.b[slot][1][e], op.b[1] + base + foff[q]);
+        cp_async8(&S.b[slot][2][e], op.b[2] + base + foff[q]);
+        cp_async8(&S.c[slot][e], op.c + base + foff[q]);
+      }
+  };
+  auto issue_rows = [&](int slot, int p) {
+    if (rton) {
+      const PlaneMap pm = plane_map(g, p);
+      cp_async8(&S.rowt[slot][rtab][rhj], rbase + row2(g, pm.row, rjj));
     }
   };
 
-  // ---- prologue: planes i0-1, i0, i0+1 and E_{0,+}(i0-1)
-  load_T(0, i0 - 1);
-  load_T(1, i0);
-  load_T(2, i0 + 1);
-  load_bc(i0 - 1);
+  // ---- prologue
+  issue_T(0, i0 - 1);
+  issue_T(1, i0);
+  issue_T(2, i0 + 1);
+  issue_bc(1, i0 - 1);
+  issue_rows(2, i0 - 1);
+  issue_bc(0, i0);
+  issue_rows(0, i0);
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
-  double E0p_prev2 = 0.0;  // E_{0,+} at plane t-2 (relative to the finalised plane t-1)
+  double E0p_prev2 = 0.0;
   {
-    PlaneMap pm = plane_map(g, i0 - 1);
+    const PlaneMap pm = plane_map(g, i0 - 1);
     if (pm.exists && inside) {
-      // E_{0,+} at (i0-1): needs T(i0) at own position (slot 1) and in-plane
-      // neighbours of plane i0-1 (slot 0); p[0][-] is not formed.
       NodeIn n;
-      gather(g, S, 0, 0, 1, hown, pm.row, jg, kg, n);
+      gather(S, 0, 0, 1, 1, 2, hown, ty + 1, col, n);
       double E[3][2];
       node_E(n, 0, 0, E);
       E0p_prev2 = E[0][0];
     }
   }
-  __syncthreads();
-  load_bc(i0);
-  __syncthreads();
+  __syncthreads();  // b/c slot 1 and row slot 2 are refilled below
 
   double Eprev[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-  double ucprev = 0.0;
+  int s_m = 0, s_c = 1, s_p = 2, s_n = 3;  // T slots of planes t-1, t, t+1, t+2
+  int r_c = 0, r_p = 2;                    // row-table slots of planes t, t-1
   for (int t = i0; t <= iend; ++t) {
-    const int sm = (t - i0) % 3, sc = (t - i0 + 1) % 3, sp = (t - i0 + 2) % 3;  // slot(p) = (p - i0 + 1) % 3
-    const int par = t & 1;
-    PlaneMap pm = plane_map(g, t);
+    const int bsl = t & 1;  // b/c slot of plane t
+    const int r_n = 3 - r_c - r_p;  // free row slot -> plane t+1
+    // ---- async prefetch of the next planes (overlaps the compute below)
+    if (t + 2 <= iend) issue_T(s_n, t + 2);
+    if (t + 1 <= iend) {
+      issue_bc(bsl ^ 1, t + 1);
+      issue_rows(r_n, t + 1);
+    }
+    cp_async_commit();
+    // epilogue operands of plane t-1
+    const int64_t of = off3(g, t - 1, jg, kg);
+    if (t > i0 && inside) epi.prefetch(of);
+
+    const PlaneMap pm = plane_map(g, t);
     const bool last = (t == iend);
     double Ecur[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-    double uccur = 0.0;
+    const int par = t & 1;
     if (pm.exists) {
-      // threads of a partial tile evaluate the (wrapped) node they map to, so
-      // in-tile neighbour fluxes are right at domain edges too
-      bool ojo, oko;
-      const int jm = map_j(g, jg, ojo), km = map_k(g, kg, oko);
-      if (ojo && oko) {
+      if (own_ok) {
         NodeIn n;
-        gather(g, S, sm, sc, sp, hown, pm.row, jm, km, n);
-        uccur = n.Tv;
+        gather(S, s_m, s_c, s_p, bsl, r_c, hown, ty + 1, col, n);
         node_E(n, last ? 0 : -1, 1, Ecur);  // last plane: only E_{0,-} is consumed
-        if (!last) {
-          S.E[par][0][hown] = Ecur[1][0];
-          S.E[par][1][hown] = Ecur[1][1];
-          S.E[par][2][hown] = Ecur[2][0];
-          S.E[par][3][hown] = Ecur[2][1];
-        }
-      } else if (!last) {
-        S.E[par][0][hown] = 0.0;
-        S.E[par][1][hown] = 0.0;
-        S.E[par][2][hown] = 0.0;
-        S.E[par][3][hown] = 0.0;
       }
       if (!last) {
-        // halo ring: one component per ring node
-        int a = -1, s = 0, hj = 0, hk = 0;
-        if (tid < 2 * MTK) {
-          a = 1;
-          s = tid < MTK ? 0 : 1;
-          hk = 1 + (tid % MTK);
-          hj = s == 0 ? 0 : MTJ + 1;
-        } else if (tid < 2 * MTK + 2 * MTJ) {
-          const int q = tid - 2 * MTK;
-          a = 2;
-          s = q < MTJ ? 0 : 1;
-          hj = 1 + (q % MTJ);
-          hk = s == 0 ? 0 : MTK + 1;
-        }
-        if (a >= 0) {
-          bool oj, ok;
-          const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
-          // the ring node must exist and its tile-side neighbour must be inside
-          const bool partner = (a == 1) ? (k0 - 1 + hk < g.n2) : (j0 - 1 + hj < g.n1);
+        S.E[par][0][hown] = Ecur[1][0];
+        S.E[par][1][hown] = Ecur[1][1];
+        S.E[par][2][hown] = Ecur[2][0];
+        S.E[par][3][hown] = Ecur[2][1];
+        if (ra >= 0) {
           double Ev = 0.0;
-          if (oj && ok && partner) {
+          if (ring_on) {
+            ColT rcol;
+            if (ra == 2) load_col(g, rk, rcol);
+            else rcol = col;
             NodeIn n;
-            gather(g, S, sm, sc, sp, hj * MHK + hk, pm.row, jj, kk, n);
+            gather(S, s_m, s_c, s_p, bsl, r_c, rhj_ * MHK + rhk_, rhj_, rcol, n);
             double E[3][2];
-            node_E(n, a, s, E);
-            Ev = E[a][s];
+            node_E(n, ra, rs_, E);
+            Ev = E[ra][rs_];
           }
-          S.E[par][(a - 1) * 2 + s][hj * MHK + hk] = Ev;
+          S.E[par][(ra - 1) * 2 + rs_][rhj_ * MHK + rhk_] = Ev;
         }
       }
     }
@@ -267,31 +329,38 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     // ---- finalise plane t-1
     if (t > i0 && inside) {
       const int tf = t - 1;
-      const int pp = (t - 1) & 1;
+      const int pp = par ^ 1;
       const double E1pm = S.E[pp][0][hown - MHK], E1mp = S.E[pp][1][hown + MHK];
       const double E2pm = S.E[pp][2][hown - 1], E2mp = S.E[pp][3][hown + 1];
       double G = (E0p_prev2 - Eprev[0][0]) + (Eprev[0][1] - Ecur[0][1]);
       G = G + ((E1pm - Eprev[1][0]) + (Eprev[1][1] - E1mp));
       G = G + ((E2pm - Eprev[2][0]) + (Eprev[2][1] - E2mp));
-      const int64_t o = off3(g, tf, jg, kg);
-      const double iv = __ldg(g.iVal2 + row2(g, tf, jg)) * __ldg(g.iValg + kg);
+      const double iv = S.rowt[r_p][10][ty + 1] * col.ivg;
       double f = ((0.0 - G) * iv) * op.pref;
-      if (op.rho) f = f / __ldg(op.rho + o);
-      if (pinned(g, tf, jg, kg)) f = 0.0;
-      epi(g, tf, jg, kg, o, f, ucprev);
+      if (op.rho) f = f / __ldg(op.rho + of);
+      const int ig = tf + g.i0g;
+      const bool pin = pin_jk || (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
+      if (pin) f = 0.0;
+      epi(g, tf, jg, kg, of, f, S.T[s_m][hown], pin);
     }
-    // rotate carried fluxes (E_{0,+}(i0-1) from the prologue survives step i0)
     if (t > i0) E0p_prev2 = Eprev[0][0];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       Eprev[a][0] = Ecur[a][0];
       Eprev[a][1] = Ecur[a][1];
     }
-    ucprev = uccur;
     if (last) break;
-    __syncthreads();  // everyone done with the slots about to be overwritten
-    if (t + 2 <= iend) load_T(sm, t + 2);  // the last step never reads T(iend + 1)
-    load_bc(t + 1);
+    // rotate slots
+    {
+      const int tmp = s_m;
+      s_m = s_c;
+      s_c = s_p;
+      s_p = s_n;
+      s_n = tmp;
+      r_p = r_c;
+      r_c = r_n;
+    }
+    cp_async_wait_all();
     __syncthreads();
   }
   epi.finish(g);
@@ -309,6 +378,7 @@ struct PValDev {
   double beta;
   __device__ __forceinline__ bool skip() const { return st->done != 0; }  // solve finished
   __device__ __forceinline__ void init() { beta = st->beta; }
+  __device__ __forceinline__ void stage(double* dst, int64_t o, int) const { *dst = (*this)(0, o, 0, 0, 0); }
   __device__ __forceinline__ double operator()(int, int64_t o, int, int, int) const {
     double dvec = (adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o);
     double z = __ldg(r + o) / dvec;
@@ -319,7 +389,8 @@ struct PValDev {
 // ---- epilogues ----------------------------------------------------------
 struct EpiStore {  // F = op(u)
   double* F;
-  __device__ __forceinline__ void operator()(const GridDev&, int, int, int, int64_t o, double f, double) {
+  __device__ __forceinline__ void prefetch(int64_t) {}
+  __device__ __forceinline__ void operator()(const GridDev&, int, int, int, int64_t o, double f, double, bool) {
     F[o] = f;
   }
   __device__ __forceinline__ void finish(const GridDev&) {}
@@ -333,12 +404,17 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   StageCoef sc;
   int stage;
   int* bad;
-  __device__ __forceinline__ void operator()(const GridDev& g, int i, int j, int k, int64_t o, double f,
-                                             double um1) {
-    const double a0 = __ldg(u0 + o);
-    double v = ((((sc.mu * um1) + (sc.nu * __ldg(um2 + o))) + (sc.kap * a0)) + (sc.mtdt * f)) +
-               (sc.gtdt * __ldg(y0 + o));
-    v = pinned(g, i, j, k) ? a0 : v;
+  double pa0, pm2, py0;
+  __device__ __forceinline__ void prefetch(int64_t o) {
+    pa0 = __ldg(u0 + o);
+    pm2 = __ldg(um2 + o);
+    py0 = __ldg(y0 + o);
+  }
+  __device__ __forceinline__ void operator()(const GridDev&, int, int, int, int64_t o, double f, double um1,
+                                             bool pin) {
+    const double a0 = pa0;
+    double v = ((((sc.mu * um1) + (sc.nu * pm2)) + (sc.kap * a0)) + (sc.mtdt * f)) + (sc.gtdt * py0);
+    v = pin ? a0 : v;
     out[o] = v;
     if (!isfinite(v)) atomicMin(bad, stage);
   }
@@ -352,7 +428,9 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
   unsigned int* counter;
   ArgRes* res;
   ArgMax best;
-  __device__ __forceinline__ void operator()(const GridDev& g, int i, int j, int k, int64_t o, double f, double) {
+  __device__ __forceinline__ void prefetch(int64_t) {}
+  __device__ __forceinline__ void operator()(const GridDev& g, int i, int j, int k, int64_t o, double f, double,
+                                             bool) {
     F[o] = f;
     best = am_better(best, ArgMax{fabs(f), aos_index(g, i, j, k, 0, 1)});
   }
@@ -422,8 +500,9 @@ struct EpiMatvec {  // PCG K7: p_new = (loaded value), Ap = a p - dt F(p); (W p,
   PcgDev* st;
   AlignedOp op;
   double acc;
+  __device__ __forceinline__ void prefetch(int64_t) {}
   __device__ __forceinline__ void operator()(const GridDev& g, int i, int j, int k, int64_t o, double f,
-                                             double pv) {
+                                             double pv, bool) {
     const double ap = (adiag ? __ldg(adiag + o) * pv : pv) - dt * f;
     pnew[o] = pv;
     Ap[o] = ap;

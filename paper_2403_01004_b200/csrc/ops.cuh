@@ -18,6 +18,11 @@ struct PlainVal {
   __device__ __forceinline__ double operator()(int c, int64_t o, int, int, int) const {
     return __ldg(p[c] + o);
   }
+  // asynchronous shared-memory staging of component 0 (LDGSTS, 8 bytes)
+  __device__ __forceinline__ void stage(double* dst, int64_t o, int) const {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(p[0] + o) : "memory");
+  }
 };
 
 // ------------------------------------------------------------------ scalar
