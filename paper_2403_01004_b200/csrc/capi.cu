@@ -713,7 +713,7 @@ static int launch_march(pc_op* op, const Val& val, const Epi& epi, const char* w
                                   (int)sizeof(MarchSmem)));
     attr = true;
   }
-  k_aligned_march<Val, Epi><<<grid, dim3(MTK, MTJ), sizeof(MarchSmem), c->s>>>(g->g, op->ao, val, epi, R);
+  k_aligned_march<Val, Epi><<<grid, dim3(MTK, MTY), sizeof(MarchSmem), c->s>>>(g->g, op->ao, val, epi, R);
   c->st.launches++;
   return check_launch(what);
 }

@@ -18,12 +18,15 @@
 
 namespace pc {
 
-constexpr int MTJ = 8;
-constexpr int MTK = 32;
+constexpr int MTK = 32;          // phi extent of a tile (lanes)
+constexpr int MTY = 8;           // thread rows
+constexpr int NPT = 2;           // tile nodes per thread (rows ty, ty + MTY)
+constexpr int MTJ = MTY * NPT;   // theta extent of a tile
 constexpr int MHJ = MTJ + 2;
 constexpr int MHK = MTK + 2;
 constexpr int MHP = MHJ * MHK;
-constexpr int MNT = MTJ * MTK;
+constexpr int MNT = MTY * MTK;   // threads per block
+constexpr int NFILL = (MHP + MNT - 1) / MNT;
 
 struct PlaneMap {
   int mem;      // memory plane to read (ghost planes allowed)
@@ -55,7 +58,8 @@ __device__ __forceinline__ int map_k(const GridDev& g, int k, bool& ok) {
 }
 
 // Oracle-order evaluation of E_{a,s} at one node from its six neighbour
-// values.  want[a][s] selects the components to form (others untouched).
+// values (oracle/operators.py aligned_E).  only_a >= 0 forms just E_{only_a,
+// only_s} (and only the one-sided differences it needs).
 struct NodeIn {
   double Tv;
   double Tn[3][2];   // neighbour T (self if missing), s: 0 '+', 1 '-'
@@ -109,9 +113,11 @@ __device__ __forceinline__ void node_E(const NodeIn& n, int only_a, int only_s, 
 }
 
 // ---- async copy helpers (LDGSTS) -----------------------------------------
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+__device__ __forceinline__ void cp_async8s(unsigned s, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  cp_async8s(static_cast<unsigned>(__cvta_generic_to_shared(smem)), gmem);
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
@@ -162,8 +168,10 @@ __device__ __forceinline__ void gather(const MarchSmem& S, int sm, int sc, int s
   n.w2[1] = col.w2[1];
 }
 
-// Epilogue contract: epi.prefetch(o) early in the step, then
-// epi(g, i, j, k, o, F, uc) (uc = input value at the node), epi.finish(g).
+// Epilogue contract (per tile node n of the thread):
+//   epi.prefetch(n, o)                 early in the step (operands of plane t-1)
+//   epi(n, g, i, j, k, o, F, uc, pin)   uc = input value at the node
+//   epi.finish(g)                       block reduction, if any
 template <class Val, class Epi>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp op, Val val, Epi epi, int R) {
   extern __shared__ __align__(16) unsigned char march_smem[];
@@ -174,21 +182,17 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   const int tid = ty * MTK + tx;
   const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * MTJ, i0 = blockIdx.z * R;
   const int iend = min(i0 + R, g.n0);
-  const int jg = j0 + ty, kg = k0 + tx;
-  const bool inside = jg < g.n1 && kg < g.n2;
-  const int hown = (ty + 1) * MHK + (tx + 1);
+  const int kg = k0 + tx;
 
   // smem fill slots of this thread (tile + halo, wrapped / clamped in-plane)
-  int foff[2];  // in-plane offsets (plane < 2^31 elements)
-  bool fon[2];
+  int foff[NFILL];  // in-plane offsets (plane < 2^31 elements)
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < NFILL; ++q) {
     const int e = tid + q * MNT;
-    fon[q] = e < MHP;
     const int hj = e / MHK, hk = e - hj * MHK;
     bool oj, ok;
     const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
-    foff[q] = jj * g.n2 + kk;
+    foff[q] = e < MHP ? jj * g.n2 + kk : -1;
   }
   // row-table slot of this thread: tid < NROWT * MHJ
   const bool rton = tid < NROWT * MHJ;
@@ -197,13 +201,11 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   const int rjj = map_j(g, j0 - 1 + rhj, rok);
   const double* rbase = !rton ? nullptr : (rtab < 6 ? g.iL2[rtab] : (rtab < 10 ? g.wo01[rtab - 6] : g.iVal2));
 
-  bool ojo, oko;
-  const int jm = map_j(g, jg, ojo), km = map_k(g, kg, oko);
-  const bool own_ok = ojo && oko;
+  bool oko;
+  const int km = map_k(g, kg, oko);
   ColT col;
   load_col(g, km, col);
-  const bool pin_jk = (g.pin_lo1 && jg == 0) || (g.pin_hi1 && jg == g.n1 - 1) || (g.pin_lo2 && kg == 0) ||
-                      (g.pin_hi2 && kg == g.n2 - 1);
+  const bool pin_k = (g.pin_lo2 && kg == 0) || (g.pin_hi2 && kg == g.n2 - 1);
 
   // ring assignment: j-rings (tid < 2 MTK) and k-rings (next 2 MTJ threads)
   int ra = -1, rs_ = 0, rhj_ = 0, rhk_ = 0;
@@ -220,30 +222,33 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     rhk_ = rs_ == 0 ? 0 : MTK + 1;
   }
   bool rjo = false, rko = false;
-  const int rj = ra >= 0 ? map_j(g, j0 - 1 + rhj_, rjo) : 0;
+  if (ra >= 0) {
+    map_j(g, j0 - 1 + rhj_, rjo);
+  }
   const int rk = ra >= 0 ? map_k(g, k0 - 1 + rhk_, rko) : 0;
   const bool ring_on = ra >= 0 && rjo && rko &&
                        ((ra == 1) ? (k0 - 1 + rhk_ < g.n2) : (j0 - 1 + rhj_ < g.n1));
-  (void)rj;
+  const int rh = rhj_ * MHK + rhk_;
 
   auto issue_T = [&](int slot, int p) {
     const PlaneMap pm = plane_map(g, p);
     const int64_t base = (int64_t)pm.mem * g.plane;
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (fon[q]) val.stage(&S.T[slot][tid + q * MNT], base + foff[q], pm.mem);
+    for (int q = 0; q < NFILL; ++q)
+      if (foff[q] >= 0) val.stage(&S.T[slot][tid + q * MNT], base + foff[q], pm.mem);
   };
   auto issue_bc = [&](int slot, int p) {
     const PlaneMap pm = plane_map(g, p);
     const int64_t base = (int64_t)pm.mem * g.plane;
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (fon[q]) {
+    for (int q = 0; q < NFILL; ++q)
+      if (foff[q] >= 0) {
         const int e = tid + q * MNT;
-        cp_async8(&S.b[slot][0][e], op.b[0] + base + foff[q]);
-        cp_async8(&S.b[slot][1][e], op.b[1] + base + foff[q]);
-        cp_async8(&S.b[slot][2][e], op.b[2] + base + foff[q]);
-        cp_async8(&S.c[slot][e], op.c + base + foff[q]);
+        const int64_t o = base + foff[q];
+        cp_async8(&S.b[slot][0][e], op.b[0] + o);
+        cp_async8(&S.b[slot][1][e], op.b[1] + o);
+        cp_async8(&S.b[slot][2][e], op.b[2] + o);
+        cp_async8(&S.c[slot][e], op.c + o);
       }
   };
   auto issue_rows = [&](int slot, int p) {
@@ -253,36 +258,56 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     }
   };
 
-  // ---- prologue
+  // own nodes
+  int jn[NPT], hn[NPT];
+  bool inside[NPT], own_ok[NPT], pin_j[NPT];
+#pragma unroll
+  for (int n = 0; n < NPT; ++n) {
+    jn[n] = j0 + ty + n * MTY;
+    hn[n] = (ty + n * MTY + 1) * MHK + (tx + 1);
+    inside[n] = jn[n] < g.n1 && kg < g.n2;
+    bool ojo;
+    map_j(g, jn[n], ojo);
+    own_ok[n] = ojo && oko;
+    pin_j[n] = (g.pin_lo1 && jn[n] == 0) || (g.pin_hi1 && jn[n] == g.n1 - 1);
+  }
+
+  // ---- prologue: T(i0-1), T(i0), T(i0+1); b/c and rows of i0-1 and i0
   issue_T(0, i0 - 1);
   issue_T(1, i0);
   issue_T(2, i0 + 1);
-  issue_bc(1, i0 - 1);
+  issue_bc((i0 - 1) & 1, i0 - 1);
   issue_rows(2, i0 - 1);
-  issue_bc(0, i0);
+  issue_bc(i0 & 1, i0);
   issue_rows(0, i0);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  double E0p_prev2 = 0.0;
+  double E0p[NPT];     // E_{0,+} at plane t-2 (relative to the finalised plane t-1)
+  double Eprev[NPT][3][2];
   {
     const PlaneMap pm = plane_map(g, i0 - 1);
-    if (pm.exists && inside) {
-      NodeIn n;
-      gather(S, 0, 0, 1, 1, 2, hown, ty + 1, col, n);
-      double E[3][2];
-      node_E(n, 0, 0, E);
-      E0p_prev2 = E[0][0];
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+      E0p[n] = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) Eprev[n][a][0] = Eprev[n][a][1] = 0.0;
+      if (pm.exists && inside[n]) {
+        NodeIn in;
+        gather(S, 0, 0, 1, (i0 - 1) & 1, 2, hn[n], ty + n * MTY + 1, col, in);
+        double E[3][2];
+        node_E(in, 0, 0, E);
+        E0p[n] = E[0][0];
+      }
     }
   }
-  __syncthreads();  // b/c slot 1 and row slot 2 are refilled below
+  __syncthreads();  // b/c slot of i0-1 and row slot 2 are refilled by step i0
 
-  double Eprev[3][2] = {{0, 0}, {0, 0}, {0, 0}};
   int s_m = 0, s_c = 1, s_p = 2, s_n = 3;  // T slots of planes t-1, t, t+1, t+2
   int r_c = 0, r_p = 2;                    // row-table slots of planes t, t-1
   for (int t = i0; t <= iend; ++t) {
     const int bsl = t & 1;  // b/c slot of plane t
-    const int r_n = 3 - r_c - r_p;  // free row slot -> plane t+1
+    const int r_n = 3 - r_c - r_p;
     // ---- async prefetch of the next planes (overlaps the compute below)
     if (t + 2 <= iend) issue_T(s_n, t + 2);
     if (t + 1 <= iend) {
@@ -290,67 +315,69 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
       issue_rows(r_n, t + 1);
     }
     cp_async_commit();
-    // epilogue operands of plane t-1
-    const int64_t of = off3(g, t - 1, jg, kg);
-    if (t > i0 && inside) epi.prefetch(of);
 
     const PlaneMap pm = plane_map(g, t);
     const bool last = (t == iend);
-    double Ecur[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-    const int par = t & 1;
-    if (pm.exists) {
-      if (own_ok) {
-        NodeIn n;
-        gather(S, s_m, s_c, s_p, bsl, r_c, hown, ty + 1, col, n);
-        node_E(n, last ? 0 : -1, 1, Ecur);  // last plane: only E_{0,-} is consumed
+    const int par = t & 1, pp = par ^ 1;
+    const int tf = t - 1;
+    const int ig = tf + g.i0g;
+    const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+      const int64_t of = off3(g, tf, jn[n], kg);
+      const bool fin = t > i0 && inside[n];
+      if (fin) epi.prefetch(n, of);
+      double Ec[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+      if (pm.exists && own_ok[n]) {
+        NodeIn in;
+        gather(S, s_m, s_c, s_p, bsl, r_c, hn[n], ty + n * MTY + 1, col, in);
+        node_E(in, last ? 0 : -1, 1, Ec);  // last plane: only E_{0,-} is consumed
       }
       if (!last) {
-        S.E[par][0][hown] = Ecur[1][0];
-        S.E[par][1][hown] = Ecur[1][1];
-        S.E[par][2][hown] = Ecur[2][0];
-        S.E[par][3][hown] = Ecur[2][1];
-        if (ra >= 0) {
-          double Ev = 0.0;
-          if (ring_on) {
-            ColT rcol;
-            if (ra == 2) load_col(g, rk, rcol);
-            else rcol = col;
-            NodeIn n;
-            gather(S, s_m, s_c, s_p, bsl, r_c, rhj_ * MHK + rhk_, rhj_, rcol, n);
-            double E[3][2];
-            node_E(n, ra, rs_, E);
-            Ev = E[ra][rs_];
-          }
-          S.E[par][(ra - 1) * 2 + rs_][rhj_ * MHK + rhk_] = Ev;
-        }
+        S.E[par][0][hn[n]] = Ec[1][0];
+        S.E[par][1][hn[n]] = Ec[1][1];
+        S.E[par][2][hn[n]] = Ec[2][0];
+        S.E[par][3][hn[n]] = Ec[2][1];
+      }
+      // ---- finalise plane t-1 of this node (its in-plane neighbours' fluxes
+      // were published before the previous barrier)
+      if (fin) {
+        const int h = hn[n];
+        const double E1pm = S.E[pp][0][h - MHK], E1mp = S.E[pp][1][h + MHK];
+        const double E2pm = S.E[pp][2][h - 1], E2mp = S.E[pp][3][h + 1];
+        double G = (E0p[n] - Eprev[n][0][0]) + (Eprev[n][0][1] - Ec[0][1]);
+        G = G + ((E1pm - Eprev[n][1][0]) + (Eprev[n][1][1] - E1mp));
+        G = G + ((E2pm - Eprev[n][2][0]) + (Eprev[n][2][1] - E2mp));
+        const double iv = S.rowt[r_p][10][ty + n * MTY + 1] * col.ivg;
+        double f = ((0.0 - G) * iv) * op.pref;
+        if (op.rho) f = f / __ldg(op.rho + of);
+        const bool pin = pin_i || pin_j[n] || pin_k;
+        if (pin) f = 0.0;
+        epi(n, g, tf, jn[n], kg, of, f, S.T[s_m][h], pin);
+      }
+      if (t > i0) E0p[n] = Eprev[n][0][0];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        Eprev[n][a][0] = Ec[a][0];
+        Eprev[n][a][1] = Ec[a][1];
       }
     }
-    __syncthreads();
-    // ---- finalise plane t-1
-    if (t > i0 && inside) {
-      const int tf = t - 1;
-      const int pp = par ^ 1;
-      const double E1pm = S.E[pp][0][hown - MHK], E1mp = S.E[pp][1][hown + MHK];
-      const double E2pm = S.E[pp][2][hown - 1], E2mp = S.E[pp][3][hown + 1];
-      double G = (E0p_prev2 - Eprev[0][0]) + (Eprev[0][1] - Ecur[0][1]);
-      G = G + ((E1pm - Eprev[1][0]) + (Eprev[1][1] - E1mp));
-      G = G + ((E2pm - Eprev[2][0]) + (Eprev[2][1] - E2mp));
-      const double iv = S.rowt[r_p][10][ty + 1] * col.ivg;
-      double f = ((0.0 - G) * iv) * op.pref;
-      if (op.rho) f = f / __ldg(op.rho + of);
-      const int ig = tf + g.i0g;
-      const bool pin = pin_jk || (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
-      if (pin) f = 0.0;
-      epi(g, tf, jg, kg, of, f, S.T[s_m][hown], pin);
-    }
-    if (t > i0) E0p_prev2 = Eprev[0][0];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      Eprev[a][0] = Ecur[a][0];
-      Eprev[a][1] = Ecur[a][1];
+    // ---- halo ring of plane t: one flux component per ring node
+    if (!last && ra >= 0) {
+      double Ev = 0.0;
+      if (ring_on && pm.exists) {
+        ColT rcol;
+        if (ra == 2) load_col(g, rk, rcol);
+        else rcol = col;
+        NodeIn in;
+        gather(S, s_m, s_c, s_p, bsl, r_c, rh, rhj_, rcol, in);
+        double E[3][2];
+        node_E(in, ra, rs_, E);
+        Ev = E[ra][rs_];
+      }
+      S.E[par][(ra - 1) * 2 + rs_][rh] = Ev;
     }
     if (last) break;
-    // rotate slots
     {
       const int tmp = s_m;
       s_m = s_c;
@@ -389,8 +416,8 @@ struct PValDev {
 // ---- epilogues ----------------------------------------------------------
 struct EpiStore {  // F = op(u)
   double* F;
-  __device__ __forceinline__ void prefetch(int64_t) {}
-  __device__ __forceinline__ void operator()(const GridDev&, int, int, int, int64_t o, double f, double, bool) {
+  __device__ __forceinline__ void prefetch(int, int64_t) {}
+  __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double, bool) {
     F[o] = f;
   }
   __device__ __forceinline__ void finish(const GridDev&) {}
@@ -404,16 +431,16 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   StageCoef sc;
   int stage;
   int* bad;
-  double pa0, pm2, py0;
-  __device__ __forceinline__ void prefetch(int64_t o) {
-    pa0 = __ldg(u0 + o);
-    pm2 = __ldg(um2 + o);
-    py0 = __ldg(y0 + o);
+  double pa0[NPT], pm2[NPT], py0[NPT];
+  __device__ __forceinline__ void prefetch(int n, int64_t o) {
+    pa0[n] = __ldg(u0 + o);
+    pm2[n] = __ldg(um2 + o);
+    py0[n] = __ldg(y0 + o);
   }
-  __device__ __forceinline__ void operator()(const GridDev&, int, int, int, int64_t o, double f, double um1,
+  __device__ __forceinline__ void operator()(int n, const GridDev&, int, int, int, int64_t o, double f, double um1,
                                              bool pin) {
-    const double a0 = pa0;
-    double v = ((((sc.mu * um1) + (sc.nu * pm2)) + (sc.kap * a0)) + (sc.mtdt * f)) + (sc.gtdt * py0);
+    const double a0 = pa0[n];
+    double v = ((((sc.mu * um1) + (sc.nu * pm2[n])) + (sc.kap * a0)) + (sc.mtdt * f)) + (sc.gtdt * py0[n]);
     v = pin ? a0 : v;
     out[o] = v;
     if (!isfinite(v)) atomicMin(bad, stage);
@@ -428,8 +455,8 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
   unsigned int* counter;
   ArgRes* res;
   ArgMax best;
-  __device__ __forceinline__ void prefetch(int64_t) {}
-  __device__ __forceinline__ void operator()(const GridDev& g, int i, int j, int k, int64_t o, double f, double,
+  __device__ __forceinline__ void prefetch(int, int64_t) {}
+  __device__ __forceinline__ void operator()(int, const GridDev& g, int i, int j, int k, int64_t o, double f, double,
                                              bool) {
     F[o] = f;
     best = am_better(best, ArgMax{fabs(f), aos_index(g, i, j, k, 0, 1)});
@@ -500,8 +527,8 @@ struct EpiMatvec {  // PCG K7: p_new = (loaded value), Ap = a p - dt F(p); (W p,
   PcgDev* st;
   AlignedOp op;
   double acc;
-  __device__ __forceinline__ void prefetch(int64_t) {}
-  __device__ __forceinline__ void operator()(const GridDev& g, int i, int j, int k, int64_t o, double f,
+  __device__ __forceinline__ void prefetch(int, int64_t) {}
+  __device__ __forceinline__ void operator()(int, const GridDev& g, int i, int j, int k, int64_t o, double f,
                                              double pv, bool) {
     const double ap = (adiag ? __ldg(adiag + o) * pv : pv) - dt * f;
     pnew[o] = pv;
