@@ -11,7 +11,8 @@ Restates SPEC.md ``operators``:
 * ``aligned_apply``  -- F = pref/rho div(c b b . grad T), c = f_c f_m(T0)
   kappa0 T0^{5/2} evaluated at nodes.  The
   symmetric 19-point discretisation is the gradient of the quadratic form
-  Q = 1/2 sum_{v,sigma} W_{v,sigma} c_v (b_v . g_{v,sigma})^2 over the 8
+  Q = 1/2 sum_{v,sigma} W_{v,sigma} (beta_v . g_{v,sigma})^2, beta = sqrt(c) b
+  (so c_v (b_v . g)^2 = (beta_v . g)^2), over the 8
   one-sided "corner tetrahedra" of every node: symmetric in the rho*V inner
   product, negative semi-definite, and identical to the scalar stencil with
   arithmetic face-averaged c when b is axis-aligned in 1-D.
@@ -223,24 +224,32 @@ def _iL(geom, a, s):
     return _b2(geom.iL2[(a, s)]) * _b1(geom.iL1[(a, s)])
 
 
-def aligned_E(geom, T, b, c):
-    """Per-node edge fluxes E[(a, s)] of the corner-tetrahedron quadratic form."""
+def aligned_beta(b, c):
+    """beta_a = b_a * sqrt(c): c b b^T = beta beta^T, so the frozen operator
+    needs three nodal arrays instead of four ("Spitzer stencil")."""
+    return b * np.sqrt(c)[None]
+
+
+def aligned_E(geom, T, beta):
+    """Per-node edge fluxes E[(a, s)] of the corner-tetrahedron quadratic form.
+
+    bil[(a,s)] = beta_a * (iL2 * iL1); p = bil * dT (one-sided difference);
+    f_sigma = (wo01 * wo2) * ((p_0 + p_1) + p_2); E = bil * sum_sigma f_sigma
+    (octants in canonical order)."""
     per = geom.periodic
     p = {}
-    iL = {}
+    bil = {}
     for a in range(3):
         Tp = shift(T, a, 1, per[a])
         Tm = shift(T, a, -1, per[a])
-        iL[(a, "+")] = _iL(geom, a, "+")
-        iL[(a, "-")] = _iL(geom, a, "-")
-        dp = (Tp - T) * iL[(a, "+")]
-        dm = (T - Tm) * iL[(a, "-")]
-        p[(a, "+")] = b[a] * dp
-        p[(a, "-")] = b[a] * dm
+        bil[(a, "+")] = beta[a] * _iL(geom, a, "+")
+        bil[(a, "-")] = beta[a] * _iL(geom, a, "-")
+        p[(a, "+")] = bil[(a, "+")] * (Tp - T)
+        p[(a, "-")] = bil[(a, "-")] * (T - Tm)
     f = {}
     for sg in SIG:
         s = (p[(0, sg[0])] + p[(1, sg[1])]) + p[(2, sg[2])]
-        om = (c * _b2(geom.wo01[(sg[0], sg[1])])) * _b1(geom.wo2[sg[2]])
+        om = _b2(geom.wo01[(sg[0], sg[1])]) * _b1(geom.wo2[sg[2]])
         f[sg] = om * s
     E = {}
     for a in range(3):
@@ -249,7 +258,7 @@ def aligned_E(geom, T, b, c):
             for sg in SIG:
                 if sg[a] == s:
                     acc = f[sg] if acc is None else acc + f[sg]
-            E[(a, s)] = (b[a] * iL[(a, s)]) * acc
+            E[(a, s)] = bil[(a, s)] * acc
     return E
 
 
@@ -257,14 +266,18 @@ def aligned_apply(geom, T, b, c, rho=None, pref=1.0):
     """F(T) = -((G * iVal) * pref) / rho, G = dQ/dT (see module docstring).
 
     T: (n0, n1, n2); b: (3, n0, n1, n2); c: (n0, n1, n2) nodal conductivity.
+    G is summed in the order an r-marching kernel produces it:
+      own = ((E0- - E0+) + (E1- - E1+)) + (E2- - E2+)          at the node
+      nbr = (E1+(j-1) - E1-(j+1)) + (E2+(k-1) - E2-(k+1))     in-plane neighbours
+      G   = (E0+(i-1) - E0-(i+1)) + (own + nbr)
+    with missing neighbours contributing 0.
     """
     per = geom.periodic
-    E = aligned_E(geom, T, b, c)
-    G = None
-    for a in range(3):
-        term = (shift_zero(E[(a, "+")], a, -1, per[a]) - E[(a, "+")]) + (
-            E[(a, "-")] - shift_zero(E[(a, "-")], a, 1, per[a]))
-        G = term if G is None else G + term
+    E = aligned_E(geom, T, aligned_beta(b, c))
+    own = ((E[(0, "-")] - E[(0, "+")]) + (E[(1, "-")] - E[(1, "+")])) + (E[(2, "-")] - E[(2, "+")])
+    nbr = (shift_zero(E[(1, "+")], 1, -1, per[1]) - shift_zero(E[(1, "-")], 1, 1, per[1])) + (
+        shift_zero(E[(2, "+")], 2, -1, per[2]) - shift_zero(E[(2, "-")], 2, 1, per[2]))
+    G = (shift_zero(E[(0, "+")], 0, -1, per[0]) - shift_zero(E[(0, "-")], 0, 1, per[0])) + (own + nbr)
     iv = _b2(geom.iVal2) * _b1(geom.iValg)
     F = ((0.0 - G) * iv) * pref
     if rho is not None:
@@ -296,7 +309,7 @@ def _sgn(s):
     return 1.0 if s == "+" else -1.0
 
 
-def aligned_hessian_rows(geom, b, c):
+def aligned_hessian_rows(geom, beta):
     """H[m, off] = d^2 Q / dT_m dT_{m+off} for the 19 offsets, accumulated per
     row in a fixed order: first the 8 tets with apex v = m (canonical sigma
     order: diagonal, then the three edge ends), then the 24 tets with v = m -
@@ -305,14 +318,14 @@ def aligned_hessian_rows(geom, b, c):
     per = geom.periodic
     shape = geom.shape
     H = [np.zeros(shape) for _ in OFFSETS]
-    # q[(a, s)] at every node v: sigma_a * b_a * iL_{a, s}
+    # q[(a, s)] at every node v: sigma_a * (beta_a * iL_{a, s})
     q = {}
     for a in range(3):
         for s in "+-":
-            q[(a, s)] = (_sgn(s) * b[a]) * _iL(geom, a, s)
+            q[(a, s)] = _sgn(s) * (beta[a] * _iL(geom, a, s))
     om = {}
     for sg in SIG:
-        om[sg] = (c * _b2(geom.wo01[(sg[0], sg[1])])) * _b1(geom.wo2[sg[2]])
+        om[sg] = _b2(geom.wo01[(sg[0], sg[1])]) * _b1(geom.wo2[sg[2]]) * np.ones(geom.shape)
     # (A) apex tets
     for sg in SIG:
         qa = [q[(a, sg[a])] for a in range(3)]
@@ -351,7 +364,7 @@ def aligned_hessian_rows(geom, b, c):
 def aligned_gershgorin(geom, b, c, rho=None, pref=1.0):
     """lam_m = ((sum_off |H[m, off]| * iVal) * pref) / rho over non-pinned rows,
     and the Jacobi diagonal -J_mm = ((H[m,0] * iVal) * pref) / rho."""
-    H = aligned_hessian_rows(geom, b, c)
+    H = aligned_hessian_rows(geom, aligned_beta(b, c))
     S = None
     for h in H:
         S = np.abs(h) if S is None else S + np.abs(h)

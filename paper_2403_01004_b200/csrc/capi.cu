@@ -14,6 +14,7 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -109,7 +110,8 @@ struct pc_op {
   int ncomp;
   ScalarOp so{};
   AlignedOp ao{};
-  double* cbuf = nullptr;   // aligned conductivity (component-sized buffer)
+  const double* bsrc[3] = {nullptr, nullptr, nullptr};  // aligned: b-hat (caller's field)
+  double* betabuf = nullptr;  // aligned: beta = sqrt(c) b, 3 component-sized buffers
   double* dbuf = nullptr;   // Jacobi diagonal -J_ii
   double* kfc = nullptr;    // kappa0 * f_c(r) per axis-0 row (n0 + 2)
   double Tfloor = 1e-10;
@@ -599,7 +601,7 @@ int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, 
   op->grid = g;
   op->kind = K_ALIGNED;
   op->ncomp = 1;
-  for (int q = 0; q < 3; ++q) op->ao.b[q] = bhat->base(q);
+  for (int q = 0; q < 3; ++q) op->bsrc[q] = bhat->base(q);
   op->ao.rho = rho ? rho->base(0) : nullptr;
   op->ao.pref = pref;
   op->ao.ncomp = 1;
@@ -609,10 +611,13 @@ int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, 
   for (int r = 0; r < rows; ++r) k[r] = fc_table ? kappa0 * fc_table[r] : kappa0;
   CUDA_TRY(cudaMalloc(&op->kfc, sizeof(double) * rows));
   CUDA_TRY(cudaMemcpy(op->kfc, k.data(), sizeof(double) * rows, cudaMemcpyHostToDevice));
-  if (cudaMalloc(&op->cbuf, g->comp_elems * sizeof(double)) != cudaSuccess)
-    return fail(PC_E_CUDA, "conductivity allocation failed");
-  cudaMemsetAsync(op->cbuf, 0, g->comp_elems * sizeof(double), c->s);
-  op->ao.c = op->cbuf + g->g.plane;
+  if (cudaMalloc(&op->betabuf, 3 * g->comp_elems * sizeof(double)) != cudaSuccess) {
+    cudaFree(op->kfc);
+    delete op;
+    return fail(PC_E_CUDA, "beta allocation failed (out of device memory)");
+  }
+  cudaMemsetAsync(op->betabuf, 0, 3 * g->comp_elems * sizeof(double), c->s);
+  for (int q = 0; q < 3; ++q) op->ao.beta[q] = op->betabuf + q * g->comp_elems + g->g.plane;
   *out = op;
   return PC_OK;
 }
@@ -620,7 +625,7 @@ int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, 
 int pc_op_destroy(pc_op* op) {
   if (!op) return PC_OK;
   cudaStreamSynchronize(op->grid->ctx->s);
-  cudaFree(op->cbuf);
+  cudaFree(op->betabuf);
   cudaFree(op->dbuf);
   cudaFree(op->kfc);
   delete op;
@@ -655,15 +660,18 @@ int pc_op_freeze(pc_op* op, const pc_field* T0) {
   if (op->kind == K_ALIGNED) {
     if (!T0 || T0->ncomp != 1 || T0->grid != g) return fail(PC_E_INVALID, "aligned freeze needs a scalar T0 on the grid");
     CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
-    k_aligned_coef<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, T0->base(0), op->kfc + 1, op->Tfloor,
-                                                                   op->cbuf + g->g.plane, c->bad);
+    CFld bsrc{{op->bsrc[0], op->bsrc[1], op->bsrc[2]}};
+    Fld beta{{const_cast<double*>(op->ao.beta[0]), const_cast<double*>(op->ao.beta[1]),
+              const_cast<double*>(op->ao.beta[2])}};
+    k_aligned_beta<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, T0->base(0), op->kfc + 1, op->Tfloor,
+                                                                   bsrc, beta, c->bad);
     c->st.launches++;
-    TRY(check_launch("k_aligned_coef"));
+    TRY(check_launch("k_aligned_beta"));
     CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CUDA_TRY(cudaStreamSynchronize(c->s));
     if (*c->h_bad == 1) return fail(PC_E_DOMAIN, "aligned conduction: non-positive T0 (SPEC.md:120)");
-    double* cb[1] = {op->cbuf};
-    TRY(halo_exchange(c, g, cb, 1));
+    double* bb[3] = {op->betabuf, op->betabuf + g->comp_elems, op->betabuf + 2 * g->comp_elems};
+    TRY(halo_exchange(c, g, bb, 3));
     TRY(run_bound(op, op->ao));
   } else {
     TRY(run_bound(op, op->so));
@@ -700,8 +708,8 @@ static int march_R(const pc_grid* g) {
 static dim3 march_grid(const pc_grid* g, int R) {
   return dim3((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + MTJ - 1) / MTJ, (g->g.n0 + R - 1) / R);
 }
-template <class Val, class Epi>
-static int launch_march(pc_op* op, const Val& val, const Epi& epi, const char* what) {
+template <class Epi>
+static int launch_march(pc_op* op, const double* Tin, const Epi& epi, const int* skip, const char* what) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   const int R = march_R(g);
@@ -709,11 +717,11 @@ static int launch_march(pc_op* op, const Val& val, const Epi& epi, const char* w
   if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
   static bool attr = false;  // one per template instantiation
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_aligned_march<Val, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(k_aligned_march<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(MarchSmem)));
     attr = true;
   }
-  k_aligned_march<Val, Epi><<<grid, dim3(MTK, MTY), sizeof(MarchSmem), c->s>>>(g->g, op->ao, val, epi, R);
+  k_aligned_march<Epi><<<grid, dim3(MTK, MTY), sizeof(MarchSmem), c->s>>>(g->g, op->ao, Tin, epi, R, skip);
   c->st.launches++;
   return check_launch(what);
 }
@@ -734,12 +742,11 @@ static int launch_apply(pc_op* op, const Op& o, CFld u, Fld F, bool argmax) {
 static int apply_any(pc_op* op, CFld u, Fld F, bool argmax) {
   if (op->kind == K_ALIGNED) {
     pc_ctx* c = op->grid->ctx;
-    PlainVal val{{u.p[0], u.p[1], u.p[2]}};
     if (argmax) {
       EpiArgmax e{F.p[0], c->red_v, c->red_i, c->counter, c->res, ArgMax{-1.0, 0x7fffffffffffffffLL}};
-      return launch_march(op, val, e, "k_aligned_march<argmax>");
+      return launch_march(op, u.p[0], e, nullptr, "k_aligned_march<argmax>");
     }
-    return launch_march(op, val, EpiStore{F.p[0]}, "k_aligned_march<apply>");
+    return launch_march(op, u.p[0], EpiStore{F.p[0]}, nullptr, "k_aligned_march<apply>");
   }
   return launch_apply(op, op->so, u, F, argmax);
 }
@@ -916,9 +923,8 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     if (rc) break;
     CFld m2 = um2w ? um2w->cf() : cfld(u);
     if constexpr (std::is_same<Op, AlignedOp>::value) {
-      PlainVal val{{um1->base(0), um1->base(0), um1->base(0)}};
       EpiStage e{m2.p[0], cfld(u).p[0], y0.base(0), out->base(0), sc, k, c->bad};
-      rc = launch_march(op, val, e, "k_aligned_march<stage>");
+      rc = launch_march(op, um1->base(0), e, nullptr, "k_aligned_march<stage>");
     } else {
       k_stage<<<nb, kThreads, 0, c->s>>>(g->g, o, um1->cf(), m2, cfld(u), y0.cf(), out->f(), sc, k, c->bad);
       c->st.launches++;
@@ -1040,23 +1046,29 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   while (rc == PC_OK && !stop && it < max_iter) {
     for (int q = 0; q < batch && it < max_iter && rc == PC_OK; ++q) {
       ++it;
-      rc = halo_work(g, r);
-      if (rc == PC_OK) rc = halo_work(g, *pold);
-      if (rc) break;
       if constexpr (std::is_same<Op, AlignedOp>::value) {
-        // beta is read on the device inside PVal via the state pointer
-        PValDev val{r.base(0), pold->base(0), dg, adiag, dt, c->pcg, 0.0};
-        EpiMatvec e{pnew->base(0), Ap.base(0), adiag, dt, c->red_v, c->counter, c->pcg, op->ao, 0.0};
-        rc = launch_march(op, val, e, "k_aligned_march<matvec>");
-        c->st.launches--;  // counted below with the update kernel
+        // p = z + beta p_old (beta from the device-side PCG state), then the
+        // marching matvec stages p like any other field
+        k_pcg_pupdate<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
+                                                 c->pcg);
+        c->st.launches++;
+        rc = check_launch("k_pcg_pupdate");
+        if (rc == PC_OK) rc = halo_work(g, *pnew);
+        if (rc) break;
+        EpiMatvec e{Ap.base(0), adiag, dt, c->red_v, c->counter, c->pcg, op->ao, 0.0};
+        const int* done = reinterpret_cast<const int*>(reinterpret_cast<const char*>(c->pcg) + offsetof(PcgDev, done));
+        rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
       } else {
+        rc = halo_work(g, r);
+        if (rc == PC_OK) rc = halo_work(g, *pold);
+        if (rc) break;
         k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
                                                 c->red_v, c->counter, c->pcg);
       }
       k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, tol, it,
                                               c->red_v, c->red_v2, c->counter, c->pcg);
-      c->st.launches += 2;
-      c->st.stage_launches += 2;
+      c->st.launches += std::is_same<Op, AlignedOp>::value ? 1 : 2;  // (march counted at launch)
+      c->st.stage_launches += std::is_same<Op, AlignedOp>::value ? 3 : 2;
       rc = check_launch("k_pcg");
       std::swap(pold, pnew);
     }

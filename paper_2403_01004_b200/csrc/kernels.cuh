@@ -241,9 +241,10 @@ __global__ void __launch_bounds__(kThreads) k_bound(GridDev g, Op op, double* di
   }
 }
 
-// c = kfc[i] * ((T0f * T0f) * sqrt(T0f)), T0f = max(T0, T_floor); bad if T0 <= 0
-__global__ void __launch_bounds__(kThreads) k_aligned_coef(GridDev g, const double* T0, const double* kfc,
-                                                           double Tfloor, double* c, int* bad) {
+// beta_a = b_a * sqrt(c), c = kfc[i] * ((T0f * T0f) * sqrt(T0f)), T0f = max(T0, T_floor)
+// (oracle aligned_coefficient + aligned_beta); bad if T0 <= 0
+__global__ void __launch_bounds__(kThreads) k_aligned_beta(GridDev g, const double* T0, const double* kfc,
+                                                           double Tfloor, CFld b, Fld beta, int* bad) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.N; q += (int64_t)gridDim.x * blockDim.x) {
     int i, j, k;
     unflatten(g, q, i, j, k);
@@ -251,7 +252,11 @@ __global__ void __launch_bounds__(kThreads) k_aligned_coef(GridDev g, const doub
     double t = T0[o];
     if (!(t > 0.0)) atomicMin(bad, 1);
     double tf = fmax(t, Tfloor);
-    c[o] = kfc[i] * ((tf * tf) * sqrt(tf));
+    const double c = kfc[i] * ((tf * tf) * sqrt(tf));
+    const double sc = sqrt(c);
+    beta.p[0][o] = b.p[0][o] * sc;
+    beta.p[1][o] = b.p[1][o] * sc;
+    beta.p[2][o] = b.p[2][o] * sc;
   }
 }
 
@@ -268,6 +273,38 @@ struct PcgDev {
   int status;    // 0 ok, 1 converged, 2 indefinite, 3 diverged
   int pad;
 };
+
+// alpha from (p, Ap)_W; breakdown / NaN stop the solve
+__device__ __forceinline__ void pcg_alpha(PcgDev* st, double pAp) {
+  st->pAp = pAp;
+  if (st->rz != 0.0) {
+    if (!(pAp > 0.0)) {
+      st->status = isnan(pAp) ? 3 : 2;
+      st->done = 1;
+    } else {
+      st->alpha = st->rz / pAp;
+    }
+  } else {
+    st->alpha = 0.0;
+  }
+}
+
+// p = z + beta p_old, z = r / (a + dt dg): the search-direction update of the
+// aligned PCG, ahead of the marching matvec (which then stages p like any T)
+__global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const double* r, const double* pold,
+                                                          double* pnew, const double* dg, const double* adiag,
+                                                          double dt, const PcgDev* st) {
+  if (st->done) return;
+  const double beta = st->beta;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    unflatten(g, c, i, j, k);
+    const int64_t o = off3(g, i, j, k);
+    const double dvec = (adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o);
+    const double z = __ldg(r + o) / dvec;
+    pnew[o] = z + beta * __ldg(pold + o);
+  }
+}
 
 // p = z + beta * p_old with z = r / (a + dt*dg)   (recomputed at neighbours)
 struct PVal {
@@ -365,17 +402,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld 
     if (threadIdx.x == 0) {
       double a = 0.0;
       for (int t = 0; t < (int)gridDim.x; ++t) a += p1[t];
-      st->pAp = a;
-      if (st->rz != 0.0) {
-        if (!(a > 0.0)) {
-          st->status = isnan(a) ? 3 : 2;
-          st->done = 1;
-        } else {
-          st->alpha = st->rz / a;
-        }
-      } else {
-        st->alpha = 0.0;
-      }
+      pcg_alpha(st, a);
       *counter = 0u;
     }
   }

@@ -1,25 +1,35 @@
-// r-marching shared-memory kernels for the 19-point aligned (Spitzer)
-// operator -- the hot path of C3/C4/C5 (K3 stage, K4 F+argmax, K7 matvec).
+// r-marching shared-memory kernel for the 19-point aligned (Spitzer)
+// operator -- the hot path of C3/C4/C5 (K3 fused stage, K4 F+argmax, K7
+// PCG matvec).  DESIGN.md §4 "K3".
 //
-// Design: a block owns a (TJ x TK) theta-phi tile (phi =
-// lanes, 256-byte coalesced rows) and marches along r over a chunk of R
-// planes.  Per plane it stages T (3-plane ring), b and c with a one-node halo
-// in shared memory, evaluates the six corner-tetrahedron edge fluxes
-// E_{a,s} of every tile node ONCE (plus one component on the halo ring), and
-// finalises the previous plane, whose r-neighbour fluxes are carried in
-// registers.  Every HBM byte of T, b, c is read once per plane (plus the
-// thin halo), so the stage is bandwidth- not recompute-bound.
+// A block owns a (MTJ x MTK) theta-phi tile (phi = lanes: 256-byte coalesced
+// rows) of an r-chunk of R planes and marches along r.  Per plane it
+//   * stages T (4-slot ring, prefetch distance 2 planes), beta (3 slots) and
+//     the per-(r,theta) metric rows (4 slots) with a one-node halo through
+//     cp.async, one group per plane;
+//   * keeps each own node's T(t-1), T(t) (r-neighbours), the r-flux queue
+//     E_{0,+}(t-2), E_{0,+}(t-1), the node part of G and the epilogue
+//     operands (LDG-prefetched one plane ahead) in registers;
+//   * evaluates the six edge fluxes E_{a,s} of every tile node once, one
+//     flux component on the 96-node halo ring, publishes the in-plane
+//     components through shared memory and finalises plane t-1 in the
+//     oracle's summation order (oracle/operators.py aligned_apply):
+//        own = ((E0- - E0+) + (E1- - E1+)) + (E2- - E2+)
+//        nbr = (E1+(j-1) - E1-(j+1)) + (E2+(k-1) - E2-(k+1))
+//        G   = (E0+(i-1) - E0-(i+1)) + (own + nbr)
+//   * one cp.async wait + one __syncthreads per plane.
+// Every HBM byte of T and beta is read once per plane (plus the thin halo), so
+// the stage streams 8 arrays: T, beta(3), u_{k-2}, u0, y0 in and u_k out.
 //
-// Arithmetic is the oracle's (oracle/operators.py aligned_E / aligned_apply)
-// expression by expression; only the evaluation schedule differs, so results
-// stay bitwise identical.
+// Arithmetic is the oracle's expression by expression (compiled with
+// -fmad=false), only the schedule differs: results are bitwise identical.
 #pragma once
 #include "kernels.cuh"
 
 namespace pc {
 
 constexpr int MTK = 32;          // phi extent of a tile (lanes)
-constexpr int MTY = 8;           // thread rows
+constexpr int MTY = 8;           // warps = thread rows
 constexpr int NPT = 2;           // tile nodes per thread (rows ty, ty + MTY)
 constexpr int MTJ = MTY * NPT;   // theta extent of a tile
 constexpr int MHJ = MTJ + 2;
@@ -27,6 +37,11 @@ constexpr int MHK = MTK + 2;
 constexpr int MHP = MHJ * MHK;
 constexpr int MNT = MTY * MTK;   // threads per block
 constexpr int NFILL = (MHP + MNT - 1) / MNT;
+constexpr int NROWT = 11;        // per-(row, j) tables: iL2[6], wo01[4], iVal2
+constexpr int TSL = 4;           // T slots: t-1 (free), t, t+1, t+2/t+3 in flight
+constexpr int BSL = 3;           // beta slots: t, t+1, t+2 in flight
+constexpr int RSL = 4;           // row-table slots: t-1 (iv), t, t+1, t+2
+constexpr int NRING = 2 * MTK + 2 * MTJ;
 
 struct PlaneMap {
   int mem;      // memory plane to read (ghost planes allowed)
@@ -57,83 +72,24 @@ __device__ __forceinline__ int map_k(const GridDev& g, int k, bool& ok) {
   return k < 0 ? 0 : g.n2 - 1;
 }
 
-// Oracle-order evaluation of E_{a,s} at one node from its six neighbour
-// values (oracle/operators.py aligned_E).  only_a >= 0 forms just E_{only_a,
-// only_s} (and only the one-sided differences it needs).
-struct NodeIn {
-  double Tv;
-  double Tn[3][2];   // neighbour T (self if missing), s: 0 '+', 1 '-'
-  double b[3];
-  double c;
-  double il[3][2];   // inverse one-sided edge lengths (0 if missing)
-  double w01[4];     // wo01 at (row, j)
-  double w2[2];      // wo2 at k
-};
-
-__device__ __forceinline__ void node_E(const NodeIn& n, int only_a, int only_s, double E[3][2]) {
-  double p[3][2];
-#pragma unroll
-  for (int x = 0; x < 3; ++x) {
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      if (only_a >= 0 && x == only_a && t != only_s) { p[x][t] = 0.0; continue; }
-      double d = t == 0 ? (n.Tn[x][0] - n.Tv) * n.il[x][0] : (n.Tv - n.Tn[x][1]) * n.il[x][1];
-      p[x][t] = n.b[x] * d;
-    }
-  }
-  double f[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int s0 = (q >> 2) & 1, s1 = (q >> 1) & 1, s2 = q & 1;
-    if (only_a >= 0) {
-      const int sa = only_a == 0 ? s0 : (only_a == 1 ? s1 : s2);
-      if (sa != only_s) { f[q] = 0.0; continue; }
-    }
-    double sv = (p[0][s0] + p[1][s1]) + p[2][s2];
-    double om = (n.c * n.w01[s0 * 2 + s1]) * n.w2[s2];
-    f[q] = om * sv;
-  }
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (only_a >= 0 && (a != only_a || s != only_s)) continue;
-      double acc = 0.0;
-      bool first = true;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int sa = a == 0 ? (q >> 2) & 1 : (a == 1 ? (q >> 1) & 1 : q & 1);
-        if (sa != s) continue;
-        acc = first ? f[q] : acc + f[q];
-        first = false;
-      }
-      E[a][s] = (n.b[a] * n.il[a][s]) * acc;
-    }
-  }
-}
-
 // ---- async copy helpers (LDGSTS) -----------------------------------------
-__device__ __forceinline__ void cp_async8s(unsigned s, const double* gmem) {
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  cp_async8s(static_cast<unsigned>(__cvta_generic_to_shared(smem)), gmem);
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-constexpr int NROWT = 11;  // per-(row, j) tables: iL2[6], wo01[4], iVal2
-constexpr int MSLOTS = 4;  // T ring: planes t-1, t, t+1 in use, t+2 in flight
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 struct MarchSmem {
-  double T[MSLOTS][MHP];
-  double b[2][3][MHP];
-  double c[2][MHP];
-  double rowt[3][NROWT][MHJ];  // row tables for planes (p mod 3)
-  double E[2][4][MHP];         // E_{1,+}, E_{1,-}, E_{2,+}, E_{2,-} per plane parity
+  double T[TSL][MHP];
+  double B[BSL][3][MHP];
+  double E[2][4][MHP];          // E_{1,+}, E_{1,-}, E_{2,+}, E_{2,-} per plane parity
+  double rowt[RSL][NROWT][MHJ];
+  double ringcol[2][9];         // column tables of the phi-ring columns k0-1, k0+MTK
 };
 
-// per-thread column constants (depend on k only)
+// per-column constants (depend on k only)
 struct ColT {
   double il1[6];
   double w2[2];
@@ -147,37 +103,67 @@ __device__ __forceinline__ void load_col(const GridDev& g, int k, ColT& c) {
   c.ivg = __ldg(g.iValg + k);
 }
 
-__device__ __forceinline__ void gather(const MarchSmem& S, int sm, int sc, int sp, int bs, int rs, int h, int hj,
-                                       const ColT& col, NodeIn& n) {
-  n.Tv = S.T[sc][h];
-  n.Tn[0][0] = S.T[sp][h];
-  n.Tn[0][1] = S.T[sm][h];
-  n.Tn[1][0] = S.T[sc][h + MHK < MHP ? h + MHK : h];  // ring rows never use the off-tile side
-  n.Tn[1][1] = S.T[sc][h >= MHK ? h - MHK : h];
-  n.Tn[2][0] = S.T[sc][h + 1];
-  n.Tn[2][1] = S.T[sc][h - 1];
-  n.b[0] = S.b[bs][0][h];
-  n.b[1] = S.b[bs][1][h];
-  n.b[2] = S.b[bs][2][h];
-  n.c = S.c[bs][h];
+// Edge fluxes of one node in the oracle's order (aligned_E).  ONLY_A < 0:
+// all six; else only E_{ONLY_A, ONLY_S} (and only the differences it needs).
+//   Tn[x][0] = T(m + e_x), Tn[x][1] = T(m - e_x) (self if missing)
+//   rw: row tables of the node's (plane, theta row): iL2[6], wo01[4]
+template <int ONLY_A, int ONLY_S>
+__device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], const double (&bv)[3],
+                                       const double* rw, int rstride, const double (&il1)[6],
+                                       const double (&w2)[2], double (&E)[3][2]) {
+  double bil[3][2], p[3][2];
 #pragma unroll
-  for (int q = 0; q < 6; ++q) n.il[q >> 1][q & 1] = S.rowt[rs][q][hj] * col.il1[q];
+  for (int x = 0; x < 3; ++x) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) n.w01[q] = S.rowt[rs][6 + q][hj];
-  n.w2[0] = col.w2[0];
-  n.w2[1] = col.w2[1];
+    for (int t = 0; t < 2; ++t) {
+      const bool need_p = !(ONLY_A >= 0 && x == ONLY_A && t != ONLY_S);
+      const bool need_bil = need_p || (ONLY_A < 0) || (x == ONLY_A && t == ONLY_S);
+      if (need_bil) bil[x][t] = bv[x] * (rw[(2 * x + t) * rstride] * il1[2 * x + t]);
+      if (need_p) p[x][t] = bil[x][t] * (t == 0 ? (Tn[x][0] - Tv) : (Tv - Tn[x][1]));
+      else p[x][t] = 0.0;
+    }
+  }
+  double f[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int s0 = (q >> 2) & 1, s1 = (q >> 1) & 1, s2 = q & 1;
+    if (ONLY_A >= 0) {
+      const int sa = ONLY_A == 0 ? s0 : (ONLY_A == 1 ? s1 : s2);
+      if (sa != ONLY_S) { f[q] = 0.0; continue; }
+    }
+    const double sv = (p[0][s0] + p[1][s1]) + p[2][s2];
+    const double om = rw[(6 + s0 * 2 + s1) * rstride] * w2[s2];
+    f[q] = om * sv;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (ONLY_A >= 0 && (a != ONLY_A || s != ONLY_S)) { E[a][s] = 0.0; continue; }
+      double acc = 0.0;
+      bool first = true;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int sa = a == 0 ? (q >> 2) & 1 : (a == 1 ? (q >> 1) & 1 : q & 1);
+        if (sa != s) continue;
+        acc = first ? f[q] : acc + f[q];
+        first = false;
+      }
+      E[a][s] = bil[a][s] * acc;
+    }
+  }
 }
 
 // Epilogue contract (per tile node n of the thread):
-//   epi.prefetch(n, o)                 early in the step (operands of plane t-1)
-//   epi(n, g, i, j, k, o, F, uc, pin)   uc = input value at the node
-//   epi.finish(g)                       block reduction, if any
-template <class Val, class Epi>
-__global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp op, Val val, Epi epi, int R) {
+//   epi.prefetch(n, o)                    operands of the node, one plane ahead
+//   epi(n, g, i, j, k, o, F, uc, pin)     uc = input value at the node
+//   epi.finish(g)                         block reduction, if any
+template <class Epi>
+__global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp op, const double* __restrict__ Tin,
+                                                          Epi epi, int R, const int* skip) {
   extern __shared__ __align__(16) unsigned char march_smem[];
   MarchSmem& S = *reinterpret_cast<MarchSmem*>(march_smem);
-  if (val.skip()) return;
-  val.init();
+  if (skip && *skip) return;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * MTK + tx;
   const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * MTJ, i0 = blockIdx.z * R;
@@ -185,7 +171,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   const int kg = k0 + tx;
 
   // smem fill slots of this thread (tile + halo, wrapped / clamped in-plane)
-  int foff[NFILL];  // in-plane offsets (plane < 2^31 elements)
+  int foff[NFILL];
 #pragma unroll
   for (int q = 0; q < NFILL; ++q) {
     const int e = tid + q * MNT;
@@ -194,71 +180,56 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
     foff[q] = e < MHP ? jj * g.n2 + kk : -1;
   }
-  // row-table slot of this thread: tid < NROWT * MHJ
+  // row-table fill slot of this thread: tid < NROWT * MHJ
   const bool rton = tid < NROWT * MHJ;
   const int rtab = tid / MHJ, rhj = tid - (tid / MHJ) * MHJ;
   bool rok;
   const int rjj = map_j(g, j0 - 1 + rhj, rok);
-  const double* rbase = !rton ? nullptr : (rtab < 6 ? g.iL2[rtab] : (rtab < 10 ? g.wo01[rtab - 6] : g.iVal2));
+  const double* rbase = !rton ? g.iVal2 : (rtab < 6 ? g.iL2[rtab] : (rtab < 10 ? g.wo01[rtab - 6] : g.iVal2));
 
   bool oko;
   const int km = map_k(g, kg, oko);
   ColT col;
   load_col(g, km, col);
   const bool pin_k = (g.pin_lo2 && kg == 0) || (g.pin_hi2 && kg == g.n2 - 1);
+  if (tid < 18) {  // phi-ring column tables
+    const int side = tid / 9, q = tid % 9;
+    bool okr;
+    const int kr = map_k(g, side == 0 ? k0 - 1 : k0 + MTK, okr);
+    const double* src = q < 6 ? g.iL1[q] : (q < 8 ? g.wo2[q - 6] : g.iValg);
+    S.ringcol[side][q] = __ldg(src + kr);
+  }
 
-  // ring assignment: j-rings (tid < 2 MTK) and k-rings (next 2 MTJ threads)
-  int ra = -1, rs_ = 0, rhj_ = 0, rhk_ = 0;
+  // ring node of this thread: tid < NRING.  ra = axis of the one flux
+  // component it supplies, rs its side (0 '+', 1 '-').
+  int ra = -1, rs = 0, rhj_ = 0, rhk_ = 0;
   if (tid < 2 * MTK) {
     ra = 1;
-    rs_ = tid < MTK ? 0 : 1;
+    rs = tid < MTK ? 0 : 1;
     rhk_ = 1 + (tid % MTK);
-    rhj_ = rs_ == 0 ? 0 : MTJ + 1;
-  } else if (tid < 2 * MTK + 2 * MTJ) {
+    rhj_ = rs == 0 ? 0 : MTJ + 1;
+  } else if (tid < NRING) {
     const int q = tid - 2 * MTK;
     ra = 2;
-    rs_ = q < MTJ ? 0 : 1;
+    rs = q < MTJ ? 0 : 1;
     rhj_ = 1 + (q % MTJ);
-    rhk_ = rs_ == 0 ? 0 : MTK + 1;
+    rhk_ = rs == 0 ? 0 : MTK + 1;
   }
-  bool rjo = false, rko = false;
+  bool ring_on = false;
   if (ra >= 0) {
-    map_j(g, j0 - 1 + rhj_, rjo);
+    bool rjo, rko;
+    const int gj = j0 - 1 + rhj_, gk = k0 - 1 + rhk_;
+    map_j(g, gj, rjo);
+    map_k(g, gk, rko);
+    // the ring node must exist and be a neighbour of an inside tile node
+    ring_on = rjo && rko && (ra == 1 ? (gk < g.n2) : (gj < g.n1));
   }
-  const int rk = ra >= 0 ? map_k(g, k0 - 1 + rhk_, rko) : 0;
-  const bool ring_on = ra >= 0 && rjo && rko &&
-                       ((ra == 1) ? (k0 - 1 + rhk_ < g.n2) : (j0 - 1 + rhj_ < g.n1));
   const int rh = rhj_ * MHK + rhk_;
 
-  auto issue_T = [&](int slot, int p) {
-    const PlaneMap pm = plane_map(g, p);
-    const int64_t base = (int64_t)pm.mem * g.plane;
-#pragma unroll
-    for (int q = 0; q < NFILL; ++q)
-      if (foff[q] >= 0) val.stage(&S.T[slot][tid + q * MNT], base + foff[q], pm.mem);
-  };
-  auto issue_bc = [&](int slot, int p) {
-    const PlaneMap pm = plane_map(g, p);
-    const int64_t base = (int64_t)pm.mem * g.plane;
-#pragma unroll
-    for (int q = 0; q < NFILL; ++q)
-      if (foff[q] >= 0) {
-        const int e = tid + q * MNT;
-        const int64_t o = base + foff[q];
-        cp_async8(&S.b[slot][0][e], op.b[0] + o);
-        cp_async8(&S.b[slot][1][e], op.b[1] + o);
-        cp_async8(&S.b[slot][2][e], op.b[2] + o);
-        cp_async8(&S.c[slot][e], op.c + o);
-      }
-  };
-  auto issue_rows = [&](int slot, int p) {
-    if (rton) {
-      const PlaneMap pm = plane_map(g, p);
-      cp_async8(&S.rowt[slot][rtab][rhj], rbase + row2(g, pm.row, rjj));
-    }
-  };
-
   // own nodes
+  // (own_ok: the tile position maps to a node, possibly wrapped across a
+  // periodic seam -- its fluxes are published for the neighbours; inside: the
+  // node is this tile's to finalise)
   int jn[NPT], hn[NPT];
   bool inside[NPT], own_ok[NPT], pin_j[NPT];
 #pragma unroll
@@ -272,146 +243,180 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     pin_j[n] = (g.pin_lo1 && jn[n] == 0) || (g.pin_hi1 && jn[n] == g.n1 - 1);
   }
 
-  // ---- prologue: T(i0-1), T(i0), T(i0+1); b/c and rows of i0-1 and i0
-  issue_T(0, i0 - 1);
-  issue_T(1, i0);
-  issue_T(2, i0 + 1);
-  issue_bc((i0 - 1) & 1, i0 - 1);
-  issue_rows(2, i0 - 1);
-  issue_bc(i0 & 1, i0);
-  issue_rows(0, i0);
+  auto tslot = [&](int p) { return (p - i0 + 1) & (TSL - 1); };
+  auto bslot = [&](int p) { return (p - i0 + 1) % BSL; };
+  auto rslot = [&](int p) { return (p - i0 + 1) & (RSL - 1); };
+  auto issue_T = [&](int p) {
+    const PlaneMap pm = plane_map(g, p);
+    const double* base = Tin + (int64_t)pm.mem * g.plane;
+    double* dst = S.T[tslot(p)];
+#pragma unroll
+    for (int q = 0; q < NFILL; ++q)
+      if (foff[q] >= 0) cp_async8(dst + tid + q * MNT, base + foff[q]);
+  };
+  auto issue_B = [&](int p) {
+    const PlaneMap pm = plane_map(g, p);
+    const int64_t base = (int64_t)pm.mem * g.plane;
+    const int sl = bslot(p);
+#pragma unroll
+    for (int q = 0; q < NFILL; ++q)
+      if (foff[q] >= 0) {
+        const int e = tid + q * MNT;
+        const int64_t o = base + foff[q];
+        cp_async8(&S.B[sl][0][e], op.beta[0] + o);
+        cp_async8(&S.B[sl][1][e], op.beta[1] + o);
+        cp_async8(&S.B[sl][2][e], op.beta[2] + o);
+      }
+  };
+  auto issue_rows = [&](int p) {
+    if (rton) {
+      const PlaneMap pm = plane_map(g, p);
+      cp_async8(&S.rowt[rslot(p)][rtab][rhj], rbase + row2(g, pm.row, rjj));
+    }
+  };
+
+  // ---- prologue: group 1 = T(i0-1..i0+1), beta/rows(i0-1, i0); group 2 = the
+  // first in-flight plane set T(i0+2), beta/rows(i0+1)
+  issue_T(i0 - 1);
+  issue_T(i0);
+  if (i0 + 1 <= iend) issue_T(i0 + 1);
+  issue_B(i0 - 1);
+  issue_rows(i0 - 1);
+  issue_B(i0);
+  issue_rows(i0);
   cp_async_commit();
-  cp_async_wait_all();
+  if (i0 + 2 <= iend) issue_T(i0 + 2);
+  if (i0 + 1 <= iend) {
+    issue_B(i0 + 1);
+    issue_rows(i0 + 1);
+  }
+  cp_async_commit();
+  cp_async_wait<1>();
   __syncthreads();
-  double E0p[NPT];     // E_{0,+} at plane t-2 (relative to the finalised plane t-1)
-  double Eprev[NPT][3][2];
+
+  double Tm[NPT], Tc[NPT], qa[NPT], qb[NPT], ownp[NPT];
+  double Tmr = 0.0;
   {
     const PlaneMap pm = plane_map(g, i0 - 1);
+    const int s0 = tslot(i0 - 1), s1 = tslot(i0), bs = bslot(i0 - 1), rsl = rslot(i0 - 1);
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
-      E0p[n] = 0.0;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) Eprev[n][a][0] = Eprev[n][a][1] = 0.0;
-      if (pm.exists && inside[n]) {
-        NodeIn in;
-        gather(S, 0, 0, 1, (i0 - 1) & 1, 2, hn[n], ty + n * MTY + 1, col, in);
+      const int h = hn[n];
+      Tm[n] = S.T[s0][h];
+      Tc[n] = S.T[s1][h];
+      qa[n] = 0.0;
+      qb[n] = 0.0;
+      ownp[n] = 0.0;
+      if (pm.exists && inside[n]) {  // E_{0,+}(i0 - 1)
+        const double Tn[3][2] = {{Tc[n], Tm[n]}, {S.T[s0][h + MHK], S.T[s0][h - MHK]},
+                                 {S.T[s0][h + 1], S.T[s0][h - 1]}};
+        const double bv[3] = {S.B[bs][0][h], S.B[bs][1][h], S.B[bs][2][h]};
         double E[3][2];
-        node_E(in, 0, 0, E);
-        E0p[n] = E[0][0];
+        node_E<0, 0>(Tm[n], Tn, bv, &S.rowt[rsl][0][ty + n * MTY + 1], MHJ, col.il1, col.w2, E);
+        qb[n] = E[0][0];
       }
     }
+    if (ra >= 0) Tmr = S.T[s0][rh];
   }
-  __syncthreads();  // b/c slot of i0-1 and row slot 2 are refilled by step i0
 
-  int s_m = 0, s_c = 1, s_p = 2, s_n = 3;  // T slots of planes t-1, t, t+1, t+2
-  int r_c = 0, r_p = 2;                    // row-table slots of planes t, t-1
   for (int t = i0; t <= iend; ++t) {
-    const int bsl = t & 1;  // b/c slot of plane t
-    const int r_n = 3 - r_c - r_p;
-    // ---- async prefetch of the next planes (overlaps the compute below)
-    if (t + 2 <= iend) issue_T(s_n, t + 2);
-    if (t + 1 <= iend) {
-      issue_bc(bsl ^ 1, t + 1);
-      issue_rows(r_n, t + 1);
+    const bool last = (t == iend);
+    // ---- async prefetch (distance 2 planes for T, beta, rows)
+    if (t + 3 <= iend) issue_T(t + 3);
+    if (t + 2 <= iend) {
+      issue_B(t + 2);
+      issue_rows(t + 2);
     }
     cp_async_commit();
 
     const PlaneMap pm = plane_map(g, t);
-    const bool last = (t == iend);
+    const int sc = tslot(t), sp = tslot(t + 1), bs = bslot(t), rsl = rslot(t), rslm = rslot(t - 1);
     const int par = t & 1, pp = par ^ 1;
     const int tf = t - 1;
     const int ig = tf + g.i0g;
     const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
-      const int64_t of = off3(g, tf, jn[n], kg);
-      const bool fin = t > i0 && inside[n];
-      if (fin) epi.prefetch(n, of);
-      double Ec[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+      const int h = hn[n];
+      const int jr = ty + n * MTY + 1;
+      double E[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      double Tp = 0.0;
+      if (!last) Tp = S.T[sp][h];
       if (pm.exists && own_ok[n]) {
-        NodeIn in;
-        gather(S, s_m, s_c, s_p, bsl, r_c, hn[n], ty + n * MTY + 1, col, in);
-        node_E(in, last ? 0 : -1, 1, Ec);  // last plane: only E_{0,-} is consumed
+        const double Tn[3][2] = {{Tp, Tm[n]}, {S.T[sc][h + MHK], S.T[sc][h - MHK]},
+                                 {S.T[sc][h + 1], S.T[sc][h - 1]}};
+        const double bv[3] = {S.B[bs][0][h], S.B[bs][1][h], S.B[bs][2][h]};
+        if (!last) node_E<-1, 0>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
+        else node_E<0, 1>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
       }
       if (!last) {
-        S.E[par][0][hn[n]] = Ec[1][0];
-        S.E[par][1][hn[n]] = Ec[1][1];
-        S.E[par][2][hn[n]] = Ec[2][0];
-        S.E[par][3][hn[n]] = Ec[2][1];
+        S.E[par][0][h] = E[1][0];
+        S.E[par][1][h] = E[1][1];
+        S.E[par][2][h] = E[2][0];
+        S.E[par][3][h] = E[2][1];
       }
-      // ---- finalise plane t-1 of this node (its in-plane neighbours' fluxes
-      // were published before the previous barrier)
-      if (fin) {
-        const int h = hn[n];
-        const double E1pm = S.E[pp][0][h - MHK], E1mp = S.E[pp][1][h + MHK];
-        const double E2pm = S.E[pp][2][h - 1], E2mp = S.E[pp][3][h + 1];
-        double G = (E0p[n] - Eprev[n][0][0]) + (Eprev[n][0][1] - Ec[0][1]);
-        G = G + ((E1pm - Eprev[n][1][0]) + (Eprev[n][1][1] - E1mp));
-        G = G + ((E2pm - Eprev[n][2][0]) + (Eprev[n][2][1] - E2mp));
-        const double iv = S.rowt[r_p][10][ty + n * MTY + 1] * col.ivg;
+      // ---- finalise plane t-1 (in-plane neighbours' fluxes were published
+      // before the previous barrier)
+      if (t > i0 && inside[n]) {
+        const double nbr = (S.E[pp][0][h - MHK] - S.E[pp][1][h + MHK]) + (S.E[pp][2][h - 1] - S.E[pp][3][h + 1]);
+        const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
+        const double iv = S.rowt[rslm][10][jr] * col.ivg;
+        const int64_t of = off3(g, tf, jn[n], kg);
         double f = ((0.0 - G) * iv) * op.pref;
         if (op.rho) f = f / __ldg(op.rho + of);
         const bool pin = pin_i || pin_j[n] || pin_k;
         if (pin) f = 0.0;
-        epi(n, g, tf, jn[n], kg, of, f, S.T[s_m][h], pin);
+        epi(n, g, tf, jn[n], kg, of, f, Tm[n], pin);
       }
-      if (t > i0) E0p[n] = Eprev[n][0][0];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        Eprev[n][a][0] = Ec[a][0];
-        Eprev[n][a][1] = Ec[a][1];
-      }
+      if (!last && inside[n]) epi.prefetch(n, off3(g, t, jn[n], kg));
+      // ---- shift the per-node queues
+      ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
+      qa[n] = qb[n];
+      qb[n] = E[0][0];
+      Tm[n] = Tc[n];
+      Tc[n] = Tp;
     }
     // ---- halo ring of plane t: one flux component per ring node
     if (!last && ra >= 0) {
+      const double Tcr = S.T[sc][rh];
+      const double Tpr = S.T[sp][rh];
       double Ev = 0.0;
       if (ring_on && pm.exists) {
-        ColT rcol;
-        if (ra == 2) load_col(g, rk, rcol);
-        else rcol = col;
-        NodeIn in;
-        gather(S, s_m, s_c, s_p, bsl, r_c, rh, rhj_, rcol, in);
+        const double Tn[3][2] = {{Tpr, Tmr}, {S.T[sc][rh + MHK < MHP ? rh + MHK : rh], S.T[sc][rh >= MHK ? rh - MHK : rh]},
+                                 {S.T[sc][rh + 1], S.T[sc][rh - 1]}};
+        const double bv[3] = {S.B[bs][0][rh], S.B[bs][1][rh], S.B[bs][2][rh]};
         double E[3][2];
-        node_E(in, ra, rs_, E);
-        Ev = E[ra][rs_];
+        const double* rw = &S.rowt[rsl][0][rhj_];
+        if (ra == 1) {
+          if (rs == 0) {
+            node_E<1, 0>(Tcr, Tn, bv, rw, MHJ, col.il1, col.w2, E);
+            Ev = E[1][0];
+          } else {
+            node_E<1, 1>(Tcr, Tn, bv, rw, MHJ, col.il1, col.w2, E);
+            Ev = E[1][1];
+          }
+        } else {
+          const double* cs = S.ringcol[rs];
+          const double il1[6] = {cs[0], cs[1], cs[2], cs[3], cs[4], cs[5]};
+          const double w2[2] = {cs[6], cs[7]};
+          if (rs == 0) {
+            node_E<2, 0>(Tcr, Tn, bv, rw, MHJ, il1, w2, E);
+            Ev = E[2][0];
+          } else {
+            node_E<2, 1>(Tcr, Tn, bv, rw, MHJ, il1, w2, E);
+            Ev = E[2][1];
+          }
+        }
       }
-      S.E[par][(ra - 1) * 2 + rs_][rh] = Ev;
+      S.E[par][(ra - 1) * 2 + rs][rh] = Ev;
+      Tmr = Tcr;
     }
     if (last) break;
-    {
-      const int tmp = s_m;
-      s_m = s_c;
-      s_c = s_p;
-      s_p = s_n;
-      s_n = tmp;
-      r_p = r_c;
-      r_c = r_n;
-    }
-    cp_async_wait_all();
+    cp_async_wait<1>();
     __syncthreads();
   }
   epi.finish(g);
 }
-
-// PCG K7 value provider: p = z + beta p_old, z = r / (a + dt dg), with beta
-// read from the device-side PCG state (set by the previous K8)
-struct PValDev {
-  const double* r;
-  const double* pold;
-  const double* dg;
-  const double* adiag;
-  double dt;
-  const PcgDev* st;
-  double beta;
-  __device__ __forceinline__ bool skip() const { return st->done != 0; }  // solve finished
-  __device__ __forceinline__ void init() { beta = st->beta; }
-  __device__ __forceinline__ void stage(double* dst, int64_t o, int) const { *dst = (*this)(0, o, 0, 0, 0); }
-  __device__ __forceinline__ double operator()(int, int64_t o, int, int, int) const {
-    double dvec = (adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o);
-    double z = __ldg(r + o) / dvec;
-    return z + beta * __ldg(pold + o);
-  }
-};
 
 // ---- epilogues ----------------------------------------------------------
 struct EpiStore {  // F = op(u)
@@ -448,6 +453,38 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   __device__ __forceinline__ void finish(const GridDev&) {}
 };
 
+__device__ __forceinline__ ArgMax block_argmax2d(ArgMax a, double* shv, long long* shi) {
+  a = warp_argmax(a);
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int lane = tid & 31, w = tid >> 5;
+  if (lane == 0) {
+    shv[w] = a.v;
+    shi[w] = a.i;
+  }
+  __syncthreads();
+  ArgMax r{-1.0, 0x7fffffffffffffffLL};
+  if (w == 0) {
+    if (lane < MNT / 32) {
+      r.v = shv[lane];
+      r.i = shi[lane];
+    }
+    r = warp_argmax(r);
+  }
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ bool last_block3(unsigned int* counter, int nblk) {
+  __shared__ bool amLast;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    amLast = (t == (unsigned)nblk - 1);
+  }
+  __syncthreads();
+  return amLast;
+}
+
 struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
   double* F;
   double* pv;
@@ -466,7 +503,7 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
     __shared__ long long shi[MNT / 32];
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblk = gridDim.x * gridDim.y * gridDim.z;
-    ArgMax b = block_argmax2(best, shv, shi);
+    ArgMax b = block_argmax2d(best, shv, shi);
     if (threadIdx.x == 0 && threadIdx.y == 0) {
       pv[bid] = b.v;
       pi[bid] = b.i;
@@ -475,7 +512,7 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
       ArgMax r{-1.0, 0x7fffffffffffffffLL};
       const int tid = threadIdx.y * blockDim.x + threadIdx.x;
       for (int q = tid; q < nblk; q += MNT) r = am_better(r, ArgMax{pv[q], pi[q]});
-      r = block_argmax2(r, shv, shi);
+      r = block_argmax2d(r, shv, shi);
       if (tid == 0) {
         res->fmax = r.v;
         res->kidx = r.i;
@@ -483,42 +520,10 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
       }
     }
   }
-
-  __device__ static ArgMax block_argmax2(ArgMax a, double* shv, long long* shi) {
-    a = warp_argmax(a);
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-    const int lane = tid & 31, w = tid >> 5;
-    if (lane == 0) {
-      shv[w] = a.v;
-      shi[w] = a.i;
-    }
-    __syncthreads();
-    ArgMax r{-1.0, 0x7fffffffffffffffLL};
-    if (w == 0) {
-      if (lane < MNT / 32) {
-        r.v = shv[lane];
-        r.i = shi[lane];
-      }
-      r = warp_argmax(r);
-    }
-    __syncthreads();
-    return r;
-  }
-  __device__ static bool last_block3(unsigned int* counter, int nblk) {
-    __shared__ bool amLast;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0 && threadIdx.y == 0) {
-      unsigned int t = atomicAdd(counter, 1u);
-      amLast = (t == (unsigned)nblk - 1);
-    }
-    __syncthreads();
-    return amLast;
-  }
 };
 
-struct EpiMatvec {  // PCG K7: p_new = (loaded value), Ap = a p - dt F(p); (W p, Ap)
-  double* pnew;
+// PCG K7: Ap = a p - dt F(p) for the staged p; partial (W p, Ap) -> alpha
+struct EpiMatvec {
   double* Ap;
   const double* adiag;
   double dt;
@@ -531,7 +536,6 @@ struct EpiMatvec {  // PCG K7: p_new = (loaded value), Ap = a p - dt F(p); (W p,
   __device__ __forceinline__ void operator()(int, const GridDev& g, int i, int j, int k, int64_t o, double f,
                                              double pv, bool) {
     const double ap = (adiag ? __ldg(adiag + o) * pv : pv) - dt * f;
-    pnew[o] = pv;
     Ap[o] = ap;
     acc += (op.weight(g, i, j, k) * pv) * ap;
   }
@@ -549,21 +553,11 @@ struct EpiMatvec {  // PCG K7: p_new = (loaded value), Ap = a p - dt F(p); (W p,
       for (int q = 0; q < MNT / 32; ++q) s += sh[q];
       p1[bid] = s;
     }
-    if (EpiArgmax::last_block3(counter, nblk)) {
+    if (last_block3(counter, nblk)) {
       if (tid == 0) {
         double a = 0.0;
         for (int q = 0; q < nblk; ++q) a += p1[q];
-        st->pAp = a;
-        if (st->rz != 0.0) {
-          if (!(a > 0.0)) {
-            st->status = isnan(a) ? 3 : 2;
-            st->done = 1;
-          } else {
-            st->alpha = st->rz / a;
-          }
-        } else {
-          st->alpha = 0.0;
-        }
+        pcg_alpha(st, a);
         *counter = 0u;
       }
     }

@@ -150,9 +150,10 @@ struct ScalarOp {
 };
 
 // ------------------------------------------------------------------ aligned
+// beta = sqrt(c) b (frozen per outer step, oracle aligned_beta): the operator
+// streams three nodal arrays and never touches c or b.
 struct AlignedOp {
-  const double* b[3];
-  const double* c;    // nodal conductivity (frozen)
+  const double* beta[3];
   const double* rho;  // nullptr -> 1
   double pref;
   int ncomp;  // always 1
@@ -160,72 +161,31 @@ struct AlignedOp {
   __device__ __forceinline__ double iL(const GridDev& g, int a, int s, int i, int j, int k) const {
     return __ldg(g.iL2[a * 2 + s] + row2(g, i, j)) * __ldg(g.iL1[a * 2 + s] + k);
   }
-  __device__ __forceinline__ double om(const GridDev& g, double cv, int s0, int s1, int s2, int i, int j,
-                                       int k) const {
-    return (cv * __ldg(g.wo01[s0 * 2 + s1] + row2(g, i, j))) * __ldg(g.wo2[s2] + k);
+  __device__ __forceinline__ double om(const GridDev& g, int s0, int s1, int s2, int i, int j, int k) const {
+    return __ldg(g.wo01[s0 * 2 + s1] + row2(g, i, j)) * __ldg(g.wo2[s2] + k);
   }
 
-  // E_{a,s} at node (i,j,k); s: 0 = '+', 1 = '-'.  Only the one-sided
-  // differences the component needs are formed (halo depth 1 suffices).
+  // E_{a,s} at node (i,j,k) (oracle aligned_E); only the one-sided
+  // differences the component needs are formed.  all: every component.
   template <class Val>
-  __device__ __forceinline__ double Ecomp(const GridDev& g, const Val& val, int a, int s, int i, int j,
-                                          int k) const {
+  __device__ __forceinline__ void Enode(const GridDev& g, const Val& val, int i, int j, int k, int only_a,
+                                        int only_s, double E[3][2]) const {
     const int64_t o = off3(g, i, j, k);
     const double Tv = val(0, o, i, j, k);
-    const double bv[3] = {__ldg(b[0] + o), __ldg(b[1] + o), __ldg(b[2] + o)};
-    const double cv = __ldg(c + o);
+    const double bv[3] = {__ldg(beta[0] + o), __ldg(beta[1] + o), __ldg(beta[2] + o)};
     const int co[3] = {i, j, k};
-    double p[3][2];
+    double p[3][2], bil[3][2];
 #pragma unroll
     for (int x = 0; x < 3; ++x) {
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        if (x == a && t != s) { p[x][t] = 0.0; continue; }
+        bil[x][t] = bv[x] * iL(g, x, t, i, j, k);
+        if (only_a >= 0 && x == only_a && t != only_s) { p[x][t] = 0.0; continue; }
         bool ok;
         int nx = nbax(g, x, co[x], t == 0 ? 1 : -1, ok);
         int ni = x == 0 ? nx : i, nj = x == 1 ? nx : j, nk = x == 2 ? nx : k;
         double Tn = ok ? val(0, off3(g, ni, nj, nk), ni, nj, nk) : Tv;
-        double il = iL(g, x, t, i, j, k);
-        double d = t == 0 ? (Tn - Tv) * il : (Tv - Tn) * il;
-        p[x][t] = bv[x] * d;
-      }
-    }
-    double acc = 0.0;
-    bool first = true;
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      const int s0 = (n >> 2) & 1, s1 = (n >> 1) & 1, s2 = n & 1;
-      const int sa = a == 0 ? s0 : (a == 1 ? s1 : s2);
-      if (sa != s) continue;
-      double sv = (p[0][s0] + p[1][s1]) + p[2][s2];
-      double f = om(g, cv, s0, s1, s2, i, j, k) * sv;
-      acc = first ? f : acc + f;
-      first = false;
-    }
-    return (bv[a] * iL(g, a, s, i, j, k)) * acc;
-  }
-
-  // all six E_{a,s} at the centre node
-  template <class Val>
-  __device__ __forceinline__ void Eall(const GridDev& g, const Val& val, int i, int j, int k,
-                                       double E[3][2]) const {
-    const int64_t o = off3(g, i, j, k);
-    const double Tv = val(0, o, i, j, k);
-    const double bv[3] = {__ldg(b[0] + o), __ldg(b[1] + o), __ldg(b[2] + o)};
-    const double cv = __ldg(c + o);
-    const int co[3] = {i, j, k};
-    double p[3][2];
-#pragma unroll
-    for (int x = 0; x < 3; ++x) {
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        bool ok;
-        int nx = nbax(g, x, co[x], t == 0 ? 1 : -1, ok);
-        int ni = x == 0 ? nx : i, nj = x == 1 ? nx : j, nk = x == 2 ? nx : k;
-        double Tn = ok ? val(0, off3(g, ni, nj, nk), ni, nj, nk) : Tv;
-        double il = iL(g, x, t, i, j, k);
-        double d = t == 0 ? (Tn - Tv) * il : (Tv - Tn) * il;
-        p[x][t] = bv[x] * d;
+        p[x][t] = bil[x][t] * (t == 0 ? (Tn - Tv) : (Tv - Tn));
       }
     }
     double f[8];
@@ -233,12 +193,13 @@ struct AlignedOp {
     for (int n = 0; n < 8; ++n) {
       const int s0 = (n >> 2) & 1, s1 = (n >> 1) & 1, s2 = n & 1;
       double sv = (p[0][s0] + p[1][s1]) + p[2][s2];
-      f[n] = om(g, cv, s0, s1, s2, i, j, k) * sv;
+      f[n] = om(g, s0, s1, s2, i, j, k) * sv;
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
+        if (only_a >= 0 && (a != only_a || s != only_s)) { E[a][s] = 0.0; continue; }
         double acc = 0.0;
         bool first = true;
 #pragma unroll
@@ -248,29 +209,37 @@ struct AlignedOp {
           acc = first ? f[n] : acc + f[n];
           first = false;
         }
-        E[a][s] = (bv[a] * iL(g, a, s, i, j, k)) * acc;
+        E[a][s] = bil[a][s] * acc;
       }
     }
   }
+  template <class Val>
+  __device__ __forceinline__ double Ecomp(const GridDev& g, const Val& val, int a, int s, int i, int j,
+                                          int k) const {
+    double E[3][2];
+    Enode(g, val, i, j, k, a, s, E);
+    return E[a][s];
+  }
 
+  // G in the marching order of oracle aligned_apply
   template <class Val>
   __device__ __forceinline__ void F(const GridDev& g, const Val& val, int i, int j, int k,
                                     double* out) const {
     double E[3][2];
-    Eall(g, val, i, j, k, E);
+    Enode(g, val, i, j, k, -1, 0, E);
     const int co[3] = {i, j, k};
-    double G = 0.0;
+    double Em[3], Ep[3];  // E_{a,+}(m - e_a), E_{a,-}(m + e_a)
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       bool okm, okp;
       int xm = nbax(g, a, co[a], -1, okm);
       int xp = nbax(g, a, co[a], 1, okp);
-      double Em = 0.0, Ep = 0.0;
-      if (okm) Em = Ecomp(g, val, a, 0, a == 0 ? xm : i, a == 1 ? xm : j, a == 2 ? xm : k);
-      if (okp) Ep = Ecomp(g, val, a, 1, a == 0 ? xp : i, a == 1 ? xp : j, a == 2 ? xp : k);
-      double term = (Em - E[a][0]) + (E[a][1] - Ep);
-      G = a == 0 ? term : G + term;
+      Em[a] = okm ? Ecomp(g, val, a, 0, a == 0 ? xm : i, a == 1 ? xm : j, a == 2 ? xm : k) : 0.0;
+      Ep[a] = okp ? Ecomp(g, val, a, 1, a == 0 ? xp : i, a == 1 ? xp : j, a == 2 ? xp : k) : 0.0;
     }
+    const double own = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
+    const double nbr = (Em[1] - Ep[1]) + (Em[2] - Ep[2]);
+    const double G = (Em[0] - Ep[0]) + (own + nbr);
     const int64_t o = off3(g, i, j, k);
     const double iv = __ldg(g.iVal2 + row2(g, i, j)) * __ldg(g.iValg + k);
     double f = ((0.0 - G) * iv) * pref;
@@ -280,7 +249,7 @@ struct AlignedOp {
 
   // Hessian rows of the quadratic form (oracle aligned_hessian_rows) -> bound, diag
   __device__ __forceinline__ double q(const GridDev& g, int a, int s, int i, int j, int k, int64_t o) const {
-    return ((s == 0 ? 1.0 : -1.0) * __ldg(b[a] + o)) * iL(g, a, s, i, j, k);
+    return (s == 0 ? 1.0 : -1.0) * (__ldg(beta[a] + o) * iL(g, a, s, i, j, k));
   }
   static __device__ __forceinline__ int face_idx(int a, int d) { return 1 + 2 * a + (d > 0 ? 1 : 0); }
   static __device__ __forceinline__ int diag_idx(int a, int da, int bb, int db) {
@@ -296,14 +265,13 @@ struct AlignedOp {
 #pragma unroll
     for (int n = 0; n < 19; ++n) H[n] = 0.0;
     const int64_t o = off3(g, i, j, k);
-    const double cm = __ldg(c + o);
     // (A) apex tets
     for (int n = 0; n < 8; ++n) {
       const int sg[3] = {(n >> 2) & 1, (n >> 1) & 1, n & 1};
       double qa[3];
       for (int x = 0; x < 3; ++x) qa[x] = q(g, x, sg[x], i, j, k, o);
       double qs = (qa[0] + qa[1]) + qa[2];
-      double w = om(g, cm, sg[0], sg[1], sg[2], i, j, k);
+      double w = om(g, sg[0], sg[1], sg[2], i, j, k) * 1.0;
       H[0] += (w * qs) * qs;
       for (int x = 0; x < 3; ++x) H[face_idx(x, sg[x] == 0 ? 1 : -1)] += (w * (0.0 - qs)) * qa[x];
     }
@@ -317,13 +285,12 @@ struct AlignedOp {
         if (!ok) continue;
         const int vi = a == 0 ? xv : i, vj = a == 1 ? xv : j, vk = a == 2 ? xv : k;
         const int64_t ov = off3(g, vi, vj, vk);
-        const double cv = __ldg(c + ov);
         for (int n = 0; n < 8; ++n) {
           const int sg[3] = {(n >> 2) & 1, (n >> 1) & 1, n & 1};
           if (sg[a] != sa) continue;
           double qv[3];
           for (int x = 0; x < 3; ++x) qv[x] = q(g, x, sg[x], vi, vj, vk, ov);
-          double wv = om(g, cv, sg[0], sg[1], sg[2], vi, vj, vk);
+          double wv = om(g, sg[0], sg[1], sg[2], vi, vj, vk) * 1.0;
           double qs = (qv[0] + qv[1]) + qv[2];
           double qa = qv[a];
           H[0] += (wv * qa) * qa;
