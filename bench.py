@@ -45,8 +45,8 @@ sys.path.insert(0, ROOT)
 
 # algorithmic bytes per cell-update of the fused stage / PCG iteration
 BYTES = {
-    ("aligned", "rkl2"): 72,   # reads u_{k-1}, u_{k-2}, u0, y0, c, b(3); writes u_k
-    ("aligned", "be"): 128,    # K7: r, p, d, c, b(3) -> p, Ap;  K8: x, r, p, Ap, d -> x, r
+    ("aligned", "rkl2"): 64,   # reads u_{k-1}, beta(3), u_{k-2}, u0, y0; writes u_k
+    ("aligned", "be"): 128,    # Kp: r, p_old, d -> p; K7: p, beta(3) -> Ap; K8: x, r, p, Ap, d -> x, r
     ("scalar", "rkl2"): 40,    # reads u_{k-1}, u_{k-2}, u0, y0; writes u_k
     ("scalar", "be"): 96,      # K7: r, p, d -> p, Ap;  K8: x, r, p, Ap, d -> x, r
     ("vector", "rkl2"): 120,   # 3 components x 40
@@ -267,9 +267,10 @@ def run_ours(args, rank, world, local_rank):
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": {"aligned": "k_stage<AlignedOp>", "scalar": "k_stage<ScalarOp>",
+                "kernel": {"aligned": "k_aligned_march<EpiStage>", "scalar": "k_stage<ScalarOp>",
                            "vector": "k_stage<ScalarOp> (3 comp)"}[opkind] if kind == "rkl2"
-                else "k_pcg_matvec + k_pcg_update",
+                else ("k_pcg_pupdate + k_aligned_march<EpiMatvec> + k_pcg_update" if opkind == "aligned"
+                      else "k_pcg_matvec + k_pcg_update"),
                 "achieved": achieved,
                 "peak": peak,
                 "unit": "GB/s",

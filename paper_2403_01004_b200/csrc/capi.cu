@@ -127,6 +127,14 @@ static int grid_blocks(pc_ctx* c, int64_t n) {
   return (int)std::min<int64_t>(b, c->max_blocks);
 }
 
+// blocks for the row-iterating node kernels (PC_FOR_NODES: one warp per row)
+static int node_blocks(pc_ctx* c, const GridDev& g) {
+  int64_t rows = (int64_t)g.n0 * g.n1;
+  int64_t b = (rows + kThreads / 32 - 1) / (kThreads / 32);
+  if (b < 1) b = 1;
+  return (int)std::min<int64_t>(b, c->max_blocks);
+}
+
 static double* pool_get(pc_ctx* c, size_t elems) {
   for (size_t q = 0; q < c->pool.size(); ++q) {
     if (c->pool[q].first == elems) {
@@ -636,7 +644,7 @@ template <class Op>
 static int run_bound(pc_op* op, const Op& o) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
-  int nb = grid_blocks(c, g->g.N);
+  int nb = node_blocks(c, g->g);
   k_bound<<<nb, kThreads, 0, c->s>>>(g->g, o, op->dbuf + g->g.plane, c->red_v, c->counter, c->maxout);
   c->st.launches++;
   TRY(check_launch("k_bound"));
@@ -663,7 +671,7 @@ int pc_op_freeze(pc_op* op, const pc_field* T0) {
     CFld bsrc{{op->bsrc[0], op->bsrc[1], op->bsrc[2]}};
     Fld beta{{const_cast<double*>(op->ao.beta[0]), const_cast<double*>(op->ao.beta[1]),
               const_cast<double*>(op->ao.beta[2])}};
-    k_aligned_beta<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, T0->base(0), op->kfc + 1, op->Tfloor,
+    k_aligned_beta<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, T0->base(0), op->kfc + 1, op->Tfloor,
                                                                    bsrc, beta, c->bad);
     c->st.launches++;
     TRY(check_launch("k_aligned_beta"));
@@ -730,7 +738,7 @@ template <class Op>
 static int launch_apply(pc_op* op, const Op& o, CFld u, Fld F, bool argmax) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
-  int nb = grid_blocks(c, g->g.N);
+  int nb = node_blocks(c, g->g);
   if (argmax) {
     k_apply_argmax<<<nb, kThreads, 0, c->s>>>(g->g, o, u, F, c->red_v, c->red_i, c->counter, c->res);
   } else {
@@ -771,7 +779,7 @@ static int ptl_device(pc_grid* g, int ncomp, CFld u, CFld F, double eps_rel, int
   pc_ctx* c = g->ctx;
   if (check_all) {
     CUDA_TRY(cudaMemsetAsync(c->minbits, 0x7f, sizeof(unsigned long long), c->s));  // huge positive
-    k_ptl_all<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, ncomp, u, F, eps_rel, c->res, c->minbits);
+    k_ptl_all<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, ncomp, u, F, eps_rel, c->res, c->minbits);
     c->st.launches++;
     TRY(check_launch("k_ptl_all"));
   } else {
@@ -812,7 +820,7 @@ int pc_ptl(pc_grid* g, const pc_field* u, const pc_field* F, double eps_rel, int
   if (!(eps_rel > 0.0)) return fail(PC_E_INVALID, "eps_rel must be > 0");
   pc_ctx* c = g->ctx;
   if (c->nranks > 1) return fail(PC_E_INVALID, "pc_ptl is single-rank; use pc_cycle");
-  k_argmax<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, u->ncomp, cfld(F), c->red_v, c->red_i,
+  k_argmax<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, u->ncomp, cfld(F), c->red_v, c->red_i,
                                                           c->counter, c->res);
   c->st.launches++;
   TRY(check_launch("k_argmax"));
@@ -902,7 +910,7 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     work_put(A);
     return rc;
   }
-  const int nb = grid_blocks(c, g->g.N);
+  const int nb = node_blocks(c, g->g);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
   k_stage1<<<nb, kThreads, 0, c->s>>>(g->g, nc, cfld(u), y0.cf(), A.f(), tab[3], c->bad);
@@ -998,7 +1006,7 @@ int pc_step_euler(pc_op* op, pc_field* u, double dt) {
   if (rc == PC_OK) rc = apply_any(op, cfld(u), y0.f(), false);
   if (rc == PC_OK) {
     CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
-    k_stage1<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, op->ncomp, cfld(u), y0.cf(), A.f(), dt, c->bad);
+    k_stage1<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ncomp, cfld(u), y0.cf(), A.f(), dt, c->bad);
     c->st.launches++;
     rc = check_launch("k_stage1");
   }
@@ -1024,7 +1032,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   TRY(work_get(g, nc, p1));
   TRY(work_get(g, nc, Ap));
   const double* dg = op->dbuf + g->g.plane;
-  const int nb = grid_blocks(c, g->g.N);
+  const int nb = node_blocks(c, g->g);
   int rc = halo_field(x);
   if (rc == PC_OK) {
     k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, c->red_v, c->red_v2,
@@ -1209,7 +1217,7 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
       rc = work_get(g, op->ncomp, A);
       if (rc) break;
       CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
-      k_stage1<<<grid_blocks(c, g->g.N), kThreads, 0, c->s>>>(g->g, op->ncomp, cfld(u), y0.cf(), A.f(), dt, c->bad);
+      k_stage1<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ncomp, cfld(u), y0.cf(), A.f(), dt, c->bad);
       c->st.launches++;
       rc = check_launch("k_stage1");
       if (rc == PC_OK) swap_storage(u, A);

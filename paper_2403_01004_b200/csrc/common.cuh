@@ -64,6 +64,13 @@ __device__ __forceinline__ void unflatten(const GridDev& g, int64_t c, int& i, i
   i = (int)(t / g.n1);
 }
 
+// Node iteration of the generic kernels: each warp takes one (i, j) row and
+// its lanes stride along phi (coalesced, no 64-bit division per node).
+#define PC_FOR_NODES(g, i, j, k)                                                                   \
+  for (int row_ = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), i = 0, j = 0;              \
+       row_ < (g).n0 * (g).n1; row_ += gridDim.x * (blockDim.x >> 5))                             \
+    for (int k = ((i = row_ / (g).n1), (j = row_ - i * (g).n1), (int)(threadIdx.x & 31)); k < (g).n2; k += 32)
+
 __device__ __forceinline__ bool pinned(const GridDev& g, int i, int j, int k) {
   int ig = i + g.i0g;
   return (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1) ||

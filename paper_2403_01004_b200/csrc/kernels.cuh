@@ -35,9 +35,7 @@ __device__ __forceinline__ long long aos_index(const GridDev& g, int i, int j, i
 template <class Op>
 __global__ void __launch_bounds__(kThreads) k_apply(GridDev g, Op op, CFld u, Fld F) {
   PlainVal val{{u.p[0], u.p[1], u.p[2]}};
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     double out[3];
     op.F(g, val, i, j, k, out);
     const int64_t o = off3(g, i, j, k);
@@ -53,9 +51,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_argmax(GridDev g, Op op, CFl
   __shared__ long long shi[kThreads / 32];
   PlainVal val{{u.p[0], u.p[1], u.p[2]}};
   ArgMax best{-1.0, 0x7fffffffffffffffLL};
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     double out[3];
     op.F(g, val, i, j, k, out);
     const int64_t o = off3(g, i, j, k);
@@ -88,9 +84,7 @@ __global__ void __launch_bounds__(kThreads) k_argmax(GridDev g, int ncomp, CFld 
   __shared__ double shv[kThreads / 32];
   __shared__ long long shi[kThreads / 32];
   ArgMax best{-1.0, 0x7fffffffffffffffLL};
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     const int64_t o = off3(g, i, j, k);
     for (int q = 0; q < ncomp; ++q) best = am_better(best, ArgMax{fabs(F.p[q][o]), aos_index(g, i, j, k, q, ncomp)});
   }
@@ -113,9 +107,7 @@ __global__ void __launch_bounds__(kThreads) k_argmax(GridDev g, int ncomp, CFld 
 
 __global__ void __launch_bounds__(kThreads) k_stage1(GridDev g, int ncomp, CFld u0, CFld y0, Fld out,
                                                      double mtdt, int* bad) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     const int64_t o = off3(g, i, j, k);
     const bool pin = pinned(g, i, j, k);
     for (int q = 0; q < ncomp; ++q) {
@@ -135,9 +127,7 @@ template <class Op>
 __global__ void __launch_bounds__(kThreads) k_stage(GridDev g, Op op, CFld um1, CFld um2, CFld u0, CFld y0,
                                                     Fld out, StageCoef sc, int stage, int* bad) {
   PlainVal val{{um1.p[0], um1.p[1], um1.p[2]}};
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     double Fk[3];
     op.F(g, val, i, j, k, Fk);
     const int64_t o = off3(g, i, j, k);
@@ -193,9 +183,7 @@ __global__ void __launch_bounds__(kThreads) k_ptl_all(GridDev g, int ncomp, CFld
                                                       const ArgRes* res, unsigned long long* minbits) {
   const double thr = eps_rel * res->fmax;
   double best = INFINITY;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     const int64_t o = off3(g, i, j, k);
     const int co[3] = {i, j, k};
     for (int a = 0; a < 3; ++a) {
@@ -220,9 +208,7 @@ __global__ void __launch_bounds__(kThreads) k_bound(GridDev g, Op op, double* di
                                                     unsigned int* counter, double* out_max) {
   __shared__ double sh[kThreads / 32];
   double m = 0.0;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     double lam[3], dg;
     op.bound(g, i, j, k, lam, dg);
     for (int q = 0; q < op.ncomp; ++q) m = fmax(m, lam[q]);
@@ -245,9 +231,7 @@ __global__ void __launch_bounds__(kThreads) k_bound(GridDev g, Op op, double* di
 // (oracle aligned_coefficient + aligned_beta); bad if T0 <= 0
 __global__ void __launch_bounds__(kThreads) k_aligned_beta(GridDev g, const double* T0, const double* kfc,
                                                            double Tfloor, CFld b, Fld beta, int* bad) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < g.N; q += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, q, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     const int64_t o = off3(g, i, j, k);
     double t = T0[o];
     if (!(t > 0.0)) atomicMin(bad, 1);
@@ -296,9 +280,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const doubl
                                                           double dt, const PcgDev* st) {
   if (st->done) return;
   const double beta = st->beta;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     const int64_t o = off3(g, i, j, k);
     const double dvec = (adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o);
     const double z = __ldg(r + o) / dvec;
@@ -329,9 +311,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b,
   __shared__ double sh[kThreads / 32];
   PlainVal val{{x.p[0], x.p[1], x.p[2]}};
   double s1 = 0.0, s2 = 0.0;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     double Fx[3];
     op.F(g, val, i, j, k, Fx);
     const int64_t o = off3(g, i, j, k);
@@ -381,9 +361,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld 
   if (st->done) return;
   PVal val{{r.p[0], r.p[1], r.p[2]}, {pold.p[0], pold.p[1], pold.p[2]}, dg, adiag, dt, st->beta};
   double s1 = 0.0;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     double Fp[3];
     op.F(g, val, i, j, k, Fp);
     const int64_t o = off3(g, i, j, k);
@@ -418,9 +396,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(GridDev g, Op op, Fld x
   if (st->done) return;
   const double alpha = st->alpha;
   double s1 = 0.0, s2 = 0.0;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.N; c += (int64_t)gridDim.x * blockDim.x) {
-    int i, j, k;
-    unflatten(g, c, i, j, k);
+  PC_FOR_NODES(g, i, j, k) {
     const int64_t o = off3(g, i, j, k);
     const double W = op.weight(g, i, j, k);
     const double dvec = (adiag ? adiag[o] : 1.0) + dt * dg[o];

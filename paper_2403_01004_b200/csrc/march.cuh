@@ -24,6 +24,8 @@
 // Arithmetic is the oracle's expression by expression (compiled with
 // -fmad=false), only the schedule differs: results are bitwise identical.
 #pragma once
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace pc {
@@ -88,6 +90,16 @@ struct MarchSmem {
   double rowt[RSL][NROWT][MHJ];
   double ringcol[2][9];         // column tables of the phi-ring columns k0-1, k0+MTK
 };
+
+// Re-define a loop-invariant register through an ALU move: its consumers in
+// the plane loop then carry no scoreboard dependency on the global load that
+// produced it (which ptxas would otherwise re-wait on every iteration, sharing
+// the scoreboard with the in-flight epilogue prefetches).
+__device__ __forceinline__ double launder(double x) {
+  double y;
+  asm volatile("mov.b64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
 
 // per-column constants (depend on k only)
 struct ColT {
@@ -191,6 +203,11 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   const int km = map_k(g, kg, oko);
   ColT col;
   load_col(g, km, col);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) col.il1[q] = launder(col.il1[q]);
+  col.w2[0] = launder(col.w2[0]);
+  col.w2[1] = launder(col.w2[1]);
+  col.ivg = launder(col.ivg);
   const bool pin_k = (g.pin_lo2 && kg == 0) || (g.pin_hi2 && kg == g.n2 - 1);
   if (tid < 18) {  // phi-ring column tables
     const int side = tid / 9, q = tid % 9;
@@ -230,17 +247,19 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   // (own_ok: the tile position maps to a node, possibly wrapped across a
   // periodic seam -- its fluxes are published for the neighbours; inside: the
   // node is this tile's to finalise)
-  int jn[NPT], hn[NPT];
+  const int h0 = (ty + 1) * MHK + (tx + 1);
+  const int onode0 = (j0 + ty) * g.n2 + kg;
   bool inside[NPT], own_ok[NPT], pin_j[NPT];
+  auto hn = [&](int n) { return h0 + n * MTY * MHK; };
+  auto jn = [&](int n) { return j0 + ty + n * MTY; };
+  auto onode = [&](int n) { return onode0 + n * MTY * g.n2; };
 #pragma unroll
   for (int n = 0; n < NPT; ++n) {
-    jn[n] = j0 + ty + n * MTY;
-    hn[n] = (ty + n * MTY + 1) * MHK + (tx + 1);
-    inside[n] = jn[n] < g.n1 && kg < g.n2;
+    inside[n] = jn(n) < g.n1 && kg < g.n2;
     bool ojo;
-    map_j(g, jn[n], ojo);
+    map_j(g, jn(n), ojo);
     own_ok[n] = ojo && oko;
-    pin_j[n] = (g.pin_lo1 && jn[n] == 0) || (g.pin_hi1 && jn[n] == g.n1 - 1);
+    pin_j[n] = (g.pin_lo1 && jn(n) == 0) || (g.pin_hi1 && jn(n) == g.n1 - 1);
   }
 
   auto tslot = [&](int p) { return (p - i0 + 1) & (TSL - 1); };
@@ -301,7 +320,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     const int s0 = tslot(i0 - 1), s1 = tslot(i0), bs = bslot(i0 - 1), rsl = rslot(i0 - 1);
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
-      const int h = hn[n];
+      const int h = hn(n);
       Tm[n] = S.T[s0][h];
       Tc[n] = S.T[s1][h];
       qa[n] = 0.0;
@@ -319,37 +338,42 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     if (ra >= 0) Tmr = S.T[s0][rh];
   }
 
-  for (int t = i0; t <= iend; ++t) {
-    const bool last = (t == iend);
+  // plane loop: planes i0 .. iend-1 compute all fluxes and finalise the
+  // previous plane; the peeled last step (t = iend) only forms E_{0,-} and
+  // finalises iend-1.
+  auto step = [&](int t, auto last_tag) {
+    constexpr bool LAST = decltype(last_tag)::value;
     // ---- async prefetch (distance 2 planes for T, beta, rows)
-    if (t + 3 <= iend) issue_T(t + 3);
-    if (t + 2 <= iend) {
-      issue_B(t + 2);
-      issue_rows(t + 2);
+    if (!LAST) {
+      if (t + 3 <= iend) issue_T(t + 3);
+      if (t + 2 <= iend) {
+        issue_B(t + 2);
+        issue_rows(t + 2);
+      }
+      cp_async_commit();
     }
-    cp_async_commit();
-
-    const PlaneMap pm = plane_map(g, t);
+    const bool exists = LAST ? plane_map(g, t).exists : true;  // t < n0 inside the loop
     const int sc = tslot(t), sp = tslot(t + 1), bs = bslot(t), rsl = rslot(t), rslm = rslot(t - 1);
     const int par = t & 1, pp = par ^ 1;
     const int tf = t - 1;
     const int ig = tf + g.i0g;
     const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
+    const int64_t pbase = (int64_t)t * g.plane;
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
-      const int h = hn[n];
+      const int h = hn(n);
       const int jr = ty + n * MTY + 1;
       double E[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
       double Tp = 0.0;
-      if (!last) Tp = S.T[sp][h];
-      if (pm.exists && own_ok[n]) {
+      if (!LAST) Tp = S.T[sp][h];
+      if (exists && own_ok[n]) {
         const double Tn[3][2] = {{Tp, Tm[n]}, {S.T[sc][h + MHK], S.T[sc][h - MHK]},
                                  {S.T[sc][h + 1], S.T[sc][h - 1]}};
         const double bv[3] = {S.B[bs][0][h], S.B[bs][1][h], S.B[bs][2][h]};
-        if (!last) node_E<-1, 0>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
+        if (!LAST) node_E<-1, 0>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
         else node_E<0, 1>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
       }
-      if (!last) {
+      if (!LAST) {
         S.E[par][0][h] = E[1][0];
         S.E[par][1][h] = E[1][1];
         S.E[par][2][h] = E[2][0];
@@ -361,27 +385,29 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
         const double nbr = (S.E[pp][0][h - MHK] - S.E[pp][1][h + MHK]) + (S.E[pp][2][h - 1] - S.E[pp][3][h + 1]);
         const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
         const double iv = S.rowt[rslm][10][jr] * col.ivg;
-        const int64_t of = off3(g, tf, jn[n], kg);
+        const int64_t of = pbase - g.plane + onode(n);
         double f = ((0.0 - G) * iv) * op.pref;
         if (op.rho) f = f / __ldg(op.rho + of);
         const bool pin = pin_i || pin_j[n] || pin_k;
         if (pin) f = 0.0;
-        epi(n, g, tf, jn[n], kg, of, f, Tm[n], pin);
+        epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin);
       }
-      if (!last && inside[n]) epi.prefetch(n, off3(g, t, jn[n], kg));
-      // ---- shift the per-node queues
-      ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
-      qa[n] = qb[n];
-      qb[n] = E[0][0];
-      Tm[n] = Tc[n];
-      Tc[n] = Tp;
+      if (!LAST) {
+        if (inside[n]) epi.prefetch(n, pbase + onode(n));
+        // ---- shift the per-node queues
+        ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
+        qa[n] = qb[n];
+        qb[n] = E[0][0];
+        Tm[n] = Tc[n];
+        Tc[n] = Tp;
+      }
     }
     // ---- halo ring of plane t: one flux component per ring node
-    if (!last && ra >= 0) {
+    if (!LAST && ra >= 0) {
       const double Tcr = S.T[sc][rh];
       const double Tpr = S.T[sp][rh];
       double Ev = 0.0;
-      if (ring_on && pm.exists) {
+      if (ring_on) {
         const double Tn[3][2] = {{Tpr, Tmr}, {S.T[sc][rh + MHK < MHP ? rh + MHK : rh], S.T[sc][rh >= MHK ? rh - MHK : rh]},
                                  {S.T[sc][rh + 1], S.T[sc][rh - 1]}};
         const double bv[3] = {S.B[bs][0][rh], S.B[bs][1][rh], S.B[bs][2][rh]};
@@ -411,10 +437,14 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
       S.E[par][(ra - 1) * 2 + rs][rh] = Ev;
       Tmr = Tcr;
     }
-    if (last) break;
-    cp_async_wait<1>();
-    __syncthreads();
-  }
+    if (!LAST) {
+      cp_async_wait<1>();
+      __syncthreads();
+    }
+  };
+#pragma unroll 1
+  for (int t = i0; t < iend; ++t) step(t, std::false_type{});
+  step(iend, std::true_type{});
   epi.finish(g);
 }
 
