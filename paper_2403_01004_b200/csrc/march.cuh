@@ -40,9 +40,11 @@ constexpr int MHP = MHJ * MHK;
 constexpr int MNT = MTY * MTK;   // threads per block
 constexpr int NFILL = (MHP + MNT - 1) / MNT;
 constexpr int NROWT = 11;        // per-(row, j) tables: iL2[6], wo01[4], iVal2
-constexpr int TSL = 4;           // T slots: t-1 (free), t, t+1, t+2/t+3 in flight
-constexpr int BSL = 3;           // beta slots: t, t+1, t+2 in flight
-constexpr int RSL = 4;           // row-table slots: t-1 (iv), t, t+1, t+2
+constexpr int TSL = 3;           // T slots: t, t+1, t+2 in flight
+constexpr int BSL = 2;           // beta slots: t, t+1 in flight
+constexpr int RSL = 3;           // row-table slots: t-1 (iv), t, t+1 in flight
+constexpr int NEO = 3;           // epilogue operand arrays staged per node (max)
+constexpr int MTN = MTJ * MTK;   // tile nodes
 constexpr int NRING = 2 * MTK + 2 * MTJ;
 
 struct PlaneMap {
@@ -83,10 +85,20 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// in-plane flux exchange of one plane (compact: only the entries readers use)
+//   e1p[(j - (j0-1))][k - k0]   E_{1,+},  e1m[(j - j0)][k - k0]       E_{1,-}
+//   e2p[j - j0][(k - (k0-1))]   E_{2,+},  e2m[j - j0][(k - k0)]       E_{2,-}
+struct FluxX {
+  double e1p[MTJ + 1][MTK];
+  double e1m[MTJ + 1][MTK];
+  double e2p[MTJ][MTK + 1];
+  double e2m[MTJ][MTK + 1];
+};
 struct MarchSmem {
   double T[TSL][MHP];
   double B[BSL][3][MHP];
-  double E[2][4][MHP];          // E_{1,+}, E_{1,-}, E_{2,+}, E_{2,-} per plane parity
+  FluxX E[2];                   // per plane parity
+  double EO[2][NEO][MTN];       // epilogue operands of planes t-1 (read), t (landing)
   double rowt[RSL][NROWT][MHJ];
   double ringcol[2][9];         // column tables of the phi-ring columns k0-1, k0+MTK
 };
@@ -167,9 +179,11 @@ __device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], cons
 }
 
 // Epilogue contract (per tile node n of the thread):
-//   epi.prefetch(n, o)                    operands of the node, one plane ahead
-//   epi(n, g, i, j, k, o, F, uc, pin)     uc = input value at the node
-//   epi.finish(g)                         block reduction, if any
+//   Epi::NOPS, epi.opnd(q)                 nodal operand arrays the kernel stages
+//                                          through cp.async one plane ahead
+//   epi(n, g, i, j, k, o, F, uc, pin, ov)  uc = input value at the node,
+//                                          ov[q] = staged operands
+//   epi.finish(g)                          block reduction, if any
 template <class Epi>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp op, const double* __restrict__ Tin,
                                                           Epi epi, int R, const int* skip) {
@@ -262,9 +276,10 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     pin_j[n] = (g.pin_lo1 && jn(n) == 0) || (g.pin_hi1 && jn(n) == g.n1 - 1);
   }
 
-  auto tslot = [&](int p) { return (p - i0 + 1) & (TSL - 1); };
-  auto bslot = [&](int p) { return (p - i0 + 1) % BSL; };
-  auto rslot = [&](int p) { return (p - i0 + 1) & (RSL - 1); };
+  auto tslot = [&](int p) { return (p - i0 + 1) % TSL; };
+  auto bslot = [&](int p) { return (p - i0 + 1) & (BSL - 1); };
+  auto rslot = [&](int p) { return (p - i0 + 1) % RSL; };
+  auto eslot = [&](int p) { return (p - i0) & 1; };
   auto issue_T = [&](int p) {
     const PlaneMap pm = plane_map(g, p);
     const double* base = Tin + (int64_t)pm.mem * g.plane;
@@ -293,9 +308,21 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
       cp_async8(&S.rowt[rslot(p)][rtab][rhj], rbase + row2(g, pm.row, rjj));
     }
   };
+  auto issue_ops = [&](int p) {  // epilogue operands of the own (inside) nodes of plane p
+    if (Epi::NOPS > 0) {
+      const int64_t base = (int64_t)p * g.plane;
+      const int es = eslot(p);
+#pragma unroll
+      for (int n = 0; n < NPT; ++n)
+        if (inside[n]) {
+#pragma unroll
+          for (int q = 0; q < Epi::NOPS; ++q)
+            cp_async8(&S.EO[es][q][tid + n * MNT], epi.opnd(q) + base + onode(n));
+        }
+    }
+  };
 
-  // ---- prologue: group 1 = T(i0-1..i0+1), beta/rows(i0-1, i0); group 2 = the
-  // first in-flight plane set T(i0+2), beta/rows(i0+1)
+  // ---- prologue: T(i0-1..i0+1), beta/rows(i0-1, i0) in one group
   issue_T(i0 - 1);
   issue_T(i0);
   if (i0 + 1 <= iend) issue_T(i0 + 1);
@@ -304,13 +331,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   issue_B(i0);
   issue_rows(i0);
   cp_async_commit();
-  if (i0 + 2 <= iend) issue_T(i0 + 2);
-  if (i0 + 1 <= iend) {
-    issue_B(i0 + 1);
-    issue_rows(i0 + 1);
-  }
-  cp_async_commit();
-  cp_async_wait<1>();
+  cp_async_wait<0>();
   __syncthreads();
 
   double Tm[NPT], Tc[NPT], qa[NPT], qb[NPT], ownp[NPT];
@@ -343,18 +364,20 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   // finalises iend-1.
   auto step = [&](int t, auto last_tag) {
     constexpr bool LAST = decltype(last_tag)::value;
-    // ---- async prefetch (distance 2 planes for T, beta, rows)
+    // ---- async prefetch, one group per plane (lands before this plane's barrier):
+    // T(t+2), beta/rows(t+1), epilogue operands of plane t
     if (!LAST) {
-      if (t + 3 <= iend) issue_T(t + 3);
-      if (t + 2 <= iend) {
-        issue_B(t + 2);
-        issue_rows(t + 2);
-      }
+      if (t + 2 <= iend) issue_T(t + 2);
+      issue_B(t + 1);
+      issue_rows(t + 1);
+      issue_ops(t);
       cp_async_commit();
     }
     const bool exists = LAST ? plane_map(g, t).exists : true;  // t < n0 inside the loop
     const int sc = tslot(t), sp = tslot(t + 1), bs = bslot(t), rsl = rslot(t), rslm = rslot(t - 1);
     const int par = t & 1, pp = par ^ 1;
+    const int esm = eslot(t - 1);
+    const int r0 = ty, c0 = tx;  // tile coordinates of node 0
     const int tf = t - 1;
     const int ig = tf + g.i0g;
     const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
@@ -373,16 +396,17 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
         if (!LAST) node_E<-1, 0>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
         else node_E<0, 1>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
       }
+      const int r = r0 + n * MTY;
       if (!LAST) {
-        S.E[par][0][h] = E[1][0];
-        S.E[par][1][h] = E[1][1];
-        S.E[par][2][h] = E[2][0];
-        S.E[par][3][h] = E[2][1];
+        S.E[par].e1p[r + 1][c0] = E[1][0];
+        S.E[par].e1m[r][c0] = E[1][1];
+        S.E[par].e2p[r][c0 + 1] = E[2][0];
+        S.E[par].e2m[r][c0] = E[2][1];
       }
       // ---- finalise plane t-1 (in-plane neighbours' fluxes were published
       // before the previous barrier)
       if (t > i0 && inside[n]) {
-        const double nbr = (S.E[pp][0][h - MHK] - S.E[pp][1][h + MHK]) + (S.E[pp][2][h - 1] - S.E[pp][3][h + 1]);
+        const double nbr = (S.E[pp].e1p[r][c0] - S.E[pp].e1m[r + 1][c0]) + (S.E[pp].e2p[r][c0] - S.E[pp].e2m[r][c0 + 1]);
         const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
         const double iv = S.rowt[rslm][10][jr] * col.ivg;
         const int64_t of = pbase - g.plane + onode(n);
@@ -390,10 +414,12 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
         if (op.rho) f = f / __ldg(op.rho + of);
         const bool pin = pin_i || pin_j[n] || pin_k;
         if (pin) f = 0.0;
-        epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin);
+        double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
+#pragma unroll
+        for (int q = 0; q < Epi::NOPS; ++q) ov[q] = S.EO[esm][q][tid + n * MNT];
+        epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov);
       }
       if (!LAST) {
-        if (inside[n]) epi.prefetch(n, pbase + onode(n));
         // ---- shift the per-node queues
         ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
         qa[n] = qb[n];
@@ -434,11 +460,17 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
           }
         }
       }
-      S.E[par][(ra - 1) * 2 + rs][rh] = Ev;
+      if (ra == 1) {
+        if (rs == 0) S.E[par].e1p[0][rhk_ - 1] = Ev;
+        else S.E[par].e1m[MTJ][rhk_ - 1] = Ev;
+      } else {
+        if (rs == 0) S.E[par].e2p[rhj_ - 1][0] = Ev;
+        else S.E[par].e2m[rhj_ - 1][MTK] = Ev;
+      }
       Tmr = Tcr;
     }
     if (!LAST) {
-      cp_async_wait<1>();
+      cp_async_wait<0>();
       __syncthreads();
     }
   };
@@ -450,15 +482,18 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
 
 // ---- epilogues ----------------------------------------------------------
 struct EpiStore {  // F = op(u)
+  static constexpr int NOPS = 0;
   double* F;
-  __device__ __forceinline__ void prefetch(int, int64_t) {}
-  __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double, bool) {
+  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double, bool,
+                                             const double*) {
     F[o] = f;
   }
   __device__ __forceinline__ void finish(const GridDev&) {}
 };
 
 struct EpiStage {  // fused RKL2/RKG2 stage
+  static constexpr int NOPS = 3;
   const double* um2;
   const double* u0;
   const double* y0;
@@ -466,16 +501,11 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   StageCoef sc;
   int stage;
   int* bad;
-  double pa0[NPT], pm2[NPT], py0[NPT];
-  __device__ __forceinline__ void prefetch(int n, int64_t o) {
-    pa0[n] = __ldg(u0 + o);
-    pm2[n] = __ldg(um2 + o);
-    py0[n] = __ldg(y0 + o);
-  }
-  __device__ __forceinline__ void operator()(int n, const GridDev&, int, int, int, int64_t o, double f, double um1,
-                                             bool pin) {
-    const double a0 = pa0[n];
-    double v = ((((sc.mu * um1) + (sc.nu * pm2[n])) + (sc.kap * a0)) + (sc.mtdt * f)) + (sc.gtdt * py0[n]);
+  __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? u0 : (q == 1 ? um2 : y0); }
+  __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double um1,
+                                             bool pin, const double* ov) {
+    const double a0 = ov[0];
+    double v = ((((sc.mu * um1) + (sc.nu * ov[1])) + (sc.kap * a0)) + (sc.mtdt * f)) + (sc.gtdt * ov[2]);
     v = pin ? a0 : v;
     out[o] = v;
     if (!isfinite(v)) atomicMin(bad, stage);
@@ -516,15 +546,16 @@ __device__ __forceinline__ bool last_block3(unsigned int* counter, int nblk) {
 }
 
 struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
+  static constexpr int NOPS = 0;
+  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   double* F;
   double* pv;
   long long* pi;
   unsigned int* counter;
   ArgRes* res;
   ArgMax best;
-  __device__ __forceinline__ void prefetch(int, int64_t) {}
   __device__ __forceinline__ void operator()(int, const GridDev& g, int i, int j, int k, int64_t o, double f, double,
-                                             bool) {
+                                             bool, const double*) {
     F[o] = f;
     best = am_better(best, ArgMax{fabs(f), aos_index(g, i, j, k, 0, 1)});
   }
@@ -554,6 +585,8 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
 
 // PCG K7: Ap = a p - dt F(p) for the staged p; partial (W p, Ap) -> alpha
 struct EpiMatvec {
+  static constexpr int NOPS = 0;
+  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   double* Ap;
   const double* adiag;
   double dt;
@@ -562,9 +595,8 @@ struct EpiMatvec {
   PcgDev* st;
   AlignedOp op;
   double acc;
-  __device__ __forceinline__ void prefetch(int, int64_t) {}
   __device__ __forceinline__ void operator()(int, const GridDev& g, int i, int j, int k, int64_t o, double f,
-                                             double pv, bool) {
+                                             double pv, bool, const double*) {
     const double ap = (adiag ? __ldg(adiag + o) * pv : pv) - dt * f;
     Ap[o] = ap;
     acc += (op.weight(g, i, j, k) * pv) * ap;
