@@ -46,10 +46,12 @@ sys.path.insert(0, ROOT)
 # algorithmic bytes per cell-update of the fused stage / PCG iteration
 BYTES = {
     ("aligned", "rkl2"): 64,   # reads u_{k-1}, beta(3), u_{k-2}, u0, y0; writes u_k
+    ("aligned_rho", "rkl2"): 72,   # + rho
     ("aligned", "be"): 128,    # Kp: r, p_old, d -> p; K7: p, beta(3) -> Ap; K8: x, r, p, Ap, d -> x, r
     ("scalar", "rkl2"): 40,    # reads u_{k-1}, u_{k-2}, u0, y0; writes u_k
     ("scalar", "be"): 96,      # K7: r, p, d -> p, Ap;  K8: x, r, p, Ap, d -> x, r
     ("vector", "rkl2"): 120,   # 3 components x 40
+    ("vector_rho", "rkl2"): 128,   # + rho (D = nu rho formed per node)
 }
 
 CONFIG_MODEL = {
@@ -57,7 +59,10 @@ CONFIG_MODEL = {
     "c2": "C2 vector viscosity 128x128x256x3 spherical, dt=2000 dtE",
     "c3": "C3 Spitzer conduction 256x256x512 spherical, dt=1e4 dtE",
     "c4": "C4 Spitzer conduction 512x512x1024 spherical, BE+PCG tol 1e-9, dt=1e4 dtE",
+    "c5": "C5 coupled Spitzer conduction + vector viscosity (rho field) 768x768x1536 spherical, "
+          "one split MAS step of 5e4 dtE",
 }
+DEFAULT_CONFIG = "c5"
 
 
 def _peaks():
@@ -127,24 +132,6 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- workloads
 
-def build_workload(name, dg_ctx=None, small=None):
-    from paper_2403_01004_b200 import configs
-    fn = {"c1": configs.c1, "c2": configs.c2, "c3": configs.c3, "c4": configs.c4}[name]
-    return fn() if small is None else fn(n=small)
-
-
-def make_operator(w, name):
-    from paper_2403_01004_b200 import operators
-    if name in ("c3", "c4"):
-        cfg = operators.AlignedConductionConfig(b_hat=w.fields["b"], m_p=3.0, k_B=1.0, bc=w.bc)
-        return operators.DiffusionOperator.aligned(cfg), "T", "aligned", 1
-    if name == "c2":
-        cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc, vector_metric=True)
-        return operators.DiffusionOperator.scalar(cfg, 3), "v", "vector", 3
-    cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc)
-    return operators.DiffusionOperator.scalar(cfg, 1), "u", "scalar", 1
-
-
 def scheme_for(name, args):
     from paper_2403_01004_b200 import schemes
     if args.scheme:
@@ -155,10 +142,101 @@ def scheme_for(name, args):
     return schemes.SchemeConfig(kind, tol=tol, max_iter=100000)
 
 
+class Problem:
+    """The device-resident state of one config: fields, operators and the
+    (name, op, kind) list split_advance cycles over.  Inputs of C3-C5 are
+    generated in HBM by the library (configs.gen_*, bit-identical to the host
+    recipes); C1/C2 are uploaded from the host recipe."""
+
+    def __init__(self, name, ctx, n=None):
+        from paper_2403_01004_b200 import configs, device, operators
+        self.name = name
+        kw = {} if n is None else {"n": n}
+        if name in ("c3", "c4", "c5"):
+            w = getattr(configs, name)(host=False, **kw)
+        else:
+            w = getattr(configs, name)(**kw)
+        self.w = w
+        dg = device.device_grid(w.grid, w.bc, ctx)
+        self.dg = dg
+        self.fields = {}
+        self.ops = []  # (state name, DiffusionOperator, ncomp, bytes key)
+        if name in ("c3", "c4", "c5"):
+            b = configs.gen_dipole(device.DeviceField(dg, 3), w.grid, w.seed)
+            rho = configs.gen_radial(device.DeviceField(dg, 1), w.meta["rho_r"]) if name == "c5" else None
+            self.fields["T"] = device.DeviceField(dg, 1)
+            cfg = operators.AlignedConductionConfig(b_hat=b, rho=rho, m_p=3.0, k_B=1.0, bc=w.bc)
+            self.ops.append(("T", operators.DiffusionOperator.aligned(cfg), 1, "aligned_rho" if rho else "aligned"))
+            self.b, self.rho = b, rho
+            if name == "c5":
+                self.fields["v"] = device.DeviceField(dg, 3)
+                vcfg = operators.ScalarDiffusionConfig(nu=1.0, rho=rho, bc=w.bc, vector_metric=True)
+                self.ops.append(("v", operators.DiffusionOperator.scalar(vcfg, 3), 3, "vector_rho"))
+        elif name == "c2":
+            self.v0 = device.DeviceField.from_values(dg, w.fields["v"])
+            self.fields["v"] = device.DeviceField(dg, 3)
+            cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc, vector_metric=True)
+            self.ops.append(("v", operators.DiffusionOperator.scalar(cfg, 3), 3, "vector"))
+        else:
+            self.u0 = device.DeviceField.from_values(dg, w.fields["u"][..., None])
+            self.fields["u"] = device.DeviceField(dg, 1)
+            cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc)
+            self.ops.append(("u", operators.DiffusionOperator.scalar(cfg, 1), 1, "scalar"))
+        self.reset()
+        dts = []
+        for fname, op, nc, _ in self.ops:
+            if op.kind == "aligned":
+                op.freeze(self.fields[fname])
+            dts.append(op.device_op(w.grid, nc, ctx).dt_euler)
+        self.dtE = min(dts)
+        self.outer_dt = w.ratio * self.dtE
+
+    def reset(self):
+        """Back to the seeded initial state (device generation / device copy)."""
+        from paper_2403_01004_b200 import configs
+        w = self.w
+        if "T" in self.fields:
+            configs.gen_temperature(self.fields["T"], w.grid, w.seed)
+        if self.name == "c5":
+            configs.gen_harmonic(self.fields["v"], w.grid, w.seed)
+        elif self.name == "c2":
+            self.fields["v"].copy_from(self.v0)
+        elif self.name == "c1":
+            self.fields["u"].copy_from(self.u0)
+
+    def step(self, sc, pcfg):
+        from paper_2403_01004_b200 import ptl
+        self.reset()
+        st, reps = ptl.split_advance([(f, op) for f, op, _, _ in self.ops], self.fields, self.outer_dt,
+                                     [(sc, pcfg)] * len(self.ops))
+        return reps
+
+    def host_inputs(self):
+        """Pinned-host copies of every input of a step (for the e2e leg)."""
+        out = {}
+        for k, f in list(self.fields.items()) + [("b", getattr(self, "b", None)), ("rho", getattr(self, "rho", None))]:
+            if f is None:
+                continue
+            out[k] = np.ascontiguousarray(f.download())
+        if self.name in ("c1", "c2"):  # the initial state (fields may have been advanced)
+            out[self.ops[0][0]] = np.ascontiguousarray((self.u0 if self.name == "c1" else self.v0).download())
+        elif "T" in self.fields:
+            self.reset()
+            out["T"] = np.ascontiguousarray(self.fields["T"].download())
+            if self.name == "c5":
+                out["v"] = np.ascontiguousarray(self.fields["v"].download())
+        return out
+
+    def free(self):
+        for f in ("fields", "ops", "b", "rho", "u0", "v0"):
+            if hasattr(self, f):
+                delattr(self, f)
+
+
 # ---------------------------------------------------------------- our arm
 
 def run_ours(args, rank, world, local_rank):
-    from paper_2403_01004_b200 import device, ptl, mesh
+    from paper_2403_01004_b200 import device, ptl
 
     uid = None
     dist = None
@@ -172,30 +250,14 @@ def run_ours(args, rank, world, local_rank):
     ctx = device.Context(local_rank, world, rank, uid)
     device.set_default_context(ctx)
     name = args.config
-    w = build_workload(name)
-    op, fname, opkind, ncomp = make_operator(w, name)
+    t_setup = time.perf_counter()
+    prob = Problem(name, ctx, None if args.n is None else tuple(int(x) for x in args.n.split(",")))
     sc = scheme_for(name, args)
-    init = w.fields[fname]
-    init4 = init if init.ndim == 4 else init[..., None]
-    dop = op.device_op(w.grid, ncomp, ctx)
-    dg = dop.dgrid
-    u0 = device.DeviceField.from_values(dg, init4)
-    u = device.DeviceField(dg, ncomp)
-    if op.kind == "aligned":
-        op.freeze(u0)
-    dtE0 = dop.dt_euler
-    outer_dt = w.ratio * dtE0
     pcfg = ptl.PtlConfig()
-
-    def step():
-        u.copy_from(u0)
-        if op.kind == "aligned":
-            dop.freeze(u)
-        _, rep = ptl.cycle_operator(op, sc, u, outer_dt, pcfg)
-        return rep
+    setup_s = time.perf_counter() - t_setup
 
     for _ in range(args.warmup):
-        rep = step()
+        prob.step(sc, pcfg)
     if dist:
         dist.barrier()
     ctx.sync()
@@ -204,39 +266,54 @@ def run_ours(args, rank, world, local_rank):
     clk = ClockSampler(local_rank)
     clk.start()
     ctx.mark(0)
-    total_iters = 0
+    total_cu = 0
     reps = []
     for _ in range(args.steps):
-        rep = step()
-        reps.append(rep)
-        total_iters += rep.total_iters
+        rr = prob.step(sc, pcfg)
+        reps.append(rr)
+        for (fname, op, nc, bkey), rep in zip(prob.ops, rr):
+            total_cu += prob.dg.ncells * rep.total_iters
     ctx.mark(1)
     ms = ctx.elapsed_ms(0, 1)
     clocks = clk.stop()
     st = ctx.stats()
+    kinds = ctx.stats_by_kind()
     ctx.enable_timing(False)
     if dist:
         import torch
         t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    cells_global = int(np.prod(dg.global_shape))
-    value = cells_global * total_iters / (ms / 1e3)
+        t = torch.tensor([total_cu], dtype=torch.float64)
+        dist.all_reduce(t)
+        total_cu = int(t.item())
+    value = total_cu / (ms / 1e3)
     kind = "be" if sc.kind == "backward_euler" else "rkl2"
-    bpc = BYTES[(opkind, kind)]
-    n_stage_cells = dg.ncells * (sum(max(e.iters - 1, 0) for r in reps for e in r.entries) if kind == "rkl2"
-                                 else total_iters)
-    achieved = bpc * n_stage_cells / (st["stage_ms"] / 1e3) / 1e9 if st["stage_ms"] > 0 else None
+    # roofline: the hot loop with the largest device time, its algorithmic bytes
+    rows = []
+    for fname, op, nc, bkey in prob.ops:
+        kk = ("pcg_" if kind == "be" else "sts_") + ("aligned" if op.kind == "aligned" else "scalar")
+        d = kinds[kk]
+        if d["ms"] > 0:
+            bpc = BYTES[(bkey, kind)]
+            rows.append({"kernel": {"sts_aligned": "k_aligned_march<EpiStage>",
+                                    "sts_scalar": "k_stage<ScalarOp>" + (" (3 comp)" if nc == 3 else ""),
+                                    "pcg_aligned": "k_pcg_pupdate + k_aligned_march<EpiMatvec> + k_pcg_update",
+                                    "pcg_scalar": "k_pcg_matvec + k_pcg_update"}[kk],
+                         "ms": d["ms"], "bytes_per_cell_update": bpc,
+                         "achieved": bpc * d["cell_updates"] / (d["ms"] / 1e3) / 1e9,
+                         "launches": d["launches"], "field": fname})
+    dom = max(rows, key=lambda r: r["ms"]) if rows else None
     peak, peak_src = _peaks()
 
-    # e2e: the public API with host buffers (rank 0 only at N=1; all ranks otherwise)
     e2e = None
     if args.e2e:
-        e2e = run_e2e(args, w, name, op, fname, ncomp, init4, outer_dt, sc, pcfg, ctx, dist)
+        e2e = run_e2e(args, prob, sc, pcfg, ctx, dist)
 
     line = None
     if rank == 0:
         rep0 = reps[-1]
+        cells_global = int(np.prod(prob.dg.global_shape))
         line = {
             "metric": "cell-updates/sec per full parabolic step (fp64)",
             "value": value,
@@ -249,87 +326,99 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (seeded recipe, configs.py; no public dataset exists)",
+            "data": "synthetic (seeded recipes, configs.py; generated in HBM bit-identically to the host recipe; "
+                    "no public dataset exists)",
             "config": {
                 "workload": CONFIG_MODEL[name],
                 "config": name.upper(),
-                "grid": list(dg.global_shape) + ([3] if ncomp == 3 else []),
+                "grid": list(prob.dg.global_shape),
                 "cells": cells_global,
+                "fields": {f: nc for f, _, nc, _ in prob.ops},
                 "scheme": sc.kind + "+PTL",
-                "outer_dt_over_dtE": w.ratio,
-                "cycles_per_step": rep0.n_cycles,
-                "cell_updates_per_step": cells_global * rep0.total_iters,
-                "stages_or_iters_per_step": rep0.total_iters,
+                "outer_dt_over_dtE": prob.w.ratio,
+                "operators": [{"field": f, "kind": op.kind, "cycles": r.n_cycles,
+                               "stages_or_iters": r.total_iters} for (f, op, _, _), r in zip(prob.ops, rep0)],
+                "cell_updates_per_step": total_cu // max(args.steps, 1),
                 "decomposition": f"r-slabs x{world}" if world > 1 else "single GPU",
                 "l2": "inputs larger than L2 (each field %.0f MB > 126 MB)" % (cells_global * 8 / 1e6)
                 if cells_global * 8 > 126e6 else "fields L2-resident (smaller than 126 MB)",
                 "parallelism": f"slab{world}",
+                "setup_s": round(setup_s, 2),
             },
-            "roofline": {
+            "roofline": None if dom is None else {
                 "bound": "hbm",
-                "kernel": {"aligned": "k_aligned_march<EpiStage>", "scalar": "k_stage<ScalarOp>",
-                           "vector": "k_stage<ScalarOp> (3 comp)"}[opkind] if kind == "rkl2"
-                else ("k_pcg_pupdate + k_aligned_march<EpiMatvec> + k_pcg_update" if opkind == "aligned"
-                      else "k_pcg_matvec + k_pcg_update"),
-                "achieved": achieved,
+                "kernel": dom["kernel"],
+                "achieved": dom["achieved"],
                 "peak": peak,
                 "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None,
-                "traffic": _traffic(name, kind),
-                "bytes_per_cell_update": bpc,
+                "frac": dom["achieved"] / peak,
+                "traffic": _traffic(name, kind, dom["field"]),
+                "bytes_per_cell_update": dom["bytes_per_cell_update"],
                 "peak_source": peak_src,
-                "kernel_ms_share": st["stage_ms"] / ms if ms > 0 else None,
+                "kernel_ms_share": dom["ms"] / ms if ms > 0 else None,
+                "all_hot_loops": [{k: v for k, v in r.items() if k != "field"} for r in rows],
             },
             "gpu_launches": st["launches"],
             "clocks": clocks,
         }
         if e2e is not None:
             line["e2e"] = e2e
-        if args.cpu_baseline and world >= 1:
+        if args.cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(name, args.cpu_sample_s)
     if dist:
         dist.barrier()
+    prob.free()
     ctx.close()
     return line
 
 
-def _traffic(name, kind):
-    """DRAM bytes per cell-update of the stage kernel from the committed ncu
+def _traffic(name, kind, field):
+    """DRAM bytes per cell-update of the dominant kernel from the committed ncu
     capture (profiles/ncu_summary.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d.get(f"{name}_{kind}", {}).get("dram_bytes_per_launch")
+        return d.get(f"{name}_{kind}_{field}", {}).get("dram_bytes_per_cell_update")
     except Exception:
         return None
 
 
-def run_e2e(args, w, name, op, fname, ncomp, init4, outer_dt, sc, pcfg, ctx, dist):
-    """The same metric through ptl.split_advance on host Fields (H2D / D2H inside)."""
+def run_e2e(args, prob, sc, pcfg, ctx, dist):
+    """The same metric through ptl.split_advance on HOST Fields: every step
+    uploads its inputs (state fields, b-hat, rho) from pinned host memory and
+    downloads the advanced fields; the device-resident problem is freed first."""
     from paper_2403_01004_b200 import mesh, operators, ptl
 
-    host_in = np.ascontiguousarray(init4)
-    ctx.pin(host_in)
-    b_host = None
-    if op.kind == "aligned":
-        b_host = np.ascontiguousarray(w.fields["b"])
-        ctx.pin(b_host)
-    h2d = host_in.nbytes + (b_host.nbytes if b_host is not None else 0)
-    d2h = host_in.nbytes
-    iters = 0
+    host = prob.host_inputs()
+    w, name = prob.w, prob.name
+    ops_desc = [(f, op.kind, nc) for f, op, nc, _ in prob.ops]
+    outer_dt = prob.outer_dt
+    prob.free()
+    for a in host.values():
+        ctx.pin(a)
+    state_names = [f for f, _, _ in ops_desc]
+    h2d = sum(host[k].nbytes for k in host)
+    d2h = sum(host[k].nbytes for k in state_names)
+    cells = int(np.prod(w.grid.shape))
+    cu = 0
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        if op.kind == "aligned":
-            cfg = operators.AlignedConductionConfig(b_hat=b_host, m_p=3.0, k_B=1.0, bc=w.bc)
-            opx = operators.DiffusionOperator.aligned(cfg)
-        else:
-            opx = op
-        state = {fname: mesh.Field(w.grid, host_in)}
-        out, reps = ptl.split_advance([(fname, opx)], state, outer_dt, [(sc, pcfg)])
-        iters += sum(r.total_iters for r in reps)
+        ops = []
+        for f, kind, nc in ops_desc:
+            if kind == "aligned":
+                cfg = operators.AlignedConductionConfig(b_hat=host["b"], rho=host.get("rho"), m_p=3.0, k_B=1.0,
+                                                        bc=w.bc)
+                ops.append((f, operators.DiffusionOperator.aligned(cfg)))
+            else:
+                cfg = operators.ScalarDiffusionConfig(nu=1.0, rho=host.get("rho"), bc=w.bc, vector_metric=nc == 3)
+                ops.append((f, operators.DiffusionOperator.scalar(cfg, nc)))
+        state = {f: mesh.Field(w.grid, host[f].reshape(tuple(w.grid.shape) + (-1,))) for f in state_names}
+        out, reps = ptl.split_advance(ops, state, outer_dt, [(sc, pcfg)] * len(ops))
+        cu += cells * sum(r.total_iters for r in reps)
+        del ops, out
     ctx.sync()
     dt = time.perf_counter() - t0
     if dist:
@@ -337,26 +426,26 @@ def run_e2e(args, w, name, op, fname, ncomp, init4, outer_dt, sc, pcfg, ctx, dis
         t = torch.tensor([dt], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
-    cells = int(np.prod(w.grid.shape))
-    ctx.unpin(host_in)
-    if b_host is not None:
-        ctx.unpin(b_host)
-    return {"value": cells * iters / dt, "unit": "cell-updates/s", "h2d_bytes_per_step": int(h2d),
+    for a in host.values():
+        ctx.unpin(a)
+    return {"value": cu / dt, "unit": "cell-updates/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / args.steps,
-            "path": "ptl.split_advance(host Field) -> pc_cycle"}
+            "path": "ptl.split_advance(host Fields, host b-hat/rho) -> pc_cycle per operator"}
 
 
 # ---------------------------------------------------------------- CPU oracle
 
 def _oracle_chunk(job):
-    """Run `stages` oracle RKL2 stages on an r-chunk (its own sub-domain)."""
+    """Run `stages` oracle RKL2 stages of each operator of the config on an
+    r-chunk (its own sub-domain); returns (cell-updates, seconds)."""
     name, lo, nplanes, stages = job
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from helpers import oracle_aligned, oracle_scalar, soa
     from oracle import schemes as osch
     from paper_2403_01004_b200 import configs, mesh
-    n = {"c1": (48, 48, 96), "c2": (128, 128, 256), "c3": (256, 256, 512), "c4": (512, 512, 1024)}[name]
-    if name in ("c3", "c4"):
+    n = {"c1": (48, 48, 96), "c2": (128, 128, 256), "c3": (256, 256, 512), "c4": (512, 512, 1024),
+         "c5": (768, 768, 1536)}[name]
+    if name in ("c3", "c4", "c5"):
         full = mesh.build_spherical_grid(configs.r_stretched_c3(n[0]), n[1], n[2])
     elif name == "c2":
         full = mesh.build_spherical_grid(configs.r_geometric_ratio(n[0], 1.0, 2.5, 1.01), n[1], n[2])
@@ -364,29 +453,38 @@ def _oracle_chunk(job):
         full = mesh.build_spherical_grid(configs.r_uniform(n[0], 1.0, 2.5), n[1], n[2])
     bc = configs.spherical_bc("dirichlet")
     sub = mesh.Grid((full.coords[0][lo:lo + nplanes], full.coords[1], full.coords[2]), full.metric)
-    if name in ("c3", "c4"):
-        T = configs.temperature(full, 3, i0=lo, n0=nplanes)
-        b = configs.dipole_bhat(full, 3, i0=lo, n0=nplanes)
-        op = oracle_aligned(sub, bc, b, T)
-        u0 = T[None].copy()
+    seed = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}[name]
+    work = []  # (oracle operator, u0)
+    if name in ("c3", "c4", "c5"):
+        T = configs.temperature(full, seed, i0=lo, n0=nplanes)
+        b = configs.dipole_bhat(full, seed, i0=lo, n0=nplanes)
+        rho = None
+        if name == "c5":
+            rho = np.exp(-10.0 * (full.coords[0][lo:lo + nplanes] - 1.0))[:, None, None] * np.ones(sub.shape)
+        work.append((oracle_aligned(sub, bc, b, T, rho=rho), T[None].copy()))
+        if name == "c5":
+            work.append((oracle_scalar(sub, bc, nu=1.0, rho=rho, ncomp=3, vector_metric=True),
+                         soa(configs.harmonic_velocity(full, seed, i0=lo, n0=nplanes))))
     elif name == "c2":
-        op = oracle_scalar(sub, bc, ncomp=3, vector_metric=True)
-        u0 = soa(configs.harmonic_velocity(full, 2, i0=lo, n0=nplanes))
+        work.append((oracle_scalar(sub, bc, ncomp=3, vector_metric=True),
+                     soa(configs.harmonic_velocity(full, 2, i0=lo, n0=nplanes))))
     else:
-        op = oracle_scalar(sub, bc)
-        u0 = configs.c1().fields["u"][lo:lo + nplanes][None].copy()
-    dtE = op.euler_dt()
-    y0 = op.apply(u0)
-    t = time.perf_counter()
-    osch.sts_step(op.apply, u0, y0, 10 * dtE, stages, "rkl2", op.geom.pinned)
-    dt = time.perf_counter() - t
-    return int(np.prod(op.geom.shape)) * (stages - 1), dt  # stages 2..s each one full pass
+        work.append((oracle_scalar(sub, bc), configs.c1().fields["u"][lo:lo + nplanes][None].copy()))
+    cu, secs = 0, 0.0
+    for op, u0 in work:
+        dtE = op.euler_dt()
+        y0 = op.apply(u0)
+        t = time.perf_counter()
+        osch.sts_step(op.apply, u0, y0, 10 * dtE, stages, "rkl2", op.geom.pinned)
+        secs += time.perf_counter() - t
+        cu += int(np.prod(op.geom.shape)) * (stages - 1)  # stages 2..s each one full pass
+    return cu, secs
 
 
 def cpu_baseline(name, budget_s=20.0, procs=1):
     """Oracle (numpy, single thread) on an r-chunk sample."""
-    n0 = {"c1": 48, "c2": 128, "c3": 256, "c4": 512}[name]
-    planes = {"c1": 48, "c2": 16, "c3": 8, "c4": 4}[name]
+    n0 = {"c1": 48, "c2": 128, "c3": 256, "c4": 512, "c5": 768}[name]
+    planes = {"c1": 48, "c2": 16, "c3": 8, "c4": 4, "c5": 3}[name]
     stages = 4
     t0 = time.perf_counter()
     jobs = [(name, (k * planes) % (n0 - planes), planes, stages) for k in range(procs)]
@@ -443,8 +541,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--scheme", default=None, choices=[None, "rkl2", "rkg2", "be"])
+    ap.add_argument("--n", default=None, help="override the grid, e.g. 96,96,192 (smoke runs only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")

@@ -9,7 +9,8 @@
  * Reference interfaces replaced (file:line in /root/reference):
  *   pc_grid_create / pc_field_*     mesh.Grid / mesh.Field / mesh.pinned_mask
  *                                   (pkg/src/paracycle/mesh.py:89-239, :311-324)
- *   pc_op_create_scalar             operators.ScalarDiffusionConfig +
+ *   pc_op_create_scalar,
+ *   pc_op_create_viscous            operators.ScalarDiffusionConfig +
  *                                   apply_scalar_diffusion
  *   pc_op_create_aligned,
  *   pc_op_freeze                    operators.AlignedConductionConfig +
@@ -117,6 +118,10 @@ int pc_host_unregister(void* ptr);
  *          T0 floored at T_floor; fc_table (n0 + 2 doubles incl. ghosts) or NULL. */
 int pc_op_create_scalar(pc_grid* g, int ncomp, int vector_metric, double D_const,
                         const pc_field* D, const pc_field* rho, pc_op** out);
+/* viscosity F = (1/rho) div(nu rho grad u) with a density FIELD and constant
+ * nu: the face coefficient nu*rho is formed per node from rho (no D array). */
+int pc_op_create_viscous(pc_grid* g, int ncomp, int vector_metric, double nu, const pc_field* rho,
+                         pc_op** out);
 int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho,
                          double pref, double kappa0, const double* fc_table,
                          double T_floor, pc_op** out);
@@ -156,11 +161,24 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd,
              int floor_mode, double floor_fraction, int64_t max_cycles, double dt_euler,
              pc_cycle_record* rec, int64_t rec_cap, int64_t* n_rec);
 
+/* ---- seeded synthetic inputs in HBM (configs.py recipes, bit-identical):
+ * tables are over the GLOBAL grid (prof/ir3/rho: n0 values, c2/st: n1,
+ * acc: ncomp x n1 x n2); noise = configs.hash_normal(seed, stream, global index). */
+int pc_gen_temperature(pc_field* T, uint64_t seed, int stream, double sigma, const double* prof);
+int pc_gen_dipole(pc_field* b, uint64_t seed, int stream0, double eps, const double* ir3, const double* c2,
+                  const double* st);
+int pc_gen_harmonic(pc_field* v, const double* acc, double checker);
+int pc_gen_radial(pc_field* f, const double* tab);
+
 /* ---- instrumentation (enabled by pc_ctx_enable_timing): device time of the
  * fused STS stage kernels (k >= 2) and of the PCG iteration kernels, their
  * launch count, and the total number of kernels this context launched. */
 int pc_ctx_stats(pc_ctx* ctx, double* stage_ms, int64_t* stage_launches, int64_t* launches_total);
 int pc_ctx_reset_stats(pc_ctx* ctx);
+/* per hot-loop kind (0 scalar/vector STS stages k >= 2, 1 aligned STS stages,
+ * 2 scalar PCG iterations, 3 aligned PCG iterations): device ms, launches and
+ * cell-updates (local cells x stages / iterations) */
+int pc_ctx_stats_kind(pc_ctx* ctx, int kind, double* ms, int64_t* launches, int64_t* cell_updates);
 int pc_ctx_enable_timing(pc_ctx* ctx, int on);
 /* CUDA events on the context stream: record mark id (0..15); elapsed ms */
 int pc_ctx_mark(pc_ctx* ctx, int id);

@@ -194,3 +194,20 @@ def cycle_operator(op, scheme, u, outer_dt, eps_rel=1e-12, floor="euler", floor_
         else:
             remaining = remaining - dt
     return u, report
+
+
+def split_advance(ops, state, outer_dt, schemes, refresh=None, eps_rel=1e-12):
+    """Lie splitting in list order: ``ops`` = [(name,
+    OracleOperator)], ``state`` = {name: SoA array}.  Aligned operators get
+    c = aligned_coefficient(T0) from the state at the START of the outer step
+    (lagged T0) through ``refresh(op, state)``.  Returns (state,
+    [report per operator])."""
+    state = dict(state)
+    for name, op in ops:
+        if op.kind == "aligned" and refresh is not None:
+            refresh(op, state)
+    reports = []
+    for (name, op), scheme in zip(ops, schemes):
+        state[name], rep = cycle_operator(op, scheme, state[name], outer_dt, eps_rel=eps_rel)
+        reports.append(rep)
+    return state, reports

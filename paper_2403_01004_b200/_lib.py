@@ -67,6 +67,7 @@ _SIGS = {
     "pc_host_register": (c_int, [c_void_p, c_size_t]),
     "pc_host_unregister": (c_int, [c_void_p]),
     "pc_op_create_scalar": (c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, POINTER(c_void_p)]),
+    "pc_op_create_viscous": (c_int, [c_void_p, c_int, c_int, c_double, c_void_p, POINTER(c_void_p)]),
     "pc_op_create_aligned": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_double, POINTER(c_double),
                                      c_double, POINTER(c_void_p)]),
     "pc_op_freeze": (c_int, [c_void_p, c_void_p]),
@@ -86,8 +87,14 @@ _SIGS = {
                              POINTER(c_double), POINTER(c_int)]),
     "pc_cycle": (c_int, [c_void_p, c_void_p, c_double, c_int, c_int, c_double, c_int, c_double, c_int, c_int,
                          c_int, c_double, c_int64, c_double, POINTER(CycleRecord), c_int64, POINTER(c_int64)]),
+    "pc_gen_temperature": (c_int, [c_void_p, ctypes.c_uint64, c_int, c_double, POINTER(c_double)]),
+    "pc_gen_dipole": (c_int, [c_void_p, ctypes.c_uint64, c_int, c_double, POINTER(c_double), POINTER(c_double),
+                              POINTER(c_double)]),
+    "pc_gen_harmonic": (c_int, [c_void_p, POINTER(c_double), c_double]),
+    "pc_gen_radial": (c_int, [c_void_p, POINTER(c_double)]),
     "pc_ctx_stats": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int64), POINTER(c_int64)]),
     "pc_ctx_reset_stats": (c_int, [c_void_p]),
+    "pc_ctx_stats_kind": (c_int, [c_void_p, c_int, POINTER(c_double), POINTER(c_int64), POINTER(c_int64)]),
     "pc_ctx_enable_timing": (c_int, [c_void_p, c_int]),
     "pc_ctx_mark": (c_int, [c_void_p, c_int]),
     "pc_ctx_elapsed": (c_int, [c_void_p, c_int, c_int, POINTER(c_double)]),

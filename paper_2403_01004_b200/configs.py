@@ -133,19 +133,15 @@ def dipole_bhat(grid, seed, eps=0.05, i0=0, n0=None):
     return np.stack([bx / nrm, by / nrm, bz / nrm], axis=-1)
 
 
-def harmonic_velocity(grid, seed, n_modes=8, lmax=16, checker=0.1, i0=0, n0=None):
-    """v_c = sum_m A_m P_l^m(cos th) cos(m phi + psi) + checker (-1)^(i+j+k), per component."""
+def harmonic_tables(grid, seed, n_modes=8, lmax=16):
+    """acc[c] = sum_m A_m P_l^m(cos th) cos(m phi + psi) on the (theta, phi) grid, per component."""
     from scipy.special import sph_harm_y
 
-    n0 = grid.shape[0] if n0 is None else n0
     rng = np.random.default_rng(seed)
     th, ph = grid.coords[1], grid.coords[2]
-    shp = (n0, grid.shape[1], grid.shape[2])
-    out = np.empty(shp + (3,))
-    ii = (np.arange(i0, i0 + n0)[:, None, None] + np.arange(shp[1])[None, :, None] + np.arange(shp[2])[None, None, :])
-    cb = np.where(ii % 2 == 0, checker, -checker)
+    out = np.empty((3, grid.shape[1], grid.shape[2]))
     for c in range(3):
-        acc = np.zeros((shp[1], shp[2]))
+        acc = np.zeros((grid.shape[1], grid.shape[2]))
         for _ in range(n_modes):
             l = int(rng.integers(0, lmax + 1))
             m = int(rng.integers(0, l + 1))
@@ -154,8 +150,62 @@ def harmonic_velocity(grid, seed, n_modes=8, lmax=16, checker=0.1, i0=0, n0=None
             Th = np.real(sph_harm_y(l, m, th, 0.0))
             Ph = np.array([math.cos(m * p + psi) for p in ph])
             acc = acc + (amp * Th)[:, None] * Ph[None, :]
-        out[..., c] = acc[None, :, :] + cb
+        out[c] = acc
     return out
+
+
+def harmonic_velocity(grid, seed, n_modes=8, lmax=16, checker=0.1, i0=0, n0=None):
+    """v_c = sum_m A_m P_l^m(cos th) cos(m phi + psi) + checker (-1)^(i+j+k), per component."""
+    n0 = grid.shape[0] if n0 is None else n0
+    acc = harmonic_tables(grid, seed, n_modes, lmax)
+    shp = (n0, grid.shape[1], grid.shape[2])
+    out = np.empty(shp + (3,))
+    ii = (np.arange(i0, i0 + n0)[:, None, None] + np.arange(shp[1])[None, :, None] + np.arange(shp[2])[None, None, :])
+    cb = np.where(ii % 2 == 0, checker, -checker)
+    for c in range(3):
+        out[..., c] = acc[c][None, :, :] + cb
+    return out
+
+
+# ---------------------------------------------------------------- device-side generation
+# The same recipes evaluated in HBM by the library (pc_gen_*), bit-identical to
+# the host functions above: only the 1-D / 2-D tables are built here.
+
+def _dptr(a):
+    from . import _lib
+    return _lib.dptr(a)
+
+
+def gen_temperature(field, grid, seed, sigma=1e-3):
+    from . import _lib
+    prof = np.ascontiguousarray(transition_profile(grid.coords[0]))
+    _lib.check(_lib.lib().pc_gen_temperature(field.handle, int(seed), 1, float(sigma), _dptr(prof)), "gen T")
+    return field
+
+
+def gen_dipole(field, grid, seed, eps=0.05):
+    from . import _lib
+    r, th = grid.coords[0], grid.coords[1]
+    ir3 = np.ascontiguousarray(1.0 / (r * r * r))
+    c2 = np.array([2.0 * math.cos(t) for t in th])
+    st = np.array([math.sin(t) for t in th])
+    _lib.check(_lib.lib().pc_gen_dipole(field.handle, int(seed), 2, float(eps), _dptr(ir3), _dptr(c2), _dptr(st)),
+               "gen b")
+    return field
+
+
+def gen_harmonic(field, grid, seed, checker=0.1):
+    from . import _lib
+    acc = np.ascontiguousarray(harmonic_tables(grid, seed))
+    _lib.check(_lib.lib().pc_gen_harmonic(field.handle, _dptr(acc), float(checker)), "gen v")
+    return field
+
+
+def gen_radial(field, table):
+    from . import _lib
+    t = np.ascontiguousarray(np.asarray(table, float))
+    _lib.check(_lib.lib().pc_gen_radial(field.handle, _dptr(t)), "gen radial")
+    return field
 
 
 @dataclass
@@ -184,23 +234,29 @@ def c2(seed=2, n=(128, 128, 256)):
     return Workload("C2", grid, bc, 2000.0, seed, {"v": v}, {"nu": 1.0})
 
 
-def c3(seed=3, n=(256, 256, 512)):
+def c3(seed=3, n=(256, 256, 512), host=True):
+    """host=False skips the host arrays (the bench generates them in HBM with gen_*)."""
     grid = mesh.build_spherical_grid(r_stretched_c3(n[0]), n[1], n[2])
     bc = spherical_bc("dirichlet")
-    T = temperature(grid, seed)
-    b = dipole_bhat(grid, seed)
-    return Workload("C3", grid, bc, 1e4, seed, {"T": T, "b": b}, {"m_p": 3.0, "k_B": 1.0})
+    fields = {"T": temperature(grid, seed), "b": dipole_bhat(grid, seed)} if host else {}
+    return Workload("C3", grid, bc, 1e4, seed, fields, {"m_p": 3.0, "k_B": 1.0})
 
 
-def c4(seed=4, n=(512, 512, 1024)):
-    w = c3(seed, n)
+def c4(seed=4, n=(512, 512, 1024), host=True):
+    w = c3(seed, n, host)
     w.name = "C4"
     w.meta["tol"] = 1e-9
     return w
 
 
-def c5(seed=5, n=(768, 768, 1536)):
+def c5(seed=5, n=(768, 768, 1536), host=False):
+    """Coupled conduction (T, b as C3) + viscosity (v as C2) with rho = exp(-10 (r - 1)),
+    one MAS step of 5e4 dt_E, dt_E = min over the two operators."""
     grid = mesh.build_spherical_grid(r_stretched_c3(n[0]), n[1], n[2])
     bc = spherical_bc("dirichlet")
     rho_r = np.exp(-10.0 * (grid.coords[0] - 1.0))
-    return Workload("C5", grid, bc, 5e4, seed, {}, {"rho_r": rho_r, "m_p": 3.0, "k_B": 1.0, "nu": 1.0})
+    fields = {}
+    if host:
+        fields = {"T": temperature(grid, seed), "b": dipole_bhat(grid, seed), "v": harmonic_velocity(grid, seed),
+                  "rho": rho_r[:, None, None] * np.ones(grid.shape)}
+    return Workload("C5", grid, bc, 5e4, seed, fields, {"rho_r": rho_r, "m_p": 3.0, "k_B": 1.0, "nu": 1.0})

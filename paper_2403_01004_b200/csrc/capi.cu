@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/paracycle_b200.h"
+#include "gen.cuh"
 #include "march.cuh"
 #include "nccl_shim.h"
 
@@ -47,10 +48,20 @@ static int fail(int code, const std::string& msg, int64_t info = 0) {
   } while (0)
 
 // ------------------------------------------------------------------ objects
+// kinds of timed hot loops: 0 scalar/vector STS stages, 1 aligned STS stages,
+// 2 scalar PCG iterations, 3 aligned PCG iterations
+enum { KIND_STS_SCALAR = 0, KIND_STS_ALIGNED = 1, KIND_PCG_SCALAR = 2, KIND_PCG_ALIGNED = 3, NKIND = 4 };
 struct Stats {
   double stage_ms = 0.0;
   int64_t stage_launches = 0;
   int64_t launches = 0;
+  double kind_ms[NKIND] = {0, 0, 0, 0};
+  int64_t kind_launches[NKIND] = {0, 0, 0, 0};
+  int64_t kind_units[NKIND] = {0, 0, 0, 0};  // cell-updates (local cells x stages / iterations)
+};
+struct TimedSpan {
+  cudaEvent_t e0, e1;
+  int kind;
 };
 
 struct pc_ctx {
@@ -83,7 +94,7 @@ struct pc_ctx {
   std::vector<std::pair<size_t, double*>> pool;
   Stats st;
   bool timing = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<TimedSpan> ev;
   cudaEvent_t marks[16] = {};
 };
 
@@ -112,7 +123,8 @@ struct pc_op {
   AlignedOp ao{};
   const double* bsrc[3] = {nullptr, nullptr, nullptr};  // aligned: b-hat (caller's field)
   double* betabuf = nullptr;  // aligned: beta = sqrt(c) b, 3 component-sized buffers
-  double* dbuf = nullptr;   // Jacobi diagonal -J_ii
+  double* dbuf = nullptr;   // Jacobi diagonal -J_ii (allocated on first BE / diagonal use)
+  bool diag_valid = false;
   double* kfc = nullptr;    // kappa0 * f_c(r) per axis-0 row (n0 + 2)
   double Tfloor = 1e-10;
   double lam_max = 0.0;
@@ -308,8 +320,8 @@ int pc_ctx_destroy(pc_ctx* c) {
   cudaStreamSynchronize(c->s);
   for (auto& p : c->pool) cudaFree(p.second);
   for (auto& e : c->ev) {
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+    cudaEventDestroy(e.e0);
+    cudaEventDestroy(e.e1);
   }
   if (c->comm) {
     nccl::Api* A = nccl::api();
@@ -369,14 +381,25 @@ int pc_ctx_reset_stats(pc_ctx* c) {
 static void flush_events(pc_ctx* c) {
   for (auto& e : c->ev) {
     float ms = 0.f;
-    cudaEventSynchronize(e.second);
-    cudaEventElapsedTime(&ms, e.first, e.second);
+    cudaEventSynchronize(e.e1);
+    cudaEventElapsedTime(&ms, e.e0, e.e1);
     c->st.stage_ms += ms;
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+    c->st.kind_ms[e.kind] += ms;
+    cudaEventDestroy(e.e0);
+    cudaEventDestroy(e.e1);
   }
   c->ev.clear();
 }
+int pc_ctx_stats_kind(pc_ctx* c, int kind, double* ms, int64_t* launches, int64_t* units) {
+  if (!c || kind < 0 || kind >= NKIND) return fail(PC_E_INVALID, "stats kind 0..3");
+  cudaStreamSynchronize(c->s);
+  flush_events(c);
+  if (ms) *ms = c->st.kind_ms[kind];
+  if (launches) *launches = c->st.kind_launches[kind];
+  if (units) *units = c->st.kind_units[kind];
+  return PC_OK;
+}
+
 int pc_ctx_stats(pc_ctx* c, double* stage_ms, int64_t* stage_launches, int64_t* launches_total) {
   cudaStreamSynchronize(c->s);
   flush_events(c);
@@ -429,6 +452,16 @@ int pc_grid_create(pc_ctx* c, const int64_t shape[3], const int32_t* fl, const d
   d.i0g = fl[12];
   d.spherical = fl[13];
   g->comp_elems = (size_t)(shape[0] + 2) * (size_t)d.plane;
+  {  // the marching kernels rely on unit axis-0/1 column factors iL1 (geometry.py)
+    int64_t A, K, J;
+    table_sizes(shape, A, K, J);
+    const double* iL1 = tables + 3 * A + 3 * K + A + K + 6 * A;
+    for (int64_t q = 0; q < 4 * K; ++q)
+      if (iL1[q] != 1.0) {
+        delete g;
+        return fail(PC_E_INVALID, "grid tables: axis-0/1 column factors iL1 must be 1");
+      }
+  }
   CUDA_TRY(cudaMalloc(&g->tables, sizeof(double) * ntables));
   CUDA_TRY(cudaMemcpy(g->tables, tables, sizeof(double) * ntables, cudaMemcpyHostToDevice));
   int64_t A, K, J;
@@ -593,10 +626,19 @@ int pc_op_create_scalar(pc_grid* g, int ncomp, int vector_metric, double D_const
   op->ncomp = ncomp;
   op->so.D = D ? D->base(0) : nullptr;
   op->so.Dc = D_const;
+  op->so.drho = 0;
   op->so.rho = rho ? rho->base(0) : nullptr;
   op->so.ncomp = ncomp;
   op->so.vector = (vector_metric && g->g.spherical) ? 1 : 0;
   *out = op;
+  return PC_OK;
+}
+
+int pc_op_create_viscous(pc_grid* g, int ncomp, int vector_metric, double nu, const pc_field* rho, pc_op** out) {
+  if (!rho || rho->ncomp != 1) return fail(PC_E_INVALID, "viscous operator needs a scalar density field");
+  if (!(nu >= 0.0)) return fail(PC_E_INVALID, "nu must be >= 0");
+  TRY(pc_op_create_scalar(g, ncomp, vector_metric, nu, nullptr, rho, out));
+  (*out)->so.drho = 1;
   return PC_OK;
 }
 
@@ -645,7 +687,8 @@ static int run_bound(pc_op* op, const Op& o) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   int nb = node_blocks(c, g->g);
-  k_bound<<<nb, kThreads, 0, c->s>>>(g->g, o, op->dbuf + g->g.plane, c->red_v, c->counter, c->maxout);
+  k_bound<<<nb, kThreads, 0, c->s>>>(g->g, o, op->dbuf ? op->dbuf + g->g.plane : nullptr, c->red_v, c->counter,
+                                     c->maxout);
   c->st.launches++;
   TRY(check_launch("k_bound"));
   TRY(allreduce_d(c, c->maxout, 1, nccl::kMax));
@@ -660,11 +703,6 @@ int pc_op_freeze(pc_op* op, const pc_field* T0) {
   if (!op) return fail(PC_E_INVALID, "null operator");
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
-  if (!op->dbuf) {
-    if (cudaMalloc(&op->dbuf, g->comp_elems * sizeof(double)) != cudaSuccess)
-      return fail(PC_E_CUDA, "diagonal allocation failed");
-    cudaMemsetAsync(op->dbuf, 0, g->comp_elems * sizeof(double), c->s);
-  }
   if (op->kind == K_ALIGNED) {
     if (!T0 || T0->ncomp != 1 || T0->grid != g) return fail(PC_E_INVALID, "aligned freeze needs a scalar T0 on the grid");
     CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
@@ -684,9 +722,30 @@ int pc_op_freeze(pc_op* op, const pc_field* T0) {
   } else {
     TRY(run_bound(op, op->so));
   }
+  op->diag_valid = op->dbuf != nullptr;
+  if (op->dbuf) {
+    double* db[1] = {op->dbuf};
+    TRY(halo_exchange(c, g, db, 1));
+  }
+  op->frozen = true;
+  return PC_OK;
+}
+
+// the Jacobi diagonal is only materialised for BE / PCG / pc_op_diagonal
+static int ensure_diag(pc_op* op) {
+  if (op->diag_valid) return PC_OK;
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  if (!op->dbuf) {
+    if (cudaMalloc(&op->dbuf, g->comp_elems * sizeof(double)) != cudaSuccess)
+      return fail(PC_E_CUDA, "diagonal allocation failed (out of device memory)");
+    CUDA_TRY(cudaMemsetAsync(op->dbuf, 0, g->comp_elems * sizeof(double), c->s));
+  }
+  if (op->kind == K_ALIGNED) TRY(run_bound(op, op->ao));
+  else TRY(run_bound(op, op->so));
   double* db[1] = {op->dbuf};
   TRY(halo_exchange(c, g, db, 1));
-  op->frozen = true;
+  op->diag_valid = true;
   return PC_OK;
 }
 
@@ -700,6 +759,7 @@ int pc_op_euler_dt(pc_op* op, double* dt) {
 int pc_op_diagonal(pc_op* op, pc_field* out) {
   if (!op || !out || out->ncomp != 1) return fail(PC_E_INVALID, "diagonal output must be a scalar field");
   if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  TRY(ensure_diag(op));
   CUDA_TRY(cudaMemcpyAsync(out->buf[0], op->dbuf, op->grid->comp_elems * sizeof(double),
                            cudaMemcpyDeviceToDevice, op->grid->ctx->s));
   CUDA_TRY(cudaStreamSynchronize(op->grid->ctx->s));
@@ -947,9 +1007,14 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     um1 = out;
     out = prev_um1;
   }
-  if (c->timing) {
-    cudaEventRecord(e1, c->s);
-    c->ev.push_back({e0, e1});
+  {
+    const int kind = std::is_same<Op, AlignedOp>::value ? KIND_STS_ALIGNED : KIND_STS_SCALAR;
+    if (c->timing) {
+      cudaEventRecord(e1, c->s);
+      c->ev.push_back({e0, e1, kind});
+    }
+    c->st.kind_launches[kind] += s - 1;
+    c->st.kind_units[kind] += (int64_t)(s - 1) * g->g.N;
   }
   if (rc == PC_OK) {
     CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
@@ -1088,12 +1153,15 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
     }
     if (c->h_pcg->done) stop = true;
   }
+  const int pkind = std::is_same<Op, AlignedOp>::value ? KIND_PCG_ALIGNED : KIND_PCG_SCALAR;
   if (c->timing) {
     cudaEventRecord(e1, c->s);
-    c->ev.push_back({e0, e1});
+    c->ev.push_back({e0, e1, pkind});
   }
   if (rc == PC_OK) {
     CUDA_TRY(cudaMemcpyAsync(c->h_pcg, c->pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, c->s));
+    c->st.kind_launches[pkind] += (int64_t)c->h_pcg->it * (std::is_same<Op, AlignedOp>::value ? 3 : 2);
+    c->st.kind_units[pkind] += (int64_t)c->h_pcg->it * g->g.N;
     CUDA_TRY(cudaStreamSynchronize(c->s));
     const PcgDev& st = *c->h_pcg;
     *iters = st.it;
@@ -1111,6 +1179,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
 
 static int pcg_any(pc_op* op, double dt, const double* adiag, CFld b, pc_field* x, double tol, int max_iter,
                    int* iters, double* relres, int* converged) {
+  TRY(ensure_diag(op));
   if (op->kind == K_ALIGNED) return pcg_run(op, op->ao, dt, adiag, b, x, tol, max_iter, iters, relres, converged);
   return pcg_run(op, op->so, dt, adiag, b, x, tol, max_iter, iters, relres, converged);
 }
@@ -1244,3 +1313,76 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
   return rc;
 }
 
+
+// ------------------------------------------------------------------ synthetic inputs
+// (configs.py recipes evaluated in HBM; tables are GLOBAL-grid tables)
+static int upload_tmp(pc_ctx* c, const double* host, size_t n, double** dev) {
+  CUDA_TRY(cudaMalloc(dev, n * sizeof(double)));
+  CUDA_TRY(cudaMemcpyAsync(*dev, host, n * sizeof(double), cudaMemcpyHostToDevice, c->s));
+  return PC_OK;
+}
+static const double kSqrt3 = 1.7320508075688772;  // math.sqrt(3.0)
+
+int pc_gen_temperature(pc_field* T, uint64_t seed, int stream, double sigma, const double* prof) {
+  if (!T || T->ncomp != 1 || !prof) return fail(PC_E_INVALID, "temperature: scalar field and profile needed");
+  pc_grid* g = T->grid;
+  pc_ctx* c = g->ctx;
+  double* dp = nullptr;
+  TRY(upload_tmp(c, prof, (size_t)g->g.n0g, &dp));
+  k_gen_temperature<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, T->base(0), stream_key(seed, stream), sigma,
+                                                                  dp, kSqrt3);
+  c->st.launches++;
+  int rc = check_launch("k_gen_temperature");
+  cudaStreamSynchronize(c->s);
+  cudaFree(dp);
+  return rc;
+}
+
+int pc_gen_dipole(pc_field* b, uint64_t seed, int stream0, double eps, const double* ir3, const double* c2,
+                  const double* st) {
+  if (!b || b->ncomp != 3 || !ir3 || !c2 || !st) return fail(PC_E_INVALID, "dipole: 3-component field and tables");
+  pc_grid* g = b->grid;
+  pc_ctx* c = g->ctx;
+  double *d0 = nullptr, *d1 = nullptr, *d2 = nullptr;
+  TRY(upload_tmp(c, ir3, (size_t)g->g.n0g, &d0));
+  TRY(upload_tmp(c, c2, (size_t)g->g.n1, &d1));
+  TRY(upload_tmp(c, st, (size_t)g->g.n1, &d2));
+  k_gen_dipole<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, fld(b), stream_key(seed, stream0),
+                                                             stream_key(seed, stream0 + 1),
+                                                             stream_key(seed, stream0 + 2), eps, d0, d1, d2, kSqrt3);
+  c->st.launches++;
+  int rc = check_launch("k_gen_dipole");
+  cudaStreamSynchronize(c->s);
+  cudaFree(d0);
+  cudaFree(d1);
+  cudaFree(d2);
+  return rc;
+}
+
+int pc_gen_harmonic(pc_field* v, const double* acc, double checker) {
+  if (!v || !acc) return fail(PC_E_INVALID, "harmonic: field and (ncomp, n1, n2) table needed");
+  pc_grid* g = v->grid;
+  pc_ctx* c = g->ctx;
+  double* da = nullptr;
+  TRY(upload_tmp(c, acc, (size_t)v->ncomp * g->g.n1 * g->g.n2, &da));
+  k_gen_harmonic<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, fld(v), v->ncomp, da, checker);
+  c->st.launches++;
+  int rc = check_launch("k_gen_harmonic");
+  cudaStreamSynchronize(c->s);
+  cudaFree(da);
+  return rc;
+}
+
+int pc_gen_radial(pc_field* f, const double* tab) {
+  if (!f || f->ncomp != 1 || !tab) return fail(PC_E_INVALID, "radial: scalar field and table needed");
+  pc_grid* g = f->grid;
+  pc_ctx* c = g->ctx;
+  double* dt = nullptr;
+  TRY(upload_tmp(c, tab, (size_t)g->g.n0g, &dt));
+  k_gen_radial<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, f->base(0), dt);
+  c->st.launches++;
+  int rc = check_launch("k_gen_radial");
+  cudaStreamSynchronize(c->s);
+  cudaFree(dt);
+  return rc;
+}

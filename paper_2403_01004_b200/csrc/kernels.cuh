@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads) k_bound(GridDev g, Op op, double* di
     double lam[3], dg;
     op.bound(g, i, j, k, lam, dg);
     for (int q = 0; q < op.ncomp; ++q) m = fmax(m, lam[q]);
-    diag[off3(g, i, j, k)] = dg;
+    if (diag) diag[off3(g, i, j, k)] = dg;
   }
   m = block_max<kThreads>(m, sh);
   if (threadIdx.x == 0) pv[blockIdx.x] = m;

@@ -114,14 +114,16 @@ __device__ __forceinline__ double launder(double x) {
 }
 
 // per-column constants (depend on k only)
+// (the axis-0 and axis-1 column factors iL1 are exactly 1 for every grid --
+// checked by pc_grid_create -- so only the phi pair is carried)
 struct ColT {
-  double il1[6];
+  double il1[2];
   double w2[2];
   double ivg;
 };
 __device__ __forceinline__ void load_col(const GridDev& g, int k, ColT& c) {
 #pragma unroll
-  for (int q = 0; q < 6; ++q) c.il1[q] = __ldg(g.iL1[q] + k);
+  for (int q = 0; q < 2; ++q) c.il1[q] = __ldg(g.iL1[4 + q] + k);
   c.w2[0] = __ldg(g.wo2[0] + k);
   c.w2[1] = __ldg(g.wo2[1] + k);
   c.ivg = __ldg(g.iValg + k);
@@ -133,7 +135,7 @@ __device__ __forceinline__ void load_col(const GridDev& g, int k, ColT& c) {
 //   rw: row tables of the node's (plane, theta row): iL2[6], wo01[4]
 template <int ONLY_A, int ONLY_S>
 __device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], const double (&bv)[3],
-                                       const double* rw, int rstride, const double (&il1)[6],
+                                       const double* rw, int rstride, const double (&il1)[2],
                                        const double (&w2)[2], double (&E)[3][2]) {
   double bil[3][2], p[3][2];
 #pragma unroll
@@ -142,7 +144,7 @@ __device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], cons
     for (int t = 0; t < 2; ++t) {
       const bool need_p = !(ONLY_A >= 0 && x == ONLY_A && t != ONLY_S);
       const bool need_bil = need_p || (ONLY_A < 0) || (x == ONLY_A && t == ONLY_S);
-      if (need_bil) bil[x][t] = bv[x] * (rw[(2 * x + t) * rstride] * il1[2 * x + t]);
+      if (need_bil) bil[x][t] = bv[x] * (x < 2 ? rw[(2 * x + t) * rstride] : rw[(2 * x + t) * rstride] * il1[t]);
       if (need_p) p[x][t] = bil[x][t] * (t == 0 ? (Tn[x][0] - Tv) : (Tv - Tn[x][1]));
       else p[x][t] = 0.0;
     }
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   ColT col;
   load_col(g, km, col);
 #pragma unroll
-  for (int q = 0; q < 6; ++q) col.il1[q] = launder(col.il1[q]);
+  for (int q = 0; q < 2; ++q) col.il1[q] = launder(col.il1[q]);
   col.w2[0] = launder(col.w2[0]);
   col.w2[1] = launder(col.w2[1]);
   col.ivg = launder(col.ivg);
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
           }
         } else {
           const double* cs = S.ringcol[rs];
-          const double il1[6] = {cs[0], cs[1], cs[2], cs[3], cs[4], cs[5]};
+          const double il1[2] = {cs[4], cs[5]};
           const double w2[2] = {cs[6], cs[7]};
           if (rs == 0) {
             node_E<2, 0>(Tcr, Tn, bv, rw, MHJ, il1, w2, E);

@@ -27,8 +27,11 @@ struct PlainVal {
 
 // ------------------------------------------------------------------ scalar
 struct ScalarOp {
-  const double* D;  // nodal nu*rho, or nullptr -> Dc
+  const double* D;  // nodal nu*rho, or nullptr -> Dc (or Dc * rho with drho)
   double Dc;
+  int drho;         // D = Dc * rho evaluated per node (viscosity with a density field)
+  __device__ __forceinline__ bool has_field() const { return D != nullptr || drho; }
+  __device__ __forceinline__ double Dat(int64_t o) const { return D ? __ldg(D + o) : Dc * __ldg(rho + o); }
   const double* rho;  // nullptr -> 1
   int ncomp;
   int vector;  // rotate 3-component spherical vectors
@@ -60,7 +63,7 @@ struct ScalarOp {
     double S[3];
     double uc[3];
     for (int c = 0; c < ncomp; ++c) uc[c] = val(c, o, i, j, k);
-    const double Dcen = D ? __ldg(D + o) : Dc;
+    const double Dcen = has_field() ? Dat(o) : Dc;
     bool first = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -73,8 +76,8 @@ struct ScalarOp {
         const int64_t on = off3(g, ni, nj, nk);
         double coef = wg(g, a, dir, ok, i, j, k, ni, nj, nk);
         double cf;
-        if (D) {
-          double Dn = __ldg(D + on);
+        if (has_field()) {
+          double Dn = Dat(on);
           cf = (0.5 * (Dcen + Dn)) * coef;
         } else {
           cf = Dc * coef;
@@ -110,7 +113,7 @@ struct ScalarOp {
   __device__ __forceinline__ void bound(const GridDev& g, int i, int j, int k, double* lam,
                                         double& dg) const {
     const int64_t o = off3(g, i, j, k);
-    const double Dcen = D ? __ldg(D + o) : Dc;
+    const double Dcen = has_field() ? Dat(o) : Dc;
     double L[3], Sd = 0.0;
     bool first = true;
     for (int a = 0; a < 3; ++a) {
@@ -120,7 +123,7 @@ struct ScalarOp {
         bool ok;
         nb_coord(g, a, dir, i, j, k, ni, nj, nk, ok);
         double coef = wg(g, a, dir, ok, i, j, k, ni, nj, nk);
-        double cf = D ? (0.5 * (Dcen + __ldg(D + off3(g, ni, nj, nk)))) * coef : Dc * coef;
+        double cf = has_field() ? (0.5 * (Dcen + Dat(off3(g, ni, nj, nk)))) * coef : Dc * coef;
         for (int c = 0; c < ncomp; ++c) {
           double R = 2.0;
           if (vector && a > 0) R = __ldg(g.Rabs[(a == 1 ? 0 : 2) + (dir > 0 ? 0 : 1)] + (int64_t)j * 3 + c);

@@ -65,6 +65,17 @@ class Context:
         _lib.lib().pc_ctx_stats(self.handle, byref(ms), byref(sl), byref(tot))
         return {"stage_ms": ms.value, "stage_launches": sl.value, "launches": tot.value}
 
+    KINDS = ("sts_scalar", "sts_aligned", "pcg_scalar", "pcg_aligned")
+
+    def stats_by_kind(self):
+        """{kind: {ms, launches, cell_updates}} of the timed hot loops."""
+        out = {}
+        for q, name in enumerate(self.KINDS):
+            ms, nl, cu = c_double(), c_int64(), c_int64()
+            _lib.check(_lib.lib().pc_ctx_stats_kind(self.handle, q, byref(ms), byref(nl), byref(cu)), "stats")
+            out[name] = {"ms": ms.value, "launches": nl.value, "cell_updates": cu.value}
+        return out
+
     def pin(self, arr: np.ndarray):
         """Page-lock a host array (kept pinned for the context's lifetime)."""
         _lib.check(_lib.lib().pc_host_register(arr.ctypes.data, arr.nbytes), "pin")

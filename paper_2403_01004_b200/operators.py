@@ -160,12 +160,25 @@ class DeviceOperator:
         L = _lib.lib()
         h = c_void_p()
         self._keep = []
-        if op.kind == "scalar":
+        if op.kind == "scalar" and isinstance(cfg.rho, device.DeviceField):
+            # device-resident density (C5-size inputs never visit the host)
+            if not isinstance(cfg.nu, (int, float)):
+                raise ValueError("a device-resident rho needs a constant nu")
+            vm = bool(cfg.vector_metric) and ncomp == 3 and getattr(grid, "metric", "cartesian") == mesh.SPHERICAL
+            _lib.check(L.pc_op_create_viscous(dg.handle, ncomp, int(vm), float(cfg.nu), cfg.rho.handle, byref(h)),
+                       "pc_op_create_viscous")
+            self._keep.append(cfg.rho)
+        elif op.kind == "scalar":
             nu = _values(cfg.nu, grid, "nu")
             rho = None if cfg.rho is None else _values(cfg.rho, grid, "rho")
             if isinstance(rho, float) and rho == 1.0:
                 rho = None
-            if isinstance(nu, float) and (rho is None or isinstance(rho, float)):
+            viscous = isinstance(nu, float) and rho is not None and not isinstance(rho, float)
+            if viscous:  # D = nu * rho formed per node on the device (no D array)
+                Dc, Dd = nu, None
+                if nu < 0:
+                    raise ValueError("nu*rho must be >= 0")
+            elif isinstance(nu, float) and (rho is None or isinstance(rho, float)):
                 Dc = nu if rho is None else nu * rho
                 Dd = None
                 if rho is not None:  # constant rho != 1: F = (1/rho) div(nu rho grad u)
@@ -192,21 +205,33 @@ class DeviceOperator:
             vm = bool(cfg.vector_metric) and ncomp == 3 and getattr(grid, "metric", "cartesian") == mesh.SPHERICAL
             if cfg.vector_metric and ncomp != 3:
                 raise ValueError("vector_metric needs a 3-component field")
-            _lib.check(L.pc_op_create_scalar(dg.handle, ncomp, int(vm), float(Dc),
-                                             Dd.handle if Dd is not None else None,
-                                             rd.handle if rd is not None else None, byref(h)),
-                       "pc_op_create_scalar")
+            if viscous:
+                _lib.check(L.pc_op_create_viscous(dg.handle, ncomp, int(vm), float(Dc), rd.handle, byref(h)),
+                           "pc_op_create_viscous")
+            else:
+                _lib.check(L.pc_op_create_scalar(dg.handle, ncomp, int(vm), float(Dc),
+                                                 Dd.handle if Dd is not None else None,
+                                                 rd.handle if rd is not None else None, byref(h)),
+                           "pc_op_create_scalar")
         else:
             if ncomp != 1:
                 raise ValueError("aligned conduction acts on a scalar temperature")
-            b = np.asarray(getattr(cfg.b_hat, "values", cfg.b_hat), dtype=float)
-            b = b.reshape(tuple(grid.shape) + (3,)) if b.size == 3 * grid.npoints else b
-            if b.shape != tuple(grid.shape) + (3,):
-                raise ValueError("b_hat needs 3 components")
-            bd = device.DeviceField.from_values(dg, b, 3)
+            if isinstance(cfg.b_hat, device.DeviceField):
+                bd = cfg.b_hat
+                if bd.ncomp != 3:
+                    raise ValueError("b_hat needs 3 components")
+            else:
+                b = np.asarray(getattr(cfg.b_hat, "values", cfg.b_hat), dtype=float)
+                b = b.reshape(tuple(grid.shape) + (3,)) if b.size == 3 * grid.npoints else b
+                if b.shape != tuple(grid.shape) + (3,):
+                    raise ValueError("b_hat needs 3 components")
+                bd = device.DeviceField.from_values(dg, b, 3)
             self._keep.append(bd)
             rd = None
-            if cfg.rho is not None and not (isinstance(cfg.rho, (int, float)) and float(cfg.rho) == 1.0):
+            if isinstance(cfg.rho, device.DeviceField):
+                rd = cfg.rho
+                self._keep.append(rd)
+            elif cfg.rho is not None and not (isinstance(cfg.rho, (int, float)) and float(cfg.rho) == 1.0):
                 rho_a = _values(cfg.rho, grid, "rho")
                 rho_a = rho_a if not isinstance(rho_a, float) else np.full(tuple(grid.shape), rho_a)
                 if np.any(~(rho_a > 0)):

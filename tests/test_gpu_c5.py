@@ -1,0 +1,75 @@
+"""C5 (coupled conduction + viscosity, rho = exp(-10 (r - 1))) at reduced size:
+the device-generated inputs are bitwise the host recipes (configs.py), and one
+split MAS step matches the oracle bit for bit (cycle and stage counts, both
+fields)."""
+import numpy as np
+import pytest
+
+from helpers import oracle_aligned, oracle_scalar, soa
+from oracle import operators as oops
+from oracle import ptl as optl
+from paper_2403_01004_b200 import configs, device, operators, ptl, schemes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c5s():
+    return configs.c5(n=(16, 20, 32), host=True)
+
+
+def test_device_generation_bitwise(gpu_ctx, c5s):
+    dg = device.device_grid(c5s.grid, c5s.bc, gpu_ctx)
+    T = configs.gen_temperature(device.DeviceField(dg, 1), c5s.grid, c5s.seed)
+    b = configs.gen_dipole(device.DeviceField(dg, 3), c5s.grid, c5s.seed)
+    v = configs.gen_harmonic(device.DeviceField(dg, 3), c5s.grid, c5s.seed)
+    rho = configs.gen_radial(device.DeviceField(dg, 1), c5s.meta["rho_r"])
+    assert np.array_equal(T.download()[..., 0], c5s.fields["T"])
+    assert np.array_equal(b.download(), c5s.fields["b"])
+    assert np.array_equal(v.download(), c5s.fields["v"])
+    assert np.array_equal(rho.download()[..., 0], c5s.fields["rho"])
+
+
+def test_viscous_rho_field_apply_bitwise(gpu_ctx, c5s):
+    rho = c5s.fields["rho"]
+    cfg = operators.ScalarDiffusionConfig(nu=1.0, rho=rho, bc=c5s.bc, vector_metric=True)
+    op = operators.DiffusionOperator.scalar(cfg, 3)
+    v = operators.Field(c5s.grid, c5s.fields["v"])
+    F = op.apply(v)
+    oop = oracle_scalar(c5s.grid, c5s.bc, nu=1.0, rho=rho, ncomp=3, vector_metric=True)
+    assert np.array_equal(np.moveaxis(F.values, -1, 0), oop.apply(soa(c5s.fields["v"])))
+    assert op.device_op(c5s.grid, 3).dt_euler == oop.euler_dt()
+
+
+def test_c5_split_step_parity(gpu_ctx, c5s):
+    w = c5s
+    dg = device.device_grid(w.grid, w.bc, gpu_ctx)
+    rho_d = configs.gen_radial(device.DeviceField(dg, 1), w.meta["rho_r"])
+    b_d = configs.gen_dipole(device.DeviceField(dg, 3), w.grid, w.seed)
+    T_d = configs.gen_temperature(device.DeviceField(dg, 1), w.grid, w.seed)
+    v_d = configs.gen_harmonic(device.DeviceField(dg, 3), w.grid, w.seed)
+    cond = operators.DiffusionOperator.aligned(
+        operators.AlignedConductionConfig(b_hat=b_d, rho=rho_d, m_p=3.0, k_B=1.0, bc=w.bc))
+    visc = operators.DiffusionOperator.scalar(
+        operators.ScalarDiffusionConfig(nu=1.0, rho=rho_d, bc=w.bc, vector_metric=True), 3)
+    cond.freeze(T_d)
+    dtE = min(cond.device_op(w.grid, 1).dt_euler, visc.device_op(w.grid, 3).dt_euler)
+    outer = 200.0 * dtE
+    sc = schemes.SchemeConfig("rkl2")
+    state, reps = ptl.split_advance([("T", cond), ("v", visc)], {"T": T_d, "v": v_d}, outer,
+                                    [(sc, ptl.PtlConfig()), (sc, ptl.PtlConfig())])
+    # oracle
+    oc = oracle_aligned(w.grid, w.bc, w.fields["b"], w.fields["T"], rho=w.fields["rho"])
+    ov = oracle_scalar(w.grid, w.bc, nu=1.0, rho=w.fields["rho"], ncomp=3, vector_metric=True)
+
+    def refresh(op, st):
+        op.c = oops.aligned_coefficient(st["T"][0])
+
+    ost, oreps = optl.split_advance([("T", oc), ("v", ov)], {"T": soa(w.fields["T"][..., None]),
+                                                             "v": soa(w.fields["v"])}, outer,
+                                    [optl.OracleScheme("rkl2")] * 2, refresh=refresh)
+    for rep, orep in zip(reps, oreps):
+        assert [e.iters for e in rep.entries] == [r.iters for r in orep]
+        assert [e.dt for e in rep.entries] == [r.dt for r in orep]
+    assert np.array_equal(state["T"].download()[..., 0], ost["T"][0])
+    assert np.array_equal(np.moveaxis(state["v"].download(), -1, 0), ost["v"])
