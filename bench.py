@@ -306,6 +306,7 @@ def run_ours(args, rank, world, local_rank):
     dom = max(rows, key=lambda r: r["ms"]) if rows else None
     peak, peak_src = _peaks()
 
+    ops_info = [(f, op.kind, nc) for f, op, nc, _ in prob.ops]
     e2e = None
     if args.e2e:
         e2e = run_e2e(args, prob, sc, pcfg, ctx, dist)
@@ -333,11 +334,11 @@ def run_ours(args, rank, world, local_rank):
                 "config": name.upper(),
                 "grid": list(prob.dg.global_shape),
                 "cells": cells_global,
-                "fields": {f: nc for f, _, nc, _ in prob.ops},
+                "fields": {f: nc for f, _, nc in ops_info},
                 "scheme": sc.kind + "+PTL",
                 "outer_dt_over_dtE": prob.w.ratio,
-                "operators": [{"field": f, "kind": op.kind, "cycles": r.n_cycles,
-                               "stages_or_iters": r.total_iters} for (f, op, _, _), r in zip(prob.ops, rep0)],
+                "operators": [{"field": f, "kind": kd, "cycles": r.n_cycles,
+                               "stages_or_iters": r.total_iters} for (f, kd, _), r in zip(ops_info, rep0)],
                 "cell_updates_per_step": total_cu // max(args.steps, 1),
                 "decomposition": f"r-slabs x{world}" if world > 1 else "single GPU",
                 "l2": "inputs larger than L2 (each field %.0f MB > 126 MB)" % (cells_global * 8 / 1e6)

@@ -22,6 +22,7 @@
 #include "../../include/paracycle_b200.h"
 #include "gen.cuh"
 #include "march.cuh"
+#include "smarch.cuh"
 #include "nccl_shim.h"
 
 using namespace pc;
@@ -794,6 +795,46 @@ static int launch_march(pc_op* op, const double* Tin, const Epi& epi, const int*
   return check_launch(what);
 }
 
+// ---- 7-point marching kernels (ScalarOp), dispatched on (ncomp, vector, D mode)
+static int smarch_R(const pc_grid* g) {
+  const int tiles = ((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + SMJ - 1) / SMJ);
+  int R = 32;
+  while (R > 4 && (int64_t)tiles * ((g->g.n0 + R - 1) / R) < 148 * 12) R /= 2;
+  return R;
+}
+static bool smarch_ok(const pc_op* op) { return op->ncomp == 1 || op->ncomp == 3; }
+template <int NC, bool VEC, int DM, class Epi>
+static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, const char* what) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int R = smarch_R(g);
+  dim3 grid((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + SMJ - 1) / SMJ, (g->g.n0 + R - 1) / R);
+  if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_scalar_march<NC, VEC, DM, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(SMarchSmem<NC>)));
+    attr = true;
+  }
+  k_scalar_march<NC, VEC, DM, Epi><<<grid, SNT, sizeof(SMarchSmem<NC>), c->s>>>(g->g, op->so, u.p[0], u.p[1], u.p[2],
+                                                                                epi, R, skip);
+  c->st.launches++;
+  return check_launch(what);
+}
+template <int NC, class Epi>
+static int launch_smarch_nc(pc_op* op, CFld u, const Epi& epi, const char* what) {
+  const int dm = op->so.drho ? 2 : (op->so.D ? 1 : 0);
+  const bool vec = NC == 3 && op->so.vector;
+  if (vec) {
+    if (dm == 0) return launch_smarch_t<NC, true, 0>(op, u, epi, nullptr, what);
+    if (dm == 1) return launch_smarch_t<NC, true, 1>(op, u, epi, nullptr, what);
+    return launch_smarch_t<NC, true, 2>(op, u, epi, nullptr, what);
+  }
+  if (dm == 0) return launch_smarch_t<NC, false, 0>(op, u, epi, nullptr, what);
+  if (dm == 1) return launch_smarch_t<NC, false, 1>(op, u, epi, nullptr, what);
+  return launch_smarch_t<NC, false, 2>(op, u, epi, nullptr, what);
+}
+
 template <class Op>
 static int launch_apply(pc_op* op, const Op& o, CFld u, Fld F, bool argmax) {
   pc_grid* g = op->grid;
@@ -815,6 +856,18 @@ static int apply_any(pc_op* op, CFld u, Fld F, bool argmax) {
       return launch_march(op, u.p[0], e, nullptr, "k_aligned_march<argmax>");
     }
     return launch_march(op, u.p[0], EpiStore{F.p[0]}, nullptr, "k_aligned_march<apply>");
+  }
+  if (smarch_ok(op)) {
+    pc_ctx* c = op->grid->ctx;
+    if (argmax) {
+      SEpiArgmax e{{F.p[0], F.p[1], F.p[2]}, c->red_v, c->red_i, c->counter, c->res,
+                   ArgMax{-1.0, 0x7fffffffffffffffLL}, op->ncomp};
+      return op->ncomp == 3 ? launch_smarch_nc<3>(op, u, e, "k_scalar_march<argmax>")
+                            : launch_smarch_nc<1>(op, u, e, "k_scalar_march<argmax>");
+    }
+    SEpiStore e{{F.p[0], F.p[1], F.p[2]}};
+    return op->ncomp == 3 ? launch_smarch_nc<3>(op, u, e, "k_scalar_march<apply>")
+                          : launch_smarch_nc<1>(op, u, e, "k_scalar_march<apply>");
   }
   return launch_apply(op, op->so, u, F, argmax);
 }
@@ -993,6 +1046,18 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     if constexpr (std::is_same<Op, AlignedOp>::value) {
       EpiStage e{m2.p[0], cfld(u).p[0], y0.base(0), out->base(0), sc, k, c->bad};
       rc = launch_march(op, um1->base(0), e, nullptr, "k_aligned_march<stage>");
+    } else if (smarch_ok(op)) {
+      CFld u0f = cfld(u), y0f = y0.cf();
+      Fld of = out->f();
+      SEpiStage e{{u0f.p[0], u0f.p[1], u0f.p[2]}, {m2.p[0], m2.p[1], m2.p[2]}, {y0f.p[0], y0f.p[1], y0f.p[2]},
+                  {of.p[0], of.p[1], of.p[2]}, nc, sc, k, c->bad};
+      if (nc == 3) {
+        rc = launch_smarch_nc<3>(op, um1->cf(), e, "k_scalar_march<stage>");
+      } else {
+        SEpiStage1 e1;
+        static_cast<SEpiStage&>(e1) = e;
+        rc = launch_smarch_nc<1>(op, um1->cf(), e1, "k_scalar_march<stage>");
+      }
     } else {
       k_stage<<<nb, kThreads, 0, c->s>>>(g->g, o, um1->cf(), m2, cfld(u), y0.cf(), out->f(), sc, k, c->bad);
       c->st.launches++;

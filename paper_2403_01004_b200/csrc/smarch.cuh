@@ -1,0 +1,352 @@
+// r-marching kernel for the 7-point rho-weighted finite-volume operator
+// (ScalarOp: scalar diffusion, and the 3-component viscosity with the
+// spherical frame rotation) -- K1 / K2 of DESIGN.md §4, the C1/C2/C5 stage.
+//
+// A 256-thread block owns an (SMJ x 32) theta-phi tile of an r-chunk and
+// marches along r.  Per plane one cp.async group stages, one plane ahead,
+//   * the NC input components (and the D / rho source) of plane t+2 with a
+//     one-node in-plane halo (wrap / clamp resolved at fill time),
+//   * the per-(r,theta) rows W2[0..2], iV2 of plane t+1,
+//   * the epilogue operands of plane t+1 (thread-private slots),
+// while each thread keeps its node's r-neighbours v(t-1), v(t) (and D) in
+// registers and the four theta/phi frame rotations of its row come from a
+// shared table loaded once.  Every face term is formed exactly as ScalarOp::F
+// forms it (same operands, same order), so the result is bitwise the generic
+// kernel's -- and the oracle's (oracle/operators.py scalar_apply).
+#pragma once
+#include "march.cuh"
+
+namespace pc {
+
+constexpr int SMJ = 8;               // theta rows per tile (one warp per row)
+constexpr int SHJ = SMJ + 2;
+constexpr int SHP = SHJ * MHK;       // halo tile (phi extent MHK = 32 + 2)
+constexpr int SNT = SMJ * MTK;       // threads = tile nodes
+constexpr int SNFILL = (SHP + SNT - 1) / SNT;
+constexpr int SROWT = 5;             // W2[0], W2[1], W2[2], iV2 per (plane, theta row), + W2[1] at j-1 via row - 1
+constexpr int SEO = 9;               // epilogue operands staged per node (max: 3 x u0, um2, y0)
+
+template <int NC>
+struct SMarchSmem {
+  double V[3][NC + 1][SHP];          // planes t, t+1, t+2 (in flight); slot NC = D / rho source
+  double rowt[3][SROWT][SHJ];        // row tables of planes t-1 (r- face), t, t+1 (in flight)
+  double EO[2][SEO][SNT];            // epilogue operands of planes t (read) and t+1 (landing)
+  double M[4][SMJ][9];               // frame rotations t+, t-, p+, p- of the tile rows
+};
+
+// DM: 0 = D constant Dc, 1 = D nodal field, 2 = D = Dc * rho (viscosity)
+template <int NC, bool VEC, int DM, class Epi>
+__global__ void __launch_bounds__(SNT, 3) k_scalar_march(GridDev g, ScalarOp op, const double* __restrict__ u0p,
+                                                         const double* __restrict__ u1p,
+                                                         const double* __restrict__ u2p, Epi epi, int R,
+                                                         const int* skip) {
+  extern __shared__ __align__(16) unsigned char smarch_smem[];
+  SMarchSmem<NC>& S = *reinterpret_cast<SMarchSmem<NC>*>(smarch_smem);
+  if (skip && *skip) return;
+  constexpr bool HASD = DM != 0;
+  const double* uin[3] = {u0p, u1p, u2p};
+  const double* dsrc = DM == 1 ? op.D : op.rho;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * SMJ, i0 = blockIdx.z * R;
+  const int iend = min(i0 + R, g.n0);
+  const int kg = k0 + tx, jg = j0 + ty;
+
+  int foff[SNFILL];
+#pragma unroll
+  for (int q = 0; q < SNFILL; ++q) {
+    const int e = tid + q * SNT;
+    const int hj = e / MHK, hk = e - hj * MHK;
+    bool oj, ok;
+    const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
+    foff[q] = e < SHP ? jj * g.n2 + kk : -1;
+  }
+  const bool rton = tid < SROWT * SHJ;
+  const int rtab = tid / SHJ, rhj = tid - (tid / SHJ) * SHJ;
+  bool rok;
+  const int rjj = map_j(g, j0 - 1 + rhj, rok);
+  const double* rbase = !rton ? g.iV2 : (rtab < 3 ? g.W2[rtab] : g.iV2);
+
+  // rotation table of the tile rows (loaded once; rows beyond n1 clamp)
+  if (VEC) {
+    for (int e = tid; e < 4 * SMJ * 9; e += SNT) {
+      const int f = e / (SMJ * 9), r = (e / 9) % SMJ, q = e % 9;
+      const int jr = min(j0 + r, g.n1 - 1);
+      S.M[f][r][q] = __ldg(g.M[f] + (int64_t)jr * 9 + q);
+    }
+  }
+
+  bool oko, ojo;
+  const int km = map_k(g, kg, oko);
+  map_j(g, jg, ojo);
+  const bool inside = jg < g.n1 && kg < g.n2;
+  (void)ojo;
+  // column constants: g1[0](k), g1[1](k), g1[2](k), g1[2](k-1), igv(k)
+  bool okkm;
+  const int kmm = nb2(g, km, -1, okkm);
+  const double g10 = launder(__ldg(g.g1[0] + km)), g11 = launder(__ldg(g.g1[1] + km));
+  const double g12 = launder(__ldg(g.g1[2] + km)), g12m = launder(okkm ? __ldg(g.g1[2] + kmm) : 0.0);
+  const double igv = launder(__ldg(g.igv + km));
+  bool okjm;
+  nb1(g, jg < g.n1 ? jg : g.n1 - 1, -1, okjm);
+  const bool pin_jk = (g.pin_lo1 && jg == 0) || (g.pin_hi1 && jg == g.n1 - 1) || (g.pin_lo2 && kg == 0) ||
+                      (g.pin_hi2 && kg == g.n2 - 1);
+  const int h = (ty + 1) * MHK + (tx + 1);
+  const int onode = jg * g.n2 + kg;
+
+  auto vslot = [&](int p) { return (p - i0 + 1) % 3; };
+  auto rslot = [&](int p) { return (p - i0 + 1) % 3; };
+  auto eslot = [&](int p) { return (p - i0) & 1; };
+  auto issue_V = [&](int p) {
+    const PlaneMap pm = plane_map(g, p);
+    const int64_t base = (int64_t)pm.mem * g.plane;
+    const int sl = vslot(p);
+#pragma unroll
+    for (int q = 0; q < SNFILL; ++q)
+      if (foff[q] >= 0) {
+        const int e = tid + q * SNT;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) cp_async8(&S.V[sl][c][e], uin[c] + base + foff[q]);
+        if (HASD) cp_async8(&S.V[sl][NC][e], dsrc + base + foff[q]);
+      }
+  };
+  auto issue_rows = [&](int p) {
+    if (rton) {
+      const PlaneMap pm = plane_map(g, p);
+      cp_async8(&S.rowt[rslot(p)][rtab][rhj], rbase + row2(g, pm.row, rjj));
+    }
+  };
+  auto issue_ops = [&](int p) {
+    if (Epi::NOPS > 0 && inside) {
+      const int64_t o = (int64_t)p * g.plane + onode;
+      const int es = eslot(p);
+#pragma unroll
+      for (int q = 0; q < Epi::NOPS; ++q) cp_async8(&S.EO[es][q][tid], epi.opnd(q) + o);
+    }
+  };
+
+  // ---- prologue: V(i0-1..i0+1), rows(i0-1, i0), operands(i0)
+  issue_V(i0 - 1);
+  issue_V(i0);
+  if (i0 + 1 <= iend) issue_V(i0 + 1);
+  issue_rows(i0 - 1);
+  issue_rows(i0);
+  issue_ops(i0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+
+  double vm[NC], vc[NC], dm = 0.0, dc = 0.0;
+  {
+    const int s0 = vslot(i0 - 1), s1 = vslot(i0);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      vm[c] = S.V[s0][c][h];
+      vc[c] = S.V[s1][c][h];
+    }
+    if (HASD) {
+      dm = S.V[s0][NC][h];
+      dc = S.V[s1][NC][h];
+    }
+  }
+  const int jr = ty + 1;  // row-table index of the own row (halo row 0 = j0 - 1)
+
+#pragma unroll 1
+  for (int t = i0; t < iend; ++t) {
+    if (t + 2 <= iend) issue_V(t + 2);
+    if (t + 1 <= iend) issue_rows(t + 1);
+    if (t + 1 < iend) issue_ops(t + 1);
+    cp_async_commit();
+
+    const int sc = vslot(t), sp = vslot(t + 1), rs = rslot(t), rm = rslot(t - 1), es = eslot(t);
+    const PlaneMap pmm = plane_map(g, t - 1);
+    const bool okim = pmm.exists;  // r- neighbour exists
+    double vp[NC], dp = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) vp[c] = S.V[sp][c][h];
+    if (HASD) dp = S.V[sp][NC][h];
+    if (inside) {
+      const int ig = t + g.i0g;
+      const bool pin = pin_jk || (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
+      const double Dcen = DM == 0 ? op.Dc : (DM == 1 ? dc : op.Dc * dc);
+      // face coefficients W*g (ScalarOp::wg): faces (a, -), (a, +) for a = 0, 1, 2
+      double coef[3][2];
+      coef[0][0] = okim ? S.rowt[rm][0][jr] * g10 : 0.0;
+      coef[0][1] = S.rowt[rs][0][jr] * g10;
+      coef[1][0] = okjm ? S.rowt[rs][1][jr - 1] * g11 : 0.0;
+      coef[1][1] = S.rowt[rs][1][jr] * g11;
+      coef[2][0] = okkm ? S.rowt[rs][2][jr] * g12m : 0.0;
+      coef[2][1] = S.rowt[rs][2][jr] * g12;
+      // neighbour values (self where missing: staging clamps) and D
+      double nv[3][2][NC], nd[3][2];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        nv[0][0][c] = vm[c];
+        nv[0][1][c] = vp[c];
+        nv[1][0][c] = S.V[sc][c][h - MHK];
+        nv[1][1][c] = S.V[sc][c][h + MHK];
+        nv[2][0][c] = S.V[sc][c][h - 1];
+        nv[2][1][c] = S.V[sc][c][h + 1];
+      }
+      if (HASD) {
+        nd[0][0] = dm;
+        nd[0][1] = dp;
+        nd[1][0] = S.V[sc][NC][h - MHK];
+        nd[1][1] = S.V[sc][NC][h + MHK];
+        nd[2][0] = S.V[sc][NC][h - 1];
+        nd[2][1] = S.V[sc][NC][h + 1];
+      }
+      double Sx[NC];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          double cf;
+          if (HASD) {
+            const double Dn = DM == 1 ? nd[a][tt] : op.Dc * nd[a][tt];
+            cf = (0.5 * (Dcen + Dn)) * coef[a][tt];
+          } else {
+            cf = op.Dc * coef[a][tt];
+          }
+          const bool first = (a == 0 && tt == 0);
+          if (VEC && a > 0) {
+            const double* M = S.M[(a == 1 ? 0 : 2) + (tt == 1 ? 0 : 1)][ty];
+            const double v0 = nv[a][tt][0], v1 = nv[a][tt][NC > 1 ? 1 : 0], v2 = nv[a][tt][NC > 2 ? 2 : 0];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              const double rv = ((M[3 * c] * v0) + (M[3 * c + 1] * v1)) + (M[3 * c + 2] * v2);
+              const double term = cf * (rv - vc[c]);
+              Sx[c] = first ? term : Sx[c] + term;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              const double term = cf * (nv[a][tt][c] - vc[c]);
+              Sx[c] = first ? term : Sx[c] + term;
+            }
+          }
+        }
+      }
+      const double iv = S.rowt[rs][3][jr] * igv;
+      const int64_t o = (int64_t)t * g.plane + onode;
+      double f[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double x = Sx[c] * iv;
+        if (op.rho) x = x / (DM == 2 ? dc : __ldg(op.rho + o));
+        f[c] = pin ? 0.0 : x;
+      }
+      double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
+#pragma unroll
+      for (int q = 0; q < Epi::NOPS; ++q) ov[q] = S.EO[es][q][tid];
+      epi.template apply<NC>(g, t, jg, kg, o, f, vc, pin, ov);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      vm[c] = vc[c];
+      vc[c] = vp[c];
+    }
+    if (HASD) {
+      dm = dc;
+      dc = dp;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  epi.finish(g);
+}
+
+// ---- epilogues of the 7-point march (NC components per node) --------------
+struct SEpiStore {
+  static constexpr int NOPS = 0;
+  double* F[3];
+  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  template <int NC>
+  __device__ __forceinline__ void apply(const GridDev&, int, int, int, int64_t o, const double (&f)[NC],
+                                        const double (&)[NC], bool, const double*) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) F[c][o] = f[c];
+  }
+  __device__ __forceinline__ void finish(const GridDev&) {}
+};
+
+// fused RKL2/RKG2 stage: operands u0[c], um2[c], y0[c] staged per node
+struct SEpiStage {
+  static constexpr int NOPS_MAX = 9;
+  static constexpr int NOPS = 9;  // (3 x NC used; NC = 1 stages slots 0..2 only -- see make_sepi_stage)
+  const double* u0[3];
+  const double* um2[3];
+  const double* y0[3];
+  double* out[3];
+  int nc;
+  StageCoef sc;
+  int stage;
+  int* bad;
+  __device__ __forceinline__ const double* opnd(int q) const {
+    const int c = q / 3, w = q % 3;
+    return w == 0 ? u0[c] : (w == 1 ? um2[c] : y0[c]);
+  }
+  template <int NC>
+  __device__ __forceinline__ void apply(const GridDev&, int, int, int, int64_t o, const double (&f)[NC],
+                                        const double (&um1)[NC], bool pin, const double* ov) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double a0 = ov[3 * c];
+      double v = ((((sc.mu * um1[c]) + (sc.nu * ov[3 * c + 1])) + (sc.kap * a0)) + (sc.mtdt * f[c])) +
+                 (sc.gtdt * ov[3 * c + 2]);
+      v = pin ? a0 : v;
+      out[c][o] = v;
+      if (!isfinite(v)) atomicMin(bad, stage);
+    }
+  }
+  __device__ __forceinline__ void finish(const GridDev&) {}
+};
+// one-component variant (only 3 operand slots are staged)
+struct SEpiStage1 : SEpiStage {
+  static constexpr int NOPS = 3;
+};
+
+struct SEpiArgmax {  // y0 = F(u0) with the |F| argmax over points x components (PTL)
+  static constexpr int NOPS = 0;
+  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  double* F[3];
+  double* pv;
+  long long* pi;
+  unsigned int* counter;
+  ArgRes* res;
+  ArgMax best;
+  int ncomp;
+  template <int NC>
+  __device__ __forceinline__ void apply(const GridDev& g, int i, int j, int k, int64_t o, const double (&f)[NC],
+                                        const double (&)[NC], bool, const double*) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      F[c][o] = f[c];
+      best = am_better(best, ArgMax{fabs(f[c]), aos_index(g, i, j, k, c, NC)});
+    }
+  }
+  __device__ __forceinline__ void finish(const GridDev&) {
+    __shared__ double shv[SNT / 32];
+    __shared__ long long shi[SNT / 32];
+    const int tid = threadIdx.x;
+    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int nblk = gridDim.x * gridDim.y * gridDim.z;
+    ArgMax b = block_argmax<SNT>(best, shv, shi);
+    if (tid == 0) {
+      pv[bid] = b.v;
+      pi[bid] = b.i;
+    }
+    if (last_block3(counter, nblk)) {
+      ArgMax r{-1.0, 0x7fffffffffffffffLL};
+      for (int q = tid; q < nblk; q += SNT) r = am_better(r, ArgMax{pv[q], pi[q]});
+      r = block_argmax<SNT>(r, shv, shi);
+      if (tid == 0) {
+        res->fmax = r.v;
+        res->kidx = r.i;
+        *counter = 0u;
+      }
+    }
+  }
+};
+
+}  // namespace pc
