@@ -23,6 +23,9 @@
 #include "gen.cuh"
 #include "march.cuh"
 #include "smarch.cuh"
+#include "tma_march.cuh"
+
+#include <cudaTypedefs.h>
 #include "nccl_shim.h"
 
 using namespace pc;
@@ -128,6 +131,8 @@ struct pc_op {
   bool diag_valid = false;
   double* kfc = nullptr;    // kappa0 * f_c(r) per axis-0 row (n0 + 2)
   double Tfloor = 1e-10;
+  bool beta_maps = false;   // cached TMA maps of beta (the buffer never moves)
+  CUtensorMap bmap[3], bsmap[3];
   double lam_max = 0.0;
   double dt_euler = INFINITY;
   bool frozen = false;
@@ -777,8 +782,79 @@ static int march_R(const pc_grid* g) {
 static dim3 march_grid(const pc_grid* g, int R) {
   return dim3((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + MTJ - 1) / MTJ, (g->g.n0 + R - 1) / R);
 }
+// ---- TMA (bulk tensor copy) maps over a field component [n0+2][n1][n2]
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static int state = 0;
+  if (state == 0) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && p) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+      state = 1;
+    } else {
+      state = -1;
+    }
+  }
+  return fn;
+}
+// base = first interior element (plane 0); the tensor starts at ghost plane -1
+static int make_field_map(CUtensorMap* m, const double* base, const GridDev& g, unsigned box0, unsigned box1) {
+  auto enc = tma_encoder();
+  if (!enc) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const double* alloc = base - g.plane;
+  cuuint64_t dims[3] = {(cuuint64_t)g.n2, (cuuint64_t)g.n1, (cuuint64_t)g.n0 + 2};
+  cuuint64_t strides[2] = {(cuuint64_t)g.n2 * 8, (cuuint64_t)g.plane * 8};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(alloc), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return PC_OK;
+}
+static bool tma_ok(const pc_grid* g) {
+  const GridDev& d = g->g;
+  return d.per2 && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && tma_encoder() != nullptr &&
+         getenv("PC_NO_TMA") == nullptr;
+}
+template <class Epi>
+static int launch_tma(pc_op* op, const double* Tin, const Epi& epi, const int* skip, const char* what) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int R = march_R(g);
+  dim3 grid = march_grid(g, R);
+  if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
+  TmaMaps maps;
+  if (!op->beta_maps) {
+    for (int q = 0; q < 3; ++q) {
+      TRY(make_field_map(&op->bmap[q], op->ao.beta[q], g->g, MTK, MHJ));
+      TRY(make_field_map(&op->bsmap[q], op->ao.beta[q], g->g, 2, MHJ));
+    }
+    op->beta_maps = true;
+  }
+  for (int q = 0; q < 3; ++q) {
+    maps.B[q] = op->bmap[q];
+    maps.BS[q] = op->bsmap[q];
+  }
+  TRY(make_field_map(&maps.T, Tin, g->g, MTK, MHJ));
+  TRY(make_field_map(&maps.TS, Tin, g->g, 2, MHJ));
+  for (int q = 0; q < Epi::NOPS; ++q) TRY(make_field_map(&maps.O[q], epi.opnd(q), g->g, MTK, MTJ));
+  const int smem = (int)sizeof(TmaSmem) + 128;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_aligned_tma<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_aligned_tma<Epi><<<grid, dim3(MTK, MTY), smem, c->s>>>(g->g, op->ao, maps, epi, R, skip);
+  c->st.launches++;
+  return check_launch(what);
+}
+
 template <class Epi>
 static int launch_march(pc_op* op, const double* Tin, const Epi& epi, const int* skip, const char* what) {
+  if (tma_ok(op->grid)) return launch_tma(op, Tin, epi, skip, what);
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   const int R = march_R(g);
