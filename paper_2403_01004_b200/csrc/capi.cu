@@ -85,6 +85,7 @@ struct pc_ctx {
   int* bad = nullptr;
   unsigned long long* minbits = nullptr;
   double* maxout = nullptr;
+  double* gath = nullptr;  // per-rank (|F| max, index) pairs
   // pinned host mirrors
   ArgRes* h_res = nullptr;
   PcgDev* h_pcg = nullptr;
@@ -259,6 +260,23 @@ static int halo_work(pc_grid* g, Work& w) {
   double* b[3] = {w.b[0], w.b[1], w.b[2]};
   return halo_exchange(g->ctx, g, b, w.ncomp);
 }
+static int allreduce_u64_min(pc_ctx* c, unsigned long long* dptr) {
+  if (c->nranks <= 1) return PC_OK;
+  nccl::Api* A = nccl::api();
+  if (!A || A->allReduce(dptr, dptr, 1, nccl::kUint64, nccl::kMin, c->comm, c->s) != 0)
+    return fail(PC_E_NCCL, "ncclAllReduce(u64 min)");
+  return PC_OK;
+}
+// the |F| argmax over all ranks (res holds this rank's pair on entry)
+static int global_argmax(pc_ctx* c) {
+  if (c->nranks <= 1) return PC_OK;
+  nccl::Api* A = nccl::api();
+  if (!A || !A->allGather_ || A->allGather(c->res, c->gath, 2, nccl::kDouble, c->comm, c->s) != 0)
+    return fail(PC_E_NCCL, "ncclAllGather(argmax)");
+  k_argmax_combine<<<1, 32, 0, c->s>>>(c->gath, c->nranks, c->res);
+  c->st.launches++;
+  return check_launch("k_argmax_combine");
+}
 static int allreduce_d(pc_ctx* c, double* dptr, size_t n, int op) {
   if (c->nranks <= 1) return PC_OK;
   nccl::Api* A = nccl::api();
@@ -302,6 +320,7 @@ int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx
   CUDA_TRY(cudaMalloc(&c->bad, sizeof(int)));
   CUDA_TRY(cudaMalloc(&c->minbits, sizeof(unsigned long long)));
   CUDA_TRY(cudaMalloc(&c->maxout, sizeof(double)));
+  CUDA_TRY(cudaMalloc(&c->gath, sizeof(double) * 2 * nranks));
   CUDA_TRY(cudaMallocHost(&c->h_res, sizeof(ArgRes)));
   CUDA_TRY(cudaMallocHost(&c->h_pcg, sizeof(PcgDev)));
   CUDA_TRY(cudaMallocHost(&c->h_bad, sizeof(int)));
@@ -342,6 +361,7 @@ int pc_ctx_destroy(pc_ctx* c) {
   cudaFree(c->bad);
   cudaFree(c->minbits);
   cudaFree(c->maxout);
+  cudaFree(c->gath);
   cudaFree(c->staging);
   cudaFreeHost(c->h_res);
   cudaFreeHost(c->h_pcg);
@@ -964,17 +984,24 @@ int pc_op_apply(pc_op* op, const pc_field* u, pc_field* F) {
 }
 
 // ------------------------------------------------------------------ PTL
-static int ptl_device(pc_grid* g, int ncomp, CFld u, CFld F, double eps_rel, int check_all) {
+// Eq. 5 after the |F| argmax.  r-slabs: the argmax pairs are allgathered and
+// combined (lowest global index on ties), F's ghost planes are exchanged so the
+// owner of k sees its r-neighbours, and the candidate minimum is allreduced.
+static int ptl_device(pc_grid* g, int ncomp, CFld u, CFld F, double* const* Fbufs, double eps_rel, int check_all) {
   pc_ctx* c = g->ctx;
+  TRY(global_argmax(c));
+  if (c->nranks > 1 && Fbufs) TRY(halo_exchange(c, g, Fbufs, ncomp));
   if (check_all) {
     CUDA_TRY(cudaMemsetAsync(c->minbits, 0x7f, sizeof(unsigned long long), c->s));  // huge positive
     k_ptl_all<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, ncomp, u, F, eps_rel, c->res, c->minbits);
     c->st.launches++;
     TRY(check_launch("k_ptl_all"));
+    TRY(allreduce_u64_min(c, c->minbits));
   } else {
     k_ptl_pairs<<<1, 32, 0, c->s>>>(g->g, ncomp, u, F, eps_rel, c->res);
     c->st.launches++;
     TRY(check_launch("k_ptl_pairs"));
+    TRY(allreduce_d(c, &c->res->ptl, 1, nccl::kMin));
   }
   return PC_OK;
 }
@@ -996,8 +1023,8 @@ static int ptl_read(pc_ctx* c, int check_all, int use_ptl, double* ptl, int* lim
     *limited = (bits != 0x7f7f7f7f7f7f7f7fULL && std::isfinite(v)) ? 1 : 0;
     *ptl = *limited ? v : INFINITY;
   } else {
-    *limited = c->h_res->limited;
-    *ptl = c->h_res->limited ? c->h_res->ptl : INFINITY;
+    *limited = std::isfinite(c->h_res->ptl) ? 1 : 0;  // (the allreduced minimum)
+    *ptl = *limited ? c->h_res->ptl : INFINITY;
   }
   return PC_OK;
 }
@@ -1008,12 +1035,13 @@ int pc_ptl(pc_grid* g, const pc_field* u, const pc_field* F, double eps_rel, int
     return fail(PC_E_INVALID, "bad PTL arguments");
   if (!(eps_rel > 0.0)) return fail(PC_E_INVALID, "eps_rel must be > 0");
   pc_ctx* c = g->ctx;
-  if (c->nranks > 1) return fail(PC_E_INVALID, "pc_ptl is single-rank; use pc_cycle");
   k_argmax<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, u->ncomp, cfld(F), c->red_v, c->red_i,
                                                           c->counter, c->res);
   c->st.launches++;
   TRY(check_launch("k_argmax"));
-  TRY(ptl_device(g, u->ncomp, cfld(u), cfld(F), eps_rel, check_all));
+  TRY(halo_field(const_cast<pc_field*>(u)));
+  double* Fb[3] = {F->buf[0], F->buf[1], F->buf[2]};
+  TRY(ptl_device(g, u->ncomp, cfld(u), cfld(F), Fb, eps_rel, check_all));
   return ptl_read(c, check_all, 1, ptl, limited, kidx);
 }
 
@@ -1226,6 +1254,15 @@ int pc_step_euler(pc_op* op, pc_field* u, double dt) {
 }
 
 // ------------------------------------------------------------------ PCG
+// r-slabs: finish a PCG reduction after the allreduce of the local sums
+static int pcg_split_fin(pc_ctx* c, int mode, int nred, double tol, int it) {
+  if (c->nranks <= 1) return PC_OK;
+  TRY(allreduce_d(c, c->pcg->red, (size_t)nred, nccl::kSum));
+  k_pcg_fin<<<1, 1, 0, c->s>>>(c->pcg, mode, tol, it);
+  c->st.launches++;
+  return check_launch("k_pcg_fin");
+}
+
 template <class Op>
 static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld b, pc_field* x, double tol,
                    int max_iter, int* iters, double* relres, int* converged) {
@@ -1240,11 +1277,14 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   const double* dg = op->dbuf + g->g.plane;
   const int nb = node_blocks(c, g->g);
   int rc = halo_field(x);
+  if (rc == PC_OK && cudaMemsetAsync(&c->pcg->split, c->nranks > 1 ? 1 : 0, sizeof(int), c->s) != cudaSuccess)
+    rc = fail(PC_E_CUDA, "PCG state");
   if (rc == PC_OK) {
     k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, c->red_v, c->red_v2,
                                           c->counter, c->pcg);
     c->st.launches++;
     rc = check_launch("k_pcg_init");
+    if (rc == PC_OK) rc = pcg_split_fin(c, 0, 2, tol, 0);
   }
   Work* pold = &p0;
   Work* pnew = &p1;
@@ -1272,18 +1312,24 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         EpiMatvec e{Ap.base(0), adiag, dt, c->red_v, c->counter, c->pcg, op->ao, 0.0};
         const int* done = reinterpret_cast<const int*>(reinterpret_cast<const char*>(c->pcg) + offsetof(PcgDev, done));
         rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
+        if (rc == PC_OK) rc = pcg_split_fin(c, 1, 1, tol, it);
+        if (rc) break;
       } else {
         rc = halo_work(g, r);
         if (rc == PC_OK) rc = halo_work(g, *pold);
         if (rc) break;
         k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
                                                 c->red_v, c->counter, c->pcg);
+        rc = check_launch("k_pcg_matvec");
+        if (rc == PC_OK) rc = pcg_split_fin(c, 1, 1, tol, it);
+        if (rc) break;
       }
       k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, tol, it,
                                               c->red_v, c->red_v2, c->counter, c->pcg);
       c->st.launches += std::is_same<Op, AlignedOp>::value ? 1 : 2;  // (march counted at launch)
       c->st.stage_launches += std::is_same<Op, AlignedOp>::value ? 3 : 2;
       rc = check_launch("k_pcg");
+      if (rc == PC_OK) rc = pcg_split_fin(c, 2, 2, tol, it);
       std::swap(pold, pnew);
     }
     if (rc) break;
@@ -1391,11 +1437,8 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
     rc = apply_any(op, cfld(u), y0.f(), true);
     if (rc) break;
     if (use_ptl) {
-      if (c->nranks > 1) {
-        rc = fail(PC_E_INVALID, "multi-rank PTL not enabled in this build");
-        break;
-      }
-      rc = ptl_device(g, op->ncomp, cfld(u), y0.cf(), eps_rel, check_all);
+      double* yb[3] = {y0.b[0], y0.b[1], y0.b[2]};
+      rc = ptl_device(g, op->ncomp, cfld(u), y0.cf(), yb, eps_rel, check_all);
       if (rc) break;
     }
     double ptl;

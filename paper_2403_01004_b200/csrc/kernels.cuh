@@ -155,7 +155,8 @@ __global__ void k_ptl_pairs(GridDev g, int ncomp, CFld u, CFld F, double eps_rel
   const int ki = (int)(t2 / g.n1) - g.i0g;
   double best = INFINITY;
   const int t = threadIdx.x;
-  if (t < 6 * ncomp) {
+  const bool owner = ki >= 0 && ki < g.n0;  // r-slabs: only the owner of k evaluates the pairs
+  if (owner && t < 6 * ncomp) {
     const int dirn = t / ncomp, q = t % ncomp;
     const int a = dirn / 2, d = (dirn & 1) ? 1 : -1;
     bool ok;
@@ -255,8 +256,38 @@ struct PcgDev {
   int it;        // completed iterations
   int done;      // 1 = stop (converged or error)
   int status;    // 0 ok, 1 converged, 2 indefinite, 3 diverged
-  int pad;
+  int split;     // multi-rank: reductions stop at the local sums red[] (allreduced, then k_pcg_fin)
+  double red[2];
 };
+
+__device__ __forceinline__ void pcg_fin_init(PcgDev* st, double rz, double bb) {
+  st->rz = rz;
+  st->bn = sqrt(bb);
+  st->beta = 0.0;
+  st->alpha = 0.0;
+  st->it = 0;
+  st->done = 0;
+  st->status = 0;
+  st->rel = INFINITY;
+}
+__device__ __forceinline__ void pcg_fin_update(PcgDev* st, double rr, double rzn, double tol, int it) {
+  st->it = it;
+  if (!isfinite(rr)) {
+    st->status = 3;
+    st->done = 1;
+  } else {
+    double rn = sqrt(rr);
+    double rel = st->bn > 0.0 ? rn / st->bn : (rn == 0.0 ? 0.0 : INFINITY);
+    st->rel = rel;
+    if (rel <= tol) {
+      st->status = 1;
+      st->done = 1;
+    } else {
+      st->beta = st->rz != 0.0 ? rzn / st->rz : 0.0;
+      st->rz = rzn;
+    }
+  }
+}
 
 // alpha from (p, Ap)_W; breakdown / NaN stop the solve
 __device__ __forceinline__ void pcg_alpha(PcgDev* st, double pAp) {
@@ -286,6 +317,27 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const doubl
     const double z = __ldg(r + o) / dvec;
     pnew[o] = z + beta * __ldg(pold + o);
   }
+}
+
+// multi-rank finish of a PCG reduction after the allreduce of red[]
+__global__ void k_pcg_fin(PcgDev* st, int mode, double tol, int it) {
+  if (mode == 0) pcg_fin_init(st, st->red[0], st->red[1]);
+  else if (st->done) return;
+  else if (mode == 1) pcg_alpha(st, st->red[0]);
+  else pcg_fin_update(st, st->red[0], st->red[1], tol, it);
+}
+
+// global |F| argmax from the per-rank (value, index) pairs (lowest index on ties)
+__global__ void k_argmax_combine(const double* gath, int nranks, ArgRes* res) {
+  if (threadIdx.x != 0) return;
+  ArgMax b{-1.0, 0x7fffffffffffffffLL};
+  for (int r = 0; r < nranks; ++r) {
+    long long idx;
+    memcpy(&idx, gath + 2 * r + 1, sizeof idx);
+    b = am_better(b, ArgMax{gath[2 * r], idx});
+  }
+  res->fmax = b.v;
+  res->kidx = b.i;
 }
 
 // p = z + beta * p_old with z = r / (a + dt*dg)   (recomputed at neighbours)
@@ -339,14 +391,12 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b,
     if (threadIdx.x == 0) {
       double a = 0.0, bb = 0.0;
       for (int t = 0; t < (int)gridDim.x; ++t) { a += p1[t]; bb += p2[t]; }
-      st->rz = a;
-      st->bn = sqrt(bb);
-      st->beta = 0.0;
-      st->alpha = 0.0;
-      st->it = 0;
-      st->done = 0;
-      st->status = 0;
-      st->rel = INFINITY;
+      if (st->split) {
+        st->red[0] = a;
+        st->red[1] = bb;
+      } else {
+        pcg_fin_init(st, a, bb);
+      }
       *counter = 0u;
     }
   }
@@ -380,7 +430,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld 
     if (threadIdx.x == 0) {
       double a = 0.0;
       for (int t = 0; t < (int)gridDim.x; ++t) a += p1[t];
-      pcg_alpha(st, a);
+      if (st->split) st->red[0] = a;
+      else pcg_alpha(st, a);
       *counter = 0u;
     }
   }
@@ -418,21 +469,11 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(GridDev g, Op op, Fld x
     if (threadIdx.x == 0) {
       double rr = 0.0, rzn = 0.0;
       for (int t = 0; t < (int)gridDim.x; ++t) { rr += p1[t]; rzn += p2[t]; }
-      st->it = it;
-      if (!isfinite(rr)) {
-        st->status = 3;
-        st->done = 1;
+      if (st->split) {
+        st->red[0] = rr;
+        st->red[1] = rzn;
       } else {
-        double rn = sqrt(rr);
-        double rel = st->bn > 0.0 ? rn / st->bn : (rn == 0.0 ? 0.0 : INFINITY);
-        st->rel = rel;
-        if (rel <= tol) {
-          st->status = 1;
-          st->done = 1;
-        } else {
-          st->beta = st->rz != 0.0 ? rzn / st->rz : 0.0;
-          st->rz = rzn;
-        }
+        pcg_fin_update(st, rr, rzn, tol, it);
       }
       *counter = 0u;
     }

@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
 struct EpiStore {  // F = op(u)
   static constexpr int NOPS = 0;
   double* F;
-  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double, bool,
                                              const double*) {
     F[o] = f;
@@ -503,7 +503,7 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   StageCoef sc;
   int stage;
   int* bad;
-  __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? u0 : (q == 1 ? um2 : y0); }
+  __host__ __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? u0 : (q == 1 ? um2 : y0); }
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double um1,
                                              bool pin, const double* ov) {
     const double a0 = ov[0];
@@ -549,7 +549,7 @@ __device__ __forceinline__ bool last_block3(unsigned int* counter, int nblk) {
 
 struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
   static constexpr int NOPS = 0;
-  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   double* F;
   double* pv;
   long long* pi;
@@ -588,7 +588,7 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
 // PCG K7: Ap = a p - dt F(p) for the staged p; partial (W p, Ap) -> alpha
 struct EpiMatvec {
   static constexpr int NOPS = 0;
-  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   double* Ap;
   const double* adiag;
   double dt;
@@ -621,7 +621,8 @@ struct EpiMatvec {
       if (tid == 0) {
         double a = 0.0;
         for (int q = 0; q < nblk; ++q) a += p1[q];
-        pcg_alpha(st, a);
+        if (st->split) st->red[0] = a;
+        else pcg_alpha(st, a);
         *counter = 0u;
       }
     }

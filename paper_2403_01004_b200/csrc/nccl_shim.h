@@ -9,7 +9,7 @@ typedef struct ncclComm* ncclComm_t;
 
 namespace nccl {
 
-enum { kDouble = 8 };                         // ncclFloat64
+enum { kUint64 = 5, kDouble = 8 };           // ncclUint64, ncclFloat64
 enum { kSum = 0, kProd = 1, kMax = 2, kMin = 3 };  // ncclRedOp_t
 
 struct UniqueId {

@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(SNT, 3) k_scalar_march(GridDev g, ScalarOp op,
 struct SEpiStore {
   static constexpr int NOPS = 0;
   double* F[3];
-  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   template <int NC>
   __device__ __forceinline__ void apply(const GridDev&, int, int, int, int64_t o, const double (&f)[NC],
                                         const double (&)[NC], bool, const double*) {
@@ -282,7 +282,7 @@ struct SEpiStage {
   StageCoef sc;
   int stage;
   int* bad;
-  __device__ __forceinline__ const double* opnd(int q) const {
+  __host__ __device__ __forceinline__ const double* opnd(int q) const {
     const int c = q / 3, w = q % 3;
     return w == 0 ? u0[c] : (w == 1 ? um2[c] : y0[c]);
   }
@@ -308,7 +308,7 @@ struct SEpiStage1 : SEpiStage {
 
 struct SEpiArgmax {  // y0 = F(u0) with the |F| argmax over points x components (PTL)
   static constexpr int NOPS = 0;
-  __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   double* F[3];
   double* pv;
   long long* pi;
