@@ -228,9 +228,13 @@ class Problem:
         return out
 
     def free(self):
+        """Release the device state (operators hold reference cycles with
+        their device handles: collect them so HBM is returned now)."""
+        import gc
         for f in ("fields", "ops", "b", "rho", "u0", "v0"):
             if hasattr(self, f):
                 delattr(self, f)
+        gc.collect()
 
 
 # ---------------------------------------------------------------- our arm
@@ -386,6 +390,7 @@ def _traffic(name, kind, field):
 
 
 def run_e2e(args, prob, sc, pcfg, ctx, dist):
+    import gc
     """The same metric through ptl.split_advance on HOST Fields: every step
     uploads its inputs (state fields, b-hat, rho) from pinned host memory and
     downloads the advanced fields; the device-resident problem is freed first."""
@@ -419,7 +424,8 @@ def run_e2e(args, prob, sc, pcfg, ctx, dist):
         state = {f: mesh.Field(w.grid, host[f].reshape(tuple(w.grid.shape) + (-1,))) for f in state_names}
         out, reps = ptl.split_advance(ops, state, outer_dt, [(sc, pcfg)] * len(ops))
         cu += cells * sum(r.total_iters for r in reps)
-        del ops, out
+        del ops, out, state
+        gc.collect()  # operator <-> device-handle cycles: return HBM before the next step
     ctx.sync()
     dt = time.perf_counter() - t0
     if dist:

@@ -133,10 +133,16 @@ __device__ __forceinline__ void load_col(const GridDev& g, int k, ColT& c) {
 // all six; else only E_{ONLY_A, ONLY_S} (and only the differences it needs).
 //   Tn[x][0] = T(m + e_x), Tn[x][1] = T(m - e_x) (self if missing)
 //   rw: row tables of the node's (plane, theta row): iL2[6], wo01[4]
+// Edge fluxes of one node in the oracle's order (aligned_E), from the
+// metric values of the node: il2[x][t] (iL2 row part; x < 2 are the full
+// inverse edge lengths, x = 2 is multiplied by the phi column part il1[t]),
+// w01 (wo01 row part), w2 (wo2 column part).  ONLY_A < 0: all six fluxes;
+// else only E_{ONLY_A, ONLY_S} (and only the differences it needs).
+//   Tn[x][0] = T(m + e_x), Tn[x][1] = T(m - e_x) (self if missing)
 template <int ONLY_A, int ONLY_S>
-__device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], const double (&bv)[3],
-                                       const double* rw, int rstride, const double (&il1)[2],
-                                       const double (&w2)[2], double (&E)[3][2]) {
+__device__ __forceinline__ void node_E_core(double Tv, const double (&Tn)[3][2], const double (&bv)[3],
+                                            const double (&il2)[3][2], const double (&w01)[4],
+                                            const double (&il1)[2], const double (&w2)[2], double (&E)[3][2]) {
   double bil[3][2], p[3][2];
 #pragma unroll
   for (int x = 0; x < 3; ++x) {
@@ -144,7 +150,7 @@ __device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], cons
     for (int t = 0; t < 2; ++t) {
       const bool need_p = !(ONLY_A >= 0 && x == ONLY_A && t != ONLY_S);
       const bool need_bil = need_p || (ONLY_A < 0) || (x == ONLY_A && t == ONLY_S);
-      if (need_bil) bil[x][t] = bv[x] * (x < 2 ? rw[(2 * x + t) * rstride] : rw[(2 * x + t) * rstride] * il1[t]);
+      if (need_bil) bil[x][t] = bv[x] * (x < 2 ? il2[x][t] : il2[x][t] * il1[t]);
       if (need_p) p[x][t] = bil[x][t] * (t == 0 ? (Tn[x][0] - Tv) : (Tv - Tn[x][1]));
       else p[x][t] = 0.0;
     }
@@ -158,7 +164,7 @@ __device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], cons
       if (sa != ONLY_S) { f[q] = 0.0; continue; }
     }
     const double sv = (p[0][s0] + p[1][s1]) + p[2][s2];
-    const double om = rw[(6 + s0 * 2 + s1) * rstride] * w2[s2];
+    const double om = w01[s0 * 2 + s1] * w2[s2];
     f[q] = om * sv;
   }
 #pragma unroll
@@ -178,6 +184,39 @@ __device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], cons
       E[a][s] = bil[a][s] * acc;
     }
   }
+}
+
+// row tables laid out [table][row] (stride rstride)
+template <int ONLY_A, int ONLY_S>
+__device__ __forceinline__ void node_E(double Tv, const double (&Tn)[3][2], const double (&bv)[3],
+                                       const double* rw, int rstride, const double (&il1)[2],
+                                       const double (&w2)[2], double (&E)[3][2]) {
+  double il2[3][2], w01[4];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) il2[q >> 1][q & 1] = rw[q * rstride];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) w01[q] = rw[(6 + q) * rstride];
+  node_E_core<ONLY_A, ONLY_S>(Tv, Tn, bv, il2, w01, il1, w2, E);
+}
+// row tables laid out [row][12] (16-byte aligned): pairs come in one LDS.128
+template <int ONLY_A, int ONLY_S>
+__device__ __forceinline__ void node_E_rows(double Tv, const double (&Tn)[3][2], const double (&bv)[3],
+                                            const double* rw, const double (&il1)[2], const double (&w2)[2],
+                                            double (&E)[3][2]) {
+  const double2* r2 = reinterpret_cast<const double2*>(rw);
+  double il2[3][2], w01[4];
+#pragma unroll
+  for (int x = 0; x < 3; ++x) {
+    const double2 v = r2[x];
+    il2[x][0] = v.x;
+    il2[x][1] = v.y;
+  }
+  const double2 wa = r2[3], wb = r2[4];
+  w01[0] = wa.x;
+  w01[1] = wa.y;
+  w01[2] = wb.x;
+  w01[3] = wb.y;
+  node_E_core<ONLY_A, ONLY_S>(Tv, Tn, bv, il2, w01, il1, w2, E);
 }
 
 // Epilogue contract (per tile node n of the thread):

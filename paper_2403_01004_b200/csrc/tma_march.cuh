@@ -40,12 +40,13 @@ struct FluxC {
   double e2p[MTJ][MTK];  // E_{2,+} at cols k0-1 .. k0+30
   double e2m[MTJ][MTK];  // E_{2,-} at cols k0+1 .. k0+32
 };
+constexpr int RW = 12;  // metric row record: iL2[6], wo01[4], iVal2, pad (16-byte aligned pairs)
 struct TmaSmem {
   double T[TSL][XA];
   double B[BSL][3][XA];
   double EO[2][3][XO];
   FluxC E[2];
-  double rowt[RSL][NROWT][MHJ];
+  double rowt[RSL][MHJ][RW];
   double ringcol[2][9];
   unsigned long long bar;
 };
@@ -95,19 +96,18 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * MTJ, i0 = blockIdx.z * R;
   const int iend = min(i0 + R, g.n0);
   const int kg = k0 + tx;
-  const int kL = k0 == 0 ? g.n2 - 2 : k0 - 2;           // strip of columns k0-2, k0-1
-  const int kR = k0 + MTK == g.n2 ? 0 : k0 + MTK;        // strip of columns k0+32, k0+33
+  const int kL = k0 == 0 ? g.n2 - 2 : k0 - 2;     // strip of columns k0-2, k0-1
+  const int kR = k0 + MTK == g.n2 ? 0 : k0 + MTK;  // strip of columns k0+32, k0+33
 
-  // row-table fill slot of this thread: tid < NROWT * MHJ (cp.async)
+  // metric-row fill slot of this thread (cp.async): tid < NROWT * MHJ
   const bool rton = tid < NROWT * MHJ;
   const int rtab = tid / MHJ, rhj = tid - (tid / MHJ) * MHJ;
   bool rok;
   const int rjj = map_j(g, j0 - 1 + rhj, rok);
   const double* rbase = !rton ? g.iVal2 : (rtab < 6 ? g.iL2[rtab] : (rtab < 10 ? g.wo01[rtab - 6] : g.iVal2));
 
-  const int km = kg;  // n2 % 32 == 0: every lane is a node
   ColT col;
-  load_col(g, km, col);
+  load_col(g, kg, col);
 #pragma unroll
   for (int q = 0; q < 2; ++q) col.il1[q] = launder(col.il1[q]);
   col.w2[0] = launder(col.w2[0]);
@@ -167,27 +167,27 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
     map_k(g, gk, rko);
     ring_on = rjo && rko && (ra == 1 ? true : (gj < g.n1));
   }
+  // an interior tile: every own node inside, every ring node on, no pinned theta rows
+  const bool full = j0 > 0 && j0 + MTJ < g.n1 && !g.pin_lo1 && !g.pin_hi1;
 
-  // own nodes: staged-array offsets of centre and neighbours
   const int onode0 = (j0 + ty) * g.n2 + kg;
-  bool inside[NPT], pin_j[NPT];
-  int oc[NPT], opm[NPT], opp[NPT];
   auto jn = [&](int n) { return j0 + ty + n * MTY; };
   auto onode = [&](int n) { return onode0 + n * MTY * g.n2; };
-#pragma unroll
-  for (int n = 0; n < NPT; ++n) {
-    const int hr = ty + n * MTY + 1;
-    inside[n] = jn(n) < g.n1;
-    pin_j[n] = (g.pin_lo1 && jn(n) == 0) || (g.pin_hi1 && jn(n) == g.n1 - 1);
-    oc[n] = hr * MTK + tx;
-    opm[n] = tx > 0 ? oc[n] - 1 : XM + hr * 2 + 1;
-    opp[n] = tx < MTK - 1 ? oc[n] + 1 : XM + XS + hr * 2;
-  }
 
-  auto tslot = [&](int p) { return (p - i0 + 1) % TSL; };
-  auto bslot = [&](int p) { return (p - i0 + 1) & (BSL - 1); };
-  auto rslot = [&](int p) { return (p - i0 + 1) % RSL; };
-  auto eslot = [&](int p) { return (p - i0) & 1; };
+  // rotating slots (roles advance by one plane per iteration)
+  double* sTm1 = S.T[0];  // plane t-1 (refilled with t+2 at iteration t)
+  double* sT = S.T[1];    // plane t
+  double* sTp = S.T[2];   // plane t+1
+  double* sB = S.B[1][0];   // beta of plane t
+  double* sBn = S.B[0][0];  // beta of plane t+1 (refilled at iteration t)
+  double* rM = &S.rowt[0][0][0];  // metric rows of planes t-1, t, t+1
+  double* rC = &S.rowt[1][0][0];
+  double* rN = &S.rowt[2][0][0];
+  double* eW = S.EO[0][0];  // epilogue operands of plane t (landing), t-1 (read)
+  double* eR = S.EO[1][0];
+  FluxC* Ew = &S.E[0];      // flux exchange of plane t (write), t-1 (read)
+  FluxC* Er = &S.E[1];
+
   // (thread 0 only)
   auto tma_arr = [&](double* dst, const CUtensorMap* mm, const CUtensorMap* ms, int p) {
     const int z = plane_map(g, p).mem + 1;
@@ -195,35 +195,33 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
     tma3(dst + XM, ms, kL, j0 - 1, z, &S.bar);
     tma3(dst + XM + XS, ms, kR, j0 - 1, z, &S.bar);
   };
-  auto issue_T = [&](int p) { tma_arr(S.T[tslot(p)], &maps.T, &maps.TS, p); };
-  auto issue_B = [&](int p) {
+  auto issue_B = [&](double* dst, int p) {
 #pragma unroll
-    for (int q = 0; q < 3; ++q) tma_arr(S.B[bslot(p)][q], &maps.B[q], &maps.BS[q], p);
+    for (int q = 0; q < 3; ++q) tma_arr(dst + q * XA, &maps.B[q], &maps.BS[q], p);
   };
-  auto issue_ops = [&](int p) {
+  auto issue_ops = [&](double* dst, int p) {
 #pragma unroll
-    for (int q = 0; q < Epi::NOPS; ++q) tma3(S.EO[eslot(p)][q], &maps.O[q], k0, j0, p + 1, &S.bar);
+    for (int q = 0; q < Epi::NOPS; ++q) tma3(dst + q * XO, &maps.O[q], k0, j0, p + 1, &S.bar);
   };
-  auto issue_rows = [&](int p) {
+  auto issue_rows = [&](double* dst, int p) {
     if (rton) {
       const PlaneMap pm = plane_map(g, p);
-      cp_async8(&S.rowt[rslot(p)][rtab][rhj], rbase + row2(g, pm.row, rjj));
+      cp_async8(dst + rhj * RW + rtab, rbase + row2(g, pm.row, rjj));
     }
   };
 
-  // ---- prologue
+  // ---- prologue: T(i0-1..i0+1), beta(i0-1, i0) by TMA; rows(i0-1, i0) by cp.async
   __syncthreads();  // barrier initialised
   if (tid == 0) {
-    const bool t1 = i0 + 1 <= iend;
-    mbar_expect_tx(&S.bar, (2u + (t1 ? 1u : 0u)) * kArrBytes + 6u * kArrBytes);
-    issue_T(i0 - 1);
-    issue_T(i0);
-    if (t1) issue_T(i0 + 1);
-    issue_B(i0 - 1);
-    issue_B(i0);
+    mbar_expect_tx(&S.bar, 9u * kArrBytes);
+    tma_arr(sTm1, &maps.T, &maps.TS, i0 - 1);
+    tma_arr(sT, &maps.T, &maps.TS, i0);
+    tma_arr(sTp, &maps.T, &maps.TS, i0 + 1);  // iend >= i0 + 1
+    issue_B(sBn, i0 - 1);
+    issue_B(sB, i0);
   }
-  issue_rows(i0 - 1);
-  issue_rows(i0);
+  issue_rows(rM, i0 - 1);
+  issue_rows(rC, i0);
   cp_async_commit();
   cp_async_wait<0>();
   unsigned phase = 0;
@@ -231,146 +229,181 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   phase ^= 1u;
   __syncthreads();
 
-  double Tm[NPT], Tc[NPT], qa[NPT], qb[NPT], ownp[NPT];
-  double Tmr = 0.0;
-  {
-    const PlaneMap pm = plane_map(g, i0 - 1);
-    const double* s0 = S.T[tslot(i0 - 1)];
-    const double* s1 = S.T[tslot(i0)];
-    const int bs = bslot(i0 - 1), rsl = rslot(i0 - 1);
+  auto run = [&](auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
+    bool inside[NPT], pin_j[NPT];
+    int oc[NPT], opm[NPT], opp[NPT];
 #pragma unroll
     for (int n = 0; n < NPT; ++n) {
-      Tm[n] = s0[oc[n]];
-      Tc[n] = s1[oc[n]];
-      qa[n] = 0.0;
-      qb[n] = 0.0;
-      ownp[n] = 0.0;
-      if (pm.exists && inside[n]) {  // E_{0,+}(i0 - 1)
-        const double Tn[3][2] = {{Tc[n], Tm[n]}, {s0[oc[n] + MTK], s0[oc[n] - MTK]}, {s0[opp[n]], s0[opm[n]]}};
-        const double bv[3] = {S.B[bs][0][oc[n]], S.B[bs][1][oc[n]], S.B[bs][2][oc[n]]};
-        double E[3][2];
-        node_E<0, 0>(Tm[n], Tn, bv, &S.rowt[rsl][0][ty + n * MTY + 1], MHJ, col.il1, col.w2, E);
-        qb[n] = E[0][0];
-      }
+      const int hr = ty + n * MTY + 1;
+      inside[n] = FULL || jn(n) < g.n1;
+      pin_j[n] = !FULL && ((g.pin_lo1 && jn(n) == 0) || (g.pin_hi1 && jn(n) == g.n1 - 1));
+      oc[n] = hr * MTK + tx;
+      opm[n] = tx > 0 ? oc[n] - 1 : XM + hr * 2 + 1;
+      opp[n] = tx < MTK - 1 ? oc[n] + 1 : XM + XS + hr * 2;
     }
-    if (ra >= 0) Tmr = s0[ro_c];
-  }
+    const bool ron = FULL ? (ra >= 0) : (ra >= 0 && ring_on);
 
-  auto step = [&](int t, auto last_tag) {
-    constexpr bool LAST = decltype(last_tag)::value;
-    if (!LAST) {
-      if (tid == 0) {
-        const bool t2 = t + 2 <= iend;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&S.bar, (t2 ? kArrBytes : 0u) + 3u * kArrBytes + (unsigned)Epi::NOPS * kOpBytes);
-        if (t2) issue_T(t + 2);
-        issue_B(t + 1);
-        issue_ops(t);
-      }
-      issue_rows(t + 1);
-      cp_async_commit();
-    }
-    const bool exists = LAST ? plane_map(g, t).exists : true;
-    const double* sT = S.T[tslot(t)];
-    const double* sTp = S.T[tslot(t + 1)];
-    const int bs = bslot(t), rsl = rslot(t), rslm = rslot(t - 1);
-    const int par = t & 1, pp = par ^ 1;
-    const int esm = eslot(t - 1);
-    const int tf = t - 1;
-    const int ig = tf + g.i0g;
-    const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
-    const int64_t pbase = (int64_t)t * g.plane;
+    double Tm[NPT], Tc[NPT], qa[NPT], qb[NPT], ownp[NPT];
+    double Tmr = 0.0;
+    {  // E_{0,+}(i0 - 1)
+      const bool ex = plane_map(g, i0 - 1).exists;
 #pragma unroll
-    for (int n = 0; n < NPT; ++n) {
-      const int r = ty + n * MTY;
-      const int jr = r + 1;
-      double E[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-      double Tp = 0.0;
-      if (!LAST) Tp = sTp[oc[n]];
-      if (exists && inside[n]) {
-        const double Tn[3][2] = {{Tp, Tm[n]}, {sT[oc[n] + MTK], sT[oc[n] - MTK]}, {sT[opp[n]], sT[opm[n]]}};
-        const double bv[3] = {S.B[bs][0][oc[n]], S.B[bs][1][oc[n]], S.B[bs][2][oc[n]]};
-        if (!LAST) node_E<-1, 0>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
-        else node_E<0, 1>(Tc[n], Tn, bv, &S.rowt[rsl][0][jr], MHJ, col.il1, col.w2, E);
-      }
-      if (!LAST) {
-        if (r < MTJ - 1) S.E[par].e1p[r + 1][tx] = E[1][0];
-        if (r > 0) S.E[par].e1m[r - 1][tx] = E[1][1];
-        if (tx < MTK - 1) S.E[par].e2p[r][tx + 1] = E[2][0];
-        if (tx > 0) S.E[par].e2m[r][tx - 1] = E[2][1];
-      }
-      if (t > i0 && inside[n]) {
-        const double nbr = (S.E[pp].e1p[r][tx] - S.E[pp].e1m[r][tx]) + (S.E[pp].e2p[r][tx] - S.E[pp].e2m[r][tx]);
-        const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
-        const double iv = S.rowt[rslm][10][jr] * col.ivg;
-        const int64_t of = pbase - g.plane + onode(n);
-        double f = ((0.0 - G) * iv) * op.pref;
-        if (op.rho) f = f / __ldg(op.rho + of);
-        const bool pin = pin_i || pin_j[n] || pin_k;
-        if (pin) f = 0.0;
-        double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
-#pragma unroll
-        for (int q = 0; q < Epi::NOPS; ++q) ov[q] = S.EO[esm][q][r * MTK + tx];
-        epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov);
-      }
-      if (!LAST) {
-        ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
-        qa[n] = qb[n];
-        qb[n] = E[0][0];
-        Tm[n] = Tc[n];
-        Tc[n] = Tp;
-      }
-    }
-    // ---- halo ring of plane t
-    if (!LAST && ra >= 0) {
-      const double Tcr = sT[ro_c];
-      const double Tpr = sTp[ro_c];
-      double Ev = 0.0;
-      if (ring_on) {
-        const double Tn[3][2] = {{Tpr, Tmr}, {sT[ro_tp], sT[ro_tm]}, {sT[ro_pp], sT[ro_pm]}};
-        const double bv[3] = {S.B[bs][0][ro_c], S.B[bs][1][ro_c], S.B[bs][2][ro_c]};
-        double E[3][2];
-        const double* rw = &S.rowt[rsl][0][rhj_];
-        if (ra == 1) {
-          if (rs == 0) {
-            node_E<1, 0>(Tcr, Tn, bv, rw, MHJ, col.il1, col.w2, E);
-            Ev = E[1][0];
-          } else {
-            node_E<1, 1>(Tcr, Tn, bv, rw, MHJ, col.il1, col.w2, E);
-            Ev = E[1][1];
-          }
-        } else {
-          const double* cs = S.ringcol[rs];
-          const double il1[2] = {cs[4], cs[5]};
-          const double w2[2] = {cs[6], cs[7]};
-          if (rs == 0) {
-            node_E<2, 0>(Tcr, Tn, bv, rw, MHJ, il1, w2, E);
-            Ev = E[2][0];
-          } else {
-            node_E<2, 1>(Tcr, Tn, bv, rw, MHJ, il1, w2, E);
-            Ev = E[2][1];
-          }
+      for (int n = 0; n < NPT; ++n) {
+        Tm[n] = sTm1[oc[n]];
+        Tc[n] = sT[oc[n]];
+        qa[n] = 0.0;
+        qb[n] = 0.0;
+        ownp[n] = 0.0;
+        if (ex && inside[n]) {
+          const double Tn[3][2] = {{Tc[n], Tm[n]}, {sTm1[oc[n] + MTK], sTm1[oc[n] - MTK]},
+                                   {sTm1[opp[n]], sTm1[opm[n]]}};
+          const double bv[3] = {sBn[oc[n]], sBn[XA + oc[n]], sBn[2 * XA + oc[n]]};
+          double E[3][2];
+          node_E_rows<0, 0>(Tm[n], Tn, bv, rM + (ty + n * MTY + 1) * RW, col.il1, col.w2, E);
+          qb[n] = E[0][0];
         }
       }
-      if (ra == 1) {
-        if (rs == 0) S.E[par].e1p[0][rkk] = Ev;
-        else S.E[par].e1m[MTJ - 1][rkk] = Ev;
-      } else {
-        if (rs == 0) S.E[par].e2p[rhj_ - 1][0] = Ev;
-        else S.E[par].e2m[rhj_ - 1][MTK - 1] = Ev;
+      if (ra >= 0) Tmr = sTm1[ro_c];
+    }
+
+    // one plane: fluxes of plane t, finalisation of plane t-1
+    auto step = [&](int t, auto first_tag, auto last_tag) {
+      constexpr bool FIRST = decltype(first_tag)::value;
+      constexpr bool LAST = decltype(last_tag)::value;
+      if (!LAST) {
+        if (tid == 0) {
+          const bool t2 = t + 2 <= iend;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&S.bar, (t2 ? kArrBytes : 0u) + 3u * kArrBytes + (unsigned)Epi::NOPS * kOpBytes);
+          if (t2) tma_arr(sTm1, &maps.T, &maps.TS, t + 2);
+          issue_B(sBn, t + 1);
+          issue_ops(eW, t);
+        }
+        issue_rows(rN, t + 1);
+        cp_async_commit();
       }
-      Tmr = Tcr;
-    }
-    if (!LAST) {
-      cp_async_wait<0>();
-      mbar_wait(&S.bar, phase);
-      phase ^= 1u;
-      __syncthreads();
-    }
-  };
+      const bool exists = LAST ? plane_map(g, t).exists : true;
+      const int tf = t - 1;
+      const int ig = tf + g.i0g;
+      const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
+      const int64_t pbase = (int64_t)t * g.plane;
+#pragma unroll
+      for (int n = 0; n < NPT; ++n) {
+        const int r = ty + n * MTY;
+        const int jr = r + 1;
+        double E[3][2];
+        double Tp = 0.0;
+        if (!LAST) Tp = sTp[oc[n]];
+        if ((FULL && !LAST) || (exists && inside[n])) {
+          const double Tn[3][2] = {{Tp, Tm[n]}, {sT[oc[n] + MTK], sT[oc[n] - MTK]}, {sT[opp[n]], sT[opm[n]]}};
+          const double bv[3] = {sB[oc[n]], sB[XA + oc[n]], sB[2 * XA + oc[n]]};
+          if (!LAST) node_E_rows<-1, 0>(Tc[n], Tn, bv, rC + jr * RW, col.il1, col.w2, E);
+          else node_E_rows<0, 1>(Tc[n], Tn, bv, rC + jr * RW, col.il1, col.w2, E);
+        } else {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) E[a][0] = E[a][1] = 0.0;
+        }
+        if (!LAST) {
+          if (r < MTJ - 1) Ew->e1p[r + 1][tx] = E[1][0];
+          if (r > 0) Ew->e1m[r - 1][tx] = E[1][1];
+          if (tx < MTK - 1) Ew->e2p[r][tx + 1] = E[2][0];
+          if (tx > 0) Ew->e2m[r][tx - 1] = E[2][1];
+        }
+        if (!FIRST && inside[n]) {
+          const double nbr = (Er->e1p[r][tx] - Er->e1m[r][tx]) + (Er->e2p[r][tx] - Er->e2m[r][tx]);
+          const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
+          const double iv = rM[jr * RW + 10] * col.ivg;
+          const int64_t of = pbase - g.plane + onode(n);
+          double f = ((0.0 - G) * iv) * op.pref;
+          if (op.rho) f = f / __ldg(op.rho + of);
+          const bool pin = pin_i || pin_j[n] || pin_k;
+          if (pin) f = 0.0;
+          double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
+#pragma unroll
+          for (int q = 0; q < Epi::NOPS; ++q) ov[q] = eR[q * XO + r * MTK + tx];
+          epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov);
+        }
+        if (!LAST) {
+          ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
+          qa[n] = qb[n];
+          qb[n] = E[0][0];
+          Tm[n] = Tc[n];
+          Tc[n] = Tp;
+        }
+      }
+      // ---- halo ring of plane t
+      if (!LAST && ra >= 0) {
+        const double Tcr = sT[ro_c];
+        const double Tpr = sTp[ro_c];
+        double Ev = 0.0;
+        if (ron) {
+          const double Tn[3][2] = {{Tpr, Tmr}, {sT[ro_tp], sT[ro_tm]}, {sT[ro_pp], sT[ro_pm]}};
+          const double bv[3] = {sB[ro_c], sB[XA + ro_c], sB[2 * XA + ro_c]};
+          double E[3][2];
+          const double* rw = rC + rhj_ * RW;
+          if (ra == 1) {
+            if (rs == 0) {
+              node_E_rows<1, 0>(Tcr, Tn, bv, rw, col.il1, col.w2, E);
+              Ev = E[1][0];
+            } else {
+              node_E_rows<1, 1>(Tcr, Tn, bv, rw, col.il1, col.w2, E);
+              Ev = E[1][1];
+            }
+          } else {
+            const double* cs = S.ringcol[rs];
+            const double il1[2] = {cs[4], cs[5]};
+            const double w2[2] = {cs[6], cs[7]};
+            if (rs == 0) {
+              node_E_rows<2, 0>(Tcr, Tn, bv, rw, il1, w2, E);
+              Ev = E[2][0];
+            } else {
+              node_E_rows<2, 1>(Tcr, Tn, bv, rw, il1, w2, E);
+              Ev = E[2][1];
+            }
+          }
+        }
+        if (ra == 1) {
+          if (rs == 0) Ew->e1p[0][rkk] = Ev;
+          else Ew->e1m[MTJ - 1][rkk] = Ev;
+        } else {
+          if (rs == 0) Ew->e2p[rhj_ - 1][0] = Ev;
+          else Ew->e2m[rhj_ - 1][MTK - 1] = Ev;
+        }
+        Tmr = Tcr;
+      }
+      if (!LAST) {
+        cp_async_wait<0>();
+        mbar_wait(&S.bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+        // advance the slot roles by one plane
+        double* tt = sTm1;
+        sTm1 = sT;
+        sT = sTp;
+        sTp = tt;
+        tt = sB;
+        sB = sBn;
+        sBn = tt;
+        tt = rM;
+        rM = rC;
+        rC = rN;
+        rN = tt;
+        tt = eW;
+        eW = eR;
+        eR = tt;
+        FluxC* ft = Ew;
+        Ew = Er;
+        Er = ft;
+      }
+    };
+    step(i0, std::true_type{}, std::false_type{});
 #pragma unroll 1
-  for (int t = i0; t < iend; ++t) step(t, std::false_type{});
-  step(iend, std::true_type{});
+    for (int t = i0 + 1; t < iend; ++t) step(t, std::false_type{}, std::false_type{});
+    step(iend, std::false_type{}, std::true_type{});
+  };
+  if (full) run(std::true_type{});
+  else run(std::false_type{});
   epi.finish(g);
 }
 
