@@ -359,6 +359,7 @@ def run_ours(args, rank, world, local_rank):
                 "frac": dom["achieved"] / peak,
                 "traffic": _traffic(name, kind, dom["field"]),
                 "bytes_per_cell_update": dom["bytes_per_cell_update"],
+                "algorithmic_bytes_per_launch": dom["bytes_per_cell_update"] * cells_global // world,
                 "peak_source": peak_src,
                 "kernel_ms_share": dom["ms"] / ms if ms > 0 else None,
                 "all_hot_loops": [{k: v for k, v in r.items() if k != "field"} for r in rows],
@@ -378,13 +379,14 @@ def run_ours(args, rank, world, local_rank):
 
 
 def _traffic(name, kind, field):
-    """DRAM bytes per cell-update of the dominant kernel from the committed ncu
-    capture (profiles/ncu_summary.json), or None."""
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/ncu_summary.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d.get(f"{name}_{kind}_{field}", {}).get("dram_bytes_per_cell_update")
+        e = d.get(f"{name}_{kind}_{field}")
+        return None if e is None else e["dram_bytes_per_launch"]
     except Exception:
         return None
 
