@@ -268,19 +268,24 @@ struct AlignedOp {
 #pragma unroll
     for (int n = 0; n < 19; ++n) H[n] = 0.0;
     const int64_t o = off3(g, i, j, k);
-    // (A) apex tets
+    // (A) apex tets (loops fully unrolled: H stays in registers)
+#pragma unroll
     for (int n = 0; n < 8; ++n) {
       const int sg[3] = {(n >> 2) & 1, (n >> 1) & 1, n & 1};
       double qa[3];
+#pragma unroll
       for (int x = 0; x < 3; ++x) qa[x] = q(g, x, sg[x], i, j, k, o);
       double qs = (qa[0] + qa[1]) + qa[2];
       double w = om(g, sg[0], sg[1], sg[2], i, j, k) * 1.0;
       H[0] += (w * qs) * qs;
+#pragma unroll
       for (int x = 0; x < 3; ++x) H[face_idx(x, sg[x] == 0 ? 1 : -1)] += (w * (0.0 - qs)) * qa[x];
     }
     // (B) end-point tets, v = m - sigma_a e_a
     const int co[3] = {i, j, k};
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
+#pragma unroll
       for (int sa = 0; sa < 2; ++sa) {
         const int d = sa == 0 ? -1 : 1;
         bool ok;
@@ -288,16 +293,19 @@ struct AlignedOp {
         if (!ok) continue;
         const int vi = a == 0 ? xv : i, vj = a == 1 ? xv : j, vk = a == 2 ? xv : k;
         const int64_t ov = off3(g, vi, vj, vk);
+#pragma unroll
         for (int n = 0; n < 8; ++n) {
           const int sg[3] = {(n >> 2) & 1, (n >> 1) & 1, n & 1};
           if (sg[a] != sa) continue;
           double qv[3];
+#pragma unroll
           for (int x = 0; x < 3; ++x) qv[x] = q(g, x, sg[x], vi, vj, vk, ov);
           double wv = om(g, sg[0], sg[1], sg[2], vi, vj, vk) * 1.0;
           double qs = (qv[0] + qv[1]) + qv[2];
           double qa = qv[a];
           H[0] += (wv * qa) * qa;
           H[face_idx(a, d)] += (wv * qa) * (0.0 - qs);
+#pragma unroll
           for (int bb = 0; bb < 3; ++bb) {
             if (bb == a) continue;
             H[diag_idx(a, d, bb, sg[bb] == 0 ? 1 : -1)] += (wv * qa) * qv[bb];
@@ -306,6 +314,7 @@ struct AlignedOp {
       }
     }
     double S = fabs(H[0]);
+#pragma unroll
     for (int n = 1; n < 19; ++n) S = S + fabs(H[n]);
     const double iv = __ldg(g.iVal2 + row2(g, i, j)) * __ldg(g.iValg + k);
     double l = (S * iv) * pref;

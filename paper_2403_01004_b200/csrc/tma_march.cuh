@@ -245,6 +245,12 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
     const bool ron = FULL ? (ra >= 0) : (ra >= 0 && ring_on);
 
     double Tm[NPT], Tc[NPT], qa[NPT], qb[NPT], ownp[NPT];
+    // rho of the own nodes of the plane being finalised: loaded one plane
+    // ahead into the same register right after its previous use (no move of a
+    // pending load, no dependent global load on the finalisation path)
+    double rr[NPT];
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) rr[n] = 1.0;
     double Tmr = 0.0;
     {  // E_{0,+}(i0 - 1)
       const bool ex = plane_map(g, i0 - 1).exists;
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           const double iv = rM[jr * RW + 10] * col.ivg;
           const int64_t of = pbase - g.plane + onode(n);
           double f = ((0.0 - G) * iv) * op.pref;
-          if (op.rho) f = f / __ldg(op.rho + of);
+          if (op.rho) f = f / rr[n];
           const bool pin = pin_i || pin_j[n] || pin_k;
           if (pin) f = 0.0;
           double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
@@ -325,6 +331,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov);
         }
         if (!LAST) {
+          if (op.rho && inside[n]) rr[n] = __ldg(op.rho + pbase + onode(n));
           ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
           qa[n] = qb[n];
           qb[n] = E[0][0];
