@@ -107,6 +107,9 @@ struct pc_grid {
   pc_ctx* ctx;
   GridDev g;
   double* tables = nullptr;
+  double* rowrec = nullptr;  // [n0+2][n1][RW] interleaved row records (TMA march)
+  CUtensorMap rowmap;
+  bool rowmap_ok = false;
   int64_t shape[3];
   size_t comp_elems;  // (n0 + 2) * plane
 };
@@ -511,6 +514,20 @@ int pc_grid_create(pc_ctx* c, const int64_t shape[3], const int32_t* fl, const d
   d.gv = takeK();
   d.Val2 = takeA();
   d.Valg = takeK();
+  {  // interleaved row records from the host copy of the tables (same bits)
+    const double* h = tables + 3 * A + 3 * K + A + K;  // iL2[0]
+    const double* hw = h + 6 * A + 6 * K;               // wo01[0]
+    const double* hv = hw + 4 * A + 2 * K;              // iVal2
+    std::vector<double> rec((size_t)A * RW, 0.0);
+    for (int64_t q = 0; q < A; ++q) {
+      double* r = rec.data() + q * RW;
+      for (int t = 0; t < 6; ++t) r[t] = h[t * A + q];
+      for (int t = 0; t < 4; ++t) r[6 + t] = hw[t * A + q];
+      r[10] = hv[q];
+    }
+    CUDA_TRY(cudaMalloc(&g->rowrec, sizeof(double) * rec.size()));
+    CUDA_TRY(cudaMemcpy(g->rowrec, rec.data(), sizeof(double) * rec.size(), cudaMemcpyHostToDevice));
+  }
   *out = g;
   return PC_OK;
 }
@@ -518,6 +535,7 @@ int pc_grid_create(pc_ctx* c, const int64_t shape[3], const int32_t* fl, const d
 int pc_grid_destroy(pc_grid* g) {
   if (!g) return PC_OK;
   cudaFree(g->tables);
+  cudaFree(g->rowrec);
   delete g;
   return PC_OK;
 }
@@ -834,18 +852,48 @@ static int make_field_map(CUtensorMap* m, const double* base, const GridDev& g, 
   if (r != CUDA_SUCCESS) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return PC_OK;
 }
+// interleaved per-(r, theta) metric records [n0+2][n1][12] (iL2[6], wo01[4],
+// iVal2, 0) for the TMA march: one 12 x 18 box per plane
+static int make_rows_map(pc_grid* g) {
+  auto enc = tma_encoder();
+  if (!enc) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const GridDev& d = g->g;
+  cuuint64_t dims[3] = {(cuuint64_t)RW, (cuuint64_t)d.n1, (cuuint64_t)d.n0 + 2};
+  cuuint64_t strides[2] = {(cuuint64_t)RW * 8, (cuuint64_t)d.n1 * RW * 8};
+  cuuint32_t box[3] = {(cuuint32_t)RW, (cuuint32_t)MHJ, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(&g->rowmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, g->rowrec, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled (row records) failed (" + std::to_string((int)r) + ")");
+  g->rowmap_ok = true;
+  return PC_OK;
+}
 static bool tma_ok(const pc_grid* g) {
   const GridDev& d = g->g;
   return d.per2 && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && tma_encoder() != nullptr &&
          getenv("PC_NO_TMA") == nullptr;
 }
-template <class Epi>
-static int launch_tma(pc_op* op, const double* Tin, const Epi& epi, const int* skip, const char* what) {
+template <class Epi, bool RHO>
+static int launch_tma_t(pc_op* op, const TmaMaps& maps, const Epi& epi, const int* skip, const char* what) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   const int R = march_R(g);
   dim3 grid = march_grid(g, R);
   if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
+  const int smem = (int)sizeof(TmaSmem) + 128;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_aligned_tma<Epi, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_aligned_tma<Epi, RHO><<<grid, dim3(MTK, MTY), smem, c->s>>>(g->g, op->ao, maps, epi, R, skip);
+  c->st.launches++;
+  return check_launch(what);
+}
+template <class Epi>
+static int launch_tma(pc_op* op, const double* Tin, const Epi& epi, const int* skip, const char* what) {
+  pc_grid* g = op->grid;
   TmaMaps maps;
   if (!op->beta_maps) {
     for (int q = 0; q < 3; ++q) {
@@ -854,22 +902,19 @@ static int launch_tma(pc_op* op, const double* Tin, const Epi& epi, const int* s
     }
     op->beta_maps = true;
   }
+  if (!g->rowmap_ok) {
+    TRY(make_rows_map(g));
+  }
   for (int q = 0; q < 3; ++q) {
     maps.B[q] = op->bmap[q];
     maps.BS[q] = op->bsmap[q];
   }
+  maps.RW = g->rowmap;
   TRY(make_field_map(&maps.T, Tin, g->g, MTK, MHJ));
   TRY(make_field_map(&maps.TS, Tin, g->g, 2, MHJ));
   for (int q = 0; q < Epi::NOPS; ++q) TRY(make_field_map(&maps.O[q], epi.opnd(q), g->g, MTK, MTJ));
-  const int smem = (int)sizeof(TmaSmem) + 128;
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_aligned_tma<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
-  k_aligned_tma<Epi><<<grid, dim3(MTK, MTY), smem, c->s>>>(g->g, op->ao, maps, epi, R, skip);
-  c->st.launches++;
-  return check_launch(what);
+  if (op->ao.rho) return launch_tma_t<Epi, true>(op, maps, epi, skip, what);
+  return launch_tma_t<Epi, false>(op, maps, epi, skip, what);
 }
 
 template <class Epi>

@@ -542,6 +542,7 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   StageCoef sc;
   int stage;
   int* bad;
+  bool nonfinite = false;  // any non-finite value written by this thread (reported once, in finish)
   __host__ __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? u0 : (q == 1 ? um2 : y0); }
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double um1,
                                              bool pin, const double* ov) {
@@ -549,9 +550,11 @@ struct EpiStage {  // fused RKL2/RKG2 stage
     double v = ((((sc.mu * um1) + (sc.nu * ov[1])) + (sc.kap * a0)) + (sc.mtdt * f)) + (sc.gtdt * ov[2]);
     v = pin ? a0 : v;
     out[o] = v;
-    if (!isfinite(v)) atomicMin(bad, stage);
+    nonfinite |= (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
   }
-  __device__ __forceinline__ void finish(const GridDev&) {}
+  __device__ __forceinline__ void finish(const GridDev&) {
+    if (nonfinite) atomicMin(bad, stage);
+  }
 };
 
 __device__ __forceinline__ ArgMax block_argmax2d(ArgMax a, double* shv, long long* shi) {

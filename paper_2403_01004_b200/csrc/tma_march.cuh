@@ -7,10 +7,17 @@
 // completion counted on one mbarrier): for T and each beta component a
 // 32 x 18 main box (256-byte rows, phi-aligned) plus two 2 x 18 halo strips
 // whose phi coordinates wrap across the periodic seam; the epilogue operands
-// as 32 x 16 boxes.  Rows outside the theta range are zero-filled by the TMA
+// as 32 x 16 boxes; the per-(r, theta) metric records (iL2[6], wo01[4],
+// iVal2, pad: one interleaved [n0+2][n1][12] table built at grid creation) as
+// one 12 x 18 box.  Rows outside the theta range are zero-filled by the TMA
 // unit: they only ever meet an inverse edge length of 0 (no flux through the
-// pole faces), exactly as the clamped values of the oracle do.  The metric
-// rows stay on cp.async (one 8-byte copy for 198 threads).
+// pole faces), exactly as the clamped values of the oracle do, and their
+// metric records are never read.  No per-thread async copies remain.
+//
+// Per-node overheads kept off the hot loop: the 1/rho division exists only in
+// the RHO instantiation (rho prefetched one plane ahead into a register), the
+// flux-exchange stores are unconditional (padded FluxX layout), and the
+// epilogue folds its non-finite test into a flag reduced once per thread.
 #pragma once
 #include <cuda.h>
 
@@ -24,6 +31,7 @@ constexpr int XA = XM + 2 * XS;    // one staged array of one plane
 constexpr int XO = MTJ * MTK;      // epilogue operand box 16 x 32
 constexpr unsigned kArrBytes = (unsigned)(XM + 2 * MHJ * 2) * 8u;  // bytes a T / beta plane delivers
 constexpr unsigned kOpBytes = (unsigned)XO * 8u;
+constexpr int kIssuer = MNT - 32;  // lane 0 of the last warp issues the bulk copies
 
 struct TmaMaps {
   CUtensorMap T;     // stage input, box {32, 18, 1}
@@ -31,22 +39,18 @@ struct TmaMaps {
   CUtensorMap B[3];  // beta, box {32, 18, 1}
   CUtensorMap BS[3]; // beta strips
   CUtensorMap O[3];  // epilogue operands, box {32, 16, 1}
+  CUtensorMap RW;    // row records [n0+2][n1][12], box {12, 18, 1}
 };
 
-// compact in-plane flux exchange: entries readers use only
-struct FluxC {
-  double e1p[MTJ][MTK];  // E_{1,+} at rows j0-1 .. j0+14
-  double e1m[MTJ][MTK];  // E_{1,-} at rows j0+1 .. j0+16
-  double e2p[MTJ][MTK];  // E_{2,+} at cols k0-1 .. k0+30
-  double e2m[MTJ][MTK];  // E_{2,-} at cols k0+1 .. k0+32
-};
 constexpr int RW = 12;  // metric row record: iL2[6], wo01[4], iVal2, pad (16-byte aligned pairs)
+constexpr int RSLOT = 224;  // one plane of row records (18 x 12) padded to a 128-byte multiple
+constexpr unsigned kRowBytes = (unsigned)(MHJ * RW) * 8u;
 struct TmaSmem {
   double T[TSL][XA];
   double B[BSL][3][XA];
   double EO[2][3][XO];
-  FluxC E[2];
-  double rowt[RSL][MHJ][RW];
+  FluxX E[2];
+  double rowt[RSL][RSLOT];
   double ringcol[2][9];
   unsigned long long bar;
 };
@@ -83,7 +87,7 @@ __device__ __forceinline__ void tma3(double* dst, const CUtensorMap* map, int c0
       : "memory");
 }
 
-template <class Epi>
+template <class Epi, bool RHO>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op, const __grid_constant__ TmaMaps maps,
                                                         Epi epi, int R, const int* skip) {
   extern __shared__ __align__(128) unsigned char tma_smem[];
@@ -98,13 +102,6 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   const int kg = k0 + tx;
   const int kL = k0 == 0 ? g.n2 - 2 : k0 - 2;     // strip of columns k0-2, k0-1
   const int kR = k0 + MTK == g.n2 ? 0 : k0 + MTK;  // strip of columns k0+32, k0+33
-
-  // metric-row fill slot of this thread (cp.async): tid < NROWT * MHJ
-  const bool rton = tid < NROWT * MHJ;
-  const int rtab = tid / MHJ, rhj = tid - (tid / MHJ) * MHJ;
-  bool rok;
-  const int rjj = map_j(g, j0 - 1 + rhj, rok);
-  const double* rbase = !rton ? g.iVal2 : (rtab < 6 ? g.iL2[rtab] : (rtab < 10 ? g.wo01[rtab - 6] : g.iVal2));
 
   ColT col;
   load_col(g, kg, col);
@@ -126,7 +123,11 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
 
-  // ring node of this thread (tid < NRING): offsets of centre, theta+-, phi+- in a staged array
+  // ring node of this thread: each ring group is one whole warp, so every
+  // warp runs one uniform flux variant (no divergence):
+  //   warp 0: row j0-1 (E_{1,+}), warp 1: row j0+16 (E_{1,-}),
+  //   warp 2 lanes 0-15: column k0-1 (E_{2,+}), warp 3 lanes 0-15: column k0+32 (E_{2,-});
+  // the TMA issue runs on warp 7 (no ring work)
   int ra = -1, rs = 0, rhj_ = 0, rkk = 0;
   int ro_c = 0, ro_tp = 0, ro_tm = 0, ro_pm = 0, ro_pp = 0;
   if (tid < 2 * MTK) {
@@ -140,11 +141,11 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
     ro_tm = rs == 0 ? ro_c : ro_c - MTK;
     ro_pm = c > 0 ? ro_c - 1 : XM + rhj_ * 2 + 1;
     ro_pp = c < MTK - 1 ? ro_c + 1 : XM + XS + rhj_ * 2;
-  } else if (tid < NRING) {
-    const int q = tid - 2 * MTK;
+  } else if (tid < 4 * MTK && (tid & 31) < MTJ) {
+    const int q = tid & 31;
     ra = 2;
-    rs = q < MTJ ? 0 : 1;
-    rhj_ = 1 + (q % MTJ);
+    rs = tid < 3 * MTK ? 0 : 1;
+    rhj_ = 1 + q;
     if (rs == 0) {  // column k0-1: left strip, slot 1
       ro_c = XM + rhj_ * 2 + 1;
       ro_tp = ro_c + 2;
@@ -159,6 +160,12 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       ro_pp = ro_c + 1;
     }
   }
+  // flux-exchange slot the ring value goes to (padded FluxX: every slot exists)
+  int ring_slot = 0;
+  if (ra == 1) ring_slot = rs == 0 ? (int)(&S.E[0].e1p[0][rkk] - &S.E[0].e1p[0][0])
+                                   : (int)(&S.E[0].e1m[MTJ][rkk] - &S.E[0].e1p[0][0]);
+  if (ra == 2) ring_slot = rs == 0 ? (int)(&S.E[0].e2p[rhj_ - 1][0] - &S.E[0].e1p[0][0])
+                                   : (int)(&S.E[0].e2m[rhj_ - 1][MTK] - &S.E[0].e1p[0][0]);
   bool ring_on = false;
   if (ra >= 0) {
     bool rjo, rko;
@@ -180,15 +187,15 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   double* sTp = S.T[2];   // plane t+1
   double* sB = S.B[1][0];   // beta of plane t
   double* sBn = S.B[0][0];  // beta of plane t+1 (refilled at iteration t)
-  double* rM = &S.rowt[0][0][0];  // metric rows of planes t-1, t, t+1
-  double* rC = &S.rowt[1][0][0];
-  double* rN = &S.rowt[2][0][0];
+  double* rM = S.rowt[0];   // metric rows of planes t-1, t, t+1
+  double* rC = S.rowt[1];
+  double* rN = S.rowt[2];
   double* eW = S.EO[0][0];  // epilogue operands of plane t (landing), t-1 (read)
   double* eR = S.EO[1][0];
-  FluxC* Ew = &S.E[0];      // flux exchange of plane t (write), t-1 (read)
-  FluxC* Er = &S.E[1];
+  FluxX* Ew = &S.E[0];      // flux exchange of plane t (write), t-1 (read)
+  FluxX* Er = &S.E[1];
 
-  // (thread 0 only)
+  // (issuer thread only)
   auto tma_arr = [&](double* dst, const CUtensorMap* mm, const CUtensorMap* ms, int p) {
     const int z = plane_map(g, p).mem + 1;
     tma3(dst, mm, k0, j0 - 1, z, &S.bar);
@@ -203,27 +210,20 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
 #pragma unroll
     for (int q = 0; q < Epi::NOPS; ++q) tma3(dst + q * XO, &maps.O[q], k0, j0, p + 1, &S.bar);
   };
-  auto issue_rows = [&](double* dst, int p) {
-    if (rton) {
-      const PlaneMap pm = plane_map(g, p);
-      cp_async8(dst + rhj * RW + rtab, rbase + row2(g, pm.row, rjj));
-    }
-  };
+  auto issue_rows = [&](double* dst, int p) { tma3(dst, &maps.RW, 0, j0 - 1, plane_map(g, p).row + 1, &S.bar); };
 
-  // ---- prologue: T(i0-1..i0+1), beta(i0-1, i0) by TMA; rows(i0-1, i0) by cp.async
+  // ---- prologue: T(i0-1..i0+1), beta and row records of (i0-1, i0)
   __syncthreads();  // barrier initialised
-  if (tid == 0) {
-    mbar_expect_tx(&S.bar, 9u * kArrBytes);
+  if (tid == kIssuer) {
+    mbar_expect_tx(&S.bar, 9u * kArrBytes + 2u * kRowBytes);
     tma_arr(sTm1, &maps.T, &maps.TS, i0 - 1);
     tma_arr(sT, &maps.T, &maps.TS, i0);
     tma_arr(sTp, &maps.T, &maps.TS, i0 + 1);  // iend >= i0 + 1
     issue_B(sBn, i0 - 1);
     issue_B(sB, i0);
+    issue_rows(rM, i0 - 1);
+    issue_rows(rC, i0);
   }
-  issue_rows(rM, i0 - 1);
-  issue_rows(rC, i0);
-  cp_async_commit();
-  cp_async_wait<0>();
   unsigned phase = 0;
   mbar_wait(&S.bar, phase);
   phase ^= 1u;
@@ -272,28 +272,30 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       }
       if (ra >= 0) Tmr = sTm1[ro_c];
     }
+    // global offset of own node 0 in the plane being finalised (t - 1)
+    int64_t pofs = (int64_t)(i0 - 1) * g.plane + onode0;
+    const int64_t nstride = (int64_t)MTY * g.n2;
 
     // one plane: fluxes of plane t, finalisation of plane t-1
     auto step = [&](int t, auto first_tag, auto last_tag) {
       constexpr bool FIRST = decltype(first_tag)::value;
       constexpr bool LAST = decltype(last_tag)::value;
       if (!LAST) {
-        if (tid == 0) {
+        if (tid == kIssuer) {
           const bool t2 = t + 2 <= iend;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_expect_tx(&S.bar, (t2 ? kArrBytes : 0u) + 3u * kArrBytes + (unsigned)Epi::NOPS * kOpBytes);
+          mbar_expect_tx(&S.bar, (t2 ? kArrBytes : 0u) + 3u * kArrBytes + (unsigned)Epi::NOPS * kOpBytes +
+                                     kRowBytes);
           if (t2) tma_arr(sTm1, &maps.T, &maps.TS, t + 2);
           issue_B(sBn, t + 1);
           issue_ops(eW, t);
+          issue_rows(rN, t + 1);
         }
-        issue_rows(rN, t + 1);
-        cp_async_commit();
       }
       const bool exists = LAST ? plane_map(g, t).exists : true;
       const int tf = t - 1;
       const int ig = tf + g.i0g;
       const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
-      const int64_t pbase = (int64_t)t * g.plane;
 #pragma unroll
       for (int n = 0; n < NPT; ++n) {
         const int r = ty + n * MTY;
@@ -310,19 +312,19 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
 #pragma unroll
           for (int a = 0; a < 3; ++a) E[a][0] = E[a][1] = 0.0;
         }
-        if (!LAST) {
-          if (r < MTJ - 1) Ew->e1p[r + 1][tx] = E[1][0];
-          if (r > 0) Ew->e1m[r - 1][tx] = E[1][1];
-          if (tx < MTK - 1) Ew->e2p[r][tx + 1] = E[2][0];
-          if (tx > 0) Ew->e2m[r][tx - 1] = E[2][1];
+        if (!LAST) {  // publish the in-plane fluxes (padded slots: no conditions)
+          Ew->e1p[r + 1][tx] = E[1][0];
+          Ew->e1m[r][tx] = E[1][1];
+          Ew->e2p[r][tx + 1] = E[2][0];
+          Ew->e2m[r][tx] = E[2][1];
         }
         if (!FIRST && inside[n]) {
-          const double nbr = (Er->e1p[r][tx] - Er->e1m[r][tx]) + (Er->e2p[r][tx] - Er->e2m[r][tx]);
+          const double nbr = (Er->e1p[r][tx] - Er->e1m[r + 1][tx]) + (Er->e2p[r][tx] - Er->e2m[r][tx + 1]);
           const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
           const double iv = rM[jr * RW + 10] * col.ivg;
-          const int64_t of = pbase - g.plane + onode(n);
+          const int64_t of = pofs + n * nstride;
           double f = ((0.0 - G) * iv) * op.pref;
-          if (op.rho) f = f / rr[n];
+          if constexpr (RHO) f = f / rr[n];
           const bool pin = pin_i || pin_j[n] || pin_k;
           if (pin) f = 0.0;
           double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
@@ -331,7 +333,9 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov);
         }
         if (!LAST) {
-          if (op.rho && inside[n]) rr[n] = __ldg(op.rho + pbase + onode(n));
+          if constexpr (RHO) {
+            if (inside[n]) rr[n] = __ldg(op.rho + pofs + g.plane + n * nstride);
+          }
           ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);
           qa[n] = qb[n];
           qb[n] = E[0][0];
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           Tc[n] = Tp;
         }
       }
-      // ---- halo ring of plane t
+      // ---- halo ring of plane t (warp-uniform variant)
       if (!LAST && ra >= 0) {
         const double Tcr = sT[ro_c];
         const double Tpr = sTp[ro_c];
@@ -370,20 +374,14 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
             }
           }
         }
-        if (ra == 1) {
-          if (rs == 0) Ew->e1p[0][rkk] = Ev;
-          else Ew->e1m[MTJ - 1][rkk] = Ev;
-        } else {
-          if (rs == 0) Ew->e2p[rhj_ - 1][0] = Ev;
-          else Ew->e2m[rhj_ - 1][MTK - 1] = Ev;
-        }
+        (&Ew->e1p[0][0])[ring_slot] = Ev;
         Tmr = Tcr;
       }
       if (!LAST) {
-        cp_async_wait<0>();
         mbar_wait(&S.bar, phase);
         phase ^= 1u;
         __syncthreads();
+        pofs += g.plane;
         // advance the slot roles by one plane
         double* tt = sTm1;
         sTm1 = sT;
@@ -399,7 +397,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
         tt = eW;
         eW = eR;
         eR = tt;
-        FluxC* ft = Ew;
+        FluxX* ft = Ew;
         Ew = Er;
         Er = ft;
       }
