@@ -103,6 +103,9 @@ int pc_field_create(pc_grid* g, int ncomp, pc_field** out);
 int pc_field_destroy(pc_field* f);
 int pc_field_upload(pc_field* f, const double* host, int layout);
 int pc_field_download(const pc_field* f, double* host, int layout);
+/* axis-0 planes [i0, i0 + n) of every component, SoA [ncomp][n][n1][n2] (full-size
+   parity checks read a window without moving the whole field) */
+int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* host);
 int pc_field_copy(pc_field* dst, const pc_field* src);
 int pc_field_fill(pc_field* f, double value);
 int pc_field_exchange_halo(pc_field* f); /* axis-0 ghost planes (no-op on 1 rank) */

@@ -61,6 +61,7 @@ _SIGS = {
     "pc_field_destroy": (c_int, [c_void_p]),
     "pc_field_upload": (c_int, [c_void_p, POINTER(c_double), c_int]),
     "pc_field_download": (c_int, [c_void_p, POINTER(c_double), c_int]),
+    "pc_field_download_planes": (c_int, [c_void_p, c_int64, c_int64, POINTER(c_double)]),
     "pc_field_copy": (c_int, [c_void_p, c_void_p]),
     "pc_field_fill": (c_int, [c_void_p, c_double]),
     "pc_field_exchange_halo": (c_int, [c_void_p]),

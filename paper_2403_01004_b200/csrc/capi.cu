@@ -628,6 +628,18 @@ int pc_field_download(const pc_field* f, double* host, int layout) {
   return PC_OK;
 }
 
+int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* host) {
+  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+  pc_grid* g = f->grid;
+  if (i0 < 0 || n < 0 || i0 + n > g->g.n0) return fail(PC_E_INVALID, "plane window out of range");
+  const size_t pl = (size_t)g->g.plane;
+  for (int q = 0; q < f->ncomp; ++q)
+    CUDA_TRY(cudaMemcpyAsync(host + (size_t)q * n * pl, f->base(q) + (size_t)i0 * pl, (size_t)n * pl * sizeof(double),
+                             cudaMemcpyDeviceToHost, g->ctx->s));
+  CUDA_TRY(cudaStreamSynchronize(g->ctx->s));
+  return PC_OK;
+}
+
 int pc_field_copy(pc_field* dst, const pc_field* src) {
   if (!dst || !src || dst->ncomp != src->ncomp || dst->grid->comp_elems != src->grid->comp_elems)
     return fail(PC_E_INVALID, "field copy: shape mismatch");

@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
     }
     if (ra >= 0) Tmr = S.T[s0][rh];
   }
+  // the prologue reads of the plane i0-1 slots (T, beta) finish before the
+  // first refill of those slots (issue_T(i0 + 2), issue_B(i0 + 1)) may land
+  __syncthreads();
 
   // plane loop: planes i0 .. iend-1 compute all fluxes and finalise the
   // previous plane; the peeled last step (t = iend) only forms E_{0,-} and

@@ -150,6 +150,9 @@ __global__ void __launch_bounds__(SNT, 3) k_scalar_march(GridDev g, ScalarOp op,
     }
   }
   const int jr = ty + 1;  // row-table index of the own row (halo row 0 = j0 - 1)
+  // every thread has read its plane i0-1 values before the first refill of
+  // that slot (issue_V(i0 + 2) below) may land
+  __syncthreads();
 
 #pragma unroll 1
   for (int t = i0; t < iend; ++t) {

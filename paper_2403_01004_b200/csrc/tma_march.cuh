@@ -272,6 +272,9 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       }
       if (ra >= 0) Tmr = sTm1[ro_c];
     }
+    // the prologue reads of the plane i0-1 slots (T, beta, rows) finish before
+    // the first step's bulk copies refill them
+    __syncthreads();
     // global offset of own node 0 in the plane being finalised (t - 1)
     int64_t pofs = (int64_t)(i0 - 1) * g.plane + onode0;
     const int64_t nstride = (int64_t)MTY * g.n2;

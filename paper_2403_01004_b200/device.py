@@ -212,6 +212,14 @@ class DeviceField:
         _lib.check(_lib.lib().pc_field_download(self.handle, _lib.dptr(out), layout), "download")
         return out.reshape(shape)
 
+    def download_planes(self, i0: int, n: int) -> np.ndarray:
+        """Axis-0 planes [i0, i0 + n) as SoA (ncomp, n, n1, n2)."""
+        n1, n2 = self.dgrid.shape[1], self.dgrid.shape[2]
+        out = np.empty((self.ncomp, n, n1, n2))
+        _lib.check(_lib.lib().pc_field_download_planes(self.handle, int(i0), int(n), _lib.dptr(out)),
+                   "download_planes")
+        return out
+
     def copy_from(self, other: "DeviceField"):
         _lib.check(_lib.lib().pc_field_copy(self.handle, other.handle), "copy")
         return self

@@ -56,3 +56,15 @@ def oracle_aligned(grid, bc, b_aos, T0, pref=1.0, rho=None, kappa0=1.0, T_floor=
     c = oops.aligned_coefficient(np.asarray(T0, float).reshape(g.shape), kappa0, None, T_floor)
     r3 = None if rho is None else np.asarray(rho, float).reshape(g.shape)
     return optl.OracleOperator(g, "aligned", 1, None, r3, False, b, c, pref)
+
+
+def window_geometry(geom, a, b):
+    """The oracle geometry restricted to axis-0 planes [a, b) of a global
+    geometry (2-D tables sliced, pinned rows kept, axis 0 not periodic): an
+    operator evaluated on it is exact on every plane whose axis-0 neighbours
+    lie inside the window, so windows of a full-size grid check the GPU at
+    full size (oracle/distributed.py Slab slicing)."""
+    from oracle.distributed import Slab
+    s = Slab.__new__(Slab)
+    s.i0, s.n, s.glo, s.ghi = a, b - a, 0, 0
+    return s._slice_geometry(geom)
