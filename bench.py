@@ -301,7 +301,7 @@ def run_ours(args, rank, world, local_rank):
         if d["ms"] > 0:
             bpc = BYTES[(bkey, kind)]
             rows.append({"kernel": {"sts_aligned": "k_aligned_march<EpiStage>",
-                                    "sts_scalar": "k_stage<ScalarOp>" + (" (3 comp)" if nc == 3 else ""),
+                                    "sts_scalar": "k_scalar_march<" + str(nc) + " comp, SEpiStage>",
                                     "pcg_aligned": "k_pcg_pupdate + k_aligned_march<EpiMatvec> + k_pcg_update",
                                     "pcg_scalar": "k_pcg_matvec + k_pcg_update"}[kk],
                          "ms": d["ms"], "bytes_per_cell_update": bpc,

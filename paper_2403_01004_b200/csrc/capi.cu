@@ -518,12 +518,14 @@ int pc_grid_create(pc_ctx* c, const int64_t shape[3], const int32_t* fl, const d
     const double* h = tables + 3 * A + 3 * K + A + K;  // iL2[0]
     const double* hw = h + 6 * A + 6 * K;               // wo01[0]
     const double* hv = hw + 4 * A + 2 * K;              // iVal2
+    const double* hV = hv + A + K + 48 * J + A + K;     // Val2 (after iValg, M, Rabs, V2, gv)
     std::vector<double> rec((size_t)A * RW, 0.0);
     for (int64_t q = 0; q < A; ++q) {
       double* r = rec.data() + q * RW;
       for (int t = 0; t < 6; ++t) r[t] = h[t * A + q];
       for (int t = 0; t < 4; ++t) r[6 + t] = hw[t * A + q];
       r[10] = hv[q];
+      r[11] = hV[q];
     }
     CUDA_TRY(cudaMalloc(&g->rowrec, sizeof(double) * rec.size()));
     CUDA_TRY(cudaMemcpy(g->rowrec, rec.data(), sizeof(double) * rec.size(), cudaMemcpyHostToDevice));
@@ -1337,10 +1339,21 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   if (rc == PC_OK && cudaMemsetAsync(&c->pcg->split, c->nranks > 1 ? 1 : 0, sizeof(int), c->s) != cudaSuccess)
     rc = fail(PC_E_CUDA, "PCG state");
   if (rc == PC_OK) {
-    k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, c->red_v, c->red_v2,
-                                          c->counter, c->pcg);
-    c->st.launches++;
-    rc = check_launch("k_pcg_init");
+    if constexpr (std::is_same<Op, AlignedOp>::value) {
+      // r = b - A x0 through the marching kernel (x0 staged like any T)
+      if (adiag) {
+        EpiPcgInitT<true> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg};
+        rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
+      } else {
+        EpiPcgInitT<false> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg};
+        rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
+      }
+    } else {
+      k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, c->red_v, c->red_v2,
+                                            c->counter, c->pcg);
+      c->st.launches++;
+      rc = check_launch("k_pcg_init");
+    }
     if (rc == PC_OK) rc = pcg_split_fin(c, 0, 2, tol, 0);
   }
   Work* pold = &p0;
@@ -1366,9 +1379,14 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         rc = check_launch("k_pcg_pupdate");
         if (rc == PC_OK) rc = halo_work(g, *pnew);
         if (rc) break;
-        EpiMatvec e{Ap.base(0), adiag, dt, c->red_v, c->counter, c->pcg, op->ao, 0.0};
         const int* done = reinterpret_cast<const int*>(reinterpret_cast<const char*>(c->pcg) + offsetof(PcgDev, done));
-        rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
+        if (adiag) {
+          EpiMatvecT<true> e{adiag, Ap.base(0), dt, c->red_v, c->counter, c->pcg};
+          rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
+        } else {
+          EpiMatvecT<false> e{adiag, Ap.base(0), dt, c->red_v, c->counter, c->pcg};
+          rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
+        }
         if (rc == PC_OK) rc = pcg_split_fin(c, 1, 1, tol, it);
         if (rc) break;
       } else {
@@ -1381,8 +1399,15 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         if (rc == PC_OK) rc = pcg_split_fin(c, 1, 1, tol, it);
         if (rc) break;
       }
-      k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, tol, it,
-                                              c->red_v, c->red_v2, c->counter, c->pcg);
+      if constexpr (std::is_same<Op, AlignedOp>::value) {
+        auto upd = o.rho ? (adiag ? k_pcg_update1<true, true> : k_pcg_update1<true, false>)
+                         : (adiag ? k_pcg_update1<false, true> : k_pcg_update1<false, false>);
+        upd<<<nb, kThreads, 0, c->s>>>(g->g, x->base(0), r.base(0), pnew->base(0), Ap.base(0), dg, adiag, o.rho, dt,
+                                       tol, it, c->red_v, c->red_v2, c->counter, c->pcg);
+      } else {
+        k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, tol, it,
+                                                c->red_v, c->red_v2, c->counter, c->pcg);
+      }
       c->st.launches += std::is_same<Op, AlignedOp>::value ? 1 : 2;  // (march counted at launch)
       c->st.stage_launches += std::is_same<Op, AlignedOp>::value ? 3 : 2;
       rc = check_launch("k_pcg");

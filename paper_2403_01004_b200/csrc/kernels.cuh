@@ -319,6 +319,89 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const doubl
   }
 }
 
+// K8 for one-component operators (the aligned PCG): x += alpha p,
+// r -= alpha Ap, partial (W r, r), (W r, z), z = r / (a + dt d).  One warp per
+// (r, theta) row (the row weight Val2 read once), four phi nodes per lane in
+// flight (all loads issued before the arithmetic), parallel fixed-order final
+// sum in the last block.
+template <bool RHO, bool ADIAG>
+__global__ void __launch_bounds__(kThreads) k_pcg_update1(GridDev g, double* __restrict__ x, double* __restrict__ r,
+                                                          const double* __restrict__ p,
+                                                          const double* __restrict__ Ap,
+                                                          const double* __restrict__ dg,
+                                                          const double* __restrict__ adiag,
+                                                          const double* __restrict__ rho, double dt, double tol,
+                                                          int it, double* p1, double* p2, unsigned int* counter,
+                                                          PcgDev* st) {
+  __shared__ double sh[kThreads / 32];
+  if (st->done) return;
+  const double alpha = st->alpha;
+  const int lane = threadIdx.x & 31;
+  double s1 = 0.0, s2 = 0.0;
+  const int nrows = g.n0 * g.n1;
+  for (int row = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < nrows; row += gridDim.x * (kThreads / 32)) {
+    const int i = row / g.n1, j = row - i * g.n1;
+    const double V2 = __ldg(g.Val2 + row2(g, i, j));
+    const int64_t base = (int64_t)i * g.plane + (int64_t)j * g.n2;
+    for (int k0 = lane; k0 < g.n2; k0 += 128) {
+      double xv[4], pv[4], rv[4], av[4], dv[4], wv[4], mv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + 32 * u;
+        if (k < g.n2) {
+          const int64_t o = base + k;
+          xv[u] = x[o];
+          pv[u] = __ldg(p + o);
+          rv[u] = r[o];
+          av[u] = __ldg(Ap + o);
+          dv[u] = __ldg(dg + o);
+          wv[u] = __ldg(g.Valg + k);
+          mv[u] = ADIAG ? __ldg(adiag + o) : 1.0;
+          if (RHO) wv[u] = __ldg(rho + o) * (V2 * wv[u]);
+          else wv[u] = V2 * wv[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + 32 * u;
+        if (k < g.n2) {
+          const int64_t o = base + k;
+          x[o] = xv[u] + alpha * pv[u];
+          const double rn = rv[u] - alpha * av[u];
+          r[o] = rn;
+          const double dvec = mv[u] + dt * dv[u];
+          s1 += (wv[u] * rn) * rn;
+          s2 += (wv[u] * rn) * (rn / dvec);
+        }
+      }
+    }
+  }
+  s1 = block_sum<kThreads>(s1, sh);
+  s2 = block_sum<kThreads>(s2, sh);
+  if (threadIdx.x == 0) {
+    p1[blockIdx.x] = s1;
+    p2[blockIdx.x] = s2;
+  }
+  if (last_block(counter)) {
+    double a = 0.0, b = 0.0;
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += kThreads) {
+      a += p1[t];
+      b += p2[t];
+    }
+    const double rr = block_sum<kThreads>(a, sh);
+    const double rzn = block_sum<kThreads>(b, sh);
+    if (threadIdx.x == 0) {
+      if (st->split) {
+        st->red[0] = rr;
+        st->red[1] = rzn;
+      } else {
+        pcg_fin_update(st, rr, rzn, tol, it);
+      }
+      *counter = 0u;
+    }
+  }
+}
+
 // multi-rank finish of a PCG reduction after the allreduce of red[]
 __global__ void k_pcg_fin(PcgDev* st, int mode, double tol, int it) {
   if (mode == 0) pcg_fin_init(st, st->red[0], st->red[1]);

@@ -222,8 +222,10 @@ __device__ __forceinline__ void node_E_rows(double Tv, const double (&Tn)[3][2],
 // Epilogue contract (per tile node n of the thread):
 //   Epi::NOPS, epi.opnd(q)                 nodal operand arrays the kernel stages
 //                                          through cp.async one plane ahead
-//   epi(n, g, i, j, k, o, F, uc, pin, ov)  uc = input value at the node,
-//                                          ov[q] = staged operands
+//   epi(n, g, i, j, k, o, F, uc, pin, ov, W)  uc = input value at the node,
+//                                          ov[q] = staged operands, W = the
+//                                          node's inner-product weight rho V
+//                                          (formed only if Epi::NEEDS_W)
 //   epi.finish(g)                          block reduction, if any
 template <class Epi>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp op, const double* __restrict__ Tin,
@@ -461,7 +463,8 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
         double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
 #pragma unroll
         for (int q = 0; q < Epi::NOPS; ++q) ov[q] = S.EO[esm][q][tid + n * MNT];
-        epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov);
+        const double W = Epi::NEEDS_W ? op.weight(g, tf, jn(n), kg) : 0.0;
+        epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov, W);
       }
       if (!LAST) {
         // ---- shift the per-node queues
@@ -527,10 +530,11 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
 // ---- epilogues ----------------------------------------------------------
 struct EpiStore {  // F = op(u)
   static constexpr int NOPS = 0;
+  static constexpr bool NEEDS_W = false;
   double* F;
   __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double, bool,
-                                             const double*) {
+                                             const double*, double) {
     F[o] = f;
   }
   __device__ __forceinline__ void finish(const GridDev&) {}
@@ -538,6 +542,7 @@ struct EpiStore {  // F = op(u)
 
 struct EpiStage {  // fused RKL2/RKG2 stage
   static constexpr int NOPS = 3;
+  static constexpr bool NEEDS_W = false;
   const double* um2;
   const double* u0;
   const double* y0;
@@ -548,7 +553,7 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   bool nonfinite = false;  // any non-finite value written by this thread (reported once, in finish)
   __host__ __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? u0 : (q == 1 ? um2 : y0); }
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double um1,
-                                             bool pin, const double* ov) {
+                                             bool pin, const double* ov, double) {
     const double a0 = ov[0];
     double v = ((((sc.mu * um1) + (sc.nu * ov[1])) + (sc.kap * a0)) + (sc.mtdt * f)) + (sc.gtdt * ov[2]);
     v = pin ? a0 : v;
@@ -594,6 +599,7 @@ __device__ __forceinline__ bool last_block3(unsigned int* counter, int nblk) {
 
 struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
   static constexpr int NOPS = 0;
+  static constexpr bool NEEDS_W = false;
   __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
   double* F;
   double* pv;
@@ -602,7 +608,7 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
   ArgRes* res;
   ArgMax best;
   __device__ __forceinline__ void operator()(int, const GridDev& g, int i, int j, int k, int64_t o, double f, double,
-                                             bool, const double*) {
+                                             bool, const double*, double) {
     F[o] = f;
     best = am_better(best, ArgMax{fabs(f), aos_index(g, i, j, k, 0, 1)});
   }
@@ -630,44 +636,126 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
   }
 };
 
-// PCG K7: Ap = a p - dt F(p) for the staged p; partial (W p, Ap) -> alpha
-struct EpiMatvec {
-  static constexpr int NOPS = 0;
-  __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
-  double* Ap;
+// parallel, fixed-order final sum of per-block partials by the last block
+// (thread t sums partials t, t + MNT, ...; then the block tree) -- the same
+// order on every run for a given grid
+__device__ __forceinline__ double sum_partials(const double* part, int nblk, double* sh) {
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  double a = 0.0;
+  for (int q = tid; q < nblk; q += MNT) a += part[q];
+  a = warp_sum(a);
+  const int lane = tid & 31, w = tid >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = a;
+  __syncthreads();
+  double s = 0.0;
+  if (tid == 0)
+    for (int q = 0; q < MNT / 32; ++q) s += sh[q];
+  return s;  // valid on thread 0
+}
+__device__ __forceinline__ double block_sum2d(double v, double* sh) {
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  v = warp_sum(v);
+  const int lane = tid & 31, w = tid >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (tid == 0)
+    for (int q = 0; q < MNT / 32; ++q) s += sh[q];
+  return s;  // valid on thread 0
+}
+
+// PCG K7: Ap = a p - dt F(p) for the staged p; partial (W p, Ap) -> alpha.
+// ADIAG: the optional mass diagonal a of (a - dt J) is a staged operand.
+template <bool ADIAG>
+struct EpiMatvecT {
+  static constexpr int NOPS = ADIAG ? 1 : 0;
+  static constexpr bool NEEDS_W = true;
   const double* adiag;
+  double* Ap;
   double dt;
   double* p1;
   unsigned int* counter;
   PcgDev* st;
-  AlignedOp op;
-  double acc;
-  __device__ __forceinline__ void operator()(int, const GridDev& g, int i, int j, int k, int64_t o, double f,
-                                             double pv, bool, const double*) {
-    const double ap = (adiag ? __ldg(adiag + o) * pv : pv) - dt * f;
+  double acc = 0.0;
+  __host__ __device__ __forceinline__ const double* opnd(int) const { return adiag; }
+  __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double pv, bool,
+                                             const double* ov, double W) {
+    const double ap = (ADIAG ? ov[0] * pv : pv) - dt * f;
     Ap[o] = ap;
-    acc += (op.weight(g, i, j, k) * pv) * ap;
+    acc += (W * pv) * ap;
   }
   __device__ __forceinline__ void finish(const GridDev&) {
     __shared__ double sh[MNT / 32];
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblk = gridDim.x * gridDim.y * gridDim.z;
-    double v = warp_sum(acc);
-    const int lane = tid & 31, w = tid >> 5;
-    if (lane == 0) sh[w] = v;
-    __syncthreads();
-    if (tid == 0) {
-      double s = 0.0;
-      for (int q = 0; q < MNT / 32; ++q) s += sh[q];
-      p1[bid] = s;
-    }
+    const double v = block_sum2d(acc, sh);
+    if (tid == 0) p1[bid] = v;
     if (last_block3(counter, nblk)) {
+      const double a = sum_partials(p1, nblk, sh);
       if (tid == 0) {
-        double a = 0.0;
-        for (int q = 0; q < nblk; ++q) a += p1[q];
         if (st->split) st->red[0] = a;
         else pcg_alpha(st, a);
+        *counter = 0u;
+      }
+    }
+  }
+};
+
+// PCG start (the marching form of k_pcg_init): r = b - (a x - dt F(x)),
+// p_old = 0, partial (W r, z) and (W b, b), z = r / (a + dt d).
+// Operands: b, d (Jacobi diagonal), [a].
+template <bool ADIAG>
+struct EpiPcgInitT {
+  static constexpr int NOPS = ADIAG ? 3 : 2;
+  static constexpr bool NEEDS_W = true;
+  const double* b;
+  const double* dg;
+  const double* adiag;
+  double* r;
+  double* pold;
+  double dt;
+  double* p1;
+  double* p2;
+  unsigned int* counter;
+  PcgDev* st;
+  double s1 = 0.0, s2 = 0.0;
+  __host__ __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? b : (q == 1 ? dg : adiag); }
+  __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double xv, bool,
+                                             const double* ov, double W) {
+    const double bv = ov[0];
+    const double dvec = (ADIAG ? ov[2] : 1.0) + dt * ov[1];
+    const double Ax = (ADIAG ? ov[2] * xv : xv) - dt * f;
+    const double rv = bv - Ax;
+    r[o] = rv;
+    pold[o] = 0.0;
+    const double z = rv / dvec;
+    s1 += (W * rv) * z;
+    s2 += (W * bv) * bv;
+  }
+  __device__ __forceinline__ void finish(const GridDev&) {
+    __shared__ double sh[MNT / 32];
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int nblk = gridDim.x * gridDim.y * gridDim.z;
+    const double v1 = block_sum2d(s1, sh);
+    const double v2 = block_sum2d(s2, sh);
+    if (tid == 0) {
+      p1[bid] = v1;
+      p2[bid] = v2;
+    }
+    if (last_block3(counter, nblk)) {
+      const double a = sum_partials(p1, nblk, sh);
+      const double bb = sum_partials(p2, nblk, sh);
+      if (tid == 0) {
+        if (st->split) {
+          st->red[0] = a;
+          st->red[1] = bb;
+        } else {
+          pcg_fin_init(st, a, bb);
+        }
         *counter = 0u;
       }
     }

@@ -9,7 +9,8 @@
 // whose phi coordinates wrap across the periodic seam; the epilogue operands
 // as 32 x 16 boxes; the per-(r, theta) metric records (iL2[6], wo01[4],
 // iVal2, pad: one interleaved [n0+2][n1][12] table built at grid creation) as
-// one 12 x 18 box.  Rows outside the theta range are zero-filled by the TMA
+// one 12 x 18 box (slot 11 carries the aligned-volume row factor Val2 for
+// the PCG inner-product weight).  Rows outside the theta range are zero-filled by the TMA
 // unit: they only ever meet an inverse edge length of 0 (no flux through the
 // pole faces), exactly as the clamped values of the oracle do, and their
 // metric records are never read.  No per-thread async copies remain.
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   col.w2[1] = launder(col.w2[1]);
   col.ivg = launder(col.ivg);
   const bool pin_k = (g.pin_lo2 && kg == 0) || (g.pin_hi2 && kg == g.n2 - 1);
+  const double valg = Epi::NEEDS_W ? launder(__ldg(g.Valg + kg)) : 0.0;
   if (tid < 18) {  // phi-ring column tables
     const int side = tid / 9, q = tid % 9;
     bool okr;
@@ -333,7 +335,12 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
 #pragma unroll
           for (int q = 0; q < Epi::NOPS; ++q) ov[q] = eR[q * XO + r * MTK + tx];
-          epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov);
+          double W = 0.0;  // inner-product weight rho V = rho * (Val2(row) * Valg(k)) (record slot 11)
+          if constexpr (Epi::NEEDS_W) {
+            W = rM[jr * RW + 11] * valg;
+            if constexpr (RHO) W = rr[n] * W;
+          }
+          epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov, W);
         }
         if (!LAST) {
           if constexpr (RHO) {
