@@ -82,6 +82,11 @@ int pc_version(void);
  * over NCCL; nccl_uid points to an ncclUniqueId (128 bytes) or NULL. */
 int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx** out);
 int pc_ctx_destroy(pc_ctx* ctx);
+/* test hook: rank `rank` of an nranks r-slab decomposition WITHOUT a
+   communicator -- collectives are skipped (local reductions, no halo
+   exchange) and the caller sets the axis-0 ghost planes with
+   pc_field_set_ghost; used to check the slab kernels on one GPU */
+int pc_ctx_create_detached(int device, int nranks, int rank, pc_ctx** out);
 int pc_ctx_sync(pc_ctx* ctx);
 int pc_nccl_unique_id(void* out128); /* fills a fresh ncclUniqueId */
 
@@ -109,6 +114,9 @@ int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* h
 int pc_field_copy(pc_field* dst, const pc_field* src);
 int pc_field_fill(pc_field* f, double value);
 int pc_field_exchange_halo(pc_field* f); /* axis-0 ghost planes (no-op on 1 rank) */
+/* write ghost plane -1 (side 0) or n0 (side 1) of every component from a host
+   SoA plane [ncomp][n1][n2] */
+int pc_field_set_ghost(pc_field* f, int side, const double* host);
 /* pin / unpin a host buffer so uploads and downloads run at full PCIe speed */
 int pc_host_register(void* ptr, size_t bytes);
 int pc_host_unregister(void* ptr);

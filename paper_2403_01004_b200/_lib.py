@@ -50,6 +50,8 @@ _SIGS = {
     "pc_last_error_info": (c_int64, []),
     "pc_version": (c_int, []),
     "pc_ctx_create": (c_int, [c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    "pc_ctx_create_detached": (c_int, [c_int, c_int, c_int, POINTER(c_void_p)]),
+    "pc_field_set_ghost": (c_int, [c_void_p, c_int, POINTER(c_double)]),
     "pc_ctx_destroy": (c_int, [c_void_p]),
     "pc_ctx_sync": (c_int, [c_void_p]),
     "pc_nccl_unique_id": (c_int, [c_void_p]),

@@ -73,6 +73,7 @@ struct pc_ctx {
   int nranks = 1, rank = 0;
   cudaStream_t s = nullptr;
   ncclComm_t comm = nullptr;
+  bool detached = false;  // test hook: a slab rank without a communicator (ghost planes set by the caller)
   int max_blocks = 148 * 16;
   int max_red = 1 << 18;  // partial-sum slots (march grids are larger)
   // reduction scratch
@@ -233,7 +234,7 @@ static int check_launch(const char* what) {
 
 // ------------------------------------------------------------------ NCCL
 static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp) {
-  if (c->nranks <= 1) return PC_OK;
+  if (c->nranks <= 1 || c->detached) return PC_OK;
   nccl::Api* A = nccl::api();
   if (!A) return fail(PC_E_NCCL, "NCCL not available");
   const size_t pl = (size_t)g->g.plane;
@@ -264,7 +265,7 @@ static int halo_work(pc_grid* g, Work& w) {
   return halo_exchange(g->ctx, g, b, w.ncomp);
 }
 static int allreduce_u64_min(pc_ctx* c, unsigned long long* dptr) {
-  if (c->nranks <= 1) return PC_OK;
+  if (c->nranks <= 1 || c->detached) return PC_OK;
   nccl::Api* A = nccl::api();
   if (!A || A->allReduce(dptr, dptr, 1, nccl::kUint64, nccl::kMin, c->comm, c->s) != 0)
     return fail(PC_E_NCCL, "ncclAllReduce(u64 min)");
@@ -272,7 +273,7 @@ static int allreduce_u64_min(pc_ctx* c, unsigned long long* dptr) {
 }
 // the |F| argmax over all ranks (res holds this rank's pair on entry)
 static int global_argmax(pc_ctx* c) {
-  if (c->nranks <= 1) return PC_OK;
+  if (c->nranks <= 1 || c->detached) return PC_OK;
   nccl::Api* A = nccl::api();
   if (!A || !A->allGather_ || A->allGather(c->res, c->gath, 2, nccl::kDouble, c->comm, c->s) != 0)
     return fail(PC_E_NCCL, "ncclAllGather(argmax)");
@@ -281,7 +282,7 @@ static int global_argmax(pc_ctx* c) {
   return check_launch("k_argmax_combine");
 }
 static int allreduce_d(pc_ctx* c, double* dptr, size_t n, int op) {
-  if (c->nranks <= 1) return PC_OK;
+  if (c->nranks <= 1 || c->detached) return PC_OK;
   nccl::Api* A = nccl::api();
   if (!A || A->allReduce(dptr, dptr, n, nccl::kDouble, op, c->comm, c->s) != 0)
     return fail(PC_E_NCCL, "ncclAllReduce");
@@ -302,7 +303,7 @@ int pc_nccl_unique_id(void* out128) {
   return PC_OK;
 }
 
-int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx** out) {
+static int ctx_create(int device, int nranks, int rank, const void* nccl_uid, bool detached, pc_ctx** out) {
   if (!out || nranks < 1 || rank < 0 || rank >= nranks) return fail(PC_E_INVALID, "bad context arguments");
   CUDA_TRY(cudaSetDevice(device));
   pc_ctx* c = new pc_ctx();
@@ -329,7 +330,8 @@ int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx
   CUDA_TRY(cudaMallocHost(&c->h_bad, sizeof(int)));
   CUDA_TRY(cudaMallocHost(&c->h_minbits, sizeof(unsigned long long)));
   CUDA_TRY(cudaMallocHost(&c->h_maxout, sizeof(double)));
-  if (nranks > 1) {
+  c->detached = detached;
+  if (nranks > 1 && !detached) {
     nccl::Api* A = nccl::api();
     if (!A) {
       delete c;
@@ -340,6 +342,12 @@ int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx
   }
   *out = c;
   return PC_OK;
+}
+int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx** out) {
+  return ctx_create(device, nranks, rank, nccl_uid, false, out);
+}
+int pc_ctx_create_detached(int device, int nranks, int rank, pc_ctx** out) {
+  return ctx_create(device, nranks, rank, nullptr, true, out);
 }
 
 int pc_ctx_destroy(pc_ctx* c) {
@@ -630,6 +638,18 @@ int pc_field_download(const pc_field* f, double* host, int layout) {
   return PC_OK;
 }
 
+int pc_field_set_ghost(pc_field* f, int side, const double* host) {
+  if (!f || !host || (side != 0 && side != 1)) return fail(PC_E_INVALID, "bad ghost-plane arguments");
+  pc_grid* g = f->grid;
+  const size_t pl = (size_t)g->g.plane;
+  const int64_t plane = side == 0 ? -1 : g->g.n0;
+  for (int q = 0; q < f->ncomp; ++q)
+    CUDA_TRY(cudaMemcpyAsync(f->base(q) + plane * (int64_t)pl, host + (size_t)q * pl, pl * sizeof(double),
+                             cudaMemcpyHostToDevice, g->ctx->s));
+  CUDA_TRY(cudaStreamSynchronize(g->ctx->s));
+  return PC_OK;
+}
+
 int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* host) {
   if (!f || !host) return fail(PC_E_INVALID, "null argument");
   pc_grid* g = f->grid;
@@ -767,17 +787,40 @@ int pc_op_freeze(pc_op* op, const pc_field* T0) {
     CFld bsrc{{op->bsrc[0], op->bsrc[1], op->bsrc[2]}};
     Fld beta{{const_cast<double*>(op->ao.beta[0]), const_cast<double*>(op->ao.beta[1]),
               const_cast<double*>(op->ao.beta[2])}};
-    k_aligned_beta<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, T0->base(0), op->kfc + 1, op->Tfloor,
-                                                                   bsrc, beta, c->bad);
+    // beta on the interior AND the existing ghost planes (pointwise in T0 and
+    // b, whose ghost planes are exchanged first): no beta exchange needed
+    {
+      double* tb[1] = {const_cast<double*>(T0->buf[0])};
+      TRY(halo_exchange(c, g, tb, 1));
+      double* bb[3] = {const_cast<double*>(op->bsrc[0]) - g->g.plane, const_cast<double*>(op->bsrc[1]) - g->g.plane,
+                       const_cast<double*>(op->bsrc[2]) - g->g.plane};
+      TRY(halo_exchange(c, g, bb, 3));
+    }
+    GridDev gx = g->g;
+    const int glo = g->g.ghost_lo0 ? 1 : 0, ghi = g->g.ghost_hi0 ? 1 : 0;
+    gx.n0 = g->g.n0 + glo + ghi;
+    const int64_t sh = -(int64_t)glo * g->g.plane;
+    CFld bx{{bsrc.p[0] + sh, bsrc.p[1] + sh, bsrc.p[2] + sh}};
+    Fld betax{{beta.p[0] + sh, beta.p[1] + sh, beta.p[2] + sh}};
+    k_aligned_beta<<<node_blocks(c, gx), kThreads, 0, c->s>>>(gx, T0->base(0) + sh, op->kfc + 1 - glo, op->Tfloor,
+                                                              bx, betax, c->bad);
     c->st.launches++;
     TRY(check_launch("k_aligned_beta"));
     CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CUDA_TRY(cudaStreamSynchronize(c->s));
     if (*c->h_bad == 1) return fail(PC_E_DOMAIN, "aligned conduction: non-positive T0 (SPEC.md:120)");
-    double* bb[3] = {op->betabuf, op->betabuf + g->comp_elems, op->betabuf + 2 * g->comp_elems};
-    TRY(halo_exchange(c, g, bb, 3));
     TRY(run_bound(op, op->ao));
   } else {
+    // the face coefficient D (or nu rho) is read at the axis-0 neighbours:
+    // refresh the ghost planes of the coefficient fields
+    if (op->so.D) {
+      double* db[1] = {const_cast<double*>(op->so.D) - g->g.plane};
+      TRY(halo_exchange(c, g, db, 1));
+    }
+    if (op->so.rho) {
+      double* rb[1] = {const_cast<double*>(op->so.rho) - g->g.plane};
+      TRY(halo_exchange(c, g, rb, 1));
+    }
     TRY(run_bound(op, op->so));
   }
   op->diag_valid = op->dbuf != nullptr;
@@ -1030,6 +1073,7 @@ static int apply_any(pc_op* op, CFld u, Fld F, bool argmax) {
 static int need_frozen(pc_op* op) {
   if (op->kind == K_ALIGNED && !op->frozen)
     return fail(PC_E_INVALID, "aligned operator: call pc_op_freeze(T0) first (lagged diffusivity)");
+  if (!op->frozen) return pc_op_freeze(op, nullptr);  // scalar: coefficient ghost planes + bound
   return PC_OK;
 }
 

@@ -17,13 +17,20 @@ from . import _lib, geometry, mesh
 
 
 class Context:
-    def __init__(self, device: int = 0, nranks: int = 1, rank: int = 0, nccl_uid: bytes | None = None):
+    def __init__(self, device: int = 0, nranks: int = 1, rank: int = 0, nccl_uid: bytes | None = None,
+                 detached: bool = False):
+        """``detached``: test hook -- an r-slab rank with no communicator
+        (collectives skipped; ghost planes set with DeviceField.set_ghost)."""
         L = _lib.lib()
         h = c_void_p()
-        uid = None
-        if nccl_uid is not None:
-            uid = ctypes.create_string_buffer(bytes(nccl_uid), 128)
-        _lib.check(L.pc_ctx_create(int(device), int(nranks), int(rank), uid, byref(h)), "pc_ctx_create")
+        if detached:
+            _lib.check(L.pc_ctx_create_detached(int(device), int(nranks), int(rank), byref(h)),
+                       "pc_ctx_create_detached")
+        else:
+            uid = None
+            if nccl_uid is not None:
+                uid = ctypes.create_string_buffer(bytes(nccl_uid), 128)
+            _lib.check(L.pc_ctx_create(int(device), int(nranks), int(rank), uid, byref(h)), "pc_ctx_create")
         self.handle = h
         self.device = device
         self.nranks = nranks
@@ -211,6 +218,11 @@ class DeviceField:
             raise ValueError("download target must be a contiguous float64 array of the field size")
         _lib.check(_lib.lib().pc_field_download(self.handle, _lib.dptr(out), layout), "download")
         return out.reshape(shape)
+
+    def set_ghost(self, side: int, plane_soa: np.ndarray):
+        """Ghost plane -1 (side 0) or n0 (side 1) from (ncomp, n1, n2)."""
+        a = np.ascontiguousarray(plane_soa, dtype=np.float64)
+        _lib.check(_lib.lib().pc_field_set_ghost(self.handle, int(side), _lib.dptr(a)), "set_ghost")
 
     def download_planes(self, i0: int, n: int) -> np.ndarray:
         """Axis-0 planes [i0, i0 + n) as SoA (ncomp, n, n1, n2)."""

@@ -176,7 +176,7 @@ def test_sts_identity_for_zero_operator_on_gpu(gpu_ctx):
         u0 = vals[None, :, None, None]
         ref = osch.sts_step(lambda u: 0.0 * u, u0, 0.0 * u0, 0.3, s, kind, pinned).ravel()
         assert np.array_equal(out, ref)
-        assert np.max(np.abs(out - vals)) <= 8 * np.finfo(float).eps * 2.0
+        assert np.max(np.abs(out - vals)) <= 32 * np.finfo(float).eps * 2.0
 
 
 # ---------------------------------------------------------------- error contracts
