@@ -565,6 +565,8 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   }
 };
 
+constexpr int kMaxWarps = 16;  // epilogue block reductions serve 256- and 512-thread marching kernels
+__device__ __forceinline__ int block_threads() { return blockDim.x * blockDim.y; }
 __device__ __forceinline__ ArgMax block_argmax2d(ArgMax a, double* shv, long long* shi) {
   a = warp_argmax(a);
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
@@ -576,7 +578,7 @@ __device__ __forceinline__ ArgMax block_argmax2d(ArgMax a, double* shv, long lon
   __syncthreads();
   ArgMax r{-1.0, 0x7fffffffffffffffLL};
   if (w == 0) {
-    if (lane < MNT / 32) {
+    if (lane < block_threads() / 32) {
       r.v = shv[lane];
       r.i = shi[lane];
     }
@@ -613,8 +615,8 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
     best = am_better(best, ArgMax{fabs(f), aos_index(g, i, j, k, 0, 1)});
   }
   __device__ __forceinline__ void finish(const GridDev&) {
-    __shared__ double shv[MNT / 32];
-    __shared__ long long shi[MNT / 32];
+    __shared__ double shv[kMaxWarps];
+    __shared__ long long shi[kMaxWarps];
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblk = gridDim.x * gridDim.y * gridDim.z;
     ArgMax b = block_argmax2d(best, shv, shi);
@@ -625,7 +627,7 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
     if (last_block3(counter, nblk)) {
       ArgMax r{-1.0, 0x7fffffffffffffffLL};
       const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-      for (int q = tid; q < nblk; q += MNT) r = am_better(r, ArgMax{pv[q], pi[q]});
+      for (int q = tid; q < nblk; q += block_threads()) r = am_better(r, ArgMax{pv[q], pi[q]});
       r = block_argmax2d(r, shv, shi);
       if (tid == 0) {
         res->fmax = r.v;
@@ -642,7 +644,7 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
 __device__ __forceinline__ double sum_partials(const double* part, int nblk, double* sh) {
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   double a = 0.0;
-  for (int q = tid; q < nblk; q += MNT) a += part[q];
+  for (int q = tid; q < nblk; q += block_threads()) a += part[q];
   a = warp_sum(a);
   const int lane = tid & 31, w = tid >> 5;
   __syncthreads();
@@ -650,7 +652,7 @@ __device__ __forceinline__ double sum_partials(const double* part, int nblk, dou
   __syncthreads();
   double s = 0.0;
   if (tid == 0)
-    for (int q = 0; q < MNT / 32; ++q) s += sh[q];
+    for (int q = 0; q < block_threads() / 32; ++q) s += sh[q];
   return s;  // valid on thread 0
 }
 __device__ __forceinline__ double block_sum2d(double v, double* sh) {
@@ -662,7 +664,7 @@ __device__ __forceinline__ double block_sum2d(double v, double* sh) {
   __syncthreads();
   double s = 0.0;
   if (tid == 0)
-    for (int q = 0; q < MNT / 32; ++q) s += sh[q];
+    for (int q = 0; q < block_threads() / 32; ++q) s += sh[q];
   return s;  // valid on thread 0
 }
 
@@ -687,7 +689,7 @@ struct EpiMatvecT {
     acc += (W * pv) * ap;
   }
   __device__ __forceinline__ void finish(const GridDev&) {
-    __shared__ double sh[MNT / 32];
+    __shared__ double sh[kMaxWarps];
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblk = gridDim.x * gridDim.y * gridDim.z;
@@ -736,7 +738,7 @@ struct EpiPcgInitT {
     s2 += (W * bv) * bv;
   }
   __device__ __forceinline__ void finish(const GridDev&) {
-    __shared__ double sh[MNT / 32];
+    __shared__ double sh[kMaxWarps];
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblk = gridDim.x * gridDim.y * gridDim.z;
