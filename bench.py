@@ -392,20 +392,27 @@ def _traffic(name, kind, field):
 
 
 def run_e2e(args, prob, sc, pcfg, ctx, dist):
+    """The same metric through the public API with every input on the HOST:
+    each step uploads its inputs (state fields, b-hat, rho) from pinned host
+    memory, advances with ptl.split_advance and downloads the advanced fields;
+    the device-resident problem is freed first.  One GPU: host mesh.Fields
+    (global arrays).  N GPUs: each rank holds its r-slab of every input in
+    pinned host memory and goes through device.DeviceField.upload/download
+    around the same split_advance (a global host array per rank would need
+    N x the C5 host footprint)."""
     import gc
-    """The same metric through ptl.split_advance on HOST Fields: every step
-    uploads its inputs (state fields, b-hat, rho) from pinned host memory and
-    downloads the advanced fields; the device-resident problem is freed first."""
-    from paper_2403_01004_b200 import mesh, operators, ptl
+    from paper_2403_01004_b200 import device, mesh, operators, ptl
 
-    host = prob.host_inputs()
+    multi = (dist is not None and ctx.nranks > 1) or os.environ.get("BENCH_E2E_SLABS") == "1"
+    host = prob.host_inputs()  # this rank's slab, AoS (n0 local, n1, n2, ncomp)
     w, name = prob.w, prob.name
     ops_desc = [(f, op.kind, nc) for f, op, nc, _ in prob.ops]
     outer_dt = prob.outer_dt
     prob.free()
-    for a in host.values():
-        ctx.pin(a)
     state_names = [f for f, _, _ in ops_desc]
+    outbuf = {f: np.empty_like(host[f]) for f in state_names} if multi else {}
+    for a in list(host.values()) + list(outbuf.values()):
+        ctx.pin(a)
     h2d = sum(host[k].nbytes for k in host)
     d2h = sum(host[k].nbytes for k in state_names)
     cells = int(np.prod(w.grid.shape))
@@ -414,19 +421,36 @@ def run_e2e(args, prob, sc, pcfg, ctx, dist):
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
+        if multi:
+            dg = device.device_grid(w.grid, w.bc, ctx)
+            dev = {}
+            for k, a in host.items():
+                dev[k] = device.DeviceField(dg, a.shape[-1])
+                dev[k].upload(a)
+            src = dev
+        else:
+            src = host
         ops = []
         for f, kind, nc in ops_desc:
             if kind == "aligned":
-                cfg = operators.AlignedConductionConfig(b_hat=host["b"], rho=host.get("rho"), m_p=3.0, k_B=1.0,
+                cfg = operators.AlignedConductionConfig(b_hat=src["b"], rho=src.get("rho"), m_p=3.0, k_B=1.0,
                                                         bc=w.bc)
                 ops.append((f, operators.DiffusionOperator.aligned(cfg)))
             else:
-                cfg = operators.ScalarDiffusionConfig(nu=1.0, rho=host.get("rho"), bc=w.bc, vector_metric=nc == 3)
+                cfg = operators.ScalarDiffusionConfig(nu=1.0, rho=src.get("rho"), bc=w.bc, vector_metric=nc == 3)
                 ops.append((f, operators.DiffusionOperator.scalar(cfg, nc)))
-        state = {f: mesh.Field(w.grid, host[f].reshape(tuple(w.grid.shape) + (-1,))) for f in state_names}
+        if multi:
+            state = {f: dev[f] for f in state_names}
+        else:
+            state = {f: mesh.Field(w.grid, host[f].reshape(tuple(w.grid.shape) + (-1,))) for f in state_names}
         out, reps = ptl.split_advance(ops, state, outer_dt, [(sc, pcfg)] * len(ops))
+        if multi:
+            for f in state_names:
+                out[f].download(outbuf[f])
         cu += cells * sum(r.total_iters for r in reps)
         del ops, out, state
+        if multi:
+            del dev, src
         gc.collect()  # operator <-> device-handle cycles: return HBM before the next step
     ctx.sync()
     dt = time.perf_counter() - t0
@@ -435,11 +459,15 @@ def run_e2e(args, prob, sc, pcfg, ctx, dist):
         t = torch.tensor([dt], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
-    for a in host.values():
+        b = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64)
+        dist.all_reduce(b)
+        h2d, d2h = b[0].item(), b[1].item()
+    for a in list(host.values()) + list(outbuf.values()):
         ctx.unpin(a)
     return {"value": cu / dt, "unit": "cell-updates/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / args.steps,
-            "path": "ptl.split_advance(host Fields, host b-hat/rho) -> pc_cycle per operator"}
+            "path": ("device.DeviceField.upload(pinned host slab) -> ptl.split_advance -> download, per rank"
+                     if multi else "ptl.split_advance(host Fields, host b-hat/rho) -> pc_cycle per operator")}
 
 
 # ---------------------------------------------------------------- CPU oracle
