@@ -74,6 +74,9 @@ struct pc_ctx {
   cudaStream_t s = nullptr;
   ncclComm_t comm = nullptr;
   bool detached = false;  // test hook: a slab rank without a communicator (ghost planes set by the caller)
+  cudaStream_t sc = nullptr;            // communication stream (halo exchange overlapped with interior chunks)
+  cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
+  int zpart = 0;                        // r-chunk partition of the next marching launch: 0 all, 1 interior, 2 boundary
   int max_blocks = 148 * 16;
   int max_red = 1 << 18;  // partial-sum slots (march grids are larger)
   // reduction scratch
@@ -233,8 +236,9 @@ static int check_launch(const char* what) {
 }
 
 // ------------------------------------------------------------------ NCCL
-static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp) {
+static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp, cudaStream_t st = nullptr) {
   if (c->nranks <= 1 || c->detached) return PC_OK;
+  if (!st) st = c->s;
   nccl::Api* A = nccl::api();
   if (!A) return fail(PC_E_NCCL, "NCCL not available");
   const size_t pl = (size_t)g->g.plane;
@@ -245,12 +249,12 @@ static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp) 
   for (int q = 0; q < ncomp; ++q) {
     double* base = bufs[q] + pl;  // interior plane 0
     if (lo >= 0) {
-      A->send(base, pl, nccl::kDouble, lo, c->comm, c->s);
-      A->recv(base - pl, pl, nccl::kDouble, lo, c->comm, c->s);
+      A->send(base, pl, nccl::kDouble, lo, c->comm, st);
+      A->recv(base - pl, pl, nccl::kDouble, lo, c->comm, st);
     }
     if (hi >= 0) {
-      A->send(base + (size_t)(n0 - 1) * pl, pl, nccl::kDouble, hi, c->comm, c->s);
-      A->recv(base + (size_t)n0 * pl, pl, nccl::kDouble, hi, c->comm, c->s);
+      A->send(base + (size_t)(n0 - 1) * pl, pl, nccl::kDouble, hi, c->comm, st);
+      A->recv(base + (size_t)n0 * pl, pl, nccl::kDouble, hi, c->comm, st);
     }
   }
   if (A->groupEnd() != 0) return fail(PC_E_NCCL, "ncclGroupEnd");
@@ -314,6 +318,9 @@ static int ctx_create(int device, int nranks, int rank, const void* nccl_uid, bo
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   c->max_blocks = sms * 16;
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->sc, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
   CUDA_TRY(cudaMalloc(&c->red_v, sizeof(double) * c->max_red));
   CUDA_TRY(cudaMalloc(&c->red_v2, sizeof(double) * c->max_red));
   CUDA_TRY(cudaMalloc(&c->red_i, sizeof(long long) * c->max_red));
@@ -351,6 +358,11 @@ int pc_ctx_create_detached(int device, int nranks, int rank, pc_ctx** out) {
 }
 
 int pc_ctx_destroy(pc_ctx* c) {
+  if (c) {
+    if (c->sc) cudaStreamDestroy(c->sc);
+    if (c->ev_in) cudaEventDestroy(c->ev_in);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  }
   if (!c) return PC_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->s);
@@ -867,6 +879,22 @@ int pc_op_diagonal(pc_op* op, pc_field* out) {
   return PC_OK;
 }
 
+// r-chunk partition of a marching launch (ctx->zpart): the interior chunks
+// (1 .. nz-2) or the two boundary chunks, whose ghost-plane reads wait for
+// the halo exchange
+static int zsplit(const pc_ctx* c, dim3& grid) {
+  const int nz = (int)grid.z;
+  if (c->zpart == 1) {
+    grid.z = nz - 2;
+    return 1;
+  }
+  if (c->zpart == 2) {
+    grid.z = nz > 1 ? 2 : 1;
+    return -nz;
+  }
+  return 0;
+}
+
 // r-chunk length of the marching aligned kernels
 static int march_R(const pc_grid* g) {
   const int tiles = ((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + MTJ - 1) / MTJ);
@@ -944,7 +972,8 @@ static int launch_tma_t(pc_op* op, const TmaMaps& maps, const Epi& epi, const in
     CUDA_TRY(cudaFuncSetAttribute(k_aligned_tma<Epi, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  k_aligned_tma<Epi, RHO><<<grid, dim3(MTK, MTY), smem, c->s>>>(g->g, op->ao, maps, epi, R, skip);
+  const int zsel = zsplit(c, grid);
+  k_aligned_tma<Epi, RHO><<<grid, dim3(MTK, MTY), smem, c->s>>>(g->g, op->ao, maps, epi, R, zsel, skip);
   c->st.launches++;
   return check_launch(what);
 }
@@ -988,7 +1017,8 @@ static int launch_march(pc_op* op, const double* Tin, const Epi& epi, const int*
                                   (int)sizeof(MarchSmem)));
     attr = true;
   }
-  k_aligned_march<Epi><<<grid, dim3(MTK, MTY), sizeof(MarchSmem), c->s>>>(g->g, op->ao, Tin, epi, R, skip);
+  const int zsel = zsplit(c, grid);
+  k_aligned_march<Epi><<<grid, dim3(MTK, MTY), sizeof(MarchSmem), c->s>>>(g->g, op->ao, Tin, epi, R, zsel, skip);
   c->st.launches++;
   return check_launch(what);
 }
@@ -1014,8 +1044,9 @@ static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, c
                                   (int)sizeof(SMarchSmem<NC>)));
     attr = true;
   }
+  const int zsel = zsplit(c, grid);
   k_scalar_march<NC, VEC, DM, Epi><<<grid, SNT, sizeof(SMarchSmem<NC>), c->s>>>(g->g, op->so, u.p[0], u.p[1], u.p[2],
-                                                                                epi, R, skip);
+                                                                                epi, R, zsel, skip);
   c->st.launches++;
   return check_launch(what);
 }
@@ -1244,31 +1275,57 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
   Work* um1 = &A;
   Work* out = &B;
   Work* um2w = nullptr;  // nullptr -> u0
+  // multi-rank: the ghost planes of u_{k-1} travel on the communication
+  // stream while the interior r-chunks (which never read them) run; the two
+  // boundary chunks follow the exchange (PC_SPLIT_STAGE forces the split
+  // launches on one rank, for testing)
+  const bool force_split = getenv("PC_SPLIT_STAGE") != nullptr;
+  const bool marching = std::is_same<Op, AlignedOp>::value || smarch_ok(op);
+  const int Rz = std::is_same<Op, AlignedOp>::value ? march_R(g) : smarch_R(g);
+  const int nz = (g->g.n0 + Rz - 1) / Rz;
+  const bool overlap = marching && nz >= 3 && ((c->nranks > 1 && !c->detached) || force_split);
   for (int k = 2; k <= s && rc == PC_OK; ++k) {
     const double* r = tab + 5 * (k - 1);
     StageCoef sc{r[0], r[1], r[2], r[3], r[4]};
-    rc = halo_work(g, *um1);
-    if (rc) break;
     CFld m2 = um2w ? um2w->cf() : cfld(u);
-    if constexpr (std::is_same<Op, AlignedOp>::value) {
-      EpiStage e{m2.p[0], cfld(u).p[0], y0.base(0), out->base(0), sc, k, c->bad};
-      rc = launch_march(op, um1->base(0), e, nullptr, "k_aligned_march<stage>");
-    } else if (smarch_ok(op)) {
-      CFld u0f = cfld(u), y0f = y0.cf();
-      Fld of = out->f();
-      SEpiStage e{{u0f.p[0], u0f.p[1], u0f.p[2]}, {m2.p[0], m2.p[1], m2.p[2]}, {y0f.p[0], y0f.p[1], y0f.p[2]},
-                  {of.p[0], of.p[1], of.p[2]}, nc, sc, k, c->bad};
-      if (nc == 3) {
-        rc = launch_smarch_nc<3>(op, um1->cf(), e, "k_scalar_march<stage>");
-      } else {
+    auto launch_stage = [&]() -> int {
+      if constexpr (std::is_same<Op, AlignedOp>::value) {
+        EpiStage e{m2.p[0], cfld(u).p[0], y0.base(0), out->base(0), sc, k, c->bad};
+        return launch_march(op, um1->base(0), e, nullptr, "k_aligned_march<stage>");
+      } else if (smarch_ok(op)) {
+        CFld u0f = cfld(u), y0f = y0.cf();
+        Fld of = out->f();
+        SEpiStage e{{u0f.p[0], u0f.p[1], u0f.p[2]}, {m2.p[0], m2.p[1], m2.p[2]}, {y0f.p[0], y0f.p[1], y0f.p[2]},
+                    {of.p[0], of.p[1], of.p[2]}, nc, sc, k, c->bad};
+        if (nc == 3) return launch_smarch_nc<3>(op, um1->cf(), e, "k_scalar_march<stage>");
         SEpiStage1 e1;
         static_cast<SEpiStage&>(e1) = e;
-        rc = launch_smarch_nc<1>(op, um1->cf(), e1, "k_scalar_march<stage>");
+        return launch_smarch_nc<1>(op, um1->cf(), e1, "k_scalar_march<stage>");
+      } else {
+        k_stage<<<nb, kThreads, 0, c->s>>>(g->g, o, um1->cf(), m2, cfld(u), y0.cf(), out->f(), sc, k, c->bad);
+        c->st.launches++;
+        return check_launch("k_stage");
       }
+    };
+    if (overlap) {
+      CUDA_TRY(cudaEventRecord(c->ev_in, c->s));
+      CUDA_TRY(cudaStreamWaitEvent(c->sc, c->ev_in, 0));
+      double* hb[3] = {um1->b[0], um1->b[1], um1->b[2]};
+      rc = halo_exchange(c, g, hb, um1->ncomp, c->sc);
+      if (rc) break;
+      CUDA_TRY(cudaEventRecord(c->ev_halo, c->sc));
+      c->zpart = 1;
+      rc = launch_stage();
+      c->zpart = 0;
+      if (rc) break;
+      CUDA_TRY(cudaStreamWaitEvent(c->s, c->ev_halo, 0));
+      c->zpart = 2;
+      rc = launch_stage();
+      c->zpart = 0;
     } else {
-      k_stage<<<nb, kThreads, 0, c->s>>>(g->g, o, um1->cf(), m2, cfld(u), y0.cf(), out->f(), sc, k, c->bad);
-      c->st.launches++;
-      rc = check_launch("k_stage");
+      rc = halo_work(g, *um1);
+      if (rc) break;
+      rc = launch_stage();
     }
     c->st.stage_launches++;
     // rotate: u_{k-1} -> u_{k-2}, u_k -> u_{k-1}; the next stage writes into

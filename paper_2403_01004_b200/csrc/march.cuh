@@ -47,6 +47,15 @@ constexpr int NEO = 3;           // epilogue operand arrays staged per node (max
 constexpr int MTN = MTJ * MTK;   // tile nodes
 constexpr int NRING = 2 * MTK + 2 * MTJ;
 
+// r-chunk of this block: zsel == 0 all chunks (chunk = blockIdx.z); zsel > 0
+// the interior chunks 1 .. nz-2 (halo exchange overlapped, see sts_stages);
+// zsel = -nz the two boundary chunks 0 and nz-1 (after the exchange)
+__device__ __forceinline__ int chunk_of(int zsel) {
+  if (zsel == 0) return blockIdx.z;
+  if (zsel > 0) return blockIdx.z + 1;
+  return blockIdx.z == 0 ? 0 : -zsel - 1;
+}
+
 struct PlaneMap {
   int mem;      // memory plane to read (ghost planes allowed)
   int row;      // table row
@@ -229,13 +238,13 @@ __device__ __forceinline__ void node_E_rows(double Tv, const double (&Tn)[3][2],
 //   epi.finish(g)                          block reduction, if any
 template <class Epi>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp op, const double* __restrict__ Tin,
-                                                          Epi epi, int R, const int* skip) {
+                                                          Epi epi, int R, int zsel, const int* skip) {
   extern __shared__ __align__(16) unsigned char march_smem[];
   MarchSmem& S = *reinterpret_cast<MarchSmem*>(march_smem);
   if (skip && *skip) return;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * MTK + tx;
-  const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * MTJ, i0 = blockIdx.z * R;
+  const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * MTJ, i0 = chunk_of(zsel) * R;
   const int iend = min(i0 + R, g.n0);
   const int kg = k0 + tx;
 

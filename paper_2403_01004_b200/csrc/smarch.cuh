@@ -38,7 +38,7 @@ struct SMarchSmem {
 template <int NC, bool VEC, int DM, class Epi>
 __global__ void __launch_bounds__(SNT, 3) k_scalar_march(GridDev g, ScalarOp op, const double* __restrict__ u0p,
                                                          const double* __restrict__ u1p,
-                                                         const double* __restrict__ u2p, Epi epi, int R,
+                                                         const double* __restrict__ u2p, Epi epi, int R, int zsel,
                                                          const int* skip) {
   extern __shared__ __align__(16) unsigned char smarch_smem[];
   SMarchSmem<NC>& S = *reinterpret_cast<SMarchSmem<NC>*>(smarch_smem);
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(SNT, 3) k_scalar_march(GridDev g, ScalarOp op,
   const double* dsrc = DM == 1 ? op.D : op.rho;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int tid = threadIdx.x;
-  const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * SMJ, i0 = blockIdx.z * R;
+  const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * SMJ, i0 = chunk_of(zsel) * R;
   const int iend = min(i0 + R, g.n0);
   const int kg = k0 + tx, jg = j0 + ty;
 

@@ -90,7 +90,7 @@ __device__ __forceinline__ void tma3(double* dst, const CUtensorMap* map, int c0
 
 template <class Epi, bool RHO>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op, const __grid_constant__ TmaMaps maps,
-                                                        Epi epi, int R, const int* skip) {
+                                                        Epi epi, int R, int zsel, const int* skip) {
   extern __shared__ __align__(128) unsigned char tma_smem[];
   // bulk-tensor destinations must be 128-byte aligned: align the dynamic base
   // (static epilogue scratch may precede it); the launch adds 128 bytes
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   if (skip && *skip) return;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * MTK + tx;
-  const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * MTJ, i0 = blockIdx.z * R;
+  const int k0 = blockIdx.x * MTK, j0 = blockIdx.y * MTJ, i0 = chunk_of(zsel) * R;
   const int iend = min(i0 + R, g.n0);
   const int kg = k0 + tx;
   const int kL = k0 == 0 ? g.n2 - 2 : k0 - 2;     // strip of columns k0-2, k0-1

@@ -98,3 +98,35 @@ def test_tma_and_cpasync_paths_bitwise(gpu_ctx, monkeypatch):
         out.append((o.values.copy(), [e.iters for e in rep.entries]))
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+@pytest.mark.parametrize("kind,n,no_tma", [("aligned", (24, 40, 64), False), ("aligned", (24, 24, 48), True),
+                                           ("viscous", (40, 24, 64), False)],
+                         ids=["aligned-tma", "aligned-cpasync", "viscous"])
+def test_split_stage_launches_bitwise(gpu_ctx, monkeypatch, kind, n, no_tma):
+    """The multi-rank overlap schedule (interior r-chunks launched while the
+    halo planes travel, then the two boundary chunks) forced on one rank
+    (PC_SPLIT_STAGE): bitwise the single-launch stages, same counts."""
+    if no_tma:
+        monkeypatch.setenv("PC_NO_TMA", "1")
+    if kind == "aligned":
+        w = configs.c3(n=n)
+        T = operators.Field(w.grid, w.fields["T"])
+        make = lambda: _aligned(w)  # noqa: E731
+        nc = 1
+    else:
+        w = configs.c2(n=n)
+        T = operators.Field(w.grid, w.fields["v"])
+        make = lambda: operators.DiffusionOperator.scalar(  # noqa: E731
+            operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc, vector_metric=True), 3)
+        nc = 3
+    out = []
+    for split in (False, True):
+        if split:
+            monkeypatch.setenv("PC_SPLIT_STAGE", "1")
+        op = make()
+        dtE = op.device_op(w.grid, nc).dt_euler
+        o, rep = ptl.cycle_operator(op, schemes.SchemeConfig("rkl2"), T, 200 * dtE)
+        out.append((o.values.copy(), [e.iters for e in rep.entries]))
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
