@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const doubl
 // flight (all loads issued before the arithmetic), parallel fixed-order final
 // sum in the last block.
 template <bool RHO, bool ADIAG>
-__global__ void __launch_bounds__(kThreads) k_pcg_update1(GridDev g, double* __restrict__ x, double* __restrict__ r,
+__global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* __restrict__ x, double* __restrict__ r,
                                                           const double* __restrict__ p,
                                                           const double* __restrict__ Ap,
                                                           const double* __restrict__ dg,
