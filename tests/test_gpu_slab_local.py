@@ -132,3 +132,46 @@ def test_argmax_index_is_global_on_slabs(gpu_ctx):
             del T, b, op, dop, F
         finally:
             ctx.close()
+
+
+def test_ptl_pairs_across_slab_boundaries(gpu_ctx):
+    """Each rank's PTL pairs at its |F| maximum, planted on the slab's FIRST
+    (then LAST) plane so that one pair reaches into the ghost plane, equal the
+    pairs of the global arrays at that node (bitwise)."""
+    from ctypes import byref, c_double, c_int, c_int64
+    from oracle.ptl import neighbours
+    w = configs.c3(n=(24, 20, 64))
+    geom = oracle_geometry(w.grid, w.bc)
+    rng = np.random.default_rng(7)
+    P = 3
+    for side in (0, 1):
+        u = rng.normal(size=(1,) + geom.shape)
+        F = rng.normal(size=(1,) + geom.shape)
+        for r in range(P):
+            i0, nl = geometry.slab_bounds(geom.shape[0], P, r)
+            pi = i0 if side == 0 else i0 + nl - 1
+            F[0, pi, 7, 11] = 50.0 + r  # this slab's maximum
+            u[0, pi, 7, 11] = 3.0       # du of one sign against every neighbour ...
+            F[0, pi, 7, 11] *= -1.0     # ... dF of the other: every pair is a candidate
+        for r in range(P):
+            ctx = device.Context(0, P, r, detached=True)
+            try:
+                dg = device.device_grid(w.grid, w.bc, ctx)
+                uf, Ff = _slab_field(dg, u), _slab_field(dg, F)
+                v, lim, k = c_double(), c_int(), c_int64()
+                _lib.check(_lib.lib().pc_ptl(dg.handle, uf.handle, Ff.handle, 1e-12, 0, byref(v), byref(lim),
+                                             byref(k)), "pc_ptl")
+                i0, nl = dg.i0, dg.n0_local
+                pt = (i0 if side == 0 else i0 + nl - 1, 7, 11)
+                thr = 1e-12 * abs(F[(0,) + pt])
+                best = None
+                for nb in neighbours(geom, pt):
+                    du = u[(0,) + pt] - u[(0,) + nb]
+                    dF = F[(0,) + pt] - F[(0,) + nb]
+                    if du != 0.0 and abs(dF) > thr and du * dF < 0.0:
+                        best = -du / dF if best is None else min(best, -du / dF)
+                assert k.value == (pt[0] * geom.shape[1] + pt[1]) * geom.shape[2] + pt[2]
+                assert lim.value == 1 and v.value == best, f"rank {r}: PTL pairs differ"
+                del uf, Ff
+            finally:
+                ctx.close()
