@@ -78,6 +78,7 @@ struct pc_ctx {
   cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
   int zpart = 0;                        // r-chunk partition of the next marching launch: 0 all, 1 interior, 2 boundary
   int max_blocks = 148 * 16;
+  int sms = 148;
   int max_red = 1 << 18;  // partial-sum slots (march grids are larger)
   // reduction scratch
   double* red_v = nullptr;
@@ -317,6 +318,7 @@ static int ctx_create(int device, int nranks, int rank, const void* nccl_uid, bo
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   c->max_blocks = sms * 16;
+  c->sms = sms;
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->sc, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
@@ -897,10 +899,31 @@ static int zsplit(const pc_ctx* c, dim3& grid) {
 
 // r-chunk length of the marching aligned kernels
 static int march_R(const pc_grid* g) {
-  const int tiles = ((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + MTJ - 1) / MTJ);
-  int R = 32;
-  while (R > 4 && (int64_t)tiles * ((g->g.n0 + R - 1) / R) < 148 * 8) R /= 2;
-  return R;
+  // r-chunk length: a block marches R planes after a one-plane prologue, so
+  // the device time is ~ ceil(blocks / resident slots) x (R + 1) plane-steps;
+  // pick the R (4 .. 128) that maximises useful plane-steps per slot-step
+  // (PC_MARCH_R overrides, for experiments)
+  if (const char* e = getenv("PC_MARCH_R")) {
+    const int r = atoi(e);
+    if (r >= 1) return r;
+  }
+  const int64_t tiles = (int64_t)((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + MTJ - 1) / MTJ);
+  const int64_t slots = (int64_t)g->ctx->sms * 2;  // 2 resident blocks per SM
+  const int n0 = g->g.n0;
+  int best = 4;
+  double best_eff = -1.0;
+  const bool slab = g->g.ghost_lo0 || g->g.ghost_hi0;  // keep >= 3 chunks: interior chunks overlap the halo exchange
+  for (int R = 4; R <= 128; R += 4) {
+    if (slab && (n0 + R - 1) / R < 3 && R > 4) continue;
+    const int64_t blocks = tiles * ((n0 + R - 1) / R);
+    const int64_t waves = (blocks + slots - 1) / slots;
+    const double eff = (double)n0 * tiles / ((double)waves * slots * (R + 1));
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = R;
+    }
+  }
+  return best;
 }
 static dim3 march_grid(const pc_grid* g, int R) {
   return dim3((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + MTJ - 1) / MTJ, (g->g.n0 + R - 1) / R);
