@@ -140,6 +140,12 @@ int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho,
  * evaluate the Gershgorin bound and the Jacobi diagonal. */
 int pc_op_freeze(pc_op* op, const pc_field* T0);
 int pc_op_destroy(pc_op* op);
+/* BE+PCG preconditioner: PC_PC_JACOBI (SPEC PC1, default) or PC_PC_LINE_R
+   (block Jacobi over r-lines, Thomas solves; aligned operator, one rank) --
+   a GPU substitute for the SPEC's sequential ILU0 (PC2) */
+#define PC_PC_JACOBI 0
+#define PC_PC_LINE_R 1
+int pc_op_set_preconditioner(pc_op* op, int pc);
 int pc_op_apply(pc_op* op, const pc_field* u, pc_field* F);
 int pc_op_euler_dt(pc_op* op, double* dt_euler);
 /* -J_ii per node (pinned rows 0), the Jacobi building block */

@@ -379,3 +379,54 @@ def aligned_gershgorin(geom, b, c, rho=None, pref=1.0):
     lam[geom.pinned] = 0.0
     dg[geom.pinned] = 0.0
     return lam, dg
+
+
+# ---------------------------------------------------------------- line-r preconditioner
+# (PC2 substitute: block Jacobi over r-lines.  The r-line block
+# of -J is a principal submatrix of a W-symmetric positive semi-definite
+# matrix and, for the 7- and 19-point stencils, exactly tridiagonal, so
+# M = a + dt (line block of -J) is SPD and the Thomas algorithm needs no
+# pivoting.)
+
+def aligned_line_offdiag(geom, b, c, rho=None, pref=1.0):
+    """-J_{i,i-1}, -J_{i,i+1} of the aligned operator: ((H[m, -+e_r] * iVal)
+    * pref) / rho, pinned rows 0 (same expression order as the diagonal)."""
+    H = aligned_hessian_rows(geom, aligned_beta(b, c))
+    iv = _b2(geom.iVal2) * _b1(geom.iValg)
+    out = []
+    for off in ((-1, 0, 0), (1, 0, 0)):
+        j = (H[OFF_INDEX[off]] * iv) * pref
+        if rho is not None:
+            j = j / rho
+        j = j.copy()
+        j[geom.pinned] = 0.0
+        out.append(j)
+    return out[0], out[1]
+
+
+def line_factor(a, d, jl, ju, dt):
+    """Thomas factorisation of M = a + dt d (diagonal), dt jl / dt ju (off
+    diagonals) along axis 0, sequential in i and elementwise over the lines:
+    inv_i = 1 / (m_i - l_i cp_{i-1}), cp_i = u_i inv_i."""
+    n0 = d.shape[0]
+    m = a + dt * d
+    inv = np.empty_like(d)
+    cp = np.empty_like(d)
+    for i in range(n0):
+        den = m[i] if i == 0 else m[i] - (dt * jl[i]) * cp[i - 1]
+        inv[i] = 1.0 / den
+        cp[i] = (dt * ju[i]) * inv[i]
+    return inv, cp
+
+
+def line_solve(r, jl, inv, cp, dt):
+    """z = M^{-1} r: forward z'_i = (r_i - l_i z'_{i-1}) inv_i, backward
+    z_i = z'_i - cp_i z_{i+1}."""
+    n0 = r.shape[0]
+    z = np.empty_like(r)
+    z[0] = r[0] * inv[0]
+    for i in range(1, n0):
+        z[i] = (r[i] - (dt * jl[i]) * z[i - 1]) * inv[i]
+    for i in range(n0 - 2, -1, -1):
+        z[i] = z[i] - cp[i] * z[i + 1]
+    return z

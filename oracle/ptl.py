@@ -60,6 +60,12 @@ class OracleOperator:
         lam, _ = self.bound_and_diag()
         return ops.euler_dt(lam)
 
+    def line_offdiag(self):
+        """(-J_{i,i-1}, -J_{i,i+1}) for the r-line preconditioner (aligned only)."""
+        if self.kind != "aligned":
+            raise NotImplementedError("the r-line preconditioner is built for the aligned operator")
+        return ops.aligned_line_offdiag(self.geom, self.b, self.c, self.rho, self.pref)
+
     def weights(self):
         V = self.geom.volume() if self.kind == "scalar" else self.geom.aligned_volume()
         W = V if self.rho is None else self.rho * V
@@ -144,6 +150,7 @@ class OracleScheme:
     tol: float = 1e-10
     max_iter: int = 10000
     make_odd: bool = False
+    preconditioner: str = "jacobi"  # or "line-r" (aligned / scalar one-component operators)
 
 
 def step_count(scheme, dt, dt_euler):
@@ -181,8 +188,9 @@ def cycle_operator(op, scheme, u, outer_dt, eps_rel=1e-12, floor="euler", floor_
             u = sch.sts_step(op.apply, u, F, dt, s, scheme.kind, pinned)
             iters = s
         elif scheme.kind == "backward_euler":
+            line = op.line_offdiag() if scheme.preconditioner == "line-r" else None
             u, iters, rel, conv = sch.backward_euler_step(
-                op.apply, diag, W, u, dt, scheme.tol, scheme.max_iter, pinned)
+                op.apply, diag, W, u, dt, scheme.tol, scheme.max_iter, pinned, line=line)
         else:
             u = u + dt * F
             u[..., pinned] = u[..., pinned]

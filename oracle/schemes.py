@@ -187,14 +187,24 @@ def pcg_solve(A, b, dinv_apply, x0, W, tol, max_iter):
     return x, it, rel, converged
 
 
-def backward_euler_step(apply, diag, W, u, dt, tol, max_iter, pinned):
-    """Solve (I - dt J) x = u with x0 = u; ``diag`` = -J_ii (pinned rows 0)."""
+def backward_euler_step(apply, diag, W, u, dt, tol, max_iter, pinned, line=None):
+    """Solve (I - dt J) x = u with x0 = u; ``diag`` = -J_ii (pinned rows 0).
+    ``line`` = (jl, ju): the r-line preconditioner (-J_{i,i-1}, -J_{i,i+1},
+    single component) instead of point Jacobi."""
     dvec = 1.0 + dt * diag
 
     def A(x):
         return x - dt * apply(x)
 
-    def dinv(r):
-        return r / dvec
+    if line is None:
+        def dinv(r):
+            return r / dvec
+    else:
+        from .operators import line_factor, line_solve
+        jl, ju = line
+        inv, cp = line_factor(1.0, diag[0], jl, ju, dt)
+
+        def dinv(r):
+            return line_solve(r[0], jl, inv, cp, dt)[None]
 
     return pcg_solve(A, u, dinv, u, W, tol, max_iter)

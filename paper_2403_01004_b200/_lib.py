@@ -18,6 +18,7 @@ PC_OK = 0
 PC_E_INVALID, PC_E_INDEFINITE, PC_E_DIVERGED, PC_E_BLOWUP, PC_E_CAP = 1, 2, 3, 4, 5
 PC_E_CUDA, PC_E_NCCL, PC_E_DOMAIN, PC_E_NOTCONV = 6, 7, 8, 9
 LAYOUT_AOS, LAYOUT_SOA = 0, 1
+PC_JACOBI, PC_LINE_R = 0, 1
 RKL2, RKG2, BE, EULER = 0, 1, 2, 3
 FLOOR_EULER, FLOOR_FRACTION = 0, 1
 
@@ -51,6 +52,7 @@ _SIGS = {
     "pc_version": (c_int, []),
     "pc_ctx_create": (c_int, [c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
     "pc_ctx_create_detached": (c_int, [c_int, c_int, c_int, POINTER(c_void_p)]),
+    "pc_op_set_preconditioner": (c_int, [c_void_p, c_int]),
     "pc_field_set_ghost": (c_int, [c_void_p, c_int, POINTER(c_double)]),
     "pc_ctx_destroy": (c_int, [c_void_p]),
     "pc_ctx_sync": (c_int, [c_void_p]),

@@ -145,6 +145,9 @@ struct pc_op {
   double lam_max = 0.0;
   double dt_euler = INFINITY;
   bool frozen = false;
+  int pc = PC_PC_JACOBI;    // BE+PCG preconditioner
+  double* lbuf = nullptr;   // r-line preconditioner: -J_{i,i-1}, -J_{i,i+1} (2 component-sized buffers)
+  bool line_valid = false;
 };
 
 // ------------------------------------------------------------------ helpers
@@ -764,7 +767,19 @@ int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, 
   return PC_OK;
 }
 
+int pc_op_set_preconditioner(pc_op* op, int pc) {
+  if (!op) return fail(PC_E_INVALID, "null operator");
+  if (pc != PC_PC_JACOBI && pc != PC_PC_LINE_R) return fail(PC_E_INVALID, "unknown preconditioner");
+  if (pc == PC_PC_LINE_R && op->kind != K_ALIGNED)
+    return fail(PC_E_INVALID, "the r-line preconditioner is built for the aligned operator");
+  if (pc == PC_PC_LINE_R && op->grid->ctx->nranks > 1)
+    return fail(PC_E_INVALID, "the r-line preconditioner needs the whole r line on one rank");
+  op->pc = pc;
+  return PC_OK;
+}
+
 int pc_op_destroy(pc_op* op) {
+  if (op && op->lbuf) cudaFree(op->lbuf);
   if (!op) return PC_OK;
   cudaStreamSynchronize(op->grid->ctx->s);
   cudaFree(op->betabuf);
@@ -838,6 +853,7 @@ int pc_op_freeze(pc_op* op, const pc_field* T0) {
     TRY(run_bound(op, op->so));
   }
   op->diag_valid = op->dbuf != nullptr;
+  op->line_valid = false;
   if (op->dbuf) {
     double* db[1] = {op->dbuf};
     TRY(halo_exchange(c, g, db, 1));
@@ -1446,6 +1462,36 @@ static int pcg_split_fin(pc_ctx* c, int mode, int nred, double tol, int it) {
   return check_launch("k_pcg_fin");
 }
 
+// ---- r-line preconditioner
+static int line_prepare(pc_op* op, double dt, const double* adiag, Work& Lf) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  if (!op->line_valid) {
+    if (!op->lbuf && cudaMalloc(&op->lbuf, 2 * g->comp_elems * sizeof(double)) != cudaSuccess)
+      return fail(PC_E_CUDA, "line preconditioner allocation failed (out of device memory)");
+    k_line_coef<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ao, op->lbuf + g->g.plane,
+                                                             op->lbuf + g->comp_elems + g->g.plane);
+    c->st.launches++;
+    TRY(check_launch("k_line_coef"));
+    op->line_valid = true;
+  }
+  const int nbl = (int)((g->g.plane + kThreads - 1) / kThreads);
+  k_line_factor<<<nbl, kThreads, 0, c->s>>>(g->g, op->dbuf + g->g.plane, op->lbuf + g->g.plane,
+                                            op->lbuf + g->comp_elems + g->g.plane, adiag, dt, Lf.base(0), Lf.base(1));
+  c->st.launches++;
+  return check_launch("k_line_factor");
+}
+static int line_apply(pc_op* op, const double* r, Work& Lf, double dt, double* z, int mode) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int nbl = (int)((g->g.plane + kThreads - 1) / kThreads);
+  if (nbl > c->max_red) return fail(PC_E_INVALID, "too many r-lines for the reduction scratch");
+  k_line_solve<<<nbl, kThreads, 0, c->s>>>(g->g, op->ao, r, op->lbuf + g->g.plane, Lf.base(0), Lf.base(1), dt, z,
+                                           mode, c->red_v, c->counter, c->pcg);
+  c->st.launches++;
+  return check_launch("k_line_solve");
+}
+
 template <class Op>
 static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld b, pc_field* x, double tol,
                    int max_iter, int* iters, double* relres, int* converged) {
@@ -1459,6 +1505,13 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   TRY(work_get(g, nc, Ap));
   const double* dg = op->dbuf + g->g.plane;
   const int nb = node_blocks(c, g->g);
+  const bool line = std::is_same<Op, AlignedOp>::value && op->pc == PC_PC_LINE_R;
+  if (line && c->nranks > 1) return fail(PC_E_INVALID, "the r-line preconditioner needs the whole r line on one rank");
+  Work z, Lf;  // r-line preconditioner: z and the factorisation (inv, cp)
+  if (line) {
+    TRY(work_get(g, 1, z));
+    TRY(work_get(g, 2, Lf));
+  }
   int rc = halo_field(x);
   if (rc == PC_OK && cudaMemsetAsync(&c->pcg->split, c->nranks > 1 ? 1 : 0, sizeof(int), c->s) != cudaSuccess)
     rc = fail(PC_E_CUDA, "PCG state");
@@ -1466,11 +1519,17 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
     if constexpr (std::is_same<Op, AlignedOp>::value) {
       // r = b - A x0 through the marching kernel (x0 staged like any T)
       if (adiag) {
-        EpiPcgInitT<true> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg};
+        EpiPcgInitT<true> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg,
+                            line};
         rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
       } else {
-        EpiPcgInitT<false> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg};
+        EpiPcgInitT<false> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg,
+                             line};
         rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
+      }
+      if (rc == PC_OK && line) {  // z0 = M^{-1} r0, (r0, z0) -> fin_init
+        rc = line_prepare(op, dt, adiag, Lf);
+        if (rc == PC_OK) rc = line_apply(op, r.base(0), Lf, dt, z.base(0), 0);
       }
     } else {
       k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, c->red_v, c->red_v2,
@@ -1497,8 +1556,11 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
       if constexpr (std::is_same<Op, AlignedOp>::value) {
         // p = z + beta p_old (beta from the device-side PCG state), then the
         // marching matvec stages p like any other field
-        k_pcg_pupdate<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
-                                                 c->pcg);
+        if (line)
+          k_pcg_pupdate_z<<<nb, kThreads, 0, c->s>>>(g->g, z.base(0), pold->base(0), pnew->base(0), c->pcg);
+        else
+          k_pcg_pupdate<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
+                                                   c->pcg);
         c->st.launches++;
         rc = check_launch("k_pcg_pupdate");
         if (rc == PC_OK) rc = halo_work(g, *pnew);
@@ -1524,8 +1586,10 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         if (rc) break;
       }
       if constexpr (std::is_same<Op, AlignedOp>::value) {
-        auto upd = o.rho ? (adiag ? k_pcg_update1<true, true> : k_pcg_update1<true, false>)
-                         : (adiag ? k_pcg_update1<false, true> : k_pcg_update1<false, false>);
+        auto upd = line ? (o.rho ? (adiag ? k_pcg_update1<true, true, true> : k_pcg_update1<true, false, true>)
+                                 : (adiag ? k_pcg_update1<false, true, true> : k_pcg_update1<false, false, true>))
+                        : (o.rho ? (adiag ? k_pcg_update1<true, true> : k_pcg_update1<true, false>)
+                                 : (adiag ? k_pcg_update1<false, true> : k_pcg_update1<false, false>));
         upd<<<nb, kThreads, 0, c->s>>>(g->g, x->base(0), r.base(0), pnew->base(0), Ap.base(0), dg, adiag, o.rho, dt,
                                        tol, it, c->red_v, c->red_v2, c->counter, c->pcg);
       } else {
@@ -1536,6 +1600,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
       c->st.stage_launches += std::is_same<Op, AlignedOp>::value ? 3 : 2;
       rc = check_launch("k_pcg");
       if (rc == PC_OK) rc = pcg_split_fin(c, 2, 2, tol, it);
+      if (rc == PC_OK && line) rc = line_apply(op, r.base(0), Lf, dt, z.base(0), 1);
       std::swap(pold, pnew);
     }
     if (rc) break;
@@ -1567,6 +1632,10 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   work_put(p0);
   work_put(p1);
   work_put(Ap);
+  if (line) {
+    work_put(z);
+    work_put(Lf);
+  }
   return rc;
 }
 

@@ -289,6 +289,28 @@ __device__ __forceinline__ void pcg_fin_update(PcgDev* st, double rr, double rzn
   }
 }
 
+// line-preconditioned PCG: the update decides convergence from (r, r)_W
+// alone; beta and (r, z)_W follow from the line solve (pcg_fin_rz)
+__device__ __forceinline__ void pcg_fin_rr(PcgDev* st, double rr, double tol, int it) {
+  st->it = it;
+  if (!isfinite(rr)) {
+    st->status = 3;
+    st->done = 1;
+  } else {
+    double rn = sqrt(rr);
+    double rel = st->bn > 0.0 ? rn / st->bn : (rn == 0.0 ? 0.0 : INFINITY);
+    st->rel = rel;
+    if (rel <= tol) {
+      st->status = 1;
+      st->done = 1;
+    }
+  }
+}
+__device__ __forceinline__ void pcg_fin_rz(PcgDev* st, double rzn) {
+  st->beta = st->rz != 0.0 ? rzn / st->rz : 0.0;
+  st->rz = rzn;
+}
+
 // alpha from (p, Ap)_W; breakdown / NaN stop the solve
 __device__ __forceinline__ void pcg_alpha(PcgDev* st, double pAp) {
   st->pAp = pAp;
@@ -324,7 +346,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const doubl
 // (r, theta) row (the row weight Val2 read once), four phi nodes per lane in
 // flight (all loads issued before the arithmetic), parallel fixed-order final
 // sum in the last block.
-template <bool RHO, bool ADIAG>
+template <bool RHO, bool ADIAG, bool LINE = false>
 __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* __restrict__ x, double* __restrict__ r,
                                                           const double* __restrict__ p,
                                                           const double* __restrict__ Ap,
@@ -354,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
           pv[u] = __ldg(p + o);
           rv[u] = r[o];
           av[u] = __ldg(Ap + o);
-          dv[u] = __ldg(dg + o);
+          dv[u] = LINE ? 0.0 : __ldg(dg + o);
           wv[u] = __ldg(g.Valg + k);
           mv[u] = ADIAG ? __ldg(adiag + o) : 1.0;
           if (RHO) wv[u] = __ldg(rho + o) * (V2 * wv[u]);
@@ -369,9 +391,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
           x[o] = xv[u] + alpha * pv[u];
           const double rn = rv[u] - alpha * av[u];
           r[o] = rn;
-          const double dvec = mv[u] + dt * dv[u];
           s1 += (wv[u] * rn) * rn;
-          s2 += (wv[u] * rn) * (rn / dvec);
+          if (!LINE) {
+            const double dvec = mv[u] + dt * dv[u];
+            s2 += (wv[u] * rn) * (rn / dvec);
+          }
         }
       }
     }
@@ -391,7 +415,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
     const double rr = block_sum<kThreads>(a, sh);
     const double rzn = block_sum<kThreads>(b, sh);
     if (threadIdx.x == 0) {
-      if (st->split) {
+      if (LINE) {
+        pcg_fin_rr(st, rr, tol, it);
+      } else if (st->split) {
         st->red[0] = rr;
         st->red[1] = rzn;
       } else {
@@ -399,6 +425,98 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
       }
       *counter = 0u;
     }
+  }
+}
+
+// ---- r-line preconditioner (PC2 substitute; oracle/operators.py line_factor,
+// line_solve): one thread per (theta, phi) line, sequential in r, coalesced
+// across the lines of a warp (phi fastest)
+
+// -J_{i,i-1}, -J_{i,i+1} of the frozen aligned operator
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_line_coef(GridDev g, Op op, double* jl, double* ju) {
+  PC_FOR_NODES(g, i, j, k) {
+    double a, b;
+    op.line_coefs(g, i, j, k, a, b);
+    const int64_t o = off3(g, i, j, k);
+    jl[o] = a;
+    ju[o] = b;
+  }
+}
+
+// Thomas factorisation of M = a + dt d, off-diagonals dt jl / dt ju
+__global__ void __launch_bounds__(kThreads) k_line_factor(GridDev g, const double* __restrict__ dg,
+                                                          const double* __restrict__ jl,
+                                                          const double* __restrict__ ju,
+                                                          const double* __restrict__ adiag, double dt,
+                                                          double* __restrict__ inv, double* __restrict__ cp) {
+  const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (line >= g.plane) return;
+  double cprev = 0.0;
+  for (int i = 0; i < g.n0; ++i) {
+    const int64_t o = (int64_t)i * g.plane + line;
+    const double m = (adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o);
+    const double den = i == 0 ? m : m - (dt * __ldg(jl + o)) * cprev;
+    const double iv = 1.0 / den;
+    const double c = (dt * __ldg(ju + o)) * iv;
+    inv[o] = iv;
+    cp[o] = c;
+    cprev = c;
+  }
+}
+
+// z = M^{-1} r, partial (W r, z); mode 0: start of the solve (fin_init with
+// ||b||^2 kept in st->red[1]), mode 1: an iteration (beta, rz)
+template <class Op>
+__global__ void __launch_bounds__(kThreads) k_line_solve(GridDev g, Op op, const double* __restrict__ r,
+                                                         const double* __restrict__ jl,
+                                                         const double* __restrict__ inv,
+                                                         const double* __restrict__ cp, double dt,
+                                                         double* __restrict__ z, int mode, double* p1,
+                                                         unsigned int* counter, PcgDev* st) {
+  __shared__ double sh[kThreads / 32];
+  if (mode == 1 && st->done) return;
+  const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0.0;
+  if (line < g.plane) {
+    const int j = (int)(line / g.n2), k = (int)(line - (int64_t)j * g.n2);
+    double zp = 0.0;
+    for (int i = 0; i < g.n0; ++i) {
+      const int64_t o = (int64_t)i * g.plane + line;
+      zp = i == 0 ? __ldg(r + o) * __ldg(inv + o) : (__ldg(r + o) - (dt * __ldg(jl + o)) * zp) * __ldg(inv + o);
+      z[o] = zp;
+    }
+    double zn = zp;  // z_{n0-1} = z'_{n0-1}
+    acc = (op.weight(g, g.n0 - 1, j, k) * __ldg(r + (int64_t)(g.n0 - 1) * g.plane + line)) * zn;
+    for (int i = g.n0 - 2; i >= 0; --i) {
+      const int64_t o = (int64_t)i * g.plane + line;
+      zn = z[o] - __ldg(cp + o) * zn;
+      z[o] = zn;
+      acc += (op.weight(g, i, j, k) * __ldg(r + o)) * zn;
+    }
+  }
+  acc = block_sum<kThreads>(acc, sh);
+  if (threadIdx.x == 0) p1[blockIdx.x] = acc;
+  if (last_block(counter)) {
+    double a = 0.0;
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += kThreads) a += p1[t];
+    const double rz = block_sum<kThreads>(a, sh);
+    if (threadIdx.x == 0) {
+      if (mode == 0) pcg_fin_init(st, rz, st->red[1]);
+      else pcg_fin_rz(st, rz);
+      *counter = 0u;
+    }
+  }
+}
+
+// p = z + beta p_old (line-preconditioned PCG)
+__global__ void __launch_bounds__(kThreads) k_pcg_pupdate_z(GridDev g, const double* z, const double* pold,
+                                                            double* pnew, const PcgDev* st) {
+  if (st->done) return;
+  const double beta = st->beta;
+  PC_FOR_NODES(g, i, j, k) {
+    const int64_t o = off3(g, i, j, k);
+    pnew[o] = __ldg(z + o) + beta * __ldg(pold + o);
   }
 }
 

@@ -732,6 +732,7 @@ struct EpiPcgInitT {
   double* p2;
   unsigned int* counter;
   PcgDev* st;
+  bool line = false;  // r-line preconditioner: keep ||b||^2 in st->red[1]; (r, z) follows from the line solve
   double s1 = 0.0, s2 = 0.0;
   __host__ __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? b : (q == 1 ? dg : adiag); }
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double xv, bool,
@@ -761,7 +762,7 @@ struct EpiPcgInitT {
       const double a = sum_partials(p1, nblk, sh);
       const double bb = sum_partials(p2, nblk, sh);
       if (tid == 0) {
-        if (st->split) {
+        if (st->split || line) {
           st->red[0] = a;
           st->red[1] = bb;
         } else {

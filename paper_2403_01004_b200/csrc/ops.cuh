@@ -262,9 +262,9 @@ struct AlignedOp {
     return 7 + 4 * pair + 2 * (dlo > 0 ? 1 : 0) + (dhi > 0 ? 1 : 0);
   }
 
-  __device__ __forceinline__ void bound(const GridDev& g, int i, int j, int k, double* lam,
-                                        double& dg) const {
-    double H[19];
+  // the node's Hessian row of Q (19 offsets, face_idx / diag_idx order),
+  // accumulated exactly as oracle aligned_hessian_rows
+  __device__ __forceinline__ void hessian_row(const GridDev& g, int i, int j, int k, double (&H)[19]) const {
 #pragma unroll
     for (int n = 0; n < 19; ++n) H[n] = 0.0;
     const int64_t o = off3(g, i, j, k);
@@ -313,6 +313,13 @@ struct AlignedOp {
         }
       }
     }
+  }
+
+  __device__ __forceinline__ void bound(const GridDev& g, int i, int j, int k, double* lam,
+                                        double& dg) const {
+    double H[19];
+    hessian_row(g, i, j, k, H);
+    const int64_t o = off3(g, i, j, k);
     double S = fabs(H[0]);
 #pragma unroll
     for (int n = 1; n < 19; ++n) S = S + fabs(H[n]);
@@ -326,6 +333,23 @@ struct AlignedOp {
     const bool pin = pinned(g, i, j, k);
     lam[0] = pin ? 0.0 : l;
     dg = pin ? 0.0 : dd;
+  }
+
+  // -J_{i,i-1}, -J_{i,i+1} (r-line preconditioner; oracle aligned_line_offdiag)
+  __device__ __forceinline__ void line_coefs(const GridDev& g, int i, int j, int k, double& jl, double& ju) const {
+    double H[19];
+    hessian_row(g, i, j, k, H);
+    const double iv = __ldg(g.iVal2 + row2(g, i, j)) * __ldg(g.iValg + k);
+    double a = (H[face_idx(0, -1)] * iv) * pref;
+    double b = (H[face_idx(0, 1)] * iv) * pref;
+    if (rho) {
+      const double rv = __ldg(rho + off3(g, i, j, k));
+      a = a / rv;
+      b = b / rv;
+    }
+    const bool pin = pinned(g, i, j, k);
+    jl = pin ? 0.0 : a;
+    ju = pin ? 0.0 : b;
   }
 
   __device__ __forceinline__ double weight(const GridDev& g, int i, int j, int k) const {

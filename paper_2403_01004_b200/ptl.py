@@ -156,6 +156,8 @@ def cycle_operator(op, scheme, u, outer_dt: float, cfg: PtlConfig | None = None,
     n = c_int64()
     floor_mode = _lib.FLOOR_EULER if cfg.dt_floor_mode == "clamp-to-euler" else _lib.FLOOR_FRACTION
     dtE = float(dt_euler) if dt_euler is not None else -1.0
+    if scheme.kind == "backward_euler":
+        _lib.check(_lib.lib().pc_op_set_preconditioner(dop.handle, scheme.pc_code), "preconditioner")
     rc = _lib.lib().pc_cycle(dop.handle, du.handle, float(outer_dt), scheme.code, int(scheme.make_odd),
                              float(scheme.tol), int(scheme.max_iter), float(cfg.eps_rel), int(cfg.check_all_points),
                              int(cfg.enabled), floor_mode, float(cfg.floor_fraction), int(cfg.max_cycles), dtE,

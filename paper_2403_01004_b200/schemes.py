@@ -39,8 +39,13 @@ class SchemeConfig:
         if self.kind == "backward_euler":
             if not (0.0 < self.tol < 1.0):
                 raise ValueError("backward_euler needs 0 < tol < 1")
-            if self.preconditioner != "jacobi":
-                raise NotImplementedError("the device PCG implements the point-Jacobi preconditioner (PC1)")
+            if self.preconditioner not in ("jacobi", "line-r"):
+                raise NotImplementedError("the device PCG implements point Jacobi (PC1) and the r-line "
+                                          "block Jacobi ('line-r', the GPU substitute for PC2 ILU0)")
+
+    @property
+    def pc_code(self) -> int:
+        return _lib.PC_LINE_R if self.preconditioner == "line-r" else _lib.PC_JACOBI
 
     @property
     def code(self) -> int:
@@ -159,10 +164,12 @@ def step_euler(op, u: Field, dt: float) -> Field:
 
 
 def step_backward_euler(op, u: Field, dt: float, solver_cfg: SchemeConfig | None = None):
-    """(I - dt J) u^{n+1} = u^n by Jacobi-PCG with x0 = u^n."""
+    """(I - dt J) u^{n+1} = u^n by PCG with x0 = u^n; point
+    Jacobi, or the r-line preconditioner with SchemeConfig(preconditioner="line-r")."""
     cfg = solver_cfg or SchemeConfig("backward_euler")
     dop, du = _bind(op, u)
     it, rel, conv = c_int(), c_double(), c_int()
+    _lib.check(_lib.lib().pc_op_set_preconditioner(dop.handle, cfg.pc_code), "preconditioner")
     _lib.check(_lib.lib().pc_step_be(dop.handle, du.handle, float(dt), float(cfg.tol), int(cfg.max_iter),
                                      byref(it), byref(rel), byref(conv)), "step_backward_euler")
     return du.to_field(), SolveStats(it.value, rel.value, bool(conv.value))
