@@ -1,5 +1,6 @@
-"""``cli run`` -- the reference harness entry point (cmd_run)
-over the B200 path.
+"""The reference harness over the B200 path: ``run``
+(cmd_run), and ``ampfactor`` / ``speedup`` / ``convergence`` over
+``analysis`` (Fig. 1).
 
     python -m paper_2403_01004_b200.cli run experiment.cfg
 
@@ -311,15 +312,64 @@ def cmd_run(path: str) -> int:
     return 0
 
 
+USAGE = """usage:
+  python -m paper_2403_01004_b200.cli run <config>
+  python -m paper_2403_01004_b200.cli ampfactor --schemes be,rkl2,rkg2,exact --r 500 --out amp.csv
+  python -m paper_2403_01004_b200.cli speedup --rmin 1 --rmax 1e4 --out speedup.csv
+  python -m paper_2403_01004_b200.cli convergence --scheme rkg2 --problem sine
+"""
+
+
+def _flags(args, names):
+    out, i = {}, 0
+    while i < len(args):
+        a = args[i]
+        if not a.startswith("--") or a[2:] not in names or i + 1 >= len(args):
+            raise ValueError(f"unexpected argument {a!r}")
+        out[a[2:]] = args[i + 1]
+        i += 2
+    return out
+
+
 def main(argv=None) -> int:
+    from . import analysis
     argv = list(sys.argv[1:] if argv is None else argv)
-    if len(argv) != 2 or argv[0] != "run":
-        sys.stderr.write("usage: python -m paper_2403_01004_b200.cli run <config>\n")
-        return 2
+    if not argv or argv[0] in ("-h", "--help"):
+        sys.stderr.write(USAGE)
+        return 0 if argv else 2
+    cmd, rest = argv[0], argv[1:]
     try:
-        return cmd_run(argv[1])
+        if cmd == "run":
+            if len(rest) != 1:
+                raise ValueError("run takes one config path")
+            return cmd_run(rest[0])
+        if cmd == "ampfactor":
+            f = _flags(rest, {"schemes", "r", "out"})
+            kinds = [k for k in f.get("schemes", "").split(",") if k]
+            if not kinds or any(k not in analysis.SCHEMES for k in kinds):
+                raise ValueError(f"schemes must be a non-empty list of {','.join(analysis.SCHEMES)}")
+            analysis.write_ampfactor_csv(f.get("out", "ampfactor.csv"), kinds, float(f.get("r", "500")))
+            return 0
+        if cmd == "speedup":
+            f = _flags(rest, {"rmin", "rmax", "out"})
+            analysis.write_speedup_csv(f.get("out", "speedup.csv"), float(f["rmin"]), float(f["rmax"]))
+            return 0
+        if cmd == "convergence":
+            f = _flags(rest, {"scheme", "problem"})
+            if f.get("problem", "sine") != "sine":
+                raise ValueError(f"unknown problem preset {f.get('problem')!r} (available: sine)")
+            kind = f.get("scheme", "rkg2")
+            if kind not in ("be", "rkl2", "rkg2", "euler"):
+                raise ValueError(f"unknown scheme {kind!r}")
+            order, dts, errs = analysis.convergence_study(kind)
+            print(f"{kind}: fitted order {order:.3f}")
+            return 0
+        raise ValueError(f"unknown command {cmd!r}")
     except ConfigError as e:
         sys.stderr.write(f"config error: {e}\n")
+        return 2
+    except (ValueError, KeyError) as e:
+        sys.stderr.write(f"usage error: {e}\n{USAGE}")
         return 2
     except OSError as e:
         sys.stderr.write(f"error: {e}\n")

@@ -49,6 +49,7 @@ def test_invalid_config_is_line_anchored(tmp_path, capsys, edit, line, msg):
 def test_usage_error(capsys):
     assert cli.main(["frobnicate"]) == 2
     assert "usage" in capsys.readouterr().err
+    assert cli.main(["run"]) == 2
 
 
 def test_shipped_examples_parse():
@@ -57,3 +58,10 @@ def test_shipped_examples_parse():
         c = cli._Cfg(os.path.join(root, f))
         grid, bc = cli.build_grid(c)
         assert grid.npoints > 0
+
+
+def test_analysis_usage_errors(capsys, tmp_path):
+    assert cli.main(["ampfactor", "--schemes", "", "--r", "500", "--out", str(tmp_path / "a.csv")]) == 2
+    assert cli.main(["speedup", "--rmin", "10", "--rmax", "1", "--out", str(tmp_path / "s.csv")]) == 2
+    assert cli.main(["convergence", "--scheme", "rkg2", "--problem", "square"]) == 2
+    assert "usage error" in capsys.readouterr().err
