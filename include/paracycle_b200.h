@@ -120,6 +120,9 @@ int pc_field_set_ghost(pc_field* f, int side, const double* host);
 /* pin / unpin a host buffer so uploads and downloads run at full PCIe speed */
 int pc_host_register(void* ptr, size_t bytes);
 int pc_host_unregister(void* ptr);
+/* page-locked host allocations (the Python layer caches them for downloads) */
+int pc_host_alloc(size_t bytes, void** out);
+int pc_host_free(void* ptr);
 
 /* ---- operators.
  * scalar:  F = (1/rho) div(D grad u), D = nu*rho nodal (field) or D_const when

@@ -71,6 +71,8 @@ _SIGS = {
     "pc_field_exchange_halo": (c_int, [c_void_p]),
     "pc_host_register": (c_int, [c_void_p, c_size_t]),
     "pc_host_unregister": (c_int, [c_void_p]),
+    "pc_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),
+    "pc_host_free": (c_int, [c_void_p]),
     "pc_op_create_scalar": (c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, POINTER(c_void_p)]),
     "pc_op_create_viscous": (c_int, [c_void_p, c_int, c_int, c_double, c_void_p, POINTER(c_void_p)]),
     "pc_op_create_aligned": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_double, POINTER(c_double),

@@ -174,7 +174,17 @@ static double* pool_get(pc_ctx* c, size_t elems) {
     }
   }
   double* p = nullptr;
-  if (cudaMalloc(&p, elems * sizeof(double)) != cudaSuccess) return nullptr;
+  if (cudaMalloc(&p, elems * sizeof(double)) != cudaSuccess) {
+    // out of memory: return every cached block to the driver and retry once
+    cudaGetLastError();
+    cudaStreamSynchronize(c->s);
+    for (auto& e : c->pool) cudaFree(e.second);
+    c->pool.clear();
+    if (cudaMalloc(&p, elems * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
   cudaMemsetAsync(p, 0, elems * sizeof(double), c->s);
   return p;
 }
@@ -573,9 +583,12 @@ int pc_field_create(pc_grid* g, int ncomp, pc_field** out) {
   f->grid = g;
   f->ncomp = ncomp;
   for (int q = 0; q < 3; ++q) f->buf[q] = nullptr;
+  // device buffers come from the context's caching pool (a public-API step
+  // creates and drops fields and operators: no cudaMalloc/cudaFree churn)
   for (int q = 0; q < ncomp; ++q) {
-    if (cudaMalloc(&f->buf[q], g->comp_elems * sizeof(double)) != cudaSuccess) {
-      for (int r = 0; r < q; ++r) cudaFree(f->buf[r]);
+    f->buf[q] = pool_get(g->ctx, g->comp_elems);
+    if (!f->buf[q]) {
+      for (int r = 0; r < q; ++r) pool_put(g->ctx, g->comp_elems, f->buf[r]);
       delete f;
       return fail(PC_E_CUDA, "field allocation failed (out of device memory)");
     }
@@ -587,8 +600,7 @@ int pc_field_create(pc_grid* g, int ncomp, pc_field** out) {
 
 int pc_field_destroy(pc_field* f) {
   if (!f) return PC_OK;
-  cudaStreamSynchronize(f->grid->ctx->s);
-  for (int q = 0; q < f->ncomp; ++q) cudaFree(f->buf[q]);
+  for (int q = 0; q < f->ncomp; ++q) pool_put(f->grid->ctx, f->grid->comp_elems, f->buf[q]);
   delete f;
   return PC_OK;
 }
@@ -700,6 +712,16 @@ int pc_field_fill(pc_field* f, double v) {
 
 int pc_field_exchange_halo(pc_field* f) { return halo_field(f); }
 
+int pc_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(PC_E_INVALID, "null argument");
+  CUDA_TRY(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+  return PC_OK;
+}
+int pc_host_free(void* p) {
+  if (p) CUDA_TRY(cudaFreeHost(p));
+  return PC_OK;
+}
+
 int pc_host_register(void* p, size_t bytes) {
   CUDA_TRY(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
   return PC_OK;
@@ -756,7 +778,7 @@ int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, 
   for (int r = 0; r < rows; ++r) k[r] = fc_table ? kappa0 * fc_table[r] : kappa0;
   CUDA_TRY(cudaMalloc(&op->kfc, sizeof(double) * rows));
   CUDA_TRY(cudaMemcpy(op->kfc, k.data(), sizeof(double) * rows, cudaMemcpyHostToDevice));
-  if (cudaMalloc(&op->betabuf, 3 * g->comp_elems * sizeof(double)) != cudaSuccess) {
+  if (!(op->betabuf = pool_get(c, 3 * g->comp_elems))) {
     cudaFree(op->kfc);
     delete op;
     return fail(PC_E_CUDA, "beta allocation failed (out of device memory)");
@@ -779,11 +801,12 @@ int pc_op_set_preconditioner(pc_op* op, int pc) {
 }
 
 int pc_op_destroy(pc_op* op) {
-  if (op && op->lbuf) cudaFree(op->lbuf);
   if (!op) return PC_OK;
-  cudaStreamSynchronize(op->grid->ctx->s);
-  cudaFree(op->betabuf);
-  cudaFree(op->dbuf);
+  pc_ctx* c = op->grid->ctx;
+  const size_t ce = op->grid->comp_elems;
+  if (op->lbuf) pool_put(c, 2 * ce, op->lbuf);
+  pool_put(c, 3 * ce, op->betabuf);
+  pool_put(c, ce, op->dbuf);
   cudaFree(op->kfc);
   delete op;
   return PC_OK;
@@ -868,7 +891,7 @@ static int ensure_diag(pc_op* op) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   if (!op->dbuf) {
-    if (cudaMalloc(&op->dbuf, g->comp_elems * sizeof(double)) != cudaSuccess)
+    if (!(op->dbuf = pool_get(g->ctx, g->comp_elems)))
       return fail(PC_E_CUDA, "diagonal allocation failed (out of device memory)");
     CUDA_TRY(cudaMemsetAsync(op->dbuf, 0, g->comp_elems * sizeof(double), c->s));
   }
@@ -1467,7 +1490,7 @@ static int line_prepare(pc_op* op, double dt, const double* adiag, Work& Lf) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   if (!op->line_valid) {
-    if (!op->lbuf && cudaMalloc(&op->lbuf, 2 * g->comp_elems * sizeof(double)) != cudaSuccess)
+    if (!op->lbuf && !(op->lbuf = pool_get(c, 2 * g->comp_elems)))
       return fail(PC_E_CUDA, "line preconditioner allocation failed (out of device memory)");
     k_line_coef<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ao, op->lbuf + g->g.plane,
                                                              op->lbuf + g->comp_elems + g->g.plane);

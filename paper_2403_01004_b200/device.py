@@ -84,7 +84,10 @@ class Context:
         return out
 
     def pin(self, arr: np.ndarray):
-        """Page-lock a host array (kept pinned for the context's lifetime)."""
+        """Page-lock a host array (kept pinned for the context's lifetime);
+        arrays already in page-locked memory (pinned_empty) are left alone."""
+        if is_page_locked(arr):
+            return arr
         _lib.check(_lib.lib().pc_host_register(arr.ctypes.data, arr.nbytes), "pin")
         self._pinned.append(arr)
         return arr
@@ -116,6 +119,77 @@ def default_context() -> Context:
 def set_default_context(ctx: Context):
     global _default
     _default = ctx
+
+
+class _PinnedBlock:
+    """A page-locked host block; returned to the cache when the last numpy
+    array (or view) over it is garbage-collected."""
+
+    def __init__(self, cache, ptr, nbytes):
+        self.cache, self.ptr, self.nbytes = cache, ptr, nbytes
+
+    def __del__(self):
+        try:
+            self.cache._release(self)
+        except Exception:
+            pass
+
+
+class _PinnedCache:
+    """Caching allocator of page-locked host memory for downloads: a fresh
+    pageable array costs a page fault per page on the device->host copy
+    (~4 GB/s), a recycled pinned block copies at PCIe speed (~50 GB/s).
+    Blocks are reused by exact size; at most ``limit`` bytes stay cached."""
+
+    def __init__(self, limit=96 << 30):
+        self.free = {}
+        self.cached = 0
+        self.limit = limit
+
+    def empty(self, shape):
+        n = int(np.prod(shape)) * 8
+        lst = self.free.get(n)
+        if lst:
+            blk = lst.pop()
+            self.cached -= n
+        else:
+            p = c_void_p()
+            if not _lib.alive() or _lib.lib().pc_host_alloc(n, byref(p)) != 0 or not p.value:
+                return np.empty(shape)  # no page-locked memory left: pageable fallback (host buffer only)
+            blk = _PinnedBlock(self, p.value, n)
+        buf = (ctypes.c_byte * n).from_address(blk.ptr)
+        buf._block = blk  # keeps the block alive as long as any array over it
+        return np.frombuffer(buf, dtype=np.float64).reshape(shape)
+
+    def _release(self, blk):
+        if not _lib.alive():
+            return
+        if self.cached + blk.nbytes <= self.limit:
+            fresh = _PinnedBlock(self, blk.ptr, blk.nbytes)
+            blk.ptr = None
+            self.free.setdefault(fresh.nbytes, []).append(fresh)
+            self.cached += fresh.nbytes
+        elif blk.ptr:
+            _lib.lib().pc_host_free(blk.ptr)
+            blk.ptr = None
+
+
+_pinned = _PinnedCache()
+
+
+def is_page_locked(arr: np.ndarray) -> bool:
+    """True if the array lives in a block of the pinned cache."""
+    b = arr
+    while b is not None:
+        if getattr(b, "_block", None) is not None:
+            return True
+        b = getattr(b, "base", None)
+    return False
+
+
+def pinned_empty(shape) -> np.ndarray:
+    """An uninitialised float64 array in (cached) page-locked host memory."""
+    return _pinned.empty(tuple(int(x) for x in shape))
 
 
 class DeviceGrid:
@@ -213,7 +287,7 @@ class DeviceField:
     def download(self, out: np.ndarray | None = None, layout: int = _lib.LAYOUT_AOS) -> np.ndarray:
         shape = tuple(self.dgrid.shape) + (self.ncomp,) if layout == _lib.LAYOUT_AOS else (self.ncomp,) + tuple(self.dgrid.shape)
         if out is None:
-            out = np.empty(shape)
+            out = pinned_empty(shape)
         elif not (out.flags.c_contiguous and out.dtype == np.float64 and out.size == int(np.prod(shape))):
             raise ValueError("download target must be a contiguous float64 array of the field size")
         _lib.check(_lib.lib().pc_field_download(self.handle, _lib.dptr(out), layout), "download")
