@@ -82,7 +82,7 @@ class ClockSampler:
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, index=0):
         self.index = index
@@ -111,7 +111,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons, under = [], [], set(), []
+        sm, mx, reasons, under, pw, plim = [], [], set(), [], [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -125,12 +125,18 @@ class ClockSampler:
             mx.append(m)
             if p > 300:
                 under.append(s)
+                pw.append(p)
+            try:
+                plim.append(float(f[8]))
+            except (IndexError, ValueError):
+                pass
             for n, v in zip(names, f[4:8]):
                 if v.lower() == "active":
                     reasons.add(n)
         use = under or sm
         return {"sm_mhz": statistics.median(use) if use else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(under)}
+                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(under),
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": max(plim) if plim else None}
 
 
 # ---------------------------------------------------------------- workloads
