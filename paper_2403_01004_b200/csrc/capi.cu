@@ -251,7 +251,7 @@ static int check_launch(const char* what) {
 
 // ------------------------------------------------------------------ NCCL
 static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp, cudaStream_t st = nullptr) {
-  if (c->nranks <= 1 || c->detached) return PC_OK;
+  if (!c->comm) return PC_OK;  // one rank, or a detached test rank (ghosts set by the caller)
   if (!st) st = c->s;
   nccl::Api* A = nccl::api();
   if (!A) return fail(PC_E_NCCL, "NCCL not available");
@@ -283,7 +283,7 @@ static int halo_work(pc_grid* g, Work& w) {
   return halo_exchange(g->ctx, g, b, w.ncomp);
 }
 static int allreduce_u64_min(pc_ctx* c, unsigned long long* dptr) {
-  if (c->nranks <= 1 || c->detached) return PC_OK;
+  if (!c->comm) return PC_OK;
   nccl::Api* A = nccl::api();
   if (!A || A->allReduce(dptr, dptr, 1, nccl::kUint64, nccl::kMin, c->comm, c->s) != 0)
     return fail(PC_E_NCCL, "ncclAllReduce(u64 min)");
@@ -291,7 +291,7 @@ static int allreduce_u64_min(pc_ctx* c, unsigned long long* dptr) {
 }
 // the |F| argmax over all ranks (res holds this rank's pair on entry)
 static int global_argmax(pc_ctx* c) {
-  if (c->nranks <= 1 || c->detached) return PC_OK;
+  if (!c->comm) return PC_OK;
   nccl::Api* A = nccl::api();
   if (!A || !A->allGather_ || A->allGather(c->res, c->gath, 2, nccl::kDouble, c->comm, c->s) != 0)
     return fail(PC_E_NCCL, "ncclAllGather(argmax)");
@@ -300,7 +300,7 @@ static int global_argmax(pc_ctx* c) {
   return check_launch("k_argmax_combine");
 }
 static int allreduce_d(pc_ctx* c, double* dptr, size_t n, int op) {
-  if (c->nranks <= 1 || c->detached) return PC_OK;
+  if (!c->comm) return PC_OK;
   nccl::Api* A = nccl::api();
   if (!A || A->allReduce(dptr, dptr, n, nccl::kDouble, op, c->comm, c->s) != 0)
     return fail(PC_E_NCCL, "ncclAllReduce");
@@ -353,11 +353,20 @@ static int ctx_create(int device, int nranks, int rank, const void* nccl_uid, bo
   CUDA_TRY(cudaMallocHost(&c->h_minbits, sizeof(unsigned long long)));
   CUDA_TRY(cudaMallocHost(&c->h_maxout, sizeof(double)));
   c->detached = detached;
-  if (nranks > 1 && !detached) {
+  // PC_FORCE_NCCL (test hook): a one-rank communicator, so every collective
+  // of the multi-rank path (allreduce, allgathered argmax, split PCG
+  // reductions) runs through NCCL on a single GPU
+  const bool force = nranks == 1 && !detached && getenv("PC_FORCE_NCCL") != nullptr;
+  if ((nranks > 1 && !detached) || force) {
     nccl::Api* A = nccl::api();
     if (!A) {
       delete c;
       return fail(PC_E_NCCL, "NCCL library not found (needed for nranks > 1)");
+    }
+    char self_uid[128];
+    if (!nccl_uid && force) {
+      if (A->getUniqueId(self_uid) != 0) return fail(PC_E_NCCL, "ncclGetUniqueId");
+      nccl_uid = self_uid;
     }
     if (!nccl_uid) return fail(PC_E_INVALID, "nranks > 1 needs an ncclUniqueId");
     if (A->commInitRank(&c->comm, nranks, nccl_uid, rank) != 0) return fail(PC_E_NCCL, "ncclCommInitRank");
@@ -1186,7 +1195,7 @@ int pc_op_apply(pc_op* op, const pc_field* u, pc_field* F) {
 static int ptl_device(pc_grid* g, int ncomp, CFld u, CFld F, double* const* Fbufs, double eps_rel, int check_all) {
   pc_ctx* c = g->ctx;
   TRY(global_argmax(c));
-  if (c->nranks > 1 && Fbufs) TRY(halo_exchange(c, g, Fbufs, ncomp));
+  if (c->comm && Fbufs) TRY(halo_exchange(c, g, Fbufs, ncomp));
   if (check_all) {
     CUDA_TRY(cudaMemsetAsync(c->minbits, 0x7f, sizeof(unsigned long long), c->s));  // huge positive
     k_ptl_all<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, ncomp, u, F, eps_rel, c->res, c->minbits);
@@ -1345,7 +1354,7 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
   const bool marching = std::is_same<Op, AlignedOp>::value || smarch_ok(op);
   const int Rz = std::is_same<Op, AlignedOp>::value ? march_R(g) : smarch_R(g);
   const int nz = (g->g.n0 + Rz - 1) / Rz;
-  const bool overlap = marching && nz >= 3 && ((c->nranks > 1 && !c->detached) || force_split);
+  const bool overlap = marching && nz >= 3 && (c->comm != nullptr || force_split);
   for (int k = 2; k <= s && rc == PC_OK; ++k) {
     const double* r = tab + 5 * (k - 1);
     StageCoef sc{r[0], r[1], r[2], r[3], r[4]};
@@ -1477,8 +1486,8 @@ int pc_step_euler(pc_op* op, pc_field* u, double dt) {
 
 // ------------------------------------------------------------------ PCG
 // r-slabs: finish a PCG reduction after the allreduce of the local sums
-static int pcg_split_fin(pc_ctx* c, int mode, int nred, double tol, int it) {
-  if (c->nranks <= 1) return PC_OK;
+static int pcg_split_fin(pc_ctx* c, bool split, int mode, int nred, double tol, int it) {
+  if (!split) return PC_OK;
   TRY(allreduce_d(c, c->pcg->red, (size_t)nred, nccl::kSum));
   k_pcg_fin<<<1, 1, 0, c->s>>>(c->pcg, mode, tol, it);
   c->st.launches++;
@@ -1536,7 +1545,10 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
     TRY(work_get(g, 2, Lf));
   }
   int rc = halo_field(x);
-  if (rc == PC_OK && cudaMemsetAsync(&c->pcg->split, c->nranks > 1 ? 1 : 0, sizeof(int), c->s) != cudaSuccess)
+  // split reductions: the kernels stop at the local sums, NCCL adds them up
+  // (the r-line preconditioner is single-rank and finishes its own reductions)
+  const bool split = c->comm != nullptr && !line;
+  if (rc == PC_OK && cudaMemsetAsync(&c->pcg->split, split ? 1 : 0, sizeof(int), c->s) != cudaSuccess)
     rc = fail(PC_E_CUDA, "PCG state");
   if (rc == PC_OK) {
     if constexpr (std::is_same<Op, AlignedOp>::value) {
@@ -1560,7 +1572,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
       c->st.launches++;
       rc = check_launch("k_pcg_init");
     }
-    if (rc == PC_OK) rc = pcg_split_fin(c, 0, 2, tol, 0);
+    if (rc == PC_OK) rc = pcg_split_fin(c, split, 0, 2, tol, 0);
   }
   Work* pold = &p0;
   Work* pnew = &p1;
@@ -1596,7 +1608,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
           EpiMatvecT<false> e{adiag, Ap.base(0), dt, c->red_v, c->counter, c->pcg};
           rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
         }
-        if (rc == PC_OK) rc = pcg_split_fin(c, 1, 1, tol, it);
+        if (rc == PC_OK) rc = pcg_split_fin(c, split, 1, 1, tol, it);
         if (rc) break;
       } else {
         rc = halo_work(g, r);
@@ -1605,7 +1617,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
                                                 c->red_v, c->counter, c->pcg);
         rc = check_launch("k_pcg_matvec");
-        if (rc == PC_OK) rc = pcg_split_fin(c, 1, 1, tol, it);
+        if (rc == PC_OK) rc = pcg_split_fin(c, split, 1, 1, tol, it);
         if (rc) break;
       }
       if constexpr (std::is_same<Op, AlignedOp>::value) {
@@ -1622,7 +1634,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
       c->st.launches += std::is_same<Op, AlignedOp>::value ? 1 : 2;  // (march counted at launch)
       c->st.stage_launches += std::is_same<Op, AlignedOp>::value ? 3 : 2;
       rc = check_launch("k_pcg");
-      if (rc == PC_OK) rc = pcg_split_fin(c, 2, 2, tol, it);
+      if (rc == PC_OK) rc = pcg_split_fin(c, split, 2, 2, tol, it);
       if (rc == PC_OK && line) rc = line_apply(op, r.base(0), Lf, dt, z.base(0), 1);
       std::swap(pold, pnew);
     }

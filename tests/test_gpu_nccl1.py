@@ -1,0 +1,59 @@
+"""The multi-rank collectives through NCCL on ONE GPU: a context with a
+one-rank communicator (PC_FORCE_NCCL test hook) sends every reduction of the
+r-slab path through NCCL -- Gershgorin allreduce(max), the allgathered |F|
+argmax and its combine kernel, the PTL allreduce(min) (and the audit mode's
+u64 min), the split PCG reductions finished by k_pcg_fin, the overlapped
+stage launches on the communication stream -- and must reproduce the oracle
+exactly as the plain single-rank path does."""
+import numpy as np
+import pytest
+
+from helpers import oracle_aligned, oracle_scalar, soa
+from oracle import ptl as optl
+from paper_2403_01004_b200 import configs, device, operators, ptl, schemes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl_ctx():
+    mp = pytest.MonkeyPatch()
+    mp.setenv("PC_FORCE_NCCL", "1")
+    ctx = device.Context(0)
+    mp.undo()
+    yield ctx
+    ctx.close()
+
+
+@pytest.mark.parametrize("kind,check_all", [("rkl2", False), ("backward_euler", False), ("rkl2", True)])
+def test_aligned_through_nccl(gpu_ctx, nccl_ctx, kind, check_all):
+    w = configs.c3(n=(24, 40, 64))
+    cfg = operators.AlignedConductionConfig(b_hat=w.fields["b"], m_p=3.0, k_B=1.0, bc=w.bc)
+    T = operators.Field(w.grid, w.fields["T"])
+    op = operators.DiffusionOperator.aligned(cfg, T)
+    dtE = op.device_op(w.grid, 1, nccl_ctx).dt_euler
+    oop = oracle_aligned(w.grid, w.bc, w.fields["b"], w.fields["T"])
+    assert dtE == oop.euler_dt()
+    sc = schemes.SchemeConfig(kind, tol=1e-9)
+    out, rep = ptl.cycle_operator(op, sc, T, 1e4 * dtE, ptl.PtlConfig(check_all_points=check_all), ctx=nccl_ctx)
+    uo, repo = optl.cycle_operator(oop, optl.OracleScheme(kind, tol=1e-9), soa(w.fields["T"][..., None]), 1e4 * dtE,
+                                   dt_euler=dtE, check_all=check_all)
+    assert [e.iters for e in rep.entries] == [r.iters for r in repo]
+    a, b = out.values[..., 0], uo[0]
+    if kind == "rkl2":
+        assert np.array_equal(a, b)
+    else:
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_viscous_through_nccl(gpu_ctx, nccl_ctx):
+    w = configs.c2(n=(40, 24, 64))
+    cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc, vector_metric=True)
+    op = operators.DiffusionOperator.scalar(cfg, 3)
+    v = operators.Field(w.grid, w.fields["v"])
+    dtE = op.device_op(w.grid, 3, nccl_ctx).dt_euler
+    oop = oracle_scalar(w.grid, w.bc, ncomp=3, vector_metric=True)
+    out, rep = ptl.cycle_operator(op, schemes.SchemeConfig("rkl2"), v, 200 * dtE, ctx=nccl_ctx)
+    uo, repo = optl.cycle_operator(oop, optl.OracleScheme("rkl2"), soa(w.fields["v"]), 200 * dtE, dt_euler=dtE)
+    assert [e.iters for e in rep.entries] == [r.iters for r in repo]
+    assert np.array_equal(np.moveaxis(out.values, -1, 0), uo)
