@@ -260,16 +260,16 @@ static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp, 
   int lo = g->g.ghost_lo0 ? (c->rank - 1 + c->nranks) % c->nranks : -1;
   int hi = g->g.ghost_hi0 ? (c->rank + 1) % c->nranks : -1;
   if (A->groupStart() != 0) return fail(PC_E_NCCL, "ncclGroupStart");
+  // NCCL matches the p2p operations of a rank pair in issue order, so every
+  // rank issues (send last plane up, receive lower ghost) before (send first
+  // plane down, receive upper ghost): the pairing stays right when the lower
+  // and upper neighbour are the same rank (a periodic ring of 1 or 2 slabs)
   for (int q = 0; q < ncomp; ++q) {
     double* base = bufs[q] + pl;  // interior plane 0
-    if (lo >= 0) {
-      A->send(base, pl, nccl::kDouble, lo, c->comm, st);
-      A->recv(base - pl, pl, nccl::kDouble, lo, c->comm, st);
-    }
-    if (hi >= 0) {
-      A->send(base + (size_t)(n0 - 1) * pl, pl, nccl::kDouble, hi, c->comm, st);
-      A->recv(base + (size_t)n0 * pl, pl, nccl::kDouble, hi, c->comm, st);
-    }
+    if (hi >= 0) A->send(base + (size_t)(n0 - 1) * pl, pl, nccl::kDouble, hi, c->comm, st);
+    if (lo >= 0) A->recv(base - pl, pl, nccl::kDouble, lo, c->comm, st);
+    if (lo >= 0) A->send(base, pl, nccl::kDouble, lo, c->comm, st);
+    if (hi >= 0) A->recv(base + (size_t)n0 * pl, pl, nccl::kDouble, hi, c->comm, st);
   }
   if (A->groupEnd() != 0) return fail(PC_E_NCCL, "ncclGroupEnd");
   return PC_OK;

@@ -196,7 +196,10 @@ class DeviceGrid:
     """A grid (+ boundary condition) resident on one rank: metric tables and
     the slab geometry."""
 
-    def __init__(self, grid, bc, ctx: Context | None = None):
+    def __init__(self, grid, bc, ctx: Context | None = None, force_ghosts: bool = False):
+        """``force_ghosts`` (test hook): a single rank of a periodic axis 0
+        reads its axis-0 neighbours from ghost planes filled by the (self)
+        NCCL exchange instead of wrapping in-kernel."""
         ctx = ctx or default_context()
         self.ctx = ctx
         self.grid = grid
@@ -209,8 +212,8 @@ class DeviceGrid:
             raise ValueError(f"{P} ranks but only {n0} axis-0 planes")
         i0, n0l = geometry.slab_bounds(n0, P, r)
         per0 = gt.periodic[0]
-        self.ghost_lo = P > 1 and (r > 0 or per0)
-        self.ghost_hi = P > 1 and (r < P - 1 or per0)
+        self.ghost_lo = (P > 1 and (r > 0 or per0)) or (force_ghosts and per0)
+        self.ghost_hi = (P > 1 and (r < P - 1 or per0)) or (force_ghosts and per0)
         self.i0, self.n0_local = i0, n0l
         self.global_shape = gt.shape
         self.shape = (n0l, gt.shape[1], gt.shape[2])
