@@ -95,6 +95,7 @@ struct pc_ctx {
   ArgRes* h_res = nullptr;
   PcgDev* h_pcg = nullptr;
   int* h_bad = nullptr;
+  bool bad_pending = false;  // pc_cycle: the last STS step's non-finite flag is in flight to h_bad
   unsigned long long* h_minbits = nullptr;
   double* h_maxout = nullptr;
   // staging for AoS conversion
@@ -1321,7 +1322,8 @@ int pc_sts_table(int kind, int s, double dt, double* out) {
 }
 
 template <class Op>
-static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, int s, Work& y0) {
+static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, int s, Work& y0,
+                      bool deferred = false) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   const int nc = op->ncomp;
@@ -1416,7 +1418,13 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     c->st.kind_launches[kind] += s - 1;
     c->st.kind_units[kind] += (int64_t)(s - 1) * g->g.N;
   }
-  if (rc == PC_OK) {
+  if (rc == PC_OK && deferred) {
+    // pc_cycle: no host sync per step -- the flag travels with the stream and
+    // is checked at the next PTL read (or the end of the cycle loop)
+    CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    c->bad_pending = true;
+    swap_storage(u, *um1);
+  } else if (rc == PC_OK) {
     CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CUDA_TRY(cudaStreamSynchronize(c->s));
     if (*c->h_bad != 0x7f7f7f7f) {
@@ -1430,9 +1438,17 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
   return rc;
 }
 
-static int sts_any(pc_op* op, pc_field* u, const double* tab, int s, Work& y0) {
-  if (op->kind == K_ALIGNED) return sts_stages(op, op->ao, u, tab, s, y0);
-  return sts_stages(op, op->so, u, tab, s, y0);
+static int sts_any(pc_op* op, pc_field* u, const double* tab, int s, Work& y0, bool deferred = false) {
+  if (op->kind == K_ALIGNED) return sts_stages(op, op->ao, u, tab, s, y0, deferred);
+  return sts_stages(op, op->so, u, tab, s, y0, deferred);
+}
+// the deferred non-finite flag of the previous STS step (stream synchronised)
+static int check_pending_bad(pc_ctx* c) {
+  if (!c->bad_pending) return PC_OK;
+  c->bad_pending = false;
+  if (*c->h_bad != 0x7f7f7f7f)
+    return fail(PC_E_BLOWUP, "non-finite value at STS stage " + std::to_string(*c->h_bad), *c->h_bad);
+  return PC_OK;
 }
 
 int pc_step_sts(pc_op* op, pc_field* u, double dt, int kind, int s, const pc_field* y0in) {
@@ -1737,8 +1753,14 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
   TRY(work_get(g, op->ncomp, y0));
   int rc = PC_OK;
   std::vector<double> tab;
+  c->bad_pending = false;
   while (remaining > 0.0) {
     if (cyc >= max_cycles) {
+      if (c->bad_pending) {
+        CUDA_TRY(cudaStreamSynchronize(c->s));
+        rc = check_pending_bad(c);
+        if (rc) break;
+      }
       rc = fail(PC_E_CAP, "max_cycles reached (partial report returned)", cyc);
       break;
     }
@@ -1755,6 +1777,8 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
     int limited;
     rc = ptl_read(c, check_all, use_ptl, &ptl, &limited, nullptr);
     if (rc) break;
+    rc = check_pending_bad(c);  // ptl_read synchronised the stream
+    if (rc) break;
     double dt;
     if (!limited) {
       dt = remaining;
@@ -1769,7 +1793,7 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
       tab.assign(5 * (size_t)s, 0.0);
       rc = pc_sts_table(scheme, s, dt, tab.data());
       if (rc) break;
-      rc = sts_any(op, u, tab.data(), s, y0);
+      rc = sts_any(op, u, tab.data(), s, y0, true);
       iters = s;
     } else if (scheme == PC_BE) {
       int conv = 0;
@@ -1803,7 +1827,11 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
     else remaining = remaining - dt;
   }
   work_put(y0);
-  if (rc == PC_OK) CUDA_TRY(cudaStreamSynchronize(c->s));
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    rc = check_pending_bad(c);
+  }
+  c->bad_pending = false;
   return rc;
 }
 

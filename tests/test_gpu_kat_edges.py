@@ -276,3 +276,22 @@ def test_edge_grids_viscous_parity(gpu_ctx, n):
     uo, repo = optl.cycle_operator(oop, optl.OracleScheme("rkl2"), soa(w.fields["v"]), 20 * dtE, dt_euler=dtE)
     assert [e.iters for e in rep.entries] == [r.iters for r in repo]
     assert np.array_equal(np.moveaxis(out.values, -1, 0), uo)
+
+
+def test_cycle_blowup_is_reported_with_the_oracle_stage(gpu_ctx):
+    """pc_cycle checks the non-finite flag one cycle late (no per-step host
+    sync): the error still names the oracle's stage."""
+    w = configs.c1(n=(12, 12, 24))
+    cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc)
+    op = operators.DiffusionOperator.scalar(cfg, 1)
+    oop = oracle_scalar(w.grid, w.bc)
+    dtE = oop.euler_dt()
+    u = w.fields["u"].copy()
+    u[6, 6, 12] = 1e305
+    with pytest.raises(optl.sch.BlowUpError) as eo:
+        optl.cycle_operator(oop, optl.OracleScheme("rkl2"), soa(u[..., None]), 300 * dtE, use_ptl=False,
+                            dt_euler=150 * dtE)
+    with pytest.raises(errors.BlowUpError) as ei:
+        ptl.cycle_operator(op, schemes.SchemeConfig("rkl2"), mesh.Field(w.grid, u[..., None]), 300 * dtE,
+                           ptl.PtlConfig(enabled=False), dt_euler=150 * dtE)
+    assert ei.value.stage == eo.value.stage
