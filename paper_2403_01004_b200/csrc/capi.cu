@@ -24,6 +24,8 @@
 #include "march.cuh"
 #include "smarch.cuh"
 #include "tma_march.cuh"
+#include "sts.cuh"
+#include "persist.cuh"
 
 #include <cudaTypedefs.h>
 #include "nccl_shim.h"
@@ -96,6 +98,8 @@ struct pc_ctx {
   PcgDev* h_pcg = nullptr;
   int* h_bad = nullptr;
   bool bad_pending = false;  // pc_cycle: the last STS step's non-finite flag is in flight to h_bad
+  CycleDev* cyc_dev = nullptr;      // persistent small-grid cycle state (allocated on first use)
+  CycleDev* h_cyc = nullptr;
   unsigned long long* h_minbits = nullptr;
   double* h_maxout = nullptr;
   // staging for AoS conversion
@@ -385,6 +389,8 @@ int pc_ctx_create_detached(int device, int nranks, int rank, pc_ctx** out) {
 int pc_ctx_destroy(pc_ctx* c) {
   if (c) {
     if (c->sc) cudaStreamDestroy(c->sc);
+    if (c->cyc_dev) cudaFree(c->cyc_dev);
+    if (c->h_cyc) cudaFreeHost(c->h_cyc);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   }
@@ -1097,6 +1103,10 @@ static int launch_march(pc_op* op, const double* Tin, const Epi& epi, const int*
 
 // ---- 7-point marching kernels (ScalarOp), dispatched on (ncomp, vector, D mode)
 static int smarch_R(const pc_grid* g) {
+  if (const char* e = getenv("PC_SMARCH_R")) {
+    const int r = atoi(e);
+    if (r >= 1) return r;
+  }
   const int tiles = ((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + SMJ - 1) / SMJ);
   int R = 32;
   while (R > 4 && (int64_t)tiles * ((g->g.n0 + R - 1) / R) < 148 * 12) R /= 2;
@@ -1253,71 +1263,14 @@ int pc_ptl(pc_grid* g, const pc_field* u, const pc_field* F, double eps_rel, int
 
 // ------------------------------------------------------------------ STS
 int pc_sts_count(int kind, double dt, double dt_euler, int make_odd) {
-  const double r = dt / dt_euler;
-  if (kind == PC_RKL2) {
-    long long s = (long long)std::ceil((std::sqrt(9.0 + 16.0 * r) - 1.0) / 2.0);
-    if (make_odd && s % 2 == 0) s += 1;
-    return (int)std::max<long long>(s, 2);
-  }
-  if (kind == PC_RKG2) {
-    long long s = (long long)std::ceil(0.5 * std::sqrt(25.0 + 24.0 * r) - 1.5);
-    if (s % 2 == 0) s += 1;
-    return (int)std::max<long long>(s, 3);
-  }
-  return -1;
+  static_assert(kRKL2 == PC_RKL2 && kRKG2 == PC_RKG2, "scheme codes");
+  return sts_count_hd(kind, dt, dt_euler, make_odd);
 }
-
 int pc_sts_table(int kind, int s, double dt, double* out) {
   if (!out) return fail(PC_E_INVALID, "null table");
-  std::vector<double> mu(s + 1, 0.0), nu(s + 1, 0.0), mut(s + 1, 0.0), gam(s + 1, 0.0), b(s + 1, 0.0);
-  if (kind == PC_RKL2) {
-    if (s < 2) return fail(PC_E_INVALID, "RKL2 needs s >= 2");
-    for (int j = 0; j <= s; ++j) {
-      const double jd = j;
-      b[j] = j <= 2 ? 1.0 / 3.0 : ((jd * jd + jd) - 2.0) / ((2.0 * jd) * (jd + 1.0));
-    }
-    const double sd = s;
-    const double w1 = 4.0 / ((sd * sd + sd) - 2.0);
-    mut[1] = b[1] * w1;
-    for (int j = 2; j <= s; ++j) {
-      const double jd = j;
-      mu[j] = (((2.0 * jd - 1.0) / jd) * b[j]) / b[j - 1];
-      nu[j] = ((-(jd - 1.0) / jd) * b[j]) / b[j - 2];
-      mut[j] = mu[j] * w1;
-      gam[j] = (-(1.0 - b[j - 1])) * mut[j];
-    }
-  } else if (kind == PC_RKG2) {
-    if (s < 3 || s % 2 == 0) return fail(PC_E_INVALID, "RKG2 needs odd s >= 3 (SPEC.md:264)");
-    const double sd = s;
-    const double w = 6.0 / ((sd + 4.0) * (sd - 1.0));
-    b[0] = 1.0;
-    b[1] = 1.0 / 3.0;
-    b[2] = 1.0 / 15.0;
-    mu[1] = 1.0;
-    mut[1] = w;
-    mu[2] = 0.5;
-    nu[2] = -0.1;
-    mut[2] = mu[2] * w;
-    gam[2] = 0.0;
-    for (int k = 3; k <= s; ++k) {
-      const double kd = k;
-      b[k] = ((4.0 * (kd - 1.0)) * (kd + 4.0)) / ((((3.0 * kd) * (kd + 1.0)) * (kd + 2.0)) * (kd + 3.0));
-      mu[k] = ((2.0 + 1.0 / kd) * b[k]) / b[k - 1];
-      nu[k] = ((-(1.0 / kd + 1.0)) * b[k]) / b[k - 2];
-      mut[k] = mu[k] * w;
-      gam[k] = ((((kd * (kd + 1.0)) / 2.0) * b[k - 1]) - 1.0) * mut[k];
-    }
-  } else {
-    return fail(PC_E_INVALID, "unknown STS kind");
-  }
-  for (int k = 1; k <= s; ++k) {
-    double* r = out + 5 * (k - 1);
-    r[0] = mu[k];
-    r[1] = nu[k];
-    r[2] = (1.0 - mu[k]) - nu[k];
-    r[3] = mut[k] * dt;
-    r[4] = gam[k] * dt;
-  }
+  if (kind != PC_RKL2 && kind != PC_RKG2) return fail(PC_E_INVALID, "unknown STS kind");
+  if (!sts_rows_hd(kind, s, dt, out))
+    return fail(PC_E_INVALID, kind == PC_RKL2 ? "RKL2 needs s >= 2" : "RKG2 needs odd s >= 3 (SPEC.md:264)");
   return PC_OK;
 }
 
@@ -1733,6 +1686,98 @@ int pc_step_be(pc_op* op, pc_field* u, double dt, double tol, int max_iter, int*
 }
 
 // ------------------------------------------------------------------ cycle
+// ---- persistent small-grid cycle loop (persist.cuh)
+static bool persist_ok(const pc_op* op) {
+  const pc_grid* g = op->grid;
+  const pc_ctx* c = g->ctx;
+  if (op->kind != K_SCALAR || (op->ncomp != 1 && op->ncomp != 3)) return false;
+  if (c->comm || c->nranks > 1 || g->g.ghost_lo0 || g->g.ghost_hi0) return false;
+  if (getenv("PC_NO_PERSIST")) return false;
+  return (int64_t)g->g.N * op->ncomp <= (int64_t)(getenv("PC_PERSIST_MAX") ? atoll(getenv("PC_PERSIST_MAX")) : 1 << 21);
+}
+static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, double eps_rel,
+                            int use_ptl, double floor_dt, double dtE, int64_t max_cycles, pc_cycle_record* rec,
+                            int64_t rec_cap, int64_t* n_rec) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int nc = op->ncomp;
+  if (!c->cyc_dev) {
+    CUDA_TRY(cudaMalloc(&c->cyc_dev, sizeof(CycleDev)));
+    CUDA_TRY(cudaMallocHost(&c->h_cyc, sizeof(CycleDev)));
+  }
+  Work A, B, y0;
+  TRY(work_get(g, nc, A));
+  TRY(work_get(g, nc, B));
+  TRY(work_get(g, nc, y0));
+  const int64_t cap = std::max<int64_t>(0, std::min<int64_t>(rec_cap, max_cycles));
+  pc_cycle_record* drec = nullptr;
+  int rc = PC_OK;
+  if (cap > 0 && cudaMalloc(&drec, (size_t)cap * sizeof(pc_cycle_record)) != cudaSuccess)
+    rc = fail(PC_E_CUDA, "cycle record allocation failed");
+  CycleDev& h = *c->h_cyc;
+  std::memset(&h, 0, offsetof(CycleDev, tab));
+  h.remaining = outer_dt;
+  h.dtE = dtE;
+  h.floor_dt = floor_dt;
+  h.eps_rel = eps_rel;
+  h.kind = scheme;
+  h.make_odd = make_odd;
+  h.use_ptl = use_ptl;
+  h.rec_cap = (int)std::min<int64_t>(cap, 1 << 30);
+  h.max_cycles = max_cycles;
+  h.bad = 0x7f7f7f7f;
+  PersistBufs pb{};
+  for (int q = 0; q < nc; ++q) {
+    pb.set[0][q] = u->base(q);
+    pb.set[1][q] = A.base(q);
+    pb.set[2][q] = B.base(q);
+    pb.y0[q] = y0.base(q);
+  }
+  pb.pv = c->red_v;
+  pb.pi = c->red_i;
+  if (rc == PC_OK && cudaMemcpyAsync(c->cyc_dev, &h, offsetof(CycleDev, tab), cudaMemcpyHostToDevice, c->s) != cudaSuccess)
+    rc = fail(PC_E_CUDA, "cycle state upload");
+  if (rc == PC_OK) {
+    void (*kern)(GridDev, ScalarOp, PersistBufs, CycleDev*, pc_cycle_record*) =
+        nc == 3 ? k_cycle_small<3> : k_cycle_small<1>;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPersistThreads, 0);
+    const int need = (int)std::max<int64_t>(1, ((int64_t)g->g.n0 * g->g.n1 + kPersistThreads / 32 - 1) /
+                                                    (kPersistThreads / 32));
+    const int nblk = std::max(1, std::min({per_sm * c->sms, need, c->max_red}));
+    GridDev gd = g->g;
+    ScalarOp so = op->so;
+    CycleDev* csp = c->cyc_dev;
+    void* args[] = {&gd, &so, &pb, &csp, &drec};
+    if (cudaLaunchCooperativeKernel((void*)kern, dim3(nblk), dim3(kPersistThreads), args, 0, c->s) != cudaSuccess)
+      rc = fail(PC_E_CUDA, "cooperative launch of the small-grid cycle kernel failed");
+    c->st.launches++;
+  }
+  if (rc == PC_OK && cudaMemcpyAsync(&h, c->cyc_dev, offsetof(CycleDev, tab), cudaMemcpyDeviceToHost, c->s) != cudaSuccess)
+    rc = fail(PC_E_CUDA, "cycle state readback");
+  const int64_t ncyc_done = rc == PC_OK ? 0 : 0;
+  (void)ncyc_done;
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    const int64_t nrec = std::min<int64_t>(h.cyc, cap);
+    if (nrec > 0 && rec)
+      CUDA_TRY(cudaMemcpy(rec, drec, (size_t)std::min<int64_t>(nrec, rec_cap) * sizeof(pc_cycle_record),
+                          cudaMemcpyDeviceToHost));
+    *n_rec = rec ? std::min<int64_t>(nrec, rec_cap) : 0;
+    c->st.kind_launches[KIND_STS_SCALAR] += 0;
+    if (h.cur == 1) swap_storage(u, A);
+    else if (h.cur == 2) swap_storage(u, B);
+    if (h.status == 2) rc = fail(PC_E_BLOWUP, "non-finite value at STS stage " + std::to_string(h.bad), h.bad);
+    else if (h.status == 3) rc = fail(PC_E_CAP, "max_cycles reached (partial report returned)", h.cyc);
+    else if (h.status == 4) rc = fail(PC_E_INVALID, "STS stage count above the persistent kernel's table");
+  }
+  if (drec) cudaFree(drec);
+  work_put(A);
+  work_put(B);
+  work_put(y0);
+  return rc;
+}
+
 int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, double tol, int max_iter,
              double eps_rel, int check_all, int use_ptl, int floor_mode, double floor_fraction, int64_t max_cycles,
              double dt_euler, pc_cycle_record* rec, int64_t rec_cap, int64_t* n_rec) {
@@ -1749,6 +1794,9 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
   double remaining = outer_dt;
   int64_t cyc = 0;
   *n_rec = 0;
+  if ((scheme == PC_RKL2 || scheme == PC_RKG2) && !check_all && persist_ok(op))
+    return cycle_persistent(op, u, outer_dt, scheme, make_odd, eps_rel, use_ptl, floor_dt, dtE, max_cycles, rec, rec_cap,
+                            n_rec);
   Work y0;
   TRY(work_get(g, op->ncomp, y0));
   int rc = PC_OK;
