@@ -543,7 +543,7 @@ def cpu_baseline(name, budget_s=20.0, procs=1):
     planes = {"c1": 48, "c2": 16, "c3": 8, "c4": 4, "c5": 3}[name]
     stages = 4
     t0 = time.perf_counter()
-    jobs = [(name, (k * planes) % (n0 - planes), planes, stages) for k in range(procs)]
+    jobs = [(name, (k * planes) % max(1, n0 - planes + 1), planes, stages) for k in range(procs)]
     if procs == 1:
         res = [_oracle_chunk(jobs[0])]
     else:
