@@ -46,7 +46,7 @@ sys.path.insert(0, ROOT)
 # algorithmic bytes per cell-update of the fused stage / PCG iteration
 BYTES = {
     ("aligned", "rkl2"): 64,   # reads u_{k-1}, beta(3), u_{k-2}, u0, y0; writes u_k
-    ("aligned_rho", "rkl2"): 72,   # + rho
+    ("aligned_rho", "rkl2"): 64,   # + rho, radial (C5: rho(r), read once per plane, not per node)
     ("aligned", "be"): 128,    # Kp: r, p_old, d -> p; K7: p, beta(3) -> Ap; K8: x, r, p, Ap, d -> x, r
     # r-line preconditioner: z, p_old -> p; p, beta(3) -> Ap; x, r, p, Ap -> x, r;
     # line solve r, jl, inv -> z' and z', cp, r -> z

@@ -152,6 +152,7 @@ struct pc_op {
   bool frozen = false;
   int pc = PC_PC_JACOBI;    // BE+PCG preconditioner
   double* lbuf = nullptr;   // r-line preconditioner: -J_{i,i-1}, -J_{i,i+1} (2 component-sized buffers)
+  double* rho_r = nullptr;  // aligned: rho(i) per interior plane when the density field is radial
   bool line_valid = false;
 };
 
@@ -823,6 +824,7 @@ int pc_op_destroy(pc_op* op) {
   if (op->lbuf) pool_put(c, 2 * ce, op->lbuf);
   pool_put(c, 3 * ce, op->betabuf);
   pool_put(c, ce, op->dbuf);
+  if (op->rho_r) cudaFree(op->rho_r);
   cudaFree(op->kfc);
   delete op;
   return PC_OK;
@@ -842,6 +844,28 @@ static int run_bound(pc_op* op, const Op& o) {
   CUDA_TRY(cudaStreamSynchronize(c->s));
   op->lam_max = *c->h_maxout;
   op->dt_euler = op->lam_max > 0.0 ? 2.0 / op->lam_max : INFINITY;
+  return PC_OK;
+}
+
+// a density field that is constant on every r-plane (C5's rho(r)) is read by
+// the TMA march as one per-plane value (8 B/cell less per stage); the values
+// are the field's own, so results are bitwise unchanged
+static int detect_radial_rho(pc_op* op) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  op->ao.rho_r = nullptr;
+  if (!op->ao.rho || getenv("PC_NO_RADIAL_RHO")) return PC_OK;
+  CUDA_TRY(cudaMemsetAsync(c->bad, 0, sizeof(int), c->s));
+  k_radial_check<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ao.rho, c->bad);
+  c->st.launches++;
+  TRY(check_launch("k_radial_check"));
+  CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  if (*c->h_bad != 0) return PC_OK;  // not radial
+  if (!op->rho_r) CUDA_TRY(cudaMalloc(&op->rho_r, sizeof(double) * (size_t)g->g.n0));
+  CUDA_TRY(cudaMemcpy2DAsync(op->rho_r, sizeof(double), op->ao.rho, (size_t)g->g.plane * sizeof(double), sizeof(double),
+                             (size_t)g->g.n0, cudaMemcpyDeviceToDevice, c->s));
+  op->ao.rho_r = op->rho_r;
   return PC_OK;
 }
 
@@ -878,6 +902,7 @@ int pc_op_freeze(pc_op* op, const pc_field* T0) {
     CUDA_TRY(cudaStreamSynchronize(c->s));
     if (*c->h_bad == 1) return fail(PC_E_DOMAIN, "aligned conduction: non-positive T0 (SPEC.md:120)");
     TRY(run_bound(op, op->ao));
+    TRY(detect_radial_rho(op));
   } else {
     // the face coefficient D (or nu rho) is read at the axis-0 neighbours:
     // refresh the ghost planes of the coefficient fields
@@ -1037,7 +1062,7 @@ static bool tma_ok(const pc_grid* g) {
   return d.per2 && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && tma_encoder() != nullptr &&
          getenv("PC_NO_TMA") == nullptr;
 }
-template <class Epi, bool RHO>
+template <class Epi, int RHO>
 static int launch_tma_t(pc_op* op, const TmaMaps& maps, const Epi& epi, const int* skip, const char* what) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
@@ -1077,8 +1102,9 @@ static int launch_tma(pc_op* op, const double* Tin, const Epi& epi, const int* s
   TRY(make_field_map(&maps.T, Tin, g->g, MTK, MHJ));
   TRY(make_field_map(&maps.TS, Tin, g->g, 2, MHJ));
   for (int q = 0; q < Epi::NOPS; ++q) TRY(make_field_map(&maps.O[q], epi.opnd(q), g->g, MTK, MTJ));
-  if (op->ao.rho) return launch_tma_t<Epi, true>(op, maps, epi, skip, what);
-  return launch_tma_t<Epi, false>(op, maps, epi, skip, what);
+  if (op->ao.rho && op->ao.rho_r) return launch_tma_t<Epi, 2>(op, maps, epi, skip, what);
+  if (op->ao.rho) return launch_tma_t<Epi, 1>(op, maps, epi, skip, what);
+  return launch_tma_t<Epi, 0>(op, maps, epi, skip, what);
 }
 
 template <class Epi>

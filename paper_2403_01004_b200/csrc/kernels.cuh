@@ -228,6 +228,14 @@ __global__ void __launch_bounds__(kThreads) k_bound(GridDev g, Op op, double* di
   }
 }
 
+// flag = 1 if some rho(i, j, k) != rho(i, 0, 0) (the density is not radial)
+__global__ void __launch_bounds__(kThreads) k_radial_check(GridDev g, const double* rho, int* flag) {
+  PC_FOR_NODES(g, i, j, k) {
+    const double a = __ldg(rho + off3(g, i, j, k)), b = __ldg(rho + (int64_t)i * g.plane);
+    if (!(a == b)) atomicExch(flag, 1);
+  }
+}
+
 // beta_a = b_a * sqrt(c), c = kfc[i] * ((T0f * T0f) * sqrt(T0f)), T0f = max(T0, T_floor)
 // (oracle aligned_coefficient + aligned_beta); bad if T0 <= 0
 __global__ void __launch_bounds__(kThreads) k_aligned_beta(GridDev g, const double* T0, const double* kfc,

@@ -158,6 +158,7 @@ struct ScalarOp {
 struct AlignedOp {
   const double* beta[3];
   const double* rho;  // nullptr -> 1
+  const double* rho_r = nullptr;  // rho(i) per interior plane when rho is radial (TMA march reads it per plane)
   double pref;
   int ncomp;  // always 1
 

@@ -88,7 +88,9 @@ __device__ __forceinline__ void tma3(double* dst, const CUtensorMap* map, int c0
       : "memory");
 }
 
-template <class Epi, bool RHO>
+// RHO: 0 no density, 1 a density field (prefetched per node), 2 a radial
+// density (rho(i, j, k) == rho(i): one uniform per-plane value, no HBM stream)
+template <class Epi, int RHO>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op, const __grid_constant__ TmaMaps maps,
                                                         Epi epi, int R, int zsel, const int* skip) {
   extern __shared__ __align__(128) unsigned char tma_smem[];
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       }
       const bool exists = LAST ? plane_map(g, t).exists : true;
       const int tf = t - 1;
+      const double rpl = (RHO == 2 && !FIRST) ? __ldg(op.rho_r + tf) : 1.0;  // radial density of plane tf
       const int ig = tf + g.i0g;
       const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
 #pragma unroll
@@ -329,7 +332,8 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           const double iv = rM[jr * RW + 10] * col.ivg;
           const int64_t of = pofs + n * nstride;
           double f = ((0.0 - G) * iv) * op.pref;
-          if constexpr (RHO) f = f / rr[n];
+          if constexpr (RHO == 1) f = f / rr[n];
+          if constexpr (RHO == 2) f = f / rpl;
           const bool pin = pin_i || pin_j[n] || pin_k;
           if (pin) f = 0.0;
           double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
@@ -338,12 +342,13 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           double W = 0.0;  // inner-product weight rho V = rho * (Val2(row) * Valg(k)) (record slot 11)
           if constexpr (Epi::NEEDS_W) {
             W = rM[jr * RW + 11] * valg;
-            if constexpr (RHO) W = rr[n] * W;
+            if constexpr (RHO == 1) W = rr[n] * W;
+            if constexpr (RHO == 2) W = rpl * W;
           }
           epi(n, g, tf, jn(n), kg, of, f, Tm[n], pin, ov, W);
         }
         if (!LAST) {
-          if constexpr (RHO) {
+          if constexpr (RHO == 1) {
             if (inside[n]) rr[n] = __ldg(op.rho + pofs + g.plane + n * nstride);
           }
           ownp[n] = ((E[0][1] - E[0][0]) + (E[1][1] - E[1][0])) + (E[2][1] - E[2][0]);

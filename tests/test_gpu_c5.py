@@ -73,3 +73,21 @@ def test_c5_split_step_parity(gpu_ctx, c5s):
         assert [e.dt for e in rep.entries] == [r.dt for r in orep]
     assert np.array_equal(state["T"].download()[..., 0], ost["T"][0])
     assert np.array_equal(np.moveaxis(state["v"].download(), -1, 0), ost["v"])
+
+
+def test_radial_rho_path_bitwise(gpu_ctx, c5s, monkeypatch):
+    """A radial density is read per plane by the TMA march (no per-node rho
+    stream); the field path (PC_NO_RADIAL_RHO) gives the same bits."""
+    w = c5s
+    T = operators.Field(w.grid, w.fields["T"])
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("PC_NO_RADIAL_RHO", env)
+        cfg = operators.AlignedConductionConfig(b_hat=w.fields["b"], rho=w.fields["rho"], m_p=3.0, k_B=1.0, bc=w.bc)
+        op = operators.DiffusionOperator.aligned(cfg, T)
+        dtE = op.device_op(w.grid, 1).dt_euler
+        o, rep = ptl.cycle_operator(op, schemes.SchemeConfig("rkl2"), T, 300 * dtE)
+        out.append((o.values.copy(), [e.iters for e in rep.entries]))
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
