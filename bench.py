@@ -312,7 +312,9 @@ def run_ours(args, rank, world, local_rank):
         if d["ms"] > 0:
             bpc = BYTES[(bkey, kind)]
             rows.append({"kernel": {"sts_aligned": "k_aligned_march<EpiStage>",
-                                    "sts_scalar": "k_scalar_march<" + str(nc) + " comp, SEpiStage>",
+                                    "sts_scalar": ("k_cycle_small<%d> (persistent cycle loop: F, argmax, stages)" % nc
+                                                   if prob.dg.ncells * nc <= (1 << 21) else
+                                                   "k_scalar_march<" + str(nc) + " comp, SEpiStage>"),
                                     "pcg_aligned": ("k_pcg_pupdate_z + k_aligned_march<EpiMatvec> + k_pcg_update1 + "
                                                     "k_line_solve") if kind == "be-line" else
                                                    "k_pcg_pupdate + k_aligned_march<EpiMatvec> + k_pcg_update",

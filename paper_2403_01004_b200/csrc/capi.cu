@@ -1775,9 +1775,20 @@ static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme,
     ScalarOp so = op->so;
     CycleDev* csp = c->cyc_dev;
     void* args[] = {&gd, &so, &pb, &csp, &drec};
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, c->s);
+    }
     if (cudaLaunchCooperativeKernel((void*)kern, dim3(nblk), dim3(kPersistThreads), args, 0, c->s) != cudaSuccess)
       rc = fail(PC_E_CUDA, "cooperative launch of the small-grid cycle kernel failed");
     c->st.launches++;
+    c->st.stage_launches++;
+    if (c->timing) {  // the whole cycle loop is the "STS" time of this path
+      cudaEventRecord(e1, c->s);
+      c->ev.push_back({e0, e1, KIND_STS_SCALAR});
+    }
   }
   if (rc == PC_OK && cudaMemcpyAsync(&h, c->cyc_dev, offsetof(CycleDev, tab), cudaMemcpyDeviceToHost, c->s) != cudaSuccess)
     rc = fail(PC_E_CUDA, "cycle state readback");
@@ -1790,7 +1801,14 @@ static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme,
       CUDA_TRY(cudaMemcpy(rec, drec, (size_t)std::min<int64_t>(nrec, rec_cap) * sizeof(pc_cycle_record),
                           cudaMemcpyDeviceToHost));
     *n_rec = rec ? std::min<int64_t>(nrec, rec_cap) : 0;
-    c->st.kind_launches[KIND_STS_SCALAR] += 0;
+    {  // stage-k>=2 cell-updates, as the host-driven path counts them
+      int64_t stages = 0;
+      std::vector<pc_cycle_record> all((size_t)nrec);
+      if (nrec > 0) CUDA_TRY(cudaMemcpy(all.data(), drec, (size_t)nrec * sizeof(pc_cycle_record), cudaMemcpyDeviceToHost));
+      for (const auto& r : all) stages += r.iters - 1;
+      c->st.kind_launches[KIND_STS_SCALAR] += 1;
+      c->st.kind_units[KIND_STS_SCALAR] += stages * g->g.N;
+    }
     if (h.cur == 1) swap_storage(u, A);
     else if (h.cur == 2) swap_storage(u, B);
     if (h.status == 2) rc = fail(PC_E_BLOWUP, "non-finite value at STS stage " + std::to_string(h.bad), h.bad);
