@@ -24,7 +24,11 @@
  *   pc_step_euler                   schemes.step_euler
  *   pc_step_be, pc_pcg_solve        schemes.step_backward_euler + linsolve.pcg_solve
  *                                   with build_jacobi
- *   pc_cycle                        ptl.cycle_operator
+ *   pc_cycle                        ptl.cycle_operator; small scalar
+ *                                   grids run the whole loop in one persistent launch
+ *   pc_op_set_preconditioner        linsolve.Preconditioner kind:
+ *                                   point Jacobi (PC1) or the r-line block Jacobi that
+ *                                   stands in for the sequential ILU0 (PC2, :201-222)
  *
  * Device layout: every field component is one contiguous fp64 array
  * [n0 + 2][n1][n2] (axis 2 = phi fastest) whose first and last axis-0 planes

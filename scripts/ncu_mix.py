@@ -18,8 +18,11 @@ def mix(path, nodes):
             continue
         o = op[1] if op[0].startswith('@') else op[0]
         o = o.split('.')[0]
-        c[o] += int(r[iE] or 0)
-        w[o] += int(r[iW] or 0)
+        try:
+            c[o] += int(r[iE] or 0)
+            w[o] += int(r[iW] or 0)
+        except ValueError:  # repeated header rows
+            continue
     return c, w
 
 
