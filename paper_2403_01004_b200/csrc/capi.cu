@@ -1792,8 +1792,6 @@ static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme,
   }
   if (rc == PC_OK && cudaMemcpyAsync(&h, c->cyc_dev, offsetof(CycleDev, tab), cudaMemcpyDeviceToHost, c->s) != cudaSuccess)
     rc = fail(PC_E_CUDA, "cycle state readback");
-  const int64_t ncyc_done = rc == PC_OK ? 0 : 0;
-  (void)ncyc_done;
   if (rc == PC_OK) {
     CUDA_TRY(cudaStreamSynchronize(c->s));
     const int64_t nrec = std::min<int64_t>(h.cyc, cap);

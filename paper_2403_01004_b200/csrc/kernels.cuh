@@ -145,7 +145,6 @@ __global__ void __launch_bounds__(kThreads) k_stage(GridDev g, Op op, CFld um1, 
 
 // PTL pair tests at k (single block); neighbours = existing orthogonal nodes.
 __global__ void k_ptl_pairs(GridDev g, int ncomp, CFld u, CFld F, double eps_rel, ArgRes* res) {
-  __shared__ double sh[32];
   const long long kid = res->kidx;
   const double thr = eps_rel * res->fmax;
   const long long pt = kid / ncomp;
