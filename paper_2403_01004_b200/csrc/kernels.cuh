@@ -174,7 +174,6 @@ __global__ void k_ptl_pairs(GridDev g, int ncomp, CFld u, CFld F, double eps_rel
     res->ptl = best;
     res->limited = isfinite(best) ? 1 : 0;
   }
-  (void)sh;
 }
 
 // audit mode: all (node, node + e_a) pairs; candidates are > 0 so their bit
