@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
+    extra = os.environ.get("PC_NVCC_EXTRA", "").split()  # experiments only, e.g. -DSMARCH_MINB=2
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(OUT_DIR, "build.log")
     with open(log, "w") as fh:

@@ -1128,14 +1128,18 @@ static int launch_march(pc_op* op, const double* Tin, const Epi& epi, const int*
 }
 
 // ---- 7-point marching kernels (ScalarOp), dispatched on (ncomp, vector, D mode)
-static int smarch_R(const pc_grid* g) {
+// r-chunk length: the longest power of two (<= 32) that still gives ~12 blocks
+// per SM (3 resident, scalar) or ~6 (2 resident, 3-component); measured on C2:
+// R = 4 / 8 / 16 / 32 -> 2.49 / 2.77 / 2.92 / 2.83e10 cell-updates/s.
+static int smarch_R(const pc_grid* g, int ncomp) {
   if (const char* e = getenv("PC_SMARCH_R")) {
     const int r = atoi(e);
     if (r >= 1) return r;
   }
   const int tiles = ((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + SMJ - 1) / SMJ);
+  const int64_t want = ncomp == 3 ? 148 * 6 : 148 * 12;
   int R = 32;
-  while (R > 4 && (int64_t)tiles * ((g->g.n0 + R - 1) / R) < 148 * 12) R /= 2;
+  while (R > 4 && (int64_t)tiles * ((g->g.n0 + R - 1) / R) < want) R /= 2;
   return R;
 }
 static bool smarch_ok(const pc_op* op) { return op->ncomp == 1 || op->ncomp == 3; }
@@ -1143,7 +1147,7 @@ template <int NC, bool VEC, int DM, class Epi>
 static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, const char* what) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
-  const int R = smarch_R(g);
+  const int R = smarch_R(g, NC);
   dim3 grid((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + SMJ - 1) / SMJ, (g->g.n0 + R - 1) / R);
   if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
   static bool attr = false;
@@ -1333,7 +1337,7 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
   // launches on one rank, for testing)
   const bool force_split = getenv("PC_SPLIT_STAGE") != nullptr;
   const bool marching = std::is_same<Op, AlignedOp>::value || smarch_ok(op);
-  const int Rz = std::is_same<Op, AlignedOp>::value ? march_R(g) : smarch_R(g);
+  const int Rz = std::is_same<Op, AlignedOp>::value ? march_R(g) : smarch_R(g, op->ncomp);
   const int nz = (g->g.n0 + Rz - 1) / Rz;
   const bool overlap = marching && nz >= 3 && (c->comm != nullptr || force_split);
   for (int k = 2; k <= s && rc == PC_OK; ++k) {

@@ -25,6 +25,15 @@ constexpr int SNT = SMJ * MTK;       // threads = tile nodes
 constexpr int SNFILL = (SHP + SNT - 1) / SNT;
 constexpr int SROWT = 5;             // W2[0], W2[1], W2[2], iV2 per (plane, theta row), + W2[1] at j-1 via row - 1
 constexpr int SEO = 9;               // epilogue operands staged per node (max: 3 x u0, um2, y0)
+// resident blocks per SM asked of ptxas: the 3-component (vector) kernels need
+// ~120 registers; capping them at 80 for 3 blocks/SM made ptxas re-load
+// operands from shared memory (C2 stage 3811 GB/s at 3 blocks vs 4429 at 2,
+// profiles/r01_c2_minb.txt).  SMARCH_MINB overrides both (experiments).
+#ifdef SMARCH_MINB
+#define SMARCH_BLOCKS(NC) SMARCH_MINB
+#else
+#define SMARCH_BLOCKS(NC) ((NC) == 3 ? 2 : 3)
+#endif
 
 template <int NC>
 struct SMarchSmem {
@@ -36,7 +45,7 @@ struct SMarchSmem {
 
 // DM: 0 = D constant Dc, 1 = D nodal field, 2 = D = Dc * rho (viscosity)
 template <int NC, bool VEC, int DM, class Epi>
-__global__ void __launch_bounds__(SNT, 3) k_scalar_march(GridDev g, ScalarOp op, const double* __restrict__ u0p,
+__global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev g, ScalarOp op, const double* __restrict__ u0p,
                                                          const double* __restrict__ u1p,
                                                          const double* __restrict__ u2p, Epi epi, int R, int zsel,
                                                          const int* skip) {
