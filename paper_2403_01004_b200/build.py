@@ -50,7 +50,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     extra = os.environ.get("PC_NVCC_EXTRA", "").split()  # experiments only, e.g. -DSMARCH_MINB=2
-    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
+    flags = NVCC_FLAGS
+    if os.environ.get("PC_FMAD") == "1":  # experiment: contraction on (NOT bitwise with the oracle)
+        flags = [f for f in flags if f != "-fmad=false"]
+        flags = [f.replace(",-ffp-contract=off", "") for f in flags]
+    cmd = [_nvcc(), *flags, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(OUT_DIR, "build.log")
     with open(log, "w") as fh:
