@@ -118,6 +118,13 @@ int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* h
 int pc_field_copy(pc_field* dst, const pc_field* src);
 int pc_field_fill(pc_field* f, double value);
 int pc_field_exchange_halo(pc_field* f); /* axis-0 ghost planes (no-op on 1 rank) */
+/* number of owned nodes x components failing a domain test, summed over all
+   ranks: PC_TEST_POSITIVE counts !(x > 0), PC_TEST_NONNEG !(x >= 0),
+   PC_TEST_FINITE !isfinite(x) (NaN fails all three).  Replaces the host-side
+   `np.any(~(rho > 0))` validation of the operator constructors
+   (reference: SPEC.md:89-93, ValueError for rho <= 0) with one pass over HBM. */
+enum pc_field_test { PC_TEST_POSITIVE = 0, PC_TEST_NONNEG = 1, PC_TEST_FINITE = 2 };
+int pc_field_count(const pc_field* f, int test, int64_t* count);
 /* write ghost plane -1 (side 0) or n0 (side 1) of every component from a host
    SoA plane [ncomp][n1][n2] */
 int pc_field_set_ghost(pc_field* f, int side, const double* host);

@@ -19,6 +19,7 @@ PC_E_INVALID, PC_E_INDEFINITE, PC_E_DIVERGED, PC_E_BLOWUP, PC_E_CAP = 1, 2, 3, 4
 PC_E_CUDA, PC_E_NCCL, PC_E_DOMAIN, PC_E_NOTCONV = 6, 7, 8, 9
 LAYOUT_AOS, LAYOUT_SOA = 0, 1
 PC_JACOBI, PC_LINE_R = 0, 1
+TEST_POSITIVE, TEST_NONNEG, TEST_FINITE = 0, 1, 2
 RKL2, RKG2, BE, EULER = 0, 1, 2, 3
 FLOOR_EULER, FLOOR_FRACTION = 0, 1
 
@@ -69,6 +70,7 @@ _SIGS = {
     "pc_field_copy": (c_int, [c_void_p, c_void_p]),
     "pc_field_fill": (c_int, [c_void_p, c_double]),
     "pc_field_exchange_halo": (c_int, [c_void_p]),
+    "pc_field_count": (c_int, [c_void_p, c_int, POINTER(c_int64)]),
     "pc_host_register": (c_int, [c_void_p, c_size_t]),
     "pc_host_unregister": (c_int, [c_void_p]),
     "pc_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),

@@ -729,6 +729,21 @@ int pc_field_fill(pc_field* f, double v) {
 
 int pc_field_exchange_halo(pc_field* f) { return halo_field(f); }
 
+int pc_field_count(const pc_field* f, int test, int64_t* count) {
+  if (!f || !count || test < 0 || test > 2) return fail(PC_E_INVALID, "bad pc_field_count arguments");
+  pc_grid* g = f->grid;
+  pc_ctx* c = g->ctx;
+  CUDA_TRY(cudaMemsetAsync(c->maxout, 0, sizeof(double), c->s));
+  k_count_fail<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, cfld(f), f->ncomp, test, c->maxout);
+  c->st.launches++;
+  TRY(check_launch("k_count_fail"));
+  TRY(allreduce_d(c, c->maxout, 1, nccl::kSum));
+  CUDA_TRY(cudaMemcpyAsync(c->h_maxout, c->maxout, sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  *count = (int64_t)*c->h_maxout;
+  return PC_OK;
+}
+
 int pc_host_alloc(size_t bytes, void** out) {
   if (!out) return fail(PC_E_INVALID, "null argument");
   CUDA_TRY(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));

@@ -234,6 +234,22 @@ __global__ void __launch_bounds__(kThreads) k_radial_check(GridDev g, const doub
   }
 }
 
+// number of owned nodes x components failing a domain test (pc_field_count):
+// 0: !(x > 0), 1: !(x >= 0), 2: !isfinite(x); NaN fails every test
+__global__ void __launch_bounds__(kThreads) k_count_fail(GridDev g, CFld f, int ncomp, int test, double* count) {
+  double n = 0.0;
+  PC_FOR_NODES(g, i, j, k) {
+    const int64_t o = off3(g, i, j, k);
+    for (int q = 0; q < ncomp; ++q) {
+      const double x = __ldg(f.p[q] + o);
+      const bool bad = test == 0 ? !(x > 0.0) : test == 1 ? !(x >= 0.0) : !isfinite(x);
+      n += bad ? 1.0 : 0.0;
+    }
+  }
+  n = warp_sum(n);
+  if ((threadIdx.x & 31) == 0 && n != 0.0) atomicAdd(count, n);
+}
+
 // beta_a = b_a * sqrt(c), c = kfc[i] * ((T0f * T0f) * sqrt(T0f)), T0f = max(T0, T_floor)
 // (oracle aligned_coefficient + aligned_beta); bad if T0 <= 0
 __global__ void __launch_bounds__(kThreads) k_aligned_beta(GridDev g, const double* T0, const double* kfc,

@@ -301,6 +301,12 @@ class DeviceField:
         a = np.ascontiguousarray(plane_soa, dtype=np.float64)
         _lib.check(_lib.lib().pc_field_set_ghost(self.handle, int(side), _lib.dptr(a)), "set_ghost")
 
+    def count_failing(self, test: int) -> int:
+        """Owned nodes x components failing ``test`` (_lib.TEST_*), all ranks."""
+        n = ctypes.c_int64()
+        _lib.check(_lib.lib().pc_field_count(self.handle, int(test), ctypes.byref(n)), "count")
+        return int(n.value)
+
     def download_planes(self, i0: int, n: int) -> np.ndarray:
         """Axis-0 planes [i0, i0 + n) as SoA (ncomp, n, n1, n2)."""
         n1, n2 = self.dgrid.shape[1], self.dgrid.shape[2]

@@ -40,6 +40,16 @@ def _values(x, grid, name, ncomp=None):
     return v
 
 
+def _positive_field(dg, values):
+    """Upload a density and validate it on the device: ValueError if any node
+    has !(rho > 0).  One counting pass over HBM instead of a
+    host-side ``np.any(~(rho > 0))`` over the whole array (~0.5 s at C5)."""
+    rd = device.DeviceField.from_values(dg, values)
+    if rd.count_failing(_lib.TEST_POSITIVE):
+        raise ValueError("rho must be > 0")
+    return rd
+
+
 @dataclass
 class ScalarDiffusionConfig:
     """F = (1/rho) div(nu rho grad u).  ``nu`` and ``rho`` are
@@ -198,9 +208,7 @@ class DeviceOperator:
             rd = None
             if rho is not None:
                 rho_a = rho if not isinstance(rho, float) else np.full(tuple(grid.shape), rho)
-                if np.any(~(rho_a > 0)):
-                    raise ValueError("rho must be > 0")
-                rd = device.DeviceField.from_values(dg, rho_a)
+                rd = _positive_field(dg, rho_a)
                 self._keep.append(rd)
             vm = bool(cfg.vector_metric) and ncomp == 3 and getattr(grid, "metric", "cartesian") == mesh.SPHERICAL
             if cfg.vector_metric and ncomp != 3:
@@ -234,9 +242,7 @@ class DeviceOperator:
             elif cfg.rho is not None and not (isinstance(cfg.rho, (int, float)) and float(cfg.rho) == 1.0):
                 rho_a = _values(cfg.rho, grid, "rho")
                 rho_a = rho_a if not isinstance(rho_a, float) else np.full(tuple(grid.shape), rho_a)
-                if np.any(~(rho_a > 0)):
-                    raise ValueError("rho must be > 0")
-                rd = device.DeviceField.from_values(dg, rho_a)
+                rd = _positive_field(dg, rho_a)
                 self._keep.append(rd)
             r = np.asarray(grid.coords[0], float)
             fc = cfg.fc_table(r)

@@ -295,3 +295,45 @@ def test_cycle_blowup_is_reported_with_the_oracle_stage(gpu_ctx):
         ptl.cycle_operator(op, schemes.SchemeConfig("rkl2"), mesh.Field(w.grid, u[..., None]), 300 * dtE,
                            ptl.PtlConfig(enabled=False), dt_euler=150 * dtE)
     assert ei.value.stage == eo.value.stage
+
+
+# ---------------------------------------------------------------- domain checks on the device
+def test_field_count_matches_numpy(gpu_ctx):
+    """pc_field_count (the device-side domain test behind the constructors'
+    rho validation) counts exactly what numpy counts, NaN failing every test."""
+    from paper_2403_01004_b200 import _lib, device
+
+    w = configs.c2(n=(12, 10, 20))
+    rng = np.random.default_rng(7)
+    v = rng.standard_normal(tuple(w.grid.shape) + (3,))
+    v.flat[rng.choice(v.size, 9, replace=False)] = 0.0
+    v.flat[rng.choice(v.size, 4, replace=False)] = np.nan
+    v.flat[rng.choice(v.size, 3, replace=False)] = np.inf
+    v.flat[rng.choice(v.size, 2, replace=False)] = -np.inf
+    dg = device.device_grid(w.grid, w.bc)
+    f = device.DeviceField.from_values(dg, v)
+    with np.errstate(invalid="ignore"):
+        want = {_lib.TEST_POSITIVE: int(np.sum(~(v > 0))), _lib.TEST_NONNEG: int(np.sum(~(v >= 0))),
+                _lib.TEST_FINITE: int(np.sum(~np.isfinite(v)))}
+    for t, n in want.items():
+        assert f.count_failing(t) == n, t
+
+
+@pytest.mark.parametrize("bad", [0.0, -1e-300, np.nan])
+@pytest.mark.parametrize("kind", ["scalar", "aligned"])
+def test_rho_validation_on_device(gpu_ctx, kind, bad):
+    """a density with any !(rho > 0) node raises ValueError at
+    operator construction (checked on the device after the upload)."""
+    w = configs.c3(n=(8, 8, 16))
+    rho = np.full(tuple(w.grid.shape), 2.0)
+    if kind == "scalar":
+        mk = lambda r: operators.DiffusionOperator.scalar(  # noqa: E731
+            operators.ScalarDiffusionConfig(nu=1.0, rho=r, bc=w.bc), 1).device_op(w.grid, 1)
+    else:
+        mk = lambda r: operators.DiffusionOperator.aligned(  # noqa: E731
+            operators.AlignedConductionConfig(b_hat=w.fields["b"], rho=r, m_p=3.0, k_B=1.0, bc=w.bc),
+            operators.Field(w.grid, w.fields["T"])).device_op(w.grid, 1)
+    mk(rho)  # valid
+    rho[3, 5, 7] = bad
+    with pytest.raises(ValueError, match="rho must be > 0"):
+        mk(rho)
