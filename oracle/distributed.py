@@ -1,7 +1,7 @@
 """Slab-decomposed restatement of the cycle (test infrastructure; see
 oracle/__init__.py) -- the algorithm the r-slab CUDA path implements
-(paper_2403_01004_b200/csrc/capi.cu: halo_exchange, global_argmax,
-ptl_device, pcg_split_fin), written over ``torch.distributed`` so it runs on
+(paper_2403_01004_b200/csrc/capi_objects.cuh: halo_exchange, global_argmax;
+capi_sts.cuh: ptl_device; capi_pcg.cuh: pcg_split_fin), written over ``torch.distributed`` so it runs on
 CPU ranks with the gloo backend.
 
 Per rank: the axis-0 slab [i0, i0 + n) of geometry.slab_bounds, stored with

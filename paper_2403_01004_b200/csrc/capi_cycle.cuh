@@ -1,0 +1,220 @@
+// paracycle_b200 C ABI, part of the single translation unit capi.cu (included
+// there in order; relies on the declarations of the parts before it).
+//
+// C ABI: pc_cycle, the PTL-cycled advance (host-driven loop, and the
+// persistent one-launch loop for small grids)
+#pragma once
+
+// ------------------------------------------------------------------ cycle
+// ---- persistent small-grid cycle loop (persist.cuh)
+static bool persist_ok(const pc_op* op) {
+  const pc_grid* g = op->grid;
+  const pc_ctx* c = g->ctx;
+  if (op->kind != K_SCALAR || (op->ncomp != 1 && op->ncomp != 3)) return false;
+  if (c->comm || c->nranks > 1 || g->g.ghost_lo0 || g->g.ghost_hi0) return false;
+  if (getenv("PC_NO_PERSIST")) return false;
+  return (int64_t)g->g.N * op->ncomp <= (int64_t)(getenv("PC_PERSIST_MAX") ? atoll(getenv("PC_PERSIST_MAX")) : 1 << 21);
+}
+static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, double eps_rel,
+                            int use_ptl, double floor_dt, double dtE, int64_t max_cycles, pc_cycle_record* rec,
+                            int64_t rec_cap, int64_t* n_rec) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int nc = op->ncomp;
+  if (!c->cyc_dev) {
+    CUDA_TRY(cudaMalloc(&c->cyc_dev, sizeof(CycleDev)));
+    CUDA_TRY(cudaMallocHost(&c->h_cyc, sizeof(CycleDev)));
+  }
+  Work A, B, y0;
+  TRY(work_get(g, nc, A));
+  TRY(work_get(g, nc, B));
+  TRY(work_get(g, nc, y0));
+  const int64_t cap = std::max<int64_t>(0, std::min<int64_t>(rec_cap, max_cycles));
+  pc_cycle_record* drec = nullptr;
+  int rc = PC_OK;
+  if (cap > 0 && cudaMalloc(&drec, (size_t)cap * sizeof(pc_cycle_record)) != cudaSuccess)
+    rc = fail(PC_E_CUDA, "cycle record allocation failed");
+  CycleDev& h = *c->h_cyc;
+  std::memset(&h, 0, offsetof(CycleDev, tab));
+  h.remaining = outer_dt;
+  h.dtE = dtE;
+  h.floor_dt = floor_dt;
+  h.eps_rel = eps_rel;
+  h.kind = scheme;
+  h.make_odd = make_odd;
+  h.use_ptl = use_ptl;
+  h.rec_cap = (int)std::min<int64_t>(cap, 1 << 30);
+  h.max_cycles = max_cycles;
+  h.bad = 0x7f7f7f7f;
+  PersistBufs pb{};
+  for (int q = 0; q < nc; ++q) {
+    pb.set[0][q] = u->base(q);
+    pb.set[1][q] = A.base(q);
+    pb.set[2][q] = B.base(q);
+    pb.y0[q] = y0.base(q);
+  }
+  pb.pv = c->red_v;
+  pb.pi = c->red_i;
+  if (rc == PC_OK && cudaMemcpyAsync(c->cyc_dev, &h, offsetof(CycleDev, tab), cudaMemcpyHostToDevice, c->s) != cudaSuccess)
+    rc = fail(PC_E_CUDA, "cycle state upload");
+  if (rc == PC_OK) {
+    void (*kern)(GridDev, ScalarOp, PersistBufs, CycleDev*, pc_cycle_record*) =
+        nc == 3 ? k_cycle_small<3> : k_cycle_small<1>;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPersistThreads, 0);
+    const int need = (int)std::max<int64_t>(1, ((int64_t)g->g.n0 * g->g.n1 + kPersistThreads / 32 - 1) /
+                                                    (kPersistThreads / 32));
+    const int nblk = std::max(1, std::min({per_sm * c->sms, need, c->max_red}));
+    GridDev gd = g->g;
+    ScalarOp so = op->so;
+    CycleDev* csp = c->cyc_dev;
+    void* args[] = {&gd, &so, &pb, &csp, &drec};
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, c->s);
+    }
+    if (cudaLaunchCooperativeKernel((void*)kern, dim3(nblk), dim3(kPersistThreads), args, 0, c->s) != cudaSuccess)
+      rc = fail(PC_E_CUDA, "cooperative launch of the small-grid cycle kernel failed");
+    c->st.launches++;
+    c->st.stage_launches++;
+    if (c->timing) {  // the whole cycle loop is the "STS" time of this path
+      cudaEventRecord(e1, c->s);
+      c->ev.push_back({e0, e1, KIND_STS_SCALAR});
+    }
+  }
+  if (rc == PC_OK && cudaMemcpyAsync(&h, c->cyc_dev, offsetof(CycleDev, tab), cudaMemcpyDeviceToHost, c->s) != cudaSuccess)
+    rc = fail(PC_E_CUDA, "cycle state readback");
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    const int64_t nrec = std::min<int64_t>(h.cyc, cap);
+    if (nrec > 0 && rec)
+      CUDA_TRY(cudaMemcpy(rec, drec, (size_t)std::min<int64_t>(nrec, rec_cap) * sizeof(pc_cycle_record),
+                          cudaMemcpyDeviceToHost));
+    *n_rec = rec ? std::min<int64_t>(nrec, rec_cap) : 0;
+    {  // stage-k>=2 cell-updates, as the host-driven path counts them
+      int64_t stages = 0;
+      std::vector<pc_cycle_record> all((size_t)nrec);
+      if (nrec > 0) CUDA_TRY(cudaMemcpy(all.data(), drec, (size_t)nrec * sizeof(pc_cycle_record), cudaMemcpyDeviceToHost));
+      for (const auto& r : all) stages += r.iters - 1;
+      c->st.kind_launches[KIND_STS_SCALAR] += 1;
+      c->st.kind_units[KIND_STS_SCALAR] += stages * g->g.N;
+    }
+    if (h.cur == 1) swap_storage(u, A);
+    else if (h.cur == 2) swap_storage(u, B);
+    if (h.status == 2) rc = fail(PC_E_BLOWUP, "non-finite value at STS stage " + std::to_string(h.bad), h.bad);
+    else if (h.status == 3) rc = fail(PC_E_CAP, "max_cycles reached (partial report returned)", h.cyc);
+    else if (h.status == 4) rc = fail(PC_E_INVALID, "STS stage count above the persistent kernel's table");
+  }
+  if (drec) cudaFree(drec);
+  work_put(A);
+  work_put(B);
+  work_put(y0);
+  return rc;
+}
+
+int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, double tol, int max_iter,
+             double eps_rel, int check_all, int use_ptl, int floor_mode, double floor_fraction, int64_t max_cycles,
+             double dt_euler, pc_cycle_record* rec, int64_t rec_cap, int64_t* n_rec) {
+  if (!op || !u || !n_rec || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "bad cycle arguments");
+  if (!(outer_dt > 0.0)) return fail(PC_E_INVALID, "outer_dt must be > 0");
+  if (max_cycles < 1 || !(eps_rel > 0.0)) return fail(PC_E_INVALID, "need max_cycles >= 1 and eps_rel > 0");
+  if (scheme < PC_RKL2 || scheme > PC_EULER) return fail(PC_E_INVALID, "unknown scheme");
+  TRY(need_frozen(op));
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const double dtE = dt_euler > 0.0 ? dt_euler : op->dt_euler;
+  const double floor_dt = floor_mode == PC_FLOOR_EULER ? dtE : floor_fraction * dtE;
+  double remaining = outer_dt;
+  int64_t cyc = 0;
+  *n_rec = 0;
+  if ((scheme == PC_RKL2 || scheme == PC_RKG2) && !check_all && persist_ok(op))
+    return cycle_persistent(op, u, outer_dt, scheme, make_odd, eps_rel, use_ptl, floor_dt, dtE, max_cycles, rec, rec_cap,
+                            n_rec);
+  Work y0;
+  TRY(work_get(g, op->ncomp, y0));
+  int rc = PC_OK;
+  std::vector<double> tab;
+  c->bad_pending = false;
+  while (remaining > 0.0) {
+    if (cyc >= max_cycles) {
+      if (c->bad_pending) {
+        CUDA_TRY(cudaStreamSynchronize(c->s));
+        rc = check_pending_bad(c);
+        if (rc) break;
+      }
+      rc = fail(PC_E_CAP, "max_cycles reached (partial report returned)", cyc);
+      break;
+    }
+    rc = halo_field(u);
+    if (rc) break;
+    rc = apply_any(op, cfld(u), y0.f(), true);
+    if (rc) break;
+    if (use_ptl) {
+      double* yb[3] = {y0.b[0], y0.b[1], y0.b[2]};
+      rc = ptl_device(g, op->ncomp, cfld(u), y0.cf(), yb, eps_rel, check_all);
+      if (rc) break;
+    }
+    double ptl;
+    int limited;
+    rc = ptl_read(c, check_all, use_ptl, &ptl, &limited, nullptr);
+    if (rc) break;
+    rc = check_pending_bad(c);  // ptl_read synchronised the stream
+    if (rc) break;
+    double dt;
+    if (!limited) {
+      dt = remaining;
+    } else {
+      dt = ptl >= floor_dt ? ptl : floor_dt;  // Python max(ptl, floor)
+      if (dt >= remaining) dt = remaining;
+    }
+    int iters = 0;
+    double rel = 0.0;
+    if (scheme == PC_RKL2 || scheme == PC_RKG2) {
+      int s = pc_sts_count(scheme, dt, dtE, make_odd);
+      tab.assign(5 * (size_t)s, 0.0);
+      rc = pc_sts_table(scheme, s, dt, tab.data());
+      if (rc) break;
+      rc = sts_any(op, u, tab.data(), s, y0, true);
+      iters = s;
+    } else if (scheme == PC_BE) {
+      int conv = 0;
+      rc = be_step(op, u, dt, tol, max_iter, &iters, &rel, &conv);
+      if (rc == PC_OK && !conv) rc = fail(PC_E_NOTCONV, "PCG did not converge within max_iter", iters);
+    } else {
+      Work A;
+      rc = work_get(g, op->ncomp, A);
+      if (rc) break;
+      CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
+      k_stage1<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ncomp, cfld(u), y0.cf(), A.f(), dt, c->bad);
+      c->st.launches++;
+      rc = check_launch("k_stage1");
+      if (rc == PC_OK) swap_storage(u, A);
+      work_put(A);
+      iters = 1;
+    }
+    ++cyc;
+    if (rec && *n_rec < rec_cap) {
+      pc_cycle_record& R = rec[*n_rec];
+      R.cycle = cyc;
+      R.dt = dt;
+      R.ptl_raw = limited ? ptl : INFINITY;
+      R.relres = rel;
+      R.limited = limited;
+      R.iters = iters;
+      ++*n_rec;
+    }
+    if (rc) break;
+    if (dt == remaining) remaining = 0.0;
+    else remaining = remaining - dt;
+  }
+  work_put(y0);
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    rc = check_pending_bad(c);
+  }
+  c->bad_pending = false;
+  return rc;
+}

@@ -1,0 +1,488 @@
+// paracycle_b200 C ABI, part of the single translation unit capi.cu (included
+// there in order; relies on the declarations of the parts before it).
+//
+// C ABI: operator construction and freezing (coefficients, Gershgorin bound,
+// radial-density detection), and the launchers of the marching kernels
+// (TMA / cp.async Spitzer march, 7-point march) every scheme goes through
+#pragma once
+
+// ------------------------------------------------------------------ operators
+int pc_op_create_scalar(pc_grid* g, int ncomp, int vector_metric, double D_const, const pc_field* D,
+                        const pc_field* rho, pc_op** out) {
+  if (!g || !out || ncomp < 1 || ncomp > 3) return fail(PC_E_INVALID, "bad scalar operator arguments");
+  if (vector_metric && ncomp != 3) return fail(PC_E_INVALID, "vector metric needs 3 components");
+  if ((D && D->ncomp != 1) || (rho && rho->ncomp != 1)) return fail(PC_E_INVALID, "D and rho are scalar fields");
+  pc_op* op = new pc_op();
+  op->grid = g;
+  op->kind = K_SCALAR;
+  op->ncomp = ncomp;
+  op->so.D = D ? D->base(0) : nullptr;
+  op->so.Dc = D_const;
+  op->so.drho = 0;
+  op->so.rho = rho ? rho->base(0) : nullptr;
+  op->so.ncomp = ncomp;
+  op->so.vector = (vector_metric && g->g.spherical) ? 1 : 0;
+  *out = op;
+  return PC_OK;
+}
+
+int pc_op_create_viscous(pc_grid* g, int ncomp, int vector_metric, double nu, const pc_field* rho, pc_op** out) {
+  if (!rho || rho->ncomp != 1) return fail(PC_E_INVALID, "viscous operator needs a scalar density field");
+  if (!(nu >= 0.0)) return fail(PC_E_INVALID, "nu must be >= 0");
+  TRY(pc_op_create_scalar(g, ncomp, vector_metric, nu, nullptr, rho, out));
+  (*out)->so.drho = 1;
+  return PC_OK;
+}
+
+int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, double pref, double kappa0,
+                         const double* fc_table, double T_floor, pc_op** out) {
+  if (!g || !out || !bhat || bhat->ncomp != 3) return fail(PC_E_INVALID, "aligned operator needs a 3-component b");
+  if (rho && rho->ncomp != 1) return fail(PC_E_INVALID, "rho is a scalar field");
+  pc_ctx* c = g->ctx;
+  pc_op* op = new pc_op();
+  op->grid = g;
+  op->kind = K_ALIGNED;
+  op->ncomp = 1;
+  for (int q = 0; q < 3; ++q) op->bsrc[q] = bhat->base(q);
+  op->ao.rho = rho ? rho->base(0) : nullptr;
+  op->ao.pref = pref;
+  op->ao.ncomp = 1;
+  op->Tfloor = T_floor;
+  const int rows = g->g.n0 + 2;
+  std::vector<double> k(rows);
+  for (int r = 0; r < rows; ++r) k[r] = fc_table ? kappa0 * fc_table[r] : kappa0;
+  CUDA_TRY(cudaMalloc(&op->kfc, sizeof(double) * rows));
+  CUDA_TRY(cudaMemcpy(op->kfc, k.data(), sizeof(double) * rows, cudaMemcpyHostToDevice));
+  if (!(op->betabuf = pool_get(c, 3 * g->comp_elems))) {
+    cudaFree(op->kfc);
+    delete op;
+    return fail(PC_E_CUDA, "beta allocation failed (out of device memory)");
+  }
+  cudaMemsetAsync(op->betabuf, 0, 3 * g->comp_elems * sizeof(double), c->s);
+  for (int q = 0; q < 3; ++q) op->ao.beta[q] = op->betabuf + q * g->comp_elems + g->g.plane;
+  *out = op;
+  return PC_OK;
+}
+
+int pc_op_set_preconditioner(pc_op* op, int pc) {
+  if (!op) return fail(PC_E_INVALID, "null operator");
+  if (pc != PC_PC_JACOBI && pc != PC_PC_LINE_R) return fail(PC_E_INVALID, "unknown preconditioner");
+  if (pc == PC_PC_LINE_R && op->kind != K_ALIGNED)
+    return fail(PC_E_INVALID, "the r-line preconditioner is built for the aligned operator");
+  if (pc == PC_PC_LINE_R && op->grid->ctx->nranks > 1)
+    return fail(PC_E_INVALID, "the r-line preconditioner needs the whole r line on one rank");
+  op->pc = pc;
+  return PC_OK;
+}
+
+int pc_op_destroy(pc_op* op) {
+  if (!op) return PC_OK;
+  pc_ctx* c = op->grid->ctx;
+  const size_t ce = op->grid->comp_elems;
+  if (op->lbuf) pool_put(c, 2 * ce, op->lbuf);
+  pool_put(c, 3 * ce, op->betabuf);
+  pool_put(c, ce, op->dbuf);
+  if (op->rho_r) cudaFree(op->rho_r);
+  cudaFree(op->kfc);
+  delete op;
+  return PC_OK;
+}
+
+template <class Op>
+static int run_bound(pc_op* op, const Op& o) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  int nb = node_blocks(c, g->g);
+  k_bound<<<nb, kThreads, 0, c->s>>>(g->g, o, op->dbuf ? op->dbuf + g->g.plane : nullptr, c->red_v, c->counter,
+                                     c->maxout);
+  c->st.launches++;
+  TRY(check_launch("k_bound"));
+  TRY(allreduce_d(c, c->maxout, 1, nccl::kMax));
+  CUDA_TRY(cudaMemcpyAsync(c->h_maxout, c->maxout, sizeof(double), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  op->lam_max = *c->h_maxout;
+  op->dt_euler = op->lam_max > 0.0 ? 2.0 / op->lam_max : INFINITY;
+  return PC_OK;
+}
+
+// a density field that is constant on every r-plane (C5's rho(r)) is read by
+// the TMA march as one per-plane value (8 B/cell less per stage); the values
+// are the field's own, so results are bitwise unchanged
+static int detect_radial_rho(pc_op* op) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  op->ao.rho_r = nullptr;
+  if (!op->ao.rho || getenv("PC_NO_RADIAL_RHO")) return PC_OK;
+  CUDA_TRY(cudaMemsetAsync(c->bad, 0, sizeof(int), c->s));
+  k_radial_check<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ao.rho, c->bad);
+  c->st.launches++;
+  TRY(check_launch("k_radial_check"));
+  CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  if (*c->h_bad != 0) return PC_OK;  // not radial
+  if (!op->rho_r) CUDA_TRY(cudaMalloc(&op->rho_r, sizeof(double) * (size_t)g->g.n0));
+  CUDA_TRY(cudaMemcpy2DAsync(op->rho_r, sizeof(double), op->ao.rho, (size_t)g->g.plane * sizeof(double), sizeof(double),
+                             (size_t)g->g.n0, cudaMemcpyDeviceToDevice, c->s));
+  op->ao.rho_r = op->rho_r;
+  return PC_OK;
+}
+
+int pc_op_freeze(pc_op* op, const pc_field* T0) {
+  if (!op) return fail(PC_E_INVALID, "null operator");
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  if (op->kind == K_ALIGNED) {
+    if (!T0 || T0->ncomp != 1 || T0->grid != g) return fail(PC_E_INVALID, "aligned freeze needs a scalar T0 on the grid");
+    CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
+    CFld bsrc{{op->bsrc[0], op->bsrc[1], op->bsrc[2]}};
+    Fld beta{{const_cast<double*>(op->ao.beta[0]), const_cast<double*>(op->ao.beta[1]),
+              const_cast<double*>(op->ao.beta[2])}};
+    // beta on the interior AND the existing ghost planes (pointwise in T0 and
+    // b, whose ghost planes are exchanged first): no beta exchange needed
+    {
+      double* tb[1] = {const_cast<double*>(T0->buf[0])};
+      TRY(halo_exchange(c, g, tb, 1));
+      double* bb[3] = {const_cast<double*>(op->bsrc[0]) - g->g.plane, const_cast<double*>(op->bsrc[1]) - g->g.plane,
+                       const_cast<double*>(op->bsrc[2]) - g->g.plane};
+      TRY(halo_exchange(c, g, bb, 3));
+    }
+    GridDev gx = g->g;
+    const int glo = g->g.ghost_lo0 ? 1 : 0, ghi = g->g.ghost_hi0 ? 1 : 0;
+    gx.n0 = g->g.n0 + glo + ghi;
+    const int64_t sh = -(int64_t)glo * g->g.plane;
+    CFld bx{{bsrc.p[0] + sh, bsrc.p[1] + sh, bsrc.p[2] + sh}};
+    Fld betax{{beta.p[0] + sh, beta.p[1] + sh, beta.p[2] + sh}};
+    k_aligned_beta<<<node_blocks(c, gx), kThreads, 0, c->s>>>(gx, T0->base(0) + sh, op->kfc + 1 - glo, op->Tfloor,
+                                                              bx, betax, c->bad);
+    c->st.launches++;
+    TRY(check_launch("k_aligned_beta"));
+    CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    if (*c->h_bad == 1) return fail(PC_E_DOMAIN, "aligned conduction: non-positive T0 (SPEC.md:120)");
+    TRY(run_bound(op, op->ao));
+    TRY(detect_radial_rho(op));
+  } else {
+    // the face coefficient D (or nu rho) is read at the axis-0 neighbours:
+    // refresh the ghost planes of the coefficient fields
+    if (op->so.D) {
+      double* db[1] = {const_cast<double*>(op->so.D) - g->g.plane};
+      TRY(halo_exchange(c, g, db, 1));
+    }
+    if (op->so.rho) {
+      double* rb[1] = {const_cast<double*>(op->so.rho) - g->g.plane};
+      TRY(halo_exchange(c, g, rb, 1));
+    }
+    TRY(run_bound(op, op->so));
+  }
+  op->diag_valid = op->dbuf != nullptr;
+  op->line_valid = false;
+  if (op->dbuf) {
+    double* db[1] = {op->dbuf};
+    TRY(halo_exchange(c, g, db, 1));
+  }
+  op->frozen = true;
+  return PC_OK;
+}
+
+// the Jacobi diagonal is only materialised for BE / PCG / pc_op_diagonal
+static int ensure_diag(pc_op* op) {
+  if (op->diag_valid) return PC_OK;
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  if (!op->dbuf) {
+    if (!(op->dbuf = pool_get(g->ctx, g->comp_elems)))
+      return fail(PC_E_CUDA, "diagonal allocation failed (out of device memory)");
+    CUDA_TRY(cudaMemsetAsync(op->dbuf, 0, g->comp_elems * sizeof(double), c->s));
+  }
+  if (op->kind == K_ALIGNED) TRY(run_bound(op, op->ao));
+  else TRY(run_bound(op, op->so));
+  double* db[1] = {op->dbuf};
+  TRY(halo_exchange(c, g, db, 1));
+  op->diag_valid = true;
+  return PC_OK;
+}
+
+int pc_op_euler_dt(pc_op* op, double* dt) {
+  if (!op || !dt) return fail(PC_E_INVALID, "null argument");
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  *dt = op->dt_euler;
+  return PC_OK;
+}
+
+int pc_op_diagonal(pc_op* op, pc_field* out) {
+  if (!op || !out || out->ncomp != 1) return fail(PC_E_INVALID, "diagonal output must be a scalar field");
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  TRY(ensure_diag(op));
+  CUDA_TRY(cudaMemcpyAsync(out->buf[0], op->dbuf, op->grid->comp_elems * sizeof(double),
+                           cudaMemcpyDeviceToDevice, op->grid->ctx->s));
+  CUDA_TRY(cudaStreamSynchronize(op->grid->ctx->s));
+  return PC_OK;
+}
+
+// r-chunk partition of a marching launch (ctx->zpart): the interior chunks
+// (1 .. nz-2) or the two boundary chunks, whose ghost-plane reads wait for
+// the halo exchange
+static int zsplit(const pc_ctx* c, dim3& grid) {
+  const int nz = (int)grid.z;
+  if (c->zpart == 1) {
+    grid.z = nz - 2;
+    return 1;
+  }
+  if (c->zpart == 2) {
+    grid.z = nz > 1 ? 2 : 1;
+    return -nz;
+  }
+  return 0;
+}
+
+// r-chunk length of the marching aligned kernels
+static int march_R(const pc_grid* g) {
+  // r-chunk length: a block marches R planes after a one-plane prologue, so
+  // the device time is ~ ceil(blocks / resident slots) x (R + 1) plane-steps;
+  // pick the R (4 .. 128) that maximises useful plane-steps per slot-step
+  // (PC_MARCH_R overrides, for experiments)
+  if (const char* e = getenv("PC_MARCH_R")) {
+    const int r = atoi(e);
+    if (r >= 1) return r;
+  }
+  const int64_t tiles = (int64_t)((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + MTJ - 1) / MTJ);
+  const int64_t slots = (int64_t)g->ctx->sms * 2;  // 2 resident blocks per SM
+  const int n0 = g->g.n0;
+  int best = 4;
+  double best_eff = -1.0;
+  const bool slab = g->g.ghost_lo0 || g->g.ghost_hi0;  // keep >= 3 chunks: interior chunks overlap the halo exchange
+  for (int R = 4; R <= 128; R += 4) {
+    if (slab && (n0 + R - 1) / R < 3 && R > 4) continue;
+    const int64_t blocks = tiles * ((n0 + R - 1) / R);
+    const int64_t waves = (blocks + slots - 1) / slots;
+    const double eff = (double)n0 * tiles / ((double)waves * slots * (R + 1));
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = R;
+    }
+  }
+  return best;
+}
+static dim3 march_grid(const pc_grid* g, int R) {
+  return dim3((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + MTJ - 1) / MTJ, (g->g.n0 + R - 1) / R);
+}
+// ---- TMA (bulk tensor copy) maps over a field component [n0+2][n1][n2]
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static int state = 0;
+  if (state == 0) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && p) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+      state = 1;
+    } else {
+      state = -1;
+    }
+  }
+  return fn;
+}
+// base = first interior element (plane 0); the tensor starts at ghost plane -1
+static int make_field_map(CUtensorMap* m, const double* base, const GridDev& g, unsigned box0, unsigned box1) {
+  auto enc = tma_encoder();
+  if (!enc) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const double* alloc = base - g.plane;
+  cuuint64_t dims[3] = {(cuuint64_t)g.n2, (cuuint64_t)g.n1, (cuuint64_t)g.n0 + 2};
+  cuuint64_t strides[2] = {(cuuint64_t)g.n2 * 8, (cuuint64_t)g.plane * 8};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(alloc), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return PC_OK;
+}
+// interleaved per-(r, theta) metric records [n0+2][n1][12] (iL2[6], wo01[4],
+// iVal2, 0) for the TMA march: one 12 x 18 box per plane
+static int make_rows_map(pc_grid* g) {
+  auto enc = tma_encoder();
+  if (!enc) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const GridDev& d = g->g;
+  cuuint64_t dims[3] = {(cuuint64_t)RW, (cuuint64_t)d.n1, (cuuint64_t)d.n0 + 2};
+  cuuint64_t strides[2] = {(cuuint64_t)RW * 8, (cuuint64_t)d.n1 * RW * 8};
+  cuuint32_t box[3] = {(cuuint32_t)RW, (cuuint32_t)MHJ, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(&g->rowmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, g->rowrec, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled (row records) failed (" + std::to_string((int)r) + ")");
+  g->rowmap_ok = true;
+  return PC_OK;
+}
+static bool tma_ok(const pc_grid* g) {
+  const GridDev& d = g->g;
+  return d.per2 && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && tma_encoder() != nullptr &&
+         getenv("PC_NO_TMA") == nullptr;
+}
+template <class Epi, int RHO>
+static int launch_tma_t(pc_op* op, const TmaMaps& maps, const Epi& epi, const int* skip, const char* what) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int R = march_R(g);
+  dim3 grid = march_grid(g, R);
+  if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
+  const int smem = (int)sizeof(TmaSmem) + 128;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_aligned_tma<Epi, RHO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int zsel = zsplit(c, grid);
+  k_aligned_tma<Epi, RHO><<<grid, dim3(MTK, MTY), smem, c->s>>>(g->g, op->ao, maps, epi, R, zsel, skip);
+  c->st.launches++;
+  return check_launch(what);
+}
+template <class Epi>
+static int launch_tma(pc_op* op, const double* Tin, const Epi& epi, const int* skip, const char* what) {
+  pc_grid* g = op->grid;
+  TmaMaps maps;
+  if (!op->beta_maps) {
+    for (int q = 0; q < 3; ++q) {
+      TRY(make_field_map(&op->bmap[q], op->ao.beta[q], g->g, MTK, MHJ));
+      TRY(make_field_map(&op->bsmap[q], op->ao.beta[q], g->g, 2, MHJ));
+    }
+    op->beta_maps = true;
+  }
+  if (!g->rowmap_ok) {
+    TRY(make_rows_map(g));
+  }
+  for (int q = 0; q < 3; ++q) {
+    maps.B[q] = op->bmap[q];
+    maps.BS[q] = op->bsmap[q];
+  }
+  maps.RW = g->rowmap;
+  TRY(make_field_map(&maps.T, Tin, g->g, MTK, MHJ));
+  TRY(make_field_map(&maps.TS, Tin, g->g, 2, MHJ));
+  for (int q = 0; q < Epi::NOPS; ++q) TRY(make_field_map(&maps.O[q], epi.opnd(q), g->g, MTK, MTJ));
+  if (op->ao.rho && op->ao.rho_r) return launch_tma_t<Epi, 2>(op, maps, epi, skip, what);
+  if (op->ao.rho) return launch_tma_t<Epi, 1>(op, maps, epi, skip, what);
+  return launch_tma_t<Epi, 0>(op, maps, epi, skip, what);
+}
+
+template <class Epi>
+static int launch_march(pc_op* op, const double* Tin, const Epi& epi, const int* skip, const char* what) {
+  if (tma_ok(op->grid)) return launch_tma(op, Tin, epi, skip, what);
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int R = march_R(g);
+  dim3 grid = march_grid(g, R);
+  if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
+  static bool attr = false;  // one per template instantiation
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_aligned_march<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(MarchSmem)));
+    attr = true;
+  }
+  const int zsel = zsplit(c, grid);
+  k_aligned_march<Epi><<<grid, dim3(MTK, MTY), sizeof(MarchSmem), c->s>>>(g->g, op->ao, Tin, epi, R, zsel, skip);
+  c->st.launches++;
+  return check_launch(what);
+}
+
+// ---- 7-point marching kernels (ScalarOp), dispatched on (ncomp, vector, D mode)
+// r-chunk length: the longest power of two (<= 32) that still gives ~12 blocks
+// per SM (3 resident, scalar) or ~6 (2 resident, 3-component); measured on C2:
+// R = 4 / 8 / 16 / 32 -> 2.49 / 2.77 / 2.92 / 2.83e10 cell-updates/s.
+static int smarch_R(const pc_grid* g, int ncomp) {
+  if (const char* e = getenv("PC_SMARCH_R")) {
+    const int r = atoi(e);
+    if (r >= 1) return r;
+  }
+  const int tiles = ((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + SMJ - 1) / SMJ);
+  const int64_t want = ncomp == 3 ? 148 * 6 : 148 * 12;
+  int R = 32;
+  while (R > 4 && (int64_t)tiles * ((g->g.n0 + R - 1) / R) < want) R /= 2;
+  return R;
+}
+static bool smarch_ok(const pc_op* op) { return op->ncomp == 1 || op->ncomp == 3; }
+template <int NC, bool VEC, int DM, class Epi>
+static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, const char* what) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int R = smarch_R(g, NC);
+  dim3 grid((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + SMJ - 1) / SMJ, (g->g.n0 + R - 1) / R);
+  if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_scalar_march<NC, VEC, DM, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(SMarchSmem<NC>)));
+    attr = true;
+  }
+  const int zsel = zsplit(c, grid);
+  k_scalar_march<NC, VEC, DM, Epi><<<grid, SNT, sizeof(SMarchSmem<NC>), c->s>>>(g->g, op->so, u.p[0], u.p[1], u.p[2],
+                                                                                epi, R, zsel, skip);
+  c->st.launches++;
+  return check_launch(what);
+}
+template <int NC, class Epi>
+static int launch_smarch_nc(pc_op* op, CFld u, const Epi& epi, const char* what) {
+  const int dm = op->so.drho ? 2 : (op->so.D ? 1 : 0);
+  const bool vec = NC == 3 && op->so.vector;
+  if (vec) {
+    if (dm == 0) return launch_smarch_t<NC, true, 0>(op, u, epi, nullptr, what);
+    if (dm == 1) return launch_smarch_t<NC, true, 1>(op, u, epi, nullptr, what);
+    return launch_smarch_t<NC, true, 2>(op, u, epi, nullptr, what);
+  }
+  if (dm == 0) return launch_smarch_t<NC, false, 0>(op, u, epi, nullptr, what);
+  if (dm == 1) return launch_smarch_t<NC, false, 1>(op, u, epi, nullptr, what);
+  return launch_smarch_t<NC, false, 2>(op, u, epi, nullptr, what);
+}
+
+template <class Op>
+static int launch_apply(pc_op* op, const Op& o, CFld u, Fld F, bool argmax) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  int nb = node_blocks(c, g->g);
+  if (argmax) {
+    k_apply_argmax<<<nb, kThreads, 0, c->s>>>(g->g, o, u, F, c->red_v, c->red_i, c->counter, c->res);
+  } else {
+    k_apply<<<nb, kThreads, 0, c->s>>>(g->g, o, u, F);
+  }
+  c->st.launches++;
+  return check_launch("k_apply");
+}
+static int apply_any(pc_op* op, CFld u, Fld F, bool argmax) {
+  if (op->kind == K_ALIGNED) {
+    pc_ctx* c = op->grid->ctx;
+    if (argmax) {
+      EpiArgmax e{F.p[0], c->red_v, c->red_i, c->counter, c->res, ArgMax{-1.0, 0x7fffffffffffffffLL}};
+      return launch_march(op, u.p[0], e, nullptr, "k_aligned_march<argmax>");
+    }
+    return launch_march(op, u.p[0], EpiStore{F.p[0]}, nullptr, "k_aligned_march<apply>");
+  }
+  if (smarch_ok(op)) {
+    pc_ctx* c = op->grid->ctx;
+    if (argmax) {
+      SEpiArgmax e{{F.p[0], F.p[1], F.p[2]}, c->red_v, c->red_i, c->counter, c->res,
+                   ArgMax{-1.0, 0x7fffffffffffffffLL}, op->ncomp};
+      return op->ncomp == 3 ? launch_smarch_nc<3>(op, u, e, "k_scalar_march<argmax>")
+                            : launch_smarch_nc<1>(op, u, e, "k_scalar_march<argmax>");
+    }
+    SEpiStore e{{F.p[0], F.p[1], F.p[2]}};
+    return op->ncomp == 3 ? launch_smarch_nc<3>(op, u, e, "k_scalar_march<apply>")
+                          : launch_smarch_nc<1>(op, u, e, "k_scalar_march<apply>");
+  }
+  return launch_apply(op, op->so, u, F, argmax);
+}
+
+static int need_frozen(pc_op* op) {
+  if (op->kind == K_ALIGNED && !op->frozen)
+    return fail(PC_E_INVALID, "aligned operator: call pc_op_freeze(T0) first (lagged diffusivity)");
+  if (!op->frozen) return pc_op_freeze(op, nullptr);  // scalar: coefficient ghost planes + bound
+  return PC_OK;
+}
+
+int pc_op_apply(pc_op* op, const pc_field* u, pc_field* F) {
+  if (!op || !u || !F || u->ncomp != op->ncomp || F->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  TRY(need_frozen(op));
+  TRY(halo_field(const_cast<pc_field*>(u)));
+  TRY(apply_any(op, cfld(u), fld(F), false));
+  CUDA_TRY(cudaStreamSynchronize(op->grid->ctx->s));
+  return PC_OK;
+}

@@ -1,0 +1,238 @@
+// paracycle_b200 C ABI, part of the single translation unit capi.cu (included
+// there in order; relies on the declarations of the parts before it).
+//
+// C ABI: device-driven PCG (Jacobi and r-line block-Jacobi preconditioners)
+// and the backward-Euler step
+#pragma once
+
+// ------------------------------------------------------------------ PCG
+// r-slabs: finish a PCG reduction after the allreduce of the local sums
+static int pcg_split_fin(pc_ctx* c, bool split, int mode, int nred, double tol, int it) {
+  if (!split) return PC_OK;
+  TRY(allreduce_d(c, c->pcg->red, (size_t)nred, nccl::kSum));
+  k_pcg_fin<<<1, 1, 0, c->s>>>(c->pcg, mode, tol, it);
+  c->st.launches++;
+  return check_launch("k_pcg_fin");
+}
+
+// ---- r-line preconditioner
+static int line_prepare(pc_op* op, double dt, const double* adiag, Work& Lf) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  if (!op->line_valid) {
+    if (!op->lbuf && !(op->lbuf = pool_get(c, 2 * g->comp_elems)))
+      return fail(PC_E_CUDA, "line preconditioner allocation failed (out of device memory)");
+    k_line_coef<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ao, op->lbuf + g->g.plane,
+                                                             op->lbuf + g->comp_elems + g->g.plane);
+    c->st.launches++;
+    TRY(check_launch("k_line_coef"));
+    op->line_valid = true;
+  }
+  const int nbl = (int)((g->g.plane + kThreads - 1) / kThreads);
+  k_line_factor<<<nbl, kThreads, 0, c->s>>>(g->g, op->dbuf + g->g.plane, op->lbuf + g->g.plane,
+                                            op->lbuf + g->comp_elems + g->g.plane, adiag, dt, Lf.base(0), Lf.base(1));
+  c->st.launches++;
+  return check_launch("k_line_factor");
+}
+static int line_apply(pc_op* op, const double* r, Work& Lf, double dt, double* z, int mode) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int nbl = (int)((g->g.plane + kThreads - 1) / kThreads);
+  if (nbl > c->max_red) return fail(PC_E_INVALID, "too many r-lines for the reduction scratch");
+  k_line_solve<<<nbl, kThreads, 0, c->s>>>(g->g, op->ao, r, op->lbuf + g->g.plane, Lf.base(0), Lf.base(1), dt, z,
+                                           mode, c->red_v, c->counter, c->pcg);
+  c->st.launches++;
+  return check_launch("k_line_solve");
+}
+
+template <class Op>
+static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld b, pc_field* x, double tol,
+                   int max_iter, int* iters, double* relres, int* converged) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  const int nc = op->ncomp;
+  Work r, p0, p1, Ap;
+  TRY(work_get(g, nc, r));
+  TRY(work_get(g, nc, p0));
+  TRY(work_get(g, nc, p1));
+  TRY(work_get(g, nc, Ap));
+  const double* dg = op->dbuf + g->g.plane;
+  const int nb = node_blocks(c, g->g);
+  const bool line = std::is_same<Op, AlignedOp>::value && op->pc == PC_PC_LINE_R;
+  if (line && c->nranks > 1) return fail(PC_E_INVALID, "the r-line preconditioner needs the whole r line on one rank");
+  Work z, Lf;  // r-line preconditioner: z and the factorisation (inv, cp)
+  if (line) {
+    TRY(work_get(g, 1, z));
+    TRY(work_get(g, 2, Lf));
+  }
+  int rc = halo_field(x);
+  // split reductions: the kernels stop at the local sums, NCCL adds them up
+  // (the r-line preconditioner is single-rank and finishes its own reductions)
+  const bool split = c->comm != nullptr && !line;
+  if (rc == PC_OK && cudaMemsetAsync(&c->pcg->split, split ? 1 : 0, sizeof(int), c->s) != cudaSuccess)
+    rc = fail(PC_E_CUDA, "PCG state");
+  if (rc == PC_OK) {
+    if constexpr (std::is_same<Op, AlignedOp>::value) {
+      // r = b - A x0 through the marching kernel (x0 staged like any T)
+      if (adiag) {
+        EpiPcgInitT<true> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg,
+                            line};
+        rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
+      } else {
+        EpiPcgInitT<false> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg,
+                             line};
+        rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
+      }
+      if (rc == PC_OK && line) {  // z0 = M^{-1} r0, (r0, z0) -> fin_init
+        rc = line_prepare(op, dt, adiag, Lf);
+        if (rc == PC_OK) rc = line_apply(op, r.base(0), Lf, dt, z.base(0), 0);
+      }
+    } else {
+      k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, c->red_v, c->red_v2,
+                                            c->counter, c->pcg);
+      c->st.launches++;
+      rc = check_launch("k_pcg_init");
+    }
+    if (rc == PC_OK) rc = pcg_split_fin(c, split, 0, 2, tol, 0);
+  }
+  Work* pold = &p0;
+  Work* pnew = &p1;
+  const int batch = 4;
+  int it = 0;
+  bool stop = false;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->s);
+  }
+  while (rc == PC_OK && !stop && it < max_iter) {
+    for (int q = 0; q < batch && it < max_iter && rc == PC_OK; ++q) {
+      ++it;
+      if constexpr (std::is_same<Op, AlignedOp>::value) {
+        // p = z + beta p_old (beta from the device-side PCG state), then the
+        // marching matvec stages p like any other field
+        if (line)
+          k_pcg_pupdate_z<<<nb, kThreads, 0, c->s>>>(g->g, z.base(0), pold->base(0), pnew->base(0), c->pcg);
+        else
+          k_pcg_pupdate<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
+                                                   c->pcg);
+        c->st.launches++;
+        rc = check_launch("k_pcg_pupdate");
+        if (rc == PC_OK) rc = halo_work(g, *pnew);
+        if (rc) break;
+        const int* done = reinterpret_cast<const int*>(reinterpret_cast<const char*>(c->pcg) + offsetof(PcgDev, done));
+        if (adiag) {
+          EpiMatvecT<true> e{adiag, Ap.base(0), dt, c->red_v, c->counter, c->pcg};
+          rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
+        } else {
+          EpiMatvecT<false> e{adiag, Ap.base(0), dt, c->red_v, c->counter, c->pcg};
+          rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
+        }
+        if (rc == PC_OK) rc = pcg_split_fin(c, split, 1, 1, tol, it);
+        if (rc) break;
+      } else {
+        rc = halo_work(g, r);
+        if (rc == PC_OK) rc = halo_work(g, *pold);
+        if (rc) break;
+        k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
+                                                c->red_v, c->counter, c->pcg);
+        rc = check_launch("k_pcg_matvec");
+        if (rc == PC_OK) rc = pcg_split_fin(c, split, 1, 1, tol, it);
+        if (rc) break;
+      }
+      if constexpr (std::is_same<Op, AlignedOp>::value) {
+        auto upd = line ? (o.rho ? (adiag ? k_pcg_update1<true, true, true> : k_pcg_update1<true, false, true>)
+                                 : (adiag ? k_pcg_update1<false, true, true> : k_pcg_update1<false, false, true>))
+                        : (o.rho ? (adiag ? k_pcg_update1<true, true> : k_pcg_update1<true, false>)
+                                 : (adiag ? k_pcg_update1<false, true> : k_pcg_update1<false, false>));
+        upd<<<nb, kThreads, 0, c->s>>>(g->g, x->base(0), r.base(0), pnew->base(0), Ap.base(0), dg, adiag, o.rho, dt,
+                                       tol, it, c->red_v, c->red_v2, c->counter, c->pcg);
+      } else {
+        k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, tol, it,
+                                                c->red_v, c->red_v2, c->counter, c->pcg);
+      }
+      c->st.launches += std::is_same<Op, AlignedOp>::value ? 1 : 2;  // (march counted at launch)
+      c->st.stage_launches += std::is_same<Op, AlignedOp>::value ? 3 : 2;
+      rc = check_launch("k_pcg");
+      if (rc == PC_OK) rc = pcg_split_fin(c, split, 2, 2, tol, it);
+      if (rc == PC_OK && line) rc = line_apply(op, r.base(0), Lf, dt, z.base(0), 1);
+      std::swap(pold, pnew);
+    }
+    if (rc) break;
+    if (cudaMemcpyAsync(c->h_pcg, c->pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, c->s) != cudaSuccess ||
+        cudaStreamSynchronize(c->s) != cudaSuccess) {
+      rc = fail(PC_E_CUDA, "PCG state readback");
+      break;
+    }
+    if (c->h_pcg->done) stop = true;
+  }
+  const int pkind = std::is_same<Op, AlignedOp>::value ? KIND_PCG_ALIGNED : KIND_PCG_SCALAR;
+  if (c->timing) {
+    cudaEventRecord(e1, c->s);
+    c->ev.push_back({e0, e1, pkind});
+  }
+  if (rc == PC_OK) {
+    CUDA_TRY(cudaMemcpyAsync(c->h_pcg, c->pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, c->s));
+    c->st.kind_launches[pkind] += (int64_t)c->h_pcg->it * (std::is_same<Op, AlignedOp>::value ? 3 : 2);
+    c->st.kind_units[pkind] += (int64_t)c->h_pcg->it * g->g.N;
+    CUDA_TRY(cudaStreamSynchronize(c->s));
+    const PcgDev& st = *c->h_pcg;
+    *iters = st.it;
+    *relres = st.rel;
+    *converged = st.status == 1 ? 1 : 0;
+    if (st.status == 2) rc = fail(PC_E_INDEFINITE, "PCG breakdown: p^T A p <= 0 (indefinite operator)");
+    if (st.status == 3) rc = fail(PC_E_DIVERGED, "PCG divergence: non-finite residual");
+  }
+  work_put(r);
+  work_put(p0);
+  work_put(p1);
+  work_put(Ap);
+  if (line) {
+    work_put(z);
+    work_put(Lf);
+  }
+  return rc;
+}
+
+static int pcg_any(pc_op* op, double dt, const double* adiag, CFld b, pc_field* x, double tol, int max_iter,
+                   int* iters, double* relres, int* converged) {
+  TRY(ensure_diag(op));
+  if (op->kind == K_ALIGNED) return pcg_run(op, op->ao, dt, adiag, b, x, tol, max_iter, iters, relres, converged);
+  return pcg_run(op, op->so, dt, adiag, b, x, tol, max_iter, iters, relres, converged);
+}
+
+int pc_pcg_solve(pc_op* op, double dt, const pc_field* diag_a, const pc_field* b, pc_field* x, double tol,
+                 int max_iter, int* iters, double* relres, int* converged) {
+  if (!op || !b || !x || !iters || !relres || !converged) return fail(PC_E_INVALID, "null argument");
+  if (b->ncomp != op->ncomp || x->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  if (!(tol > 0.0 && tol < 1.0) || max_iter < 1) return fail(PC_E_INVALID, "need 0 < tol < 1 and max_iter >= 1");
+  TRY(need_frozen(op));
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  const double* ad = diag_a ? diag_a->base(0) : nullptr;
+  return pcg_any(op, dt, ad, cfld(b), x, tol, max_iter, iters, relres, converged);
+}
+
+static int be_step(pc_op* op, pc_field* u, double dt, double tol, int max_iter, int* iters, double* relres,
+                   int* converged) {
+  pc_grid* g = op->grid;
+  Work bw;
+  TRY(work_get(g, op->ncomp, bw));
+  int rc = PC_OK;
+  for (int q = 0; q < op->ncomp && rc == PC_OK; ++q)
+    if (cudaMemcpyAsync(bw.b[q], u->buf[q], g->comp_elems * sizeof(double), cudaMemcpyDeviceToDevice, g->ctx->s) !=
+        cudaSuccess)
+      rc = fail(PC_E_CUDA, "BE rhs copy");
+  if (rc == PC_OK) rc = pcg_any(op, dt, nullptr, bw.cf(), u, tol, max_iter, iters, relres, converged);
+  work_put(bw);
+  return rc;
+}
+
+int pc_step_be(pc_op* op, pc_field* u, double dt, double tol, int max_iter, int* iters, double* relres,
+               int* converged) {
+  if (!op || !u || u->ncomp != op->ncomp || !iters || !relres || !converged) return fail(PC_E_INVALID, "bad arguments");
+  if (!(tol > 0.0 && tol < 1.0) || max_iter < 1) return fail(PC_E_INVALID, "need 0 < tol < 1 and max_iter >= 1");
+  TRY(need_frozen(op));
+  if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
+  return be_step(op, u, dt, tol, max_iter, iters, relres, converged);
+}
