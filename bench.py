@@ -56,6 +56,13 @@ BYTES = {
     ("vector", "rkl2"): 120,   # 3 components x 40
     ("vector_rho", "rkl2"): 128,   # + rho (D = nu rho formed per node)
 }
+# the fused stage-1+2 launch of the 7-point march, per cell-update (two per
+# launch and cell): reads u0, y0 (+ rho); writes u2 (f12) and u1 (f12w)
+BYTES_F12 = {
+    ("scalar", "f12"): 12, ("scalar", "f12w"): 16,
+    ("vector", "f12"): 36, ("vector", "f12w"): 48,
+    ("vector_rho", "f12"): 40, ("vector_rho", "f12w"): 52,
+}
 
 CONFIG_MODEL = {
     "c1": "C1 scalar diffusion 48x48x96 spherical, dt=500 dtE",
@@ -311,17 +318,27 @@ def run_ours(args, rank, world, local_rank):
         d = kinds[kk]
         if d["ms"] > 0:
             bpc = BYTES[(bkey, kind)]
-            rows.append({"kernel": {"sts_aligned": "k_aligned_march<EpiStage>",
+            rows.append({"kernel": {"sts_aligned": "k_aligned_tma<EpiStage> (TMA march)",
                                     "sts_scalar": ("k_cycle_small<%d> (persistent cycle loop: F, argmax, stages)" % nc
                                                    if prob.dg.ncells * nc <= (1 << 21) else
                                                    "k_scalar_march<" + str(nc) + " comp, SEpiStage>"),
-                                    "pcg_aligned": ("k_pcg_pupdate_z + k_aligned_march<EpiMatvec> + k_pcg_update1 + "
+                                    "pcg_aligned": ("k_pcg_pupdate_z + k_aligned_tma<EpiMatvecT> + k_pcg_update1 + "
                                                     "k_line_solve") if kind == "be-line" else
-                                                   "k_pcg_pupdate + k_aligned_march<EpiMatvec> + k_pcg_update",
+                                                   "k_pcg_pupdate + k_aligned_tma<EpiMatvecT> + k_pcg_update1",
                                     "pcg_scalar": "k_pcg_matvec + k_pcg_update"}[kk],
                          "ms": d["ms"], "bytes_per_cell_update": bpc,
                          "achieved": bpc * d["cell_updates"] / (d["ms"] / 1e3) / 1e9,
                          "launches": d["launches"], "field": fname})
+        if op.kind != "aligned" and not kind.startswith("be"):
+            for fk in ("f12", "f12w"):
+                d = kinds["sts_" + fk]
+                if d["ms"] > 0:
+                    bpc = BYTES_F12[(bkey, fk)]
+                    rows.append({"kernel": "k_scalar_march<%d comp, SEpiStage12> (stages 1+2%s)"
+                                           % (nc, ", u1 written" if fk == "f12w" else ""),
+                                 "ms": d["ms"], "bytes_per_cell_update": bpc,
+                                 "achieved": bpc * d["cell_updates"] / (d["ms"] / 1e3) / 1e9,
+                                 "launches": d["launches"], "field": fname})
     dom = max(rows, key=lambda r: r["ms"]) if rows else None
     peak, peak_src = _peaks()
 

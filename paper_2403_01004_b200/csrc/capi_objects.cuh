@@ -29,14 +29,25 @@ static int fail(int code, const std::string& msg, int64_t info = 0) {
 // ------------------------------------------------------------------ objects
 // kinds of timed hot loops: 0 scalar/vector STS stages, 1 aligned STS stages,
 // 2 scalar PCG iterations, 3 aligned PCG iterations
-enum { KIND_STS_SCALAR = 0, KIND_STS_ALIGNED = 1, KIND_PCG_SCALAR = 2, KIND_PCG_ALIGNED = 3, NKIND = 4 };
+// timed hot loops (pc_ctx_stats_kind): STS stages k >= 2, PCG iterations, and
+// the fused stage-1+2 launch of the 7-point march without (F12, s == 2) and
+// with (F12W, s >= 3) the u1 write; F12 units count both stages
+enum {
+  KIND_STS_SCALAR = 0,
+  KIND_STS_ALIGNED = 1,
+  KIND_PCG_SCALAR = 2,
+  KIND_PCG_ALIGNED = 3,
+  KIND_STS_F12 = 4,
+  KIND_STS_F12W = 5,
+  NKIND = 6
+};
 struct Stats {
   double stage_ms = 0.0;
   int64_t stage_launches = 0;
   int64_t launches = 0;
-  double kind_ms[NKIND] = {0, 0, 0, 0};
-  int64_t kind_launches[NKIND] = {0, 0, 0, 0};
-  int64_t kind_units[NKIND] = {0, 0, 0, 0};  // cell-updates (local cells x stages / iterations)
+  double kind_ms[NKIND] = {};
+  int64_t kind_launches[NKIND] = {};
+  int64_t kind_units[NKIND] = {};  // cell-updates (local cells x stages / iterations)
 };
 struct TimedSpan {
   cudaEvent_t e0, e1;

@@ -411,11 +411,11 @@ static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, c
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(cudaFuncSetAttribute(k_scalar_march<NC, VEC, DM, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(SMarchSmem<NC>)));
+                                  (int)sizeof(SMarchSmem<NC, fuse1_of<Epi>::value>)));
     attr = true;
   }
   const int zsel = zsplit(c, grid);
-  k_scalar_march<NC, VEC, DM, Epi><<<grid, SNT, sizeof(SMarchSmem<NC>), c->s>>>(g->g, op->so, u.p[0], u.p[1], u.p[2],
+  k_scalar_march<NC, VEC, DM, Epi><<<grid, SNT, sizeof(SMarchSmem<NC, fuse1_of<Epi>::value>), c->s>>>(g->g, op->so, u.p[0], u.p[1], u.p[2],
                                                                                 epi, R, zsel, skip);
   c->st.launches++;
   return check_launch(what);

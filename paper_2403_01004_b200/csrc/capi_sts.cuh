@@ -95,15 +95,6 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
   }
   const int nb = node_blocks(c, g->g);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
-  k_stage1<<<nb, kThreads, 0, c->s>>>(g->g, nc, cfld(u), y0.cf(), A.f(), tab[3], c->bad);
-  c->st.launches++;
-  rc = check_launch("k_stage1");
-  if (c->timing) {  // the fused stage kernels k >= 2 (the roofline kernel)
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, c->s);
-  }
   Work* um1 = &A;
   Work* out = &B;
   Work* um2w = nullptr;  // nullptr -> u0
@@ -116,7 +107,55 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
   const int Rz = std::is_same<Op, AlignedOp>::value ? march_R(g) : smarch_R(g, op->ncomp);
   const int nz = (g->g.n0 + Rz - 1) / Rz;
   const bool overlap = marching && nz >= 3 && (c->comm != nullptr || force_split);
-  for (int k = 2; k <= s && rc == PC_OK; ++k) {
+  // 7-point march, one rank without ghost planes: stages 1 and 2 in one pass
+  // (SEpiStage12: u1 formed in shared memory from u0 and y0; PC_NO_FUSE12 off)
+  const bool fuse12 = !std::is_same<Op, AlignedOp>::value && smarch_ok(op) && !overlap && !g->g.ghost_lo0 &&
+                      !g->g.ghost_hi0 && getenv("PC_NO_FUSE12") == nullptr;
+  CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
+  if (fuse12) {
+    const double* r = tab + 5;
+    const StageCoef sc{r[0], r[1], r[2], r[3], r[4]};
+    CFld u0f = cfld(u), y0f = y0.cf();
+    Fld of = B.f(), af = A.f();
+    const bool w1 = s >= 3;
+    const int kind = w1 ? KIND_STS_F12W : KIND_STS_F12;
+    cudaEvent_t f0 = nullptr, f1 = nullptr;
+    if (c->timing) {
+      cudaEventCreate(&f0);
+      cudaEventCreate(&f1);
+      cudaEventRecord(f0, c->s);
+    }
+    if (nc == 3) {
+      SEpiStage12<3> e{{u0f.p[0], u0f.p[1], u0f.p[2]}, {y0f.p[0], y0f.p[1], y0f.p[2]}, {of.p[0], of.p[1], of.p[2]},
+                       {w1 ? af.p[0] : nullptr, af.p[1], af.p[2]}, tab[3], sc, c->bad};
+      rc = launch_smarch_nc<3>(op, u0f, e, "k_scalar_march<stage 1+2>");
+    } else {
+      SEpiStage12<1> e{{u0f.p[0], nullptr, nullptr}, {y0f.p[0], nullptr, nullptr}, {of.p[0], nullptr, nullptr},
+                       {w1 ? af.p[0] : nullptr, nullptr, nullptr}, tab[3], sc, c->bad};
+      rc = launch_smarch_nc<1>(op, u0f, e, "k_scalar_march<stage 1+2>");
+    }
+    if (c->timing) {
+      cudaEventRecord(f1, c->s);
+      c->ev.push_back({f0, f1, kind});
+    }
+    c->st.kind_launches[kind] += 1;
+    c->st.kind_units[kind] += 2 * g->g.N;
+    c->st.stage_launches++;
+    // rotate as after stage 2 below: u1 (A) -> u_{k-2}, u2 (B) -> u_{k-1}
+    um2w = &A;
+    um1 = &B;
+    out = &A;
+  } else {
+    k_stage1<<<nb, kThreads, 0, c->s>>>(g->g, nc, cfld(u), y0.cf(), A.f(), tab[3], c->bad);
+    c->st.launches++;
+    rc = check_launch("k_stage1");
+  }
+  if (c->timing) {  // the fused stage kernels k >= 2 (the roofline kernel)
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->s);
+  }
+  for (int k = fuse12 ? 3 : 2; k <= s && rc == PC_OK; ++k) {
     const double* r = tab + 5 * (k - 1);
     StageCoef sc{r[0], r[1], r[2], r[3], r[4]};
     CFld m2 = um2w ? um2w->cf() : cfld(u);
@@ -174,8 +213,9 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
       cudaEventRecord(e1, c->s);
       c->ev.push_back({e0, e1, kind});
     }
-    c->st.kind_launches[kind] += s - 1;
-    c->st.kind_units[kind] += (int64_t)(s - 1) * g->g.N;
+    const int nst = s - (fuse12 ? 2 : 1);
+    c->st.kind_launches[kind] += nst;
+    c->st.kind_units[kind] += (int64_t)nst * g->g.N;
   }
   if (rc == PC_OK && deferred) {
     // pc_cycle: no host sync per step -- the flag travels with the stream and

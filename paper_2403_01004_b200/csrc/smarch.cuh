@@ -35,12 +35,26 @@ constexpr int SEO = 9;               // epilogue operands staged per node (max: 
 #define SMARCH_BLOCKS(NC) ((NC) == 3 ? 2 : 3)
 #endif
 
-template <int NC>
+// F1 (fused stages 1 + 2, Epi::FUSE1): the stencil input is u1 = u0 + mt1 y0,
+// formed into U from a u0 ring (V) and a y0 ring (Y) when each plane lands;
+// the epilogue takes u0 and y0 at the node from V and Y (no operand staging)
+template <int NC, bool F1 = false>
 struct SMarchSmem {
   double V[3][NC + 1][SHP];          // planes t, t+1, t+2 (in flight); slot NC = D / rho source
   double rowt[3][SROWT][SHJ];        // row tables of planes t-1 (r- face), t, t+1 (in flight)
-  double EO[2][SEO][SNT];            // epilogue operands of planes t (read) and t+1 (landing)
+  double EO[2][F1 ? 1 : SEO][SNT];   // epilogue operands of planes t (read) and t+1 (landing)
   double M[4][SMJ][9];               // frame rotations t+, t-, p+, p- of the tile rows
+  double Y[F1 ? 3 : 1][F1 ? NC : 1][F1 ? SHP : 1];  // y0 ring (F1 only; V then holds u0)
+  double U[F1 ? 3 : 1][F1 ? NC : 1][F1 ? SHP : 1];  // u1 ring formed from V and Y (F1 only)
+};
+
+template <class E, class = void>
+struct fuse1_of {
+  static constexpr bool value = false;
+};
+template <class E>
+struct fuse1_of<E, std::void_t<decltype(E::FUSE1)>> {
+  static constexpr bool value = E::FUSE1;
 };
 
 // DM: 0 = D constant Dc, 1 = D nodal field, 2 = D = Dc * rho (viscosity)
@@ -49,8 +63,9 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
                                                          const double* __restrict__ u1p,
                                                          const double* __restrict__ u2p, Epi epi, int R, int zsel,
                                                          const int* skip) {
+  constexpr bool F1 = fuse1_of<Epi>::value;
   extern __shared__ __align__(16) unsigned char smarch_smem[];
-  SMarchSmem<NC>& S = *reinterpret_cast<SMarchSmem<NC>*>(smarch_smem);
+  SMarchSmem<NC, F1>& S = *reinterpret_cast<SMarchSmem<NC, F1>*>(smarch_smem);
   if (skip && *skip) return;
   constexpr bool HASD = DM != 0;
   const double* uin[3] = {u0p, u1p, u2p};
@@ -62,6 +77,7 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
   const int kg = k0 + tx, jg = j0 + ty;
 
   int foff[SNFILL];
+  unsigned pinfill = 0;  // F1: fill element q sits on a theta/phi Dirichlet node (u1 = u0 there)
 #pragma unroll
   for (int q = 0; q < SNFILL; ++q) {
     const int e = tid + q * SNT;
@@ -69,6 +85,9 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
     bool oj, ok;
     const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
     foff[q] = e < SHP ? jj * g.n2 + kk : -1;
+    if ((g.pin_lo1 && jj == 0) || (g.pin_hi1 && jj == g.n1 - 1) || (g.pin_lo2 && kk == 0) ||
+        (g.pin_hi2 && kk == g.n2 - 1))
+      pinfill |= 1u << q;
   }
   const bool rton = tid < SROWT * SHJ;
   const int rtab = tid / SHJ, rhj = tid - (tid / SHJ) * SHJ;
@@ -117,7 +136,33 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
 #pragma unroll
         for (int c = 0; c < NC; ++c) cp_async8(&S.V[sl][c][e], uin[c] + base + foff[q]);
         if (HASD) cp_async8(&S.V[sl][NC][e], dsrc + base + foff[q]);
+        if constexpr (F1) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) cp_async8(&S.Y[sl][c][e], epi.y0[c] + base + foff[q]);
+        }
       }
+  };
+  // F1: u1 = pin ? u0 : u0 + mt1 y0 (k_stage1's expression) over the elements
+  // this thread staged for plane p, after its own cp.async group completed
+  // (the block barrier that follows publishes them)
+  auto form_u1 = [&](int p) {
+    if constexpr (F1) {
+      const PlaneMap pm = plane_map(g, p);
+      const int ig = pm.mem + g.i0g;
+      const bool ppin = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
+      const int sl = vslot(p);
+#pragma unroll
+      for (int q = 0; q < SNFILL; ++q)
+        if (foff[q] >= 0) {
+          const int e = tid + q * SNT;
+          const bool pn = ppin || ((pinfill >> q) & 1u);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double a = S.V[sl][c][e];
+            S.U[sl][c][e] = pn ? a : a + epi.mt1 * S.Y[sl][c][e];
+          }
+        }
+    }
   };
   auto issue_rows = [&](int p) {
     if (rton) {
@@ -125,8 +170,13 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       cp_async8(&S.rowt[rslot(p)][rtab][rhj], rbase + row2(g, pm.row, rjj));
     }
   };
+  // stencil input of component c at ring slot sl, element e
+  auto uat = [&](int sl, int c, int e) -> double {
+    if constexpr (F1) return S.U[sl][c][e];
+    else return S.V[sl][c][e];
+  };
   auto issue_ops = [&](int p) {
-    if (Epi::NOPS > 0 && inside) {
+    if (!F1 && Epi::NOPS > 0 && inside) {
       const int64_t o = (int64_t)p * g.plane + onode;
       const int es = eslot(p);
 #pragma unroll
@@ -143,6 +193,9 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
   issue_ops(i0);
   cp_async_commit();
   cp_async_wait<0>();
+  form_u1(i0 - 1);
+  form_u1(i0);
+  if (i0 + 1 <= iend) form_u1(i0 + 1);
   __syncthreads();
 
   double vm[NC], vc[NC], dm = 0.0, dc = 0.0;
@@ -150,8 +203,8 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
     const int s0 = vslot(i0 - 1), s1 = vslot(i0);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      vm[c] = S.V[s0][c][h];
-      vc[c] = S.V[s1][c][h];
+      vm[c] = uat(s0, c, h);
+      vc[c] = uat(s1, c, h);
     }
     if (HASD) {
       dm = S.V[s0][NC][h];
@@ -175,7 +228,7 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
     const bool okim = pmm.exists;  // r- neighbour exists
     double vp[NC], dp = 0.0;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) vp[c] = S.V[sp][c][h];
+    for (int c = 0; c < NC; ++c) vp[c] = uat(sp, c, h);
     if (HASD) dp = S.V[sp][NC][h];
     if (inside) {
       const int ig = t + g.i0g;
@@ -195,10 +248,10 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       for (int c = 0; c < NC; ++c) {
         nv[0][0][c] = vm[c];
         nv[0][1][c] = vp[c];
-        nv[1][0][c] = S.V[sc][c][h - MHK];
-        nv[1][1][c] = S.V[sc][c][h + MHK];
-        nv[2][0][c] = S.V[sc][c][h - 1];
-        nv[2][1][c] = S.V[sc][c][h + 1];
+        nv[1][0][c] = uat(sc, c, h - MHK);
+        nv[1][1][c] = uat(sc, c, h + MHK);
+        nv[2][0][c] = uat(sc, c, h - 1);
+        nv[2][1][c] = uat(sc, c, h + 1);
       }
       if (HASD) {
         nd[0][0] = dm;
@@ -250,7 +303,15 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       }
       double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
 #pragma unroll
-      for (int q = 0; q < Epi::NOPS; ++q) ov[q] = S.EO[es][q][tid];
+      for (int q = 0; q < Epi::NOPS; ++q)
+        if constexpr (!F1) ov[q] = S.EO[es][q][tid];
+      if constexpr (F1) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          ov[2 * c] = S.V[sc][c][h];
+          ov[2 * c + 1] = S.Y[sc][c][h];
+        }
+      }
       epi.template apply<NC>(g, t, jg, kg, o, f, vc, pin, ov);
     }
 #pragma unroll
@@ -263,6 +324,7 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       dc = dp;
     }
     cp_async_wait<0>();
+    if (t + 2 <= iend) form_u1(t + 2);
     __syncthreads();
   }
   epi.finish(g);
@@ -316,6 +378,40 @@ struct SEpiStage {
 // one-component variant (only 3 operand slots are staged)
 struct SEpiStage1 : SEpiStage {
   static constexpr int NOPS = 3;
+};
+
+// stages 1 and 2 in one pass (FUSE1): the kernel stages u0 and y0 and forms
+// u1 = u0 + mt1 y0 as each plane lands, so F(u1) never needs u1 in HBM; the
+// epilogue writes u2 = mu2 u1 + nu2 u0 + kap2 u0 + mt2 F(u1) + gt2 y0 (k_stage
+// with u_{k-2} = u0) and, when stage 3 follows, u1 itself (its u_{k-2}).
+// Non-finite u1 flags stage 1, non-finite u2 stage 2 (as the two launches did).
+template <int NCX>
+struct SEpiStage12 {
+  static constexpr bool FUSE1 = true;
+  static constexpr int NOPS = 2 * NCX;  // u0[c], y0[c] at the node
+  const double* u0[3];
+  const double* y0[3];
+  double* out[3];
+  double* u1out[3];  // nullptr: s == 2, u1 is not needed after this pass
+  double mt1;
+  StageCoef sc;
+  int* bad;
+  __host__ __device__ __forceinline__ const double* opnd(int q) const { return (q & 1) ? y0[q >> 1] : u0[q >> 1]; }
+  template <int NC>
+  __device__ __forceinline__ void apply(const GridDev&, int, int, int, int64_t o, const double (&f)[NC],
+                                        const double (&u1)[NC], bool pin, const double* ov) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double a0 = ov[2 * c];
+      if (u1out[0]) u1out[c][o] = u1[c];
+      if (!isfinite(u1[c])) atomicMin(bad, 1);
+      double v = ((((sc.mu * u1[c]) + (sc.nu * a0)) + (sc.kap * a0)) + (sc.mtdt * f[c])) + (sc.gtdt * ov[2 * c + 1]);
+      v = pin ? a0 : v;
+      out[c][o] = v;
+      if (!isfinite(v)) atomicMin(bad, 2);
+    }
+  }
+  __device__ __forceinline__ void finish(const GridDev&) {}
 };
 
 struct SEpiArgmax {  // y0 = F(u0) with the |F| argmax over points x components (PTL)

@@ -72,7 +72,9 @@ class Context:
         _lib.lib().pc_ctx_stats(self.handle, byref(ms), byref(sl), byref(tot))
         return {"stage_ms": ms.value, "stage_launches": sl.value, "launches": tot.value}
 
-    KINDS = ("sts_scalar", "sts_aligned", "pcg_scalar", "pcg_aligned")
+    # sts_f12 / sts_f12w: the fused stage-1+2 launch of the 7-point march
+    # (without / with the u1 write); their cell-updates count both stages
+    KINDS = ("sts_scalar", "sts_aligned", "pcg_scalar", "pcg_aligned", "sts_f12", "sts_f12w")
 
     def stats_by_kind(self):
         """{kind: {ms, launches, cell_updates}} of the timed hot loops."""
