@@ -106,17 +106,26 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
     cudaEventCreate(&e1);
     cudaEventRecord(e0, c->s);
   }
+  // 128-bit p-update and x/r-update kernels when phi rows have even length
+  // (every field then stays 16-byte aligned: plane and row offsets are even);
+  // C4 update 2.72 -> 2.03 ms (profiles/r01_c4_pcg_vec.txt).  PC_PCG_SCALAR_IO
+  // keeps the 64-bit kernels (tests compare the two)
+  const bool vio = g->g.n2 % 2 == 0 && getenv("PC_PCG_SCALAR_IO") == nullptr;
   while (rc == PC_OK && !stop && it < max_iter) {
     for (int q = 0; q < batch && it < max_iter && rc == PC_OK; ++q) {
       ++it;
       if constexpr (std::is_same<Op, AlignedOp>::value) {
         // p = z + beta p_old (beta from the device-side PCG state), then the
         // marching matvec stages p like any other field
-        if (line)
+        if (line) {
           k_pcg_pupdate_z<<<nb, kThreads, 0, c->s>>>(g->g, z.base(0), pold->base(0), pnew->base(0), c->pcg);
-        else
+        } else if (vio) {
+          k_pcg_pupdatev<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
+                                                    c->pcg);
+        } else {
           k_pcg_pupdate<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
                                                    c->pcg);
+        }
         c->st.launches++;
         rc = check_launch("k_pcg_pupdate");
         if (rc == PC_OK) rc = halo_work(g, *pnew);
@@ -142,10 +151,16 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         if (rc) break;
       }
       if constexpr (std::is_same<Op, AlignedOp>::value) {
-        auto upd = line ? (o.rho ? (adiag ? k_pcg_update1<true, true, true> : k_pcg_update1<true, false, true>)
-                                 : (adiag ? k_pcg_update1<false, true, true> : k_pcg_update1<false, false, true>))
-                        : (o.rho ? (adiag ? k_pcg_update1<true, true> : k_pcg_update1<true, false>)
-                                 : (adiag ? k_pcg_update1<false, true> : k_pcg_update1<false, false>));
+        auto upd = vio
+                       ? (line ? (o.rho ? (adiag ? k_pcg_update1v<true, true, true> : k_pcg_update1v<true, false, true>)
+                                        : (adiag ? k_pcg_update1v<false, true, true>
+                                                 : k_pcg_update1v<false, false, true>))
+                               : (o.rho ? (adiag ? k_pcg_update1v<true, true> : k_pcg_update1v<true, false>)
+                                        : (adiag ? k_pcg_update1v<false, true> : k_pcg_update1v<false, false>)))
+                       : (line ? (o.rho ? (adiag ? k_pcg_update1<true, true, true> : k_pcg_update1<true, false, true>)
+                                       : (adiag ? k_pcg_update1<false, true, true> : k_pcg_update1<false, false, true>))
+                              : (o.rho ? (adiag ? k_pcg_update1<true, true> : k_pcg_update1<true, false>)
+                                       : (adiag ? k_pcg_update1<false, true> : k_pcg_update1<false, false>)));
         upd<<<nb, kThreads, 0, c->s>>>(g->g, x->base(0), r.base(0), pnew->base(0), Ap.base(0), dg, adiag, o.rho, dt,
                                        tol, it, c->red_v, c->red_v2, c->counter, c->pcg);
       } else {

@@ -363,6 +363,42 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const doubl
   }
 }
 
+// k_pcg_pupdate with 128-bit accesses (n2 even): two phi pairs per lane
+__global__ void __launch_bounds__(kThreads) k_pcg_pupdatev(GridDev g, const double* __restrict__ r,
+                                                           const double* __restrict__ pold, double* __restrict__ pnew,
+                                                           const double* __restrict__ dg,
+                                                           const double* __restrict__ adiag, double dt,
+                                                           const PcgDev* st) {
+  if (st->done) return;
+  const double beta = st->beta;
+  const int lane = threadIdx.x & 31;
+  const int nrows = g.n0 * g.n1;
+  for (int row = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < nrows; row += gridDim.x * (kThreads / 32)) {
+    const int64_t base = (int64_t)(row / g.n1) * g.plane + (int64_t)(row % g.n1) * g.n2;
+    for (int k0 = 2 * lane; k0 < g.n2; k0 += 128) {
+      double2 rv[2], pv[2], dv[2], mv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t o = base + k0 + 64 * u;
+        if (k0 + 64 * u < g.n2) {
+          rv[u] = __ldg(reinterpret_cast<const double2*>(r + o));
+          pv[u] = __ldg(reinterpret_cast<const double2*>(pold + o));
+          dv[u] = __ldg(reinterpret_cast<const double2*>(dg + o));
+          mv[u] = adiag ? __ldg(reinterpret_cast<const double2*>(adiag + o)) : make_double2(1.0, 1.0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t o = base + k0 + 64 * u;
+        if (k0 + 64 * u < g.n2) {
+          const double z0 = rv[u].x / (mv[u].x + dt * dv[u].x), z1 = rv[u].y / (mv[u].y + dt * dv[u].y);
+          *reinterpret_cast<double2*>(pnew + o) = make_double2(z0 + beta * pv[u].x, z1 + beta * pv[u].y);
+        }
+      }
+    }
+  }
+}
+
 // K8 for one-component operators (the aligned PCG): x += alpha p,
 // r -= alpha Ap, partial (W r, r), (W r, z), z = r / (a + dt d).  One warp per
 // (r, theta) row (the row weight Val2 read once), four phi nodes per lane in
@@ -418,6 +454,101 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
             const double dvec = mv[u] + dt * dv[u];
             s2 += (wv[u] * rn) * (rn / dvec);
           }
+        }
+      }
+    }
+  }
+  s1 = block_sum<kThreads>(s1, sh);
+  s2 = block_sum<kThreads>(s2, sh);
+  if (threadIdx.x == 0) {
+    p1[blockIdx.x] = s1;
+    p2[blockIdx.x] = s2;
+  }
+  if (last_block(counter)) {
+    double a = 0.0, b = 0.0;
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += kThreads) {
+      a += p1[t];
+      b += p2[t];
+    }
+    const double rr = block_sum<kThreads>(a, sh);
+    const double rzn = block_sum<kThreads>(b, sh);
+    if (threadIdx.x == 0) {
+      if (LINE) {
+        pcg_fin_rr(st, rr, tol, it);
+      } else if (st->split) {
+        st->red[0] = rr;
+        st->red[1] = rzn;
+      } else {
+        pcg_fin_update(st, rr, rzn, tol, it);
+      }
+      *counter = 0u;
+    }
+  }
+}
+
+// k_pcg_update1 with 128-bit accesses: n2 even, each lane owns U phi pairs
+// (k, k+1), (k+64, k+65), ... -- half the load/store instructions per node.  Same per-node expressions; the per-thread partial sums
+// take the nodes in a different order (the final sum stays fixed-order).
+template <bool RHO, bool ADIAG, bool LINE = false, int U = 2>
+__global__ void __launch_bounds__(kThreads, U == 1 ? 4 : 2) k_pcg_update1v(GridDev g, double* __restrict__ x, double* __restrict__ r,
+                                                           const double* __restrict__ p,
+                                                           const double* __restrict__ Ap,
+                                                           const double* __restrict__ dg,
+                                                           const double* __restrict__ adiag,
+                                                           const double* __restrict__ rho, double dt, double tol,
+                                                           int it, double* p1, double* p2, unsigned int* counter,
+                                                           PcgDev* st) {
+  __shared__ double sh[kThreads / 32];
+  if (st->done) return;
+  const double alpha = st->alpha;
+  const int lane = threadIdx.x & 31;
+  double s1 = 0.0, s2 = 0.0;
+  const int nrows = g.n0 * g.n1;
+  for (int row = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < nrows; row += gridDim.x * (kThreads / 32)) {
+    const int i = row / g.n1, j = row - i * g.n1;
+    const double V2 = __ldg(g.Val2 + row2(g, i, j));
+    const int64_t base = (int64_t)i * g.plane + (int64_t)j * g.n2;
+    for (int k0 = 2 * lane; k0 < g.n2; k0 += 64 * U) {
+      double2 xv[U], pv[U], rv[U], av[U], dv[U], mv[U], rh[U];
+      double wv[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + 64 * u;
+        if (k < g.n2) {
+          const int64_t o = base + k;
+          xv[u] = *reinterpret_cast<const double2*>(x + o);
+          pv[u] = __ldg(reinterpret_cast<const double2*>(p + o));
+          rv[u] = *reinterpret_cast<const double2*>(r + o);
+          av[u] = __ldg(reinterpret_cast<const double2*>(Ap + o));
+          dv[u] = LINE ? make_double2(0.0, 0.0) : __ldg(reinterpret_cast<const double2*>(dg + o));
+          mv[u] = ADIAG ? __ldg(reinterpret_cast<const double2*>(adiag + o)) : make_double2(1.0, 1.0);
+          rh[u] = RHO ? __ldg(reinterpret_cast<const double2*>(rho + o)) : make_double2(1.0, 1.0);
+          wv[u][0] = __ldg(g.Valg + k);
+          wv[u][1] = __ldg(g.Valg + k + 1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + 64 * u;
+        if (k < g.n2) {
+          const int64_t o = base + k;
+          const double xa[2] = {xv[u].x, xv[u].y}, pa[2] = {pv[u].x, pv[u].y}, ra[2] = {rv[u].x, rv[u].y};
+          const double aa[2] = {av[u].x, av[u].y}, da[2] = {dv[u].x, dv[u].y}, ma[2] = {mv[u].x, mv[u].y};
+          const double ha[2] = {rh[u].x, rh[u].y};
+          double xn[2], rn[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double w = RHO ? ha[e] * (V2 * wv[u][e]) : V2 * wv[u][e];
+            xn[e] = xa[e] + alpha * pa[e];
+            rn[e] = ra[e] - alpha * aa[e];
+            s1 += (w * rn[e]) * rn[e];
+            if (!LINE) {
+              const double dvec = ma[e] + dt * da[e];
+              s2 += (w * rn[e]) * (rn[e] / dvec);
+            }
+          }
+          *reinterpret_cast<double2*>(x + o) = make_double2(xn[0], xn[1]);
+          *reinterpret_cast<double2*>(r + o) = make_double2(rn[0], rn[1]);
         }
       }
     }

@@ -61,6 +61,41 @@ def test_aligned_be_pcg_parity(gpu_ctx, c3s):
     assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-10
 
 
+@pytest.mark.parametrize("pc", ["jacobi", "line-r"])
+@pytest.mark.parametrize("rho", [False, True])
+def test_aligned_be_128bit_pcg_kernels(gpu_ctx, c3s, monkeypatch, pc, rho):
+    """The 128-bit p-update / x,r-update kernels (n2 even, the default) and
+    the 64-bit ones (PC_PCG_SCALAR_IO): same iteration counts, fields within
+    the PCG tolerance contract (the partial sums take nodes in another order),
+    both against the oracle."""
+    w = c3s
+    assert w.grid.shape[2] % 2 == 0
+    rr = np.exp(-2.0 * (np.asarray(w.grid.coords[0]) - 1.0))
+    rho_a = np.broadcast_to(rr[:, None, None], tuple(w.grid.shape)) * (
+        1.0 + 0.05 * np.random.default_rng(3).random(tuple(w.grid.shape))) if rho else None
+    T = operators.Field(w.grid, w.fields["T"])
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("PC_PCG_SCALAR_IO", env)
+        cfg = operators.AlignedConductionConfig(b_hat=w.fields["b"], rho=rho_a, m_p=3.0, k_B=1.0, bc=w.bc)
+        op = operators.DiffusionOperator.aligned(cfg, T)
+        dtE = op.device_op(w.grid, 1).dt_euler
+        o, rep = ptl.cycle_operator(op, schemes.SchemeConfig("backward_euler", tol=1e-9, preconditioner=pc), T,
+                                    1e4 * dtE)
+        outs.append((o.values[..., 0].copy(), [e.iters for e in rep.entries]))
+    assert outs[0][1] == outs[1][1]
+    a, b = outs
+    assert np.linalg.norm(a[0] - b[0]) / np.linalg.norm(b[0]) <= 1e-12
+    oop = oracle_aligned(w.grid, w.bc, w.fields["b"], w.fields["T"], rho=rho_a)
+    sch = optl.OracleScheme("backward_euler", tol=1e-9)
+    if pc == "line-r":
+        sch.preconditioner = "line-r"
+    uo, repo = optl.cycle_operator(oop, sch, soa(w.fields["T"][..., None]), 1e4 * dtE, dt_euler=dtE)
+    assert a[1] == [r.iters for r in repo]
+    assert np.linalg.norm(a[0] - uo[0]) / np.linalg.norm(uo[0]) <= 1e-10
+
+
 @pytest.fixture(scope="module")
 def c2s():
     return configs.c2(n=(20, 24, 48))
