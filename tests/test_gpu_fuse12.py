@@ -114,3 +114,30 @@ def test_fused_blowup_names_stage_one(gpu_ctx, monkeypatch, r):
             schemes.step_rkl2(op, mesh.Field(w.grid, u), r * dtE, dtE)
         stages.append(ei.value.stage)
     assert stages == [1, 1]
+
+
+@pytest.mark.parametrize("kind", ["scalar", "scalar_D", "vector", "vector_rho"])
+def test_persistent_cycle_bitwise_with_fused_host_loop(gpu_ctx, monkeypatch, kind):
+    """The persistent small-grid cycle kernel (separate stage-1 pass) and the
+    host-driven loop with the fused stage-1+2 march (PC_NO_PERSIST): the same
+    bits and reports as each other and as the oracle, with PTL (s = 2) and
+    without (s >= 3)."""
+    w = _case(kind)
+    op, oop, u, nc = _ops(w, kind)
+    dtE = op.device_op(w.grid, nc).dt_euler
+    for use_ptl in (True, False):
+        outs = []
+        for env in (None, "1"):
+            if env:
+                monkeypatch.setenv("PC_NO_PERSIST", env)
+            else:
+                monkeypatch.delenv("PC_NO_PERSIST", raising=False)
+            o, rep = ptl.cycle_operator(op, schemes.SchemeConfig("rkl2"), mesh.Field(w.grid, u), 300 * dtE,
+                                        ptl.PtlConfig(enabled=use_ptl))
+            outs.append((o.values.copy(), [(e.iters, e.dt, e.limited) for e in rep.entries]))
+        assert outs[0][1] == outs[1][1]
+        assert np.array_equal(outs[0][0], outs[1][0])
+        uo, repo = optl.cycle_operator(oop, optl.OracleScheme("rkl2"), soa(u), 300 * dtE, dt_euler=dtE,
+                                       use_ptl=use_ptl)
+        assert [it for it, _, _ in outs[0][1]] == [r.iters for r in repo]
+        assert np.array_equal(np.moveaxis(outs[0][0], -1, 0), uo)
