@@ -30,10 +30,20 @@ static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme,
   TRY(work_get(g, nc, B));
   TRY(work_get(g, nc, y0));
   const int64_t cap = std::max<int64_t>(0, std::min<int64_t>(rec_cap, max_cycles));
-  pc_cycle_record* drec = nullptr;
+  // device cycle records: a grow-only buffer kept by the context (a
+  // cudaMalloc / cudaFree pair per call synchronises the device and cost up
+  // to tens of ms at random, profiles/r01_c1_persist_variants.txt)
   int rc = PC_OK;
-  if (cap > 0 && cudaMalloc(&drec, (size_t)cap * sizeof(pc_cycle_record)) != cudaSuccess)
-    rc = fail(PC_E_CUDA, "cycle record allocation failed");
+  if (cap > c->cyc_rec_cap) {
+    if (c->cyc_rec) cudaFree(c->cyc_rec);
+    c->cyc_rec = nullptr;
+    c->cyc_rec_cap = 0;
+    if (cudaMalloc(&c->cyc_rec, (size_t)cap * sizeof(pc_cycle_record)) != cudaSuccess)
+      rc = fail(PC_E_CUDA, "cycle record allocation failed");
+    else
+      c->cyc_rec_cap = cap;
+  }
+  pc_cycle_record* drec = cap > 0 ? c->cyc_rec : nullptr;
   CycleDev& h = *c->h_cyc;
   std::memset(&h, 0, offsetof(CycleDev, tab));
   h.remaining = outer_dt;
@@ -107,7 +117,7 @@ static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme,
     else if (h.status == 3) rc = fail(PC_E_CAP, "max_cycles reached (partial report returned)", h.cyc);
     else if (h.status == 4) rc = fail(PC_E_INVALID, "STS stage count above the persistent kernel's table");
   }
-  if (drec) cudaFree(drec);
+
   work_put(A);
   work_put(B);
   work_put(y0);

@@ -83,6 +83,7 @@ int pc_ctx_destroy(pc_ctx* c) {
   if (c) {
     if (c->sc) cudaStreamDestroy(c->sc);
     if (c->cyc_dev) cudaFree(c->cyc_dev);
+    if (c->cyc_rec) cudaFree(c->cyc_rec);
     if (c->h_cyc) cudaFreeHost(c->h_cyc);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);

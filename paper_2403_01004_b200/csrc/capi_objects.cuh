@@ -83,6 +83,8 @@ struct pc_ctx {
   int* h_bad = nullptr;
   bool bad_pending = false;  // pc_cycle: the last STS step's non-finite flag is in flight to h_bad
   CycleDev* cyc_dev = nullptr;      // persistent small-grid cycle state (allocated on first use)
+  pc_cycle_record* cyc_rec = nullptr;  // its device cycle records (grow-only)
+  int64_t cyc_rec_cap = 0;
   CycleDev* h_cyc = nullptr;
   unsigned long long* h_minbits = nullptr;
   double* h_maxout = nullptr;

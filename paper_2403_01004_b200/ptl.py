@@ -131,6 +131,18 @@ def _report(recs, n, dt_euler, outer_step=0):
     return rep
 
 
+_RECS = {}
+
+
+def _record_buffer(cap: int):
+    """A reused ctypes array of ``cap`` cycle records (the report copies the
+    values out, so one buffer per size serves every call)."""
+    buf = _RECS.get(cap)
+    if buf is None:
+        buf = _RECS[cap] = (_lib.CycleRecord * cap)()
+    return buf
+
+
 def cycle_operator(op, scheme, u, outer_dt: float, cfg: PtlConfig | None = None, *, dt_euler: float | None = None,
                    outer_step: int = 0, ctx: device.Context | None = None, record_cap: int = 1 << 16):
     """Advance ``u`` over ``outer_dt`` with PTL cycling.
@@ -152,7 +164,7 @@ def cycle_operator(op, scheme, u, outer_dt: float, cfg: PtlConfig | None = None,
         dop = op.device_op(u.grid, u.n_components, ctx)
         du = device.DeviceField.from_values(dop.dgrid, u.values)
         host = True
-    recs = (_lib.CycleRecord * record_cap)()
+    recs = _record_buffer(record_cap)
     n = c_int64()
     floor_mode = _lib.FLOOR_EULER if cfg.dt_floor_mode == "clamp-to-euler" else _lib.FLOOR_FRACTION
     dtE = float(dt_euler) if dt_euler is not None else -1.0
