@@ -81,8 +81,8 @@ static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme,
     void* args[] = {&gd, &so, &pb, &csp, &drec};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
+      e0 = ev_new(c);
+      e1 = ev_new(c);
       cudaEventRecord(e0, c->s);
     }
     if (cudaLaunchCooperativeKernel((void*)kern, dim3(nblk), dim3(kPersistThreads), args, 0, c->s) != cudaSuccess)

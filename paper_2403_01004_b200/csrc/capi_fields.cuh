@@ -96,6 +96,7 @@ int pc_ctx_destroy(pc_ctx* c) {
     cudaEventDestroy(e.e0);
     cudaEventDestroy(e.e1);
   }
+  for (auto e : c->ev_free) cudaEventDestroy(e);
   if (c->comm) {
     nccl::Api* A = nccl::api();
     if (A) A->commDestroy(c->comm);
@@ -159,8 +160,8 @@ static void flush_events(pc_ctx* c) {
     cudaEventElapsedTime(&ms, e.e0, e.e1);
     c->st.stage_ms += ms;
     c->st.kind_ms[e.kind] += ms;
-    cudaEventDestroy(e.e0);
-    cudaEventDestroy(e.e1);
+    c->ev_free.push_back(e.e0);
+    c->ev_free.push_back(e.e1);
   }
   c->ev.clear();
 }

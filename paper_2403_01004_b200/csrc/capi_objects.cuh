@@ -96,6 +96,7 @@ struct pc_ctx {
   Stats st;
   bool timing = false;
   std::vector<TimedSpan> ev;
+  std::vector<cudaEvent_t> ev_free;  // recycled timing events (no cudaEventCreate per timed span)
   cudaEvent_t marks[16] = {};
 };
 
@@ -143,6 +144,17 @@ struct pc_op {
 };
 
 // ------------------------------------------------------------------ helpers
+// a timing event from the context's free list (created on first use)
+static cudaEvent_t ev_new(pc_ctx* c) {
+  if (!c->ev_free.empty()) {
+    cudaEvent_t e = c->ev_free.back();
+    c->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
 static int grid_blocks(pc_ctx* c, int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
   if (b < 1) b = 1;

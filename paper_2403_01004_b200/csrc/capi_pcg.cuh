@@ -102,8 +102,8 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   bool stop = false;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    e0 = ev_new(c);
+    e1 = ev_new(c);
     cudaEventRecord(e0, c->s);
   }
   // 128-bit p-update and x/r-update kernels when phi rows have even length

@@ -121,8 +121,8 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     const int kind = w1 ? KIND_STS_F12W : KIND_STS_F12;
     cudaEvent_t f0 = nullptr, f1 = nullptr;
     if (c->timing) {
-      cudaEventCreate(&f0);
-      cudaEventCreate(&f1);
+      f0 = ev_new(c);
+      f1 = ev_new(c);
       cudaEventRecord(f0, c->s);
     }
     if (nc == 3) {
@@ -151,8 +151,8 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     rc = check_launch("k_stage1");
   }
   if (c->timing) {  // the fused stage kernels k >= 2 (the roofline kernel)
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    e0 = ev_new(c);
+    e1 = ev_new(c);
     cudaEventRecord(e0, c->s);
   }
   for (int k = fuse12 ? 3 : 2; k <= s && rc == PC_OK; ++k) {
