@@ -73,6 +73,8 @@ CONFIG_MODEL = {
           "one split MAS step of 5e4 dtE",
 }
 DEFAULT_CONFIG = "c5"
+CONFIG_SHAPE = {"c1": (48, 48, 96), "c2": (128, 128, 256), "c3": (256, 256, 512), "c4": (512, 512, 1024),
+                "c5": (768, 768, 1536)}
 
 
 def _peaks():
@@ -271,7 +273,11 @@ def run_ours(args, rank, world, local_rank):
     device.set_default_context(ctx)
     name = args.config
     t_setup = time.perf_counter()
-    prob = Problem(name, ctx, None if args.n is None else tuple(int(x) for x in args.n.split(",")))
+    n_over = None if args.n is None else tuple(int(x) for x in args.n.split(","))
+    if args.weak and world > 1:  # weak scaling: the config's grid per rank, stacked in r
+        base = n_over or CONFIG_SHAPE[name]
+        n_over = (base[0] * world, base[1], base[2])
+    prob = Problem(name, ctx, n_over)
     sc = scheme_for(name, args)
     pcfg = ptl.PtlConfig()
     setup_s = time.perf_counter() - t_setup
@@ -360,7 +366,7 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup,
             "ms_per_step": ms / args.steps,
             "higher_is_better": True,
-            "scaling": "strong",
+            "scaling": "weak" if (args.weak and world > 1) else "strong",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded recipes, configs.py; generated in HBM bit-identically to the host recipe; "
@@ -621,6 +627,9 @@ def main():
     ap.add_argument("--pc", default="jacobi", choices=["jacobi", "line-r"],
                     help="BE+PCG preconditioner (default: point Jacobi, the SPEC's PC1)")
     ap.add_argument("--n", default=None, help="override the grid, e.g. 96,96,192 (smoke runs only)")
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: weak scaling, the config's grid per rank stacked in r (default: strong, the "
+                         "global grid split into r-slabs)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
