@@ -148,6 +148,29 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
   int rc = PC_OK;
   std::vector<double> tab;
   c->bad_pending = false;
+  // PC_GAP_PROFILE (diagnostic): device time per cycle of F+argmax+pairs,
+  // of the PTL read + host turnaround, and of the stages, printed at the end
+  struct GapProfile {
+    bool on = false;
+    cudaEvent_t cur[4] = {};
+    double t[3] = {0, 0, 0};
+    double host = 0.0;  // host microseconds inside sts_any
+    long n = 0;
+    void flush() {
+      cudaEventSynchronize(cur[3]);
+      float a, b, d;
+      cudaEventElapsedTime(&a, cur[0], cur[1]);
+      cudaEventElapsedTime(&b, cur[1], cur[2]);
+      cudaEventElapsedTime(&d, cur[2], cur[3]);
+      t[0] += a;
+      t[1] += b;
+      t[2] += d;
+      ++n;
+    }
+  } gp;
+  gp.on = getenv("PC_GAP_PROFILE") != nullptr;
+  if (gp.on)
+    for (auto& e : gp.cur) e = ev_new(c);
   while (remaining > 0.0) {
     if (cyc >= max_cycles) {
       if (c->bad_pending) {
@@ -158,6 +181,7 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
       rc = fail(PC_E_CAP, "max_cycles reached (partial report returned)", cyc);
       break;
     }
+    if (gp.on) cudaEventRecord(gp.cur[0], c->s);
     rc = halo_field(u);
     if (rc) break;
     rc = apply_any(op, cfld(u), y0.f(), true);
@@ -169,6 +193,7 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
     }
     double ptl;
     int limited;
+    if (gp.on) cudaEventRecord(gp.cur[1], c->s);
     rc = ptl_read(c, check_all, use_ptl, &ptl, &limited, nullptr);
     if (rc) break;
     rc = check_pending_bad(c);  // ptl_read synchronised the stream
@@ -187,7 +212,14 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
       tab.assign(5 * (size_t)s, 0.0);
       rc = pc_sts_table(scheme, s, dt, tab.data());
       if (rc) break;
+      if (gp.on) cudaEventRecord(gp.cur[2], c->s);
+      const auto h0 = std::chrono::steady_clock::now();
       rc = sts_any(op, u, tab.data(), s, y0, true);
+      if (gp.on) {
+        gp.host += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
+        cudaEventRecord(gp.cur[3], c->s);
+        gp.flush();
+      }
       iters = s;
     } else if (scheme == PC_BE) {
       int conv = 0;
@@ -221,6 +253,14 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
     else remaining = remaining - dt;
   }
   work_put(y0);
+  if (gp.on) {
+    if (gp.n)
+      fprintf(stderr,
+              "[gap] cycles %ld  per cycle us: F+argmax+pairs %.1f  read+turnaround %.1f  stages %.1f  (host in "
+              "sts %.1f)\n",
+              gp.n, 1e3 * gp.t[0] / gp.n, 1e3 * gp.t[1] / gp.n, 1e3 * gp.t[2] / gp.n, gp.host / gp.n);
+    for (auto e : gp.cur) c->ev_free.push_back(e);
+  }
   if (rc == PC_OK) {
     CUDA_TRY(cudaStreamSynchronize(c->s));
     rc = check_pending_bad(c);
