@@ -277,10 +277,21 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
           if (VEC && a > 0) {
             const double* M = S.M[(a == 1 ? 0 : 2) + (tt == 1 ? 0 : 1)][ty];
             const double v0 = nv[a][tt][0], v1 = nv[a][tt][NC > 1 ? 1 : 0], v2 = nv[a][tt][NC > 2 ? 2 : 0];
+            double rv[NC];
+            if (a == 1) {
+              // theta faces rotate about e_phi: M = [[m00 m01 0] [m10 m11 0] [0 0 1]]
+              // with exact zeros and one (geometry._rotation_tables), so the
+              // dense row sums reduce to these bits (up to the sign of a zero)
+              rv[0] = (M[0] * v0) + (M[1] * v1);
+              if (NC > 1) rv[NC > 1 ? 1 : 0] = (M[3] * v0) + (M[4] * v1);
+              if (NC > 2) rv[NC > 2 ? 2 : 0] = v2;
+            } else {
+#pragma unroll
+              for (int c = 0; c < NC; ++c) rv[c] = ((M[3 * c] * v0) + (M[3 * c + 1] * v1)) + (M[3 * c + 2] * v2);
+            }
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-              const double rv = ((M[3 * c] * v0) + (M[3 * c + 1] * v1)) + (M[3 * c + 2] * v2);
-              const double term = cf * (rv - vc[c]);
+              const double term = cf * (rv[c] - vc[c]);
               Sx[c] = first ? term : Sx[c] + term;
             }
           } else {
