@@ -112,6 +112,15 @@ int pc_field_create(pc_grid* g, int ncomp, pc_field** out);
 int pc_field_destroy(pc_field* f);
 int pc_field_upload(pc_field* f, const double* host, int layout);
 int pc_field_download(const pc_field* f, double* host, int layout);
+/* asynchronous variants on the context's copy stream (no reference
+   counterpart; they let split_advance move the next operator's state while
+   the current one computes).  They start after the work already queued on the
+   context; every later library call using the field waits for the copy on
+   the device.  The host buffer must stay valid and unchanged until
+   pc_field_wait(f) returns (or the field is destroyed, which waits). */
+int pc_field_upload_async(pc_field* f, const double* host, int layout);
+int pc_field_download_async(pc_field* f, double* host, int layout);
+int pc_field_wait(pc_field* f);
 /* axis-0 planes [i0, i0 + n) of every component, SoA [ncomp][n][n1][n2] (full-size
    parity checks read a window without moving the whole field) */
 int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* host);

@@ -71,6 +71,9 @@ _SIGS = {
     "pc_field_fill": (c_int, [c_void_p, c_double]),
     "pc_field_exchange_halo": (c_int, [c_void_p]),
     "pc_field_count": (c_int, [c_void_p, c_int, POINTER(c_int64)]),
+    "pc_field_upload_async": (c_int, [c_void_p, POINTER(c_double), c_int]),
+    "pc_field_download_async": (c_int, [c_void_p, POINTER(c_double), c_int]),
+    "pc_field_wait": (c_int, [c_void_p]),
     "pc_host_register": (c_int, [c_void_p, c_size_t]),
     "pc_host_unregister": (c_int, [c_void_p]),
     "pc_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),

@@ -127,6 +127,7 @@ static int cycle_persistent(pc_op* op, pc_field* u, double outer_dt, int scheme,
 int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, double tol, int max_iter,
              double eps_rel, int check_all, int use_ptl, int floor_mode, double floor_fraction, int64_t max_cycles,
              double dt_euler, pc_cycle_record* rec, int64_t rec_cap, int64_t* n_rec) {
+  field_dep(u);
   if (!op || !u || !n_rec || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "bad cycle arguments");
   if (!(outer_dt > 0.0)) return fail(PC_E_INVALID, "outer_dt must be > 0");
   if (max_cycles < 1 || !(eps_rel > 0.0)) return fail(PC_E_INVALID, "need max_cycles >= 1 and eps_rel > 0");

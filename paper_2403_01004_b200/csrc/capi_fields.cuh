@@ -82,6 +82,11 @@ int pc_ctx_create_detached(int device, int nranks, int rank, pc_ctx** out) {
 int pc_ctx_destroy(pc_ctx* c) {
   if (c) {
     if (c->sc) cudaStreamDestroy(c->sc);
+    if (c->cs) {
+      cudaStreamSynchronize(c->cs);
+      cudaStreamDestroy(c->cs);
+    }
+    if (c->staging_cs) cudaFree(c->staging_cs);
     if (c->cyc_dev) cudaFree(c->cyc_dev);
     if (c->cyc_rec) cudaFree(c->cyc_rec);
     if (c->h_cyc) cudaFreeHost(c->h_cyc);
@@ -311,74 +316,138 @@ int pc_field_create(pc_grid* g, int ncomp, pc_field** out) {
 
 int pc_field_destroy(pc_field* f) {
   if (!f) return PC_OK;
+  if (f->pending) cudaEventSynchronize(f->ready);  // the host side of an in-flight copy may go away next
+  f->pending = false;
+  if (f->ready) cudaEventDestroy(f->ready);
   for (int q = 0; q < f->ncomp; ++q) pool_put(f->grid->ctx, f->grid->comp_elems, f->buf[q]);
   delete f;
   return PC_OK;
 }
 
-static int ensure_staging(pc_ctx* c, size_t bytes) {
-  if (c->staging_bytes >= bytes) return PC_OK;
-  cudaStreamSynchronize(c->s);
-  cudaFree(c->staging);
-  c->staging = nullptr;
-  CUDA_TRY(cudaMalloc(&c->staging, bytes));
-  c->staging_bytes = bytes;
+// staging buffer of a stream (grow-only; the stream is drained before a regrow)
+static int ensure_staging_on(cudaStream_t st, double*& buf, size_t& have, size_t bytes) {
+  if (have >= bytes) return PC_OK;
+  cudaStreamSynchronize(st);
+  cudaFree(buf);
+  buf = nullptr;
+  have = 0;
+  CUDA_TRY(cudaMalloc(&buf, bytes));
+  have = bytes;
   return PC_OK;
 }
+static int ensure_staging(pc_ctx* c, size_t bytes) {
+  return ensure_staging_on(c->s, c->staging, c->staging_bytes, bytes);
+}
 
-int pc_field_upload(pc_field* f, const double* host, int layout) {
-  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+// host -> field on stream st (AoS components go through st's staging buffer
+// in 256 MB plane chunks and are transposed on the device)
+static int upload_on(pc_field* f, const double* host, int layout, cudaStream_t st, double*& stg, size_t& stg_bytes) {
   pc_grid* g = f->grid;
   pc_ctx* c = g->ctx;
   const size_t pl = (size_t)g->g.plane, n0 = (size_t)g->g.n0;
   if (layout == PC_LAYOUT_SOA || f->ncomp == 1) {
     for (int q = 0; q < f->ncomp; ++q)
       CUDA_TRY(cudaMemcpyAsync(f->base(q), host + (size_t)q * n0 * pl, n0 * pl * sizeof(double),
-                               cudaMemcpyHostToDevice, c->s));
+                               cudaMemcpyHostToDevice, st));
   } else {
     const size_t chunk_planes = std::max<size_t>(1, std::min<size_t>(n0, (256u << 20) / (pl * f->ncomp * 8)));
-    TRY(ensure_staging(c, chunk_planes * pl * f->ncomp * sizeof(double)));
+    TRY(ensure_staging_on(st, stg, stg_bytes, chunk_planes * pl * f->ncomp * sizeof(double)));
     for (size_t p0 = 0; p0 < n0; p0 += chunk_planes) {
       size_t np = std::min(chunk_planes, n0 - p0);
-      CUDA_TRY(cudaMemcpyAsync(c->staging, host + p0 * pl * f->ncomp, np * pl * f->ncomp * sizeof(double),
-                               cudaMemcpyHostToDevice, c->s));
-      k_aos_to_soa<<<grid_blocks(c, (int64_t)(np * pl)), kThreads, 0, c->s>>>(g->g, f->ncomp, c->staging, fld(f),
-                                                                               (int)p0, (int)np);
+      CUDA_TRY(cudaMemcpyAsync(stg, host + p0 * pl * f->ncomp, np * pl * f->ncomp * sizeof(double),
+                               cudaMemcpyHostToDevice, st));
+      k_aos_to_soa<<<grid_blocks(c, (int64_t)(np * pl)), kThreads, 0, st>>>(g->g, f->ncomp, stg, fld(f), (int)p0,
+                                                                             (int)np);
       c->st.launches++;
       TRY(check_launch("k_aos_to_soa"));
     }
   }
-  CUDA_TRY(cudaStreamSynchronize(c->s));
   return PC_OK;
 }
-
-int pc_field_download(const pc_field* f, double* host, int layout) {
-  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+static int download_on(const pc_field* f, double* host, int layout, cudaStream_t st, double*& stg,
+                       size_t& stg_bytes) {
   pc_grid* g = f->grid;
   pc_ctx* c = g->ctx;
   const size_t pl = (size_t)g->g.plane, n0 = (size_t)g->g.n0;
   if (layout == PC_LAYOUT_SOA || f->ncomp == 1) {
     for (int q = 0; q < f->ncomp; ++q)
       CUDA_TRY(cudaMemcpyAsync(host + (size_t)q * n0 * pl, f->base(q), n0 * pl * sizeof(double),
-                               cudaMemcpyDeviceToHost, c->s));
+                               cudaMemcpyDeviceToHost, st));
   } else {
     const size_t chunk_planes = std::max<size_t>(1, std::min<size_t>(n0, (256u << 20) / (pl * f->ncomp * 8)));
-    TRY(ensure_staging(c, chunk_planes * pl * f->ncomp * sizeof(double)));
+    TRY(ensure_staging_on(st, stg, stg_bytes, chunk_planes * pl * f->ncomp * sizeof(double)));
     for (size_t p0 = 0; p0 < n0; p0 += chunk_planes) {
       size_t np = std::min(chunk_planes, n0 - p0);
-      k_soa_to_aos<<<grid_blocks(c, (int64_t)(np * pl)), kThreads, 0, c->s>>>(g->g, f->ncomp, cfld(f), c->staging,
-                                                                               (int)p0, (int)np);
+      k_soa_to_aos<<<grid_blocks(c, (int64_t)(np * pl)), kThreads, 0, st>>>(g->g, f->ncomp, cfld(f), stg, (int)p0,
+                                                                             (int)np);
       c->st.launches++;
       TRY(check_launch("k_soa_to_aos"));
-      CUDA_TRY(cudaMemcpyAsync(host + p0 * pl * f->ncomp, c->staging, np * pl * f->ncomp * sizeof(double),
-                               cudaMemcpyDeviceToHost, c->s));
+      CUDA_TRY(cudaMemcpyAsync(host + p0 * pl * f->ncomp, stg, np * pl * f->ncomp * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
     }
   }
+  return PC_OK;
+}
+
+int pc_field_upload(pc_field* f, const double* host, int layout) {
+  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+  pc_ctx* c = f->grid->ctx;
+  field_dep(f);
+  TRY(upload_on(f, host, layout, c->s, c->staging, c->staging_bytes));
   CUDA_TRY(cudaStreamSynchronize(c->s));
   return PC_OK;
 }
 
+int pc_field_download(const pc_field* f, double* host, int layout) {
+  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+  pc_ctx* c = f->grid->ctx;
+  field_dep(f);
+  TRY(download_on(f, host, layout, c->s, c->staging, c->staging_bytes));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  return PC_OK;
+}
+
+// ---- asynchronous copies on the copy stream: they start after the work
+// already queued on the compute stream and the compute stream waits for them
+// only where the field is next used, so a field needed later (the next
+// operator's state) moves while the current operator computes
+static int copy_stream_begin(pc_ctx* c, pc_field* f) {
+  if (!c->cs) CUDA_TRY(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+  if (!f->ready) CUDA_TRY(cudaEventCreateWithFlags(&f->ready, cudaEventDisableTiming));
+  field_dep(f);  // an earlier copy of this field completes first (stream order on s)
+  CUDA_TRY(cudaEventRecord(c->ev_in, c->s));
+  CUDA_TRY(cudaStreamWaitEvent(c->cs, c->ev_in, 0));
+  return PC_OK;
+}
+int pc_field_upload_async(pc_field* f, const double* host, int layout) {
+  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+  pc_ctx* c = f->grid->ctx;
+  TRY(copy_stream_begin(c, f));
+  TRY(upload_on(f, host, layout, c->cs, c->staging_cs, c->staging_cs_bytes));
+  CUDA_TRY(cudaEventRecord(f->ready, c->cs));
+  f->pending = true;
+  return PC_OK;
+}
+int pc_field_download_async(pc_field* f, double* host, int layout) {
+  if (!f || !host) return fail(PC_E_INVALID, "null argument");
+  pc_ctx* c = f->grid->ctx;
+  TRY(copy_stream_begin(c, f));
+  TRY(download_on(f, host, layout, c->cs, c->staging_cs, c->staging_cs_bytes));
+  CUDA_TRY(cudaEventRecord(f->ready, c->cs));
+  f->pending = true;
+  return PC_OK;
+}
+int pc_field_wait(pc_field* f) {
+  if (!f) return fail(PC_E_INVALID, "null argument");
+  if (f->pending) {
+    CUDA_TRY(cudaEventSynchronize(f->ready));
+    f->pending = false;
+  }
+  return PC_OK;
+}
+
 int pc_field_set_ghost(pc_field* f, int side, const double* host) {
+  field_dep(f);
   if (!f || !host || (side != 0 && side != 1)) return fail(PC_E_INVALID, "bad ghost-plane arguments");
   pc_grid* g = f->grid;
   const size_t pl = (size_t)g->g.plane;
@@ -391,6 +460,7 @@ int pc_field_set_ghost(pc_field* f, int side, const double* host) {
 }
 
 int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* host) {
+  field_dep(f);
   if (!f || !host) return fail(PC_E_INVALID, "null argument");
   pc_grid* g = f->grid;
   if (i0 < 0 || n < 0 || i0 + n > g->g.n0) return fail(PC_E_INVALID, "plane window out of range");
@@ -403,6 +473,8 @@ int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* h
 }
 
 int pc_field_copy(pc_field* dst, const pc_field* src) {
+  field_dep(dst);
+  field_dep(src);
   if (!dst || !src || dst->ncomp != src->ncomp || dst->grid->comp_elems != src->grid->comp_elems)
     return fail(PC_E_INVALID, "field copy: shape mismatch");
   for (int q = 0; q < dst->ncomp; ++q)
@@ -412,6 +484,7 @@ int pc_field_copy(pc_field* dst, const pc_field* src) {
 }
 
 int pc_field_fill(pc_field* f, double v) {
+  field_dep(f);
   pc_ctx* c = f->grid->ctx;
   for (int q = 0; q < f->ncomp; ++q) {
     k_fill<<<grid_blocks(c, (int64_t)f->grid->comp_elems), kThreads, 0, c->s>>>(f->buf[q],
@@ -421,9 +494,13 @@ int pc_field_fill(pc_field* f, double v) {
   return check_launch("k_fill");
 }
 
-int pc_field_exchange_halo(pc_field* f) { return halo_field(f); }
+int pc_field_exchange_halo(pc_field* f) {
+  field_dep(f);
+  return halo_field(f);
+}
 
 int pc_field_count(const pc_field* f, int test, int64_t* count) {
+  field_dep(f);
   if (!f || !count || test < 0 || test > 2) return fail(PC_E_INVALID, "bad pc_field_count arguments");
   pc_grid* g = f->grid;
   pc_ctx* c = g->ctx;

@@ -15,6 +15,7 @@ static int upload_tmp(pc_ctx* c, const double* host, size_t n, double** dev) {
 static const double kSqrt3 = 1.7320508075688772;  // math.sqrt(3.0)
 
 int pc_gen_temperature(pc_field* T, uint64_t seed, int stream, double sigma, const double* prof) {
+  field_dep(T);
   if (!T || T->ncomp != 1 || !prof) return fail(PC_E_INVALID, "temperature: scalar field and profile needed");
   pc_grid* g = T->grid;
   pc_ctx* c = g->ctx;
@@ -31,6 +32,7 @@ int pc_gen_temperature(pc_field* T, uint64_t seed, int stream, double sigma, con
 
 int pc_gen_dipole(pc_field* b, uint64_t seed, int stream0, double eps, const double* ir3, const double* c2,
                   const double* st) {
+  field_dep(b);
   if (!b || b->ncomp != 3 || !ir3 || !c2 || !st) return fail(PC_E_INVALID, "dipole: 3-component field and tables");
   pc_grid* g = b->grid;
   pc_ctx* c = g->ctx;
@@ -51,6 +53,7 @@ int pc_gen_dipole(pc_field* b, uint64_t seed, int stream0, double eps, const dou
 }
 
 int pc_gen_harmonic(pc_field* v, const double* acc, double checker) {
+  field_dep(v);
   if (!v || !acc) return fail(PC_E_INVALID, "harmonic: field and (ncomp, n1, n2) table needed");
   pc_grid* g = v->grid;
   pc_ctx* c = g->ctx;
@@ -65,6 +68,7 @@ int pc_gen_harmonic(pc_field* v, const double* acc, double checker) {
 }
 
 int pc_gen_radial(pc_field* f, const double* tab) {
+  field_dep(f);
   if (!f || f->ncomp != 1 || !tab) return fail(PC_E_INVALID, "radial: scalar field and table needed");
   pc_grid* g = f->grid;
   pc_ctx* c = g->ctx;

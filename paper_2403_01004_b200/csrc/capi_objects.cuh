@@ -91,6 +91,10 @@ struct pc_ctx {
   // staging for AoS conversion
   double* staging = nullptr;
   size_t staging_bytes = 0;
+  // copy stream of the asynchronous uploads / downloads, and its staging
+  cudaStream_t cs = nullptr;
+  double* staging_cs = nullptr;
+  size_t staging_cs_bytes = 0;
   // workspace pool of single-component buffers
   std::vector<std::pair<size_t, double*>> pool;
   Stats st;
@@ -116,6 +120,11 @@ struct pc_field {
   int ncomp;
   double* buf[3];  // allocation base (ghost plane -1)
   double* base(int q) const { return buf[q] + grid->g.plane; }
+  // an asynchronous upload / download on the context's copy stream is in
+  // flight until `ready`; the compute stream waits for it before the field's
+  // next use (field_dep)
+  cudaEvent_t ready = nullptr;
+  mutable bool pending = false;
 };
 
 enum { K_SCALAR = 0, K_ALIGNED = 1 };
@@ -245,6 +254,14 @@ static void work_put(Work& w) {
 // swap the storage of a field with a work set (pointer rotation, no copy)
 static void swap_storage(pc_field* f, Work& w) {
   for (int q = 0; q < f->ncomp; ++q) std::swap(f->buf[q], w.b[q]);
+}
+
+// the compute stream waits for a field's in-flight asynchronous copy
+static void field_dep(const pc_field* f) {
+  if (f && f->pending) {
+    cudaStreamWaitEvent(f->grid->ctx->s, f->ready, 0);
+    f->pending = false;
+  }
 }
 
 static int check_launch(const char* what) {

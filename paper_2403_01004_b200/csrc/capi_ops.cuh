@@ -9,6 +9,7 @@
 // ------------------------------------------------------------------ operators
 int pc_op_create_scalar(pc_grid* g, int ncomp, int vector_metric, double D_const, const pc_field* D,
                         const pc_field* rho, pc_op** out) {
+  field_dep(D); field_dep(rho);
   if (!g || !out || ncomp < 1 || ncomp > 3) return fail(PC_E_INVALID, "bad scalar operator arguments");
   if (vector_metric && ncomp != 3) return fail(PC_E_INVALID, "vector metric needs 3 components");
   if ((D && D->ncomp != 1) || (rho && rho->ncomp != 1)) return fail(PC_E_INVALID, "D and rho are scalar fields");
@@ -27,6 +28,7 @@ int pc_op_create_scalar(pc_grid* g, int ncomp, int vector_metric, double D_const
 }
 
 int pc_op_create_viscous(pc_grid* g, int ncomp, int vector_metric, double nu, const pc_field* rho, pc_op** out) {
+  field_dep(rho);
   if (!rho || rho->ncomp != 1) return fail(PC_E_INVALID, "viscous operator needs a scalar density field");
   if (!(nu >= 0.0)) return fail(PC_E_INVALID, "nu must be >= 0");
   TRY(pc_op_create_scalar(g, ncomp, vector_metric, nu, nullptr, rho, out));
@@ -36,6 +38,7 @@ int pc_op_create_viscous(pc_grid* g, int ncomp, int vector_metric, double nu, co
 
 int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, double pref, double kappa0,
                          const double* fc_table, double T_floor, pc_op** out) {
+  field_dep(bhat); field_dep(rho);
   if (!g || !out || !bhat || bhat->ncomp != 3) return fail(PC_E_INVALID, "aligned operator needs a 3-component b");
   if (rho && rho->ncomp != 1) return fail(PC_E_INVALID, "rho is a scalar field");
   pc_ctx* c = g->ctx;
@@ -128,6 +131,7 @@ static int detect_radial_rho(pc_op* op) {
 }
 
 int pc_op_freeze(pc_op* op, const pc_field* T0) {
+  field_dep(T0);
   if (!op) return fail(PC_E_INVALID, "null operator");
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
@@ -210,6 +214,7 @@ int pc_op_euler_dt(pc_op* op, double* dt) {
 }
 
 int pc_op_diagonal(pc_op* op, pc_field* out) {
+  field_dep(out);
   if (!op || !out || out->ncomp != 1) return fail(PC_E_INVALID, "diagonal output must be a scalar field");
   if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
   TRY(ensure_diag(op));
@@ -479,6 +484,7 @@ static int need_frozen(pc_op* op) {
 }
 
 int pc_op_apply(pc_op* op, const pc_field* u, pc_field* F) {
+  field_dep(u); field_dep(F);
   if (!op || !u || !F || u->ncomp != op->ncomp || F->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
   TRY(need_frozen(op));
   TRY(halo_field(const_cast<pc_field*>(u)));

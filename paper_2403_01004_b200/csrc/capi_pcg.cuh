@@ -219,6 +219,7 @@ static int pcg_any(pc_op* op, double dt, const double* adiag, CFld b, pc_field* 
 
 int pc_pcg_solve(pc_op* op, double dt, const pc_field* diag_a, const pc_field* b, pc_field* x, double tol,
                  int max_iter, int* iters, double* relres, int* converged) {
+  field_dep(diag_a); field_dep(b); field_dep(x);
   if (!op || !b || !x || !iters || !relres || !converged) return fail(PC_E_INVALID, "null argument");
   if (b->ncomp != op->ncomp || x->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
   if (!(tol > 0.0 && tol < 1.0) || max_iter < 1) return fail(PC_E_INVALID, "need 0 < tol < 1 and max_iter >= 1");
@@ -245,6 +246,7 @@ static int be_step(pc_op* op, pc_field* u, double dt, double tol, int max_iter, 
 
 int pc_step_be(pc_op* op, pc_field* u, double dt, double tol, int max_iter, int* iters, double* relres,
                int* converged) {
+  field_dep(u);
   if (!op || !u || u->ncomp != op->ncomp || !iters || !relres || !converged) return fail(PC_E_INVALID, "bad arguments");
   if (!(tol > 0.0 && tol < 1.0) || max_iter < 1) return fail(PC_E_INVALID, "need 0 < tol < 1 and max_iter >= 1");
   TRY(need_frozen(op));

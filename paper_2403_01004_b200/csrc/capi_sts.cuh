@@ -53,6 +53,7 @@ static int ptl_read(pc_ctx* c, int check_all, int use_ptl, double* ptl, int* lim
 
 int pc_ptl(pc_grid* g, const pc_field* u, const pc_field* F, double eps_rel, int check_all, double* ptl,
            int* limited, int64_t* kidx) {
+  field_dep(u); field_dep(F);
   if (!g || !u || !F || !ptl || !limited || u->ncomp != F->ncomp || u->grid != g || F->grid != g)
     return fail(PC_E_INVALID, "bad PTL arguments");
   if (!(eps_rel > 0.0)) return fail(PC_E_INVALID, "eps_rel must be > 0");
@@ -251,6 +252,7 @@ static int check_pending_bad(pc_ctx* c) {
 }
 
 int pc_step_sts(pc_op* op, pc_field* u, double dt, int kind, int s, const pc_field* y0in) {
+  field_dep(u); field_dep(y0in);
   if (!op || !u || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
   if (kind != PC_RKL2 && kind != PC_RKG2) return fail(PC_E_INVALID, "unknown STS kind");
   TRY(need_frozen(op));
@@ -275,6 +277,7 @@ int pc_step_sts(pc_op* op, pc_field* u, double dt, int kind, int s, const pc_fie
 }
 
 int pc_step_euler(pc_op* op, pc_field* u, double dt) {
+  field_dep(u);
   if (!op || !u || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
   TRY(need_frozen(op));
   pc_grid* g = op->grid;

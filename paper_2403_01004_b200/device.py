@@ -281,12 +281,34 @@ class DeviceField:
     def shape(self):
         return self.dgrid.shape
 
-    def upload(self, values: np.ndarray, layout: int = _lib.LAYOUT_AOS):
-        """values: local slab, (n0, n1, n2, ncomp) AoS (or (ncomp, n0, n1, n2) SoA)."""
+    def upload(self, values: np.ndarray, layout: int = _lib.LAYOUT_AOS, async_: bool = False):
+        """values: local slab, (n0, n1, n2, ncomp) AoS (or (ncomp, n0, n1, n2) SoA).
+        ``async_``: the copy runs on the context's copy stream and the field's
+        next use waits for it on the device; the host array is held until
+        ``wait()`` (page-locked arrays overlap with compute, pageable ones
+        are copied before the call returns)."""
         a = np.ascontiguousarray(values, dtype=np.float64)
         if a.size != self.ncomp * self.dgrid.ncells:
             raise ValueError(f"upload: {a.size} values for {self.ncomp} x {self.dgrid.shape}")
-        _lib.check(_lib.lib().pc_field_upload(self.handle, _lib.dptr(a), layout), "upload")
+        if async_:
+            _lib.check(_lib.lib().pc_field_upload_async(self.handle, _lib.dptr(a), layout), "upload_async")
+            self._hold = a
+        else:
+            _lib.check(_lib.lib().pc_field_upload(self.handle, _lib.dptr(a), layout), "upload")
+        return self
+
+    def download_async(self, layout: int = _lib.LAYOUT_AOS) -> np.ndarray:
+        """Start a download into a page-locked array; valid after ``wait()``."""
+        shape = tuple(self.dgrid.shape) + (self.ncomp,) if layout == _lib.LAYOUT_AOS else (self.ncomp,) + tuple(self.dgrid.shape)
+        out = pinned_empty(shape)
+        _lib.check(_lib.lib().pc_field_download_async(self.handle, _lib.dptr(out), layout), "download_async")
+        self._hold = out
+        return out
+
+    def wait(self):
+        """Block until this field's asynchronous copy has completed."""
+        _lib.check(_lib.lib().pc_field_wait(self.handle), "wait")
+        self._hold = None
         return self
 
     def download(self, out: np.ndarray | None = None, layout: int = _lib.LAYOUT_AOS) -> np.ndarray:
@@ -335,7 +357,8 @@ class DeviceField:
         return mesh.Field(grid, vals.reshape(tuple(grid.shape) + (self.ncomp,)))
 
     @classmethod
-    def from_values(cls, dgrid: DeviceGrid, values: np.ndarray, ncomp: int | None = None) -> "DeviceField":
+    def from_values(cls, dgrid: DeviceGrid, values: np.ndarray, ncomp: int | None = None,
+                    async_: bool = False) -> "DeviceField":
         """values: global-grid-shaped (+ ncomp) AoS array; this rank's slab is uploaded."""
         v = np.asarray(values, dtype=np.float64)
         gshape = tuple(dgrid.grid.shape)
@@ -344,7 +367,7 @@ class DeviceField:
         nc = v.shape[-1] if ncomp is None else ncomp
         v = v.reshape(tuple(dgrid.global_shape) + (nc,))
         f = cls(dgrid, nc)
-        f.upload(dgrid.local_slice(v))
+        f.upload(dgrid.local_slice(v), async_=async_)
         return f
 
     def __del__(self):

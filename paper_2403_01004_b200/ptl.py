@@ -191,25 +191,43 @@ def split_advance(ops, state: dict, outer_dt: float, cfgs, *, outer_step: int = 
     Returns (state, [CycleReport per operator]).
     """
     refresh = refresh or {}
-    # host Fields go to the device once per outer step (uploaded on the grid of
-    # the first operator acting on them) and come back once at the end
+    # host Fields go to the device once per outer step and come back once at
+    # the end.  The first operator's state and coefficients go first; the
+    # other operators' states then move on the copy stream while the first
+    # operator freezes and cycles (PCIe is not shared with its inputs); a
+    # field no later operator touches starts its download as soon as its last
+    # operator is done.
     host_names = {}
     dev = dict(state)
-    for (name, op) in ops:
+    for q, (name, op) in enumerate(ops):
         if name in dev and not isinstance(dev[name], device.DeviceField):
             f = dev[name]
-            dop = op.device_op(f.grid, f.n_components)
-            dev[name] = device.DeviceField.from_values(dop.dgrid, f.values)
+            dg = device.device_grid(f.grid, op.config.bc)
+            dev[name] = device.DeviceField.from_values(dg, f.values, async_=q > 0)
             host_names[name] = True
+        if q == 0 and isinstance(dev.get(name), device.DeviceField):
+            u = dev[name]  # the first operator's coefficients upload now, ahead of the later states
+            op.device_op(u.dgrid.grid, u.ncomp, u.dgrid.ctx)
     for q, (name, op) in enumerate(ops):
         if op.kind == "aligned":
             src = dev.get(refresh.get(q, name), state.get(refresh.get(q, name)))
             op.freeze(src)
     reports = []
-    for (name, op), (scheme, pcfg) in zip(ops, cfgs):
+    pending = {}
+    for q, ((name, op), (scheme, pcfg)) in enumerate(zip(ops, cfgs)):
         dev[name], rep = cycle_operator(op, scheme, dev[name], outer_dt, pcfg, outer_step=outer_step)
         reports.append(rep)
+        last = all(n != name for n, _ in ops[q + 1:]) and all(refresh.get(p) != name for p in range(q + 1, len(ops)))
+        if host_names.get(name) and last and dev[name].dgrid.ctx.nranks == 1:
+            pending[name] = dev[name].download_async()
     out = dict(state)
     for name in dev:
-        out[name] = dev[name].to_field() if host_names.get(name) else dev[name]
+        if not host_names.get(name):
+            out[name] = dev[name]
+        elif name in pending:
+            dev[name].wait()
+            grid = dev[name].dgrid.grid
+            out[name] = mesh.Field(grid, pending[name].reshape(tuple(grid.shape) + (dev[name].ncomp,)))
+        else:
+            out[name] = dev[name].to_field()
     return out, reports

@@ -91,3 +91,66 @@ def test_radial_rho_path_bitwise(gpu_ctx, c5s, monkeypatch):
         out.append((o.values.copy(), [e.iters for e in rep.entries]))
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+def test_c5_split_step_host_fields_async_copies(gpu_ctx, c5s):
+    """split_advance on HOST Fields (the e2e path): the second operator's state
+    uploads on the copy stream while the first operator computes, and each
+    state downloads as soon as its last operator is done.  Same bits and
+    reports as the device-resident path and the oracle."""
+    w = c5s
+    T = operators.Field(w.grid, w.fields["T"])
+    v = operators.Field(w.grid, w.fields["v"])
+    pinned = [gpu_ctx.pin(a) for a in (w.fields["T"], w.fields["v"], w.fields["b"], w.fields["rho"])
+              if a.flags.c_contiguous]  # page-locked: the copies really overlap
+    try:
+        _host_split_step(gpu_ctx, w, T, v)
+    finally:
+        for a in pinned:
+            gpu_ctx.unpin(a)
+
+
+def _host_split_step(gpu_ctx, w, T, v):
+    cond = operators.DiffusionOperator.aligned(
+        operators.AlignedConductionConfig(b_hat=w.fields["b"], rho=w.fields["rho"], m_p=3.0, k_B=1.0, bc=w.bc))
+    visc = operators.DiffusionOperator.scalar(
+        operators.ScalarDiffusionConfig(nu=1.0, rho=w.fields["rho"], bc=w.bc, vector_metric=True), 3)
+    oc = oracle_aligned(w.grid, w.bc, w.fields["b"], w.fields["T"], rho=w.fields["rho"])
+    ov = oracle_scalar(w.grid, w.bc, nu=1.0, rho=w.fields["rho"], ncomp=3, vector_metric=True)
+    dtE = min(oc.euler_dt(), ov.euler_dt())
+    outer = 200.0 * dtE
+    sc = schemes.SchemeConfig("rkl2")
+    state, reps = ptl.split_advance([("T", cond), ("v", visc)], {"T": T, "v": v}, outer,
+                                    [(sc, ptl.PtlConfig()), (sc, ptl.PtlConfig())])
+    assert isinstance(state["T"], operators.Field) and isinstance(state["v"], operators.Field)
+
+    def refresh(op, st):
+        op.c = oops.aligned_coefficient(st["T"][0])
+
+    ost, oreps = optl.split_advance([("T", oc), ("v", ov)], {"T": soa(w.fields["T"][..., None]),
+                                                             "v": soa(w.fields["v"])}, outer,
+                                    [optl.OracleScheme("rkl2")] * 2, refresh=refresh)
+    for rep, orep in zip(reps, oreps):
+        assert [e.iters for e in rep.entries] == [r.iters for r in orep]
+    assert np.array_equal(state["T"].values[..., 0], ost["T"][0])
+    assert np.array_equal(np.moveaxis(state["v"].values, -1, 0), ost["v"])
+
+
+def test_async_upload_download_semantics(gpu_ctx, c5s):
+    """upload_async: the next library call on the field waits for the copy on
+    the device; download_async: valid after wait(); destroying a field with a
+    copy in flight waits for it."""
+    w = c5s
+    dg = device.device_grid(w.grid, w.bc, gpu_ctx)
+    v = device.pinned_empty(tuple(w.grid.shape) + (3,))
+    v[...] = w.fields["v"]
+    f = device.DeviceField(dg, 3).upload(v, async_=True)
+    g = device.DeviceField(dg, 3).copy_from(f)  # waits for the upload on the device
+    assert np.array_equal(g.download(), w.fields["v"])
+    out = g.download_async()
+    g.wait()
+    assert np.array_equal(out, w.fields["v"])
+    h = device.DeviceField(dg, 3).upload(v, async_=True)
+    del h  # destroy with the copy possibly in flight
+    cnt = f.count_failing(2)  # TEST_FINITE through a waited field
+    assert cnt == 0
