@@ -120,8 +120,10 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         if (line) {
           k_pcg_pupdate_z<<<nb, kThreads, 0, c->s>>>(g->g, z.base(0), pold->base(0), pnew->base(0), c->pcg);
         } else if (vio) {
-          k_pcg_pupdatev<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
-                                                    c->pcg);
+          // four phi pairs per lane at 2 blocks/SM: 1.21 ms at C4 (7.1 TB/s) against 1.32 (two pairs,
+          // 4 blocks, spills) and 1.54 (two pairs, 85 registers) -- profiles/r01_c4_pcg_vec.txt
+          k_pcg_pupdatev<4, 2><<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag,
+                                                          dt, c->pcg);
         } else {
           k_pcg_pupdate<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
                                                    c->pcg);

@@ -363,8 +363,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const doubl
   }
 }
 
-// k_pcg_pupdate with 128-bit accesses (n2 even): two phi pairs per lane
-__global__ void __launch_bounds__(kThreads) k_pcg_pupdatev(GridDev g, const double* __restrict__ r,
+// k_pcg_pupdate with 128-bit accesses (n2 even): U phi pairs per lane
+template <int U = 4, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB) k_pcg_pupdatev(GridDev g, const double* __restrict__ r,
                                                            const double* __restrict__ pold, double* __restrict__ pnew,
                                                            const double* __restrict__ dg,
                                                            const double* __restrict__ adiag, double dt,
@@ -375,10 +376,10 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdatev(GridDev g, const doub
   const int nrows = g.n0 * g.n1;
   for (int row = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < nrows; row += gridDim.x * (kThreads / 32)) {
     const int64_t base = (int64_t)(row / g.n1) * g.plane + (int64_t)(row % g.n1) * g.n2;
-    for (int k0 = 2 * lane; k0 < g.n2; k0 += 128) {
-      double2 rv[2], pv[2], dv[2], mv[2];
+    for (int k0 = 2 * lane; k0 < g.n2; k0 += 64 * U) {
+      double2 rv[U], pv[U], dv[U], mv[U];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t o = base + k0 + 64 * u;
         if (k0 + 64 * u < g.n2) {
           rv[u] = __ldg(reinterpret_cast<const double2*>(r + o));
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdatev(GridDev g, const doub
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t o = base + k0 + 64 * u;
         if (k0 + 64 * u < g.n2) {
           const double z0 = rv[u].x / (mv[u].x + dt * dv[u].x), z1 = rv[u].y / (mv[u].y + dt * dv[u].y);
