@@ -276,6 +276,7 @@ class DeviceField:
         h = c_void_p()
         _lib.check(_lib.lib().pc_field_create(dgrid.handle, self.ncomp, byref(h)), "pc_field_create")
         self.handle = h
+        self._hold = None  # host array of an in-flight asynchronous copy
 
     @property
     def shape(self):
