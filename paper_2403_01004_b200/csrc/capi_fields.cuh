@@ -316,7 +316,7 @@ int pc_field_create(pc_grid* g, int ncomp, pc_field** out) {
 
 int pc_field_destroy(pc_field* f) {
   if (!f) return PC_OK;
-  if (f->pending) cudaEventSynchronize(f->ready);  // the host side of an in-flight copy may go away next
+  if (f->copied) cudaEventSynchronize(f->ready);  // the host side of an in-flight copy may go away next
   f->pending = false;
   if (f->ready) cudaEventDestroy(f->ready);
   for (int q = 0; q < f->ncomp; ++q) pool_put(f->grid->ctx, f->grid->comp_elems, f->buf[q]);
@@ -426,6 +426,7 @@ int pc_field_upload_async(pc_field* f, const double* host, int layout) {
   TRY(upload_on(f, host, layout, c->cs, c->staging_cs, c->staging_cs_bytes));
   CUDA_TRY(cudaEventRecord(f->ready, c->cs));
   f->pending = true;
+  f->copied = true;
   return PC_OK;
 }
 int pc_field_download_async(pc_field* f, double* host, int layout) {
@@ -435,14 +436,15 @@ int pc_field_download_async(pc_field* f, double* host, int layout) {
   TRY(download_on(f, host, layout, c->cs, c->staging_cs, c->staging_cs_bytes));
   CUDA_TRY(cudaEventRecord(f->ready, c->cs));
   f->pending = true;
+  f->copied = true;
   return PC_OK;
 }
 int pc_field_wait(pc_field* f) {
   if (!f) return fail(PC_E_INVALID, "null argument");
-  if (f->pending) {
-    CUDA_TRY(cudaEventSynchronize(f->ready));
-    f->pending = false;
-  }
+  // the host waits for the copy itself, even if a device-side dependency
+  // (field_dep) has already been placed on the compute stream
+  if (f->copied) CUDA_TRY(cudaEventSynchronize(f->ready));
+  f->pending = false;
   return PC_OK;
 }
 

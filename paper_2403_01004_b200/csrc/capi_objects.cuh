@@ -124,7 +124,8 @@ struct pc_field {
   // flight until `ready`; the compute stream waits for it before the field's
   // next use (field_dep)
   cudaEvent_t ready = nullptr;
-  mutable bool pending = false;
+  mutable bool pending = false;  // the compute stream has not yet been made to wait for `ready`
+  bool copied = false;           // `ready` was recorded (host-side waits synchronise on it)
 };
 
 enum { K_SCALAR = 0, K_ALIGNED = 1 };

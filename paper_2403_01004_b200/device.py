@@ -276,7 +276,7 @@ class DeviceField:
         h = c_void_p()
         _lib.check(_lib.lib().pc_field_create(dgrid.handle, self.ncomp, byref(h)), "pc_field_create")
         self.handle = h
-        self._hold = None  # host array of an in-flight asynchronous copy
+        self._holds = []  # host arrays of in-flight asynchronous copies (released by wait())
 
     @property
     def shape(self):
@@ -293,7 +293,7 @@ class DeviceField:
             raise ValueError(f"upload: {a.size} values for {self.ncomp} x {self.dgrid.shape}")
         if async_:
             _lib.check(_lib.lib().pc_field_upload_async(self.handle, _lib.dptr(a), layout), "upload_async")
-            self._hold = a
+            self._holds.append(a)
         else:
             _lib.check(_lib.lib().pc_field_upload(self.handle, _lib.dptr(a), layout), "upload")
         return self
@@ -303,13 +303,13 @@ class DeviceField:
         shape = tuple(self.dgrid.shape) + (self.ncomp,) if layout == _lib.LAYOUT_AOS else (self.ncomp,) + tuple(self.dgrid.shape)
         out = pinned_empty(shape)
         _lib.check(_lib.lib().pc_field_download_async(self.handle, _lib.dptr(out), layout), "download_async")
-        self._hold = out
+        self._holds.append(out)
         return out
 
     def wait(self):
         """Block until this field's asynchronous copy has completed."""
         _lib.check(_lib.lib().pc_field_wait(self.handle), "wait")
-        self._hold = None
+        self._holds.clear()
         return self
 
     def download(self, out: np.ndarray | None = None, layout: int = _lib.LAYOUT_AOS) -> np.ndarray:
