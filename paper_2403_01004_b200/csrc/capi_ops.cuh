@@ -339,7 +339,10 @@ static int launch_tma_t(pc_op* op, const TmaMaps& maps, const Epi& epi, const in
     attr = true;
   }
   const int zsel = zsplit(c, grid);
-  k_aligned_tma<Epi, RHO><<<grid, dim3(MTK, MTY), smem, c->s>>>(g->g, op->ao, maps, epi, R, zsel, skip);
+  static const int split = getenv("PC_TMA_SPLIT") ? atoi(getenv("PC_TMA_SPLIT")) : 2;  // TMA issuer warps - 1
+  AlignedOp ao = op->ao;
+  ao.tma_split = split;
+  k_aligned_tma<Epi, RHO><<<grid, dim3(MTK, MTY), smem, c->s>>>(g->g, ao, maps, epi, R, zsel, skip);
   c->st.launches++;
   return check_launch(what);
 }

@@ -161,6 +161,7 @@ struct AlignedOp {
   const double* rho_r = nullptr;  // rho(i) per interior plane when rho is radial (TMA march reads it per plane)
   double pref;
   int ncomp;  // always 1
+  int tma_split = 2;  // TMA march: per-plane copies issued by 1 + tma_split warps (PC_TMA_SPLIT overrides)
 
   __device__ __forceinline__ double iL(const GridDev& g, int a, int s, int i, int j, int k) const {
     return __ldg(g.iL2[a * 2 + s] + row2(g, i, j)) * __ldg(g.iL1[a * 2 + s] + k);

@@ -294,9 +294,27 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           mbar_expect_tx(&S.bar, (t2 ? kArrBytes : 0u) + 3u * kArrBytes + (unsigned)Epi::NOPS * kOpBytes +
                                      kRowBytes);
           if (t2) tma_arr(sTm1, &maps.T, &maps.TS, t + 2);
-          issue_B(sBn, t + 1);
+          if (op.tma_split < 2) issue_B(sBn, t + 1);
+          if (op.tma_split == 0) {
+            issue_ops(eW, t);
+            issue_rows(rN, t + 1);
+          }
+        }
+        // the per-plane bulk copies are issued by lane 0 of three warps without
+        // halo-ring work: warp 7 (T, and the expect_tx of the whole plane),
+        // warp 6 (operand and row boxes), warp 5 (beta boxes).  Their bytes are
+        // all in warp 7's expect_tx and the phase cannot complete before that
+        // arrival.  One issuer serialised ~16 copies per plane behind one
+        // warp's compute: C5 7.00 -> 7.28e10, C3 6.92 -> 7.23e10 with three
+        // (profiles/r01_tma_issue_split.txt; PC_TMA_SPLIT=0/1 keep one / two)
+        if (op.tma_split >= 1 && tid == kIssuer - 32) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue_ops(eW, t);
           issue_rows(rN, t + 1);
+        }
+        if (op.tma_split == 2 && tid == kIssuer - 64) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue_B(sBn, t + 1);
         }
       }
       const bool exists = LAST ? plane_map(g, t).exists : true;
