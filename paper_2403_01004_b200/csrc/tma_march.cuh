@@ -3,8 +3,10 @@
 // every spherical grid of the configs); k_aligned_march (cp.async) is the
 // general fallback.  Same arithmetic, same schedule, bitwise-identical output.
 //
-// Per plane ONE thread issues the bulk tensor copies (cp.async.bulk.tensor,
-// completion counted on one mbarrier): for T and each beta component a
+// Per plane lane 0 of three warps without halo-ring work issues the bulk
+// tensor copies (cp.async.bulk.tensor, completion counted on one mbarrier;
+// warp 7: T and the expect_tx, warp 6: operands and rows, warp 5: beta): for
+// T and each beta component a
 // 32 x 18 main box (256-byte rows, phi-aligned) plus two 2 x 18 halo strips
 // whose phi coordinates wrap across the periodic seam; the epilogue operands
 // as 32 x 16 boxes; the per-(r, theta) metric records (iL2[6], wo01[4],
@@ -32,7 +34,7 @@ constexpr int XA = XM + 2 * XS;    // one staged array of one plane
 constexpr int XO = MTJ * MTK;      // epilogue operand box 16 x 32
 constexpr unsigned kArrBytes = (unsigned)(XM + 2 * MHJ * 2) * 8u;  // bytes a T / beta plane delivers
 constexpr unsigned kOpBytes = (unsigned)XO * 8u;
-constexpr int kIssuer = MNT - 32;  // lane 0 of the last warp issues the bulk copies
+constexpr int kIssuer = MNT - 32;  // lane 0 of the last warp: prologue copies, per-plane T + expect_tx
 
 struct TmaMaps {
   CUtensorMap T;     // stage input, box {32, 18, 1}
