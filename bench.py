@@ -225,8 +225,9 @@ class Problem:
     def step(self, sc, pcfg):
         from paper_2403_01004_b200 import ptl
         self.reset()
-        st, reps = ptl.split_advance([(f, op) for f, op, _, _ in self.ops], self.fields, self.outer_dt,
+        st = ptl.split_advance([(f, op) for f, op, _, _ in self.ops], self.fields, self.outer_dt,
                                      [(sc, pcfg)] * len(self.ops))
+        reps = st.reports
         return reps
 
     def host_inputs(self):
@@ -489,7 +490,8 @@ def run_e2e(args, prob, sc, pcfg, ctx, dist):
             state = {f: dev[f] for f in state_names}
         else:
             state = {f: mesh.Field(w.grid, host[f].reshape(tuple(w.grid.shape) + (-1,))) for f in state_names}
-        out, reps = ptl.split_advance(ops, state, outer_dt, [(sc, pcfg)] * len(ops))
+        out = ptl.split_advance(ops, state, outer_dt, [(sc, pcfg)] * len(ops))
+        reps = out.reports
         if multi:
             for f in state_names:
                 out[f].download(outbuf[f])
@@ -619,6 +621,38 @@ def run_reference(args, rank, world):
     }
 
 
+def spawn_ranks(n):
+    """``--gpus N`` without a launcher: start N copies of this command, one
+    per GPU (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* as torchrun sets
+    them, rendezvous on 127.0.0.1); rank 0's line is the output."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
+
+
+def dry_run(rank, world):
+    """The launch check: every rank joins the process group and is counted."""
+    ranks = 1
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        ranks = int(t.item())
+        dist.destroy_process_group()
+    return {"dry_run": True, "n_gpus": world, "ranks_joined": ranks, "rank0_pid": os.getpid()} if rank == 0 else None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -636,11 +670,21 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="start the N ranks, check the process group, print one line (no GPU work)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to produce a "
+                         f"mislabelled line\n")
+        sys.exit(2)
+    if args.dry_run:
+        line = dry_run(rank, world)
+    elif args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
         line = run_ours(args, rank, world, local_rank)

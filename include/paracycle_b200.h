@@ -169,6 +169,11 @@ int pc_op_destroy(pc_op* op);
 #define PC_PC_JACOBI 0
 #define PC_PC_LINE_R 1
 int pc_op_set_preconditioner(pc_op* op, int pc);
+/* lagged-T0 cadence of an aligned operator inside pc_cycle: 0 = frozen by the
+   caller once per outer step (SPEC default), 1 = re-frozen at T0 := u at the
+   start of every cycle (coefficients and Gershgorin bound; SPEC.md:385
+   "per-cycle refresh available via config") */
+int pc_op_set_refresh(pc_op* op, int per_cycle);
 int pc_op_apply(pc_op* op, const pc_field* u, pc_field* F);
 int pc_op_euler_dt(pc_op* op, double* dt_euler);
 /* -J_ii per node (pinned rows 0), the Jacobi building block */
@@ -195,7 +200,10 @@ int pc_pcg_solve(pc_op* op, double dt, const pc_field* diag_a, const pc_field* b
                  int* converged);
 
 /* ---- the cycle loop (ptl.cycle_operator).  dt_euler <= 0 uses the frozen
- * operator's bound.  rec receives min(n, rec_cap) records. */
+ * operator's bound.  rec receives min(n, rec_cap) records.  use_ptl: 0 no PTL
+ * (one cycle of the whole outer_dt), 1 dynamic re-evaluation every cycle
+ * (PAPER.md:77), 2 static first-PTL cycling (the first cycle's PTL reused by
+ * every cycle). */
 int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd,
              double tol, int max_iter, double eps_rel, int check_all, int use_ptl,
              int floor_mode, double floor_fraction, int64_t max_cycles, double dt_euler,

@@ -14,7 +14,12 @@ single-domain evaluation because every stencil has radius 1.
 PTL: local |F| argmax (lowest AoS index) -> all_gather of
 (value, global index) -> the same combine on every rank -> the owner of k
 evaluates the pairs with its ghost planes of u and F -> all_reduce(min).
-PCG dot products are all_reduce(sum) of per-rank sums.
+PCG inner products are GPU-count invariant (the CUDA path's
+kernels.cuh PlaneRed): every rank sums each of its axis-0 planes, the
+per-plane sums are all-gathered into the global plane vector, and every rank
+adds the planes in global order 0 .. n0-1 -- the same numbers in the same
+order for any number of slabs, so iteration counts and fields are bitwise
+identical for 1, 2, 3, 8 ... ranks.
 """
 from __future__ import annotations
 
@@ -101,6 +106,23 @@ class Slab:
         if self.hi:
             ext[:, -1] = recv_hi.numpy()
         return ext
+
+    def plane_sum(self, prod):
+        """Sum of an (ncomp, n, n1, n2) interior array in the slab-invariant
+        order: per plane, then over the GLOBAL planes in index order."""
+        local = [float(np.sum(prod[:, q])) for q in range(prod.shape[1])]
+        n0 = self.global_geom.shape[0]
+        if self.nranks > 1:
+            vec = torch.zeros(n0, dtype=torch.float64)
+            vec[self.i0:self.i0 + self.n] = torch.tensor(local, dtype=torch.float64)
+            dist.all_reduce(vec)  # one non-zero contribution per entry: exact
+            planes = vec.tolist()
+        else:
+            planes = local
+        s = 0.0
+        for v in planes:
+            s += v
+        return s
 
     def all_sum(self, x):
         t = torch.tensor([float(x)], dtype=torch.float64)
@@ -223,7 +245,7 @@ def slab_cycle_operator(sop, kind, u_int, outer_dt, dt_euler, eps_rel=1e-12, tol
             _, diag = sop.op.bound_and_diag()
             dvec = 1.0 + dt * slab.interior(diag)
             W = slab.interior(sop.op.weights())
-            wdot = lambda x, y: slab.all_sum(np.sum((W * x) * y))  # noqa: E731
+            wdot = lambda x, y: slab.plane_sum((W * x) * y)  # noqa: E731
             A = lambda x: x - dt * sop.apply_ext(slab.extend(x))  # noqa: E731
             u, iters = _pcg(A, u, lambda r: r / dvec, u, wdot, tol, max_iter)
         cyc += 1

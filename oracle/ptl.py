@@ -160,7 +160,14 @@ def step_count(scheme, dt, dt_euler):
 
 
 def cycle_operator(op, scheme, u, outer_dt, eps_rel=1e-12, floor="euler", floor_fraction=1.0,
-                   max_cycles=10**6, check_all=False, use_ptl=True, dt_euler=None):
+                   max_cycles=10**6, check_all=False, use_ptl=True, dt_euler=None, static=False,
+                   refresh_cycle=None):
+    """``use_ptl`` False: one cycle of the whole step.  ``static``: first-PTL
+    cycling -- the first cycle's PTL is reused by every later cycle
+    (SPEC.md:362).  ``refresh_cycle(op, u)``: re-freeze the lagged T0 := u at
+    the start of every cycle (SPEC.md:385 per-cycle knob); Delta t_E (unless
+    given) and the BE diagonal follow the refreshed operator."""
+    fixed_dtE = dt_euler is not None
     if dt_euler is None:
         dt_euler = op.euler_dt()
     pinned = op.geom.pinned
@@ -172,11 +179,23 @@ def cycle_operator(op, scheme, u, outer_dt, eps_rel=1e-12, floor="euler", floor_
         _, diag = op.bound_and_diag()
         W = op.weights()
     cyc = 0
+    first_ptl = None
     while remaining > 0.0:
         if cyc >= max_cycles:
             raise CycleCapError(report)
+        if refresh_cycle is not None:
+            refresh_cycle(op, u)
+            if not fixed_dtE:
+                dt_euler = op.euler_dt()
+                floor_dt = dt_euler if floor == "euler" else floor_fraction * dt_euler
+            if scheme.kind == "backward_euler":
+                _, diag = op.bound_and_diag()
         F = op.apply(u)
-        ptl = compute_ptl(u, F, op.geom, eps_rel, check_all) if use_ptl else None
+        if use_ptl and (not static or cyc == 0):
+            ptl = compute_ptl(u, F, op.geom, eps_rel, check_all)
+            first_ptl = ptl
+        else:
+            ptl = first_ptl if use_ptl else None
         if ptl is None:
             dt = remaining
         else:
@@ -192,8 +211,9 @@ def cycle_operator(op, scheme, u, outer_dt, eps_rel=1e-12, floor="euler", floor_
             u, iters, rel, conv = sch.backward_euler_step(
                 op.apply, diag, W, u, dt, scheme.tol, scheme.max_iter, pinned, line=line)
         else:
-            u = u + dt * F
-            u[..., pinned] = u[..., pinned]
+            un = u + dt * F
+            un[..., pinned] = u[..., pinned]  # pinned (Dirichlet) nodes keep u0 exactly
+            u = un
             iters = 1
         cyc += 1
         report.append(CycleRecord(cyc, dt, ptl, ptl is not None, iters))

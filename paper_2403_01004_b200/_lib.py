@@ -54,6 +54,7 @@ _SIGS = {
     "pc_ctx_create": (c_int, [c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
     "pc_ctx_create_detached": (c_int, [c_int, c_int, c_int, POINTER(c_void_p)]),
     "pc_op_set_preconditioner": (c_int, [c_void_p, c_int]),
+    "pc_op_set_refresh": (c_int, [c_void_p, c_int]),
     "pc_field_set_ghost": (c_int, [c_void_p, c_int, POINTER(c_double)]),
     "pc_ctx_destroy": (c_int, [c_void_p]),
     "pc_ctx_sync": (c_int, [c_void_p]),

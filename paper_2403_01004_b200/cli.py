@@ -298,9 +298,10 @@ def cmd_run(path: str) -> int:
     first = True
     for step in range(nsteps):
         if ops:
-            state, reps = ptl.split_advance([(f, op) for f, op, _ in ops], state, outer_dt,
+            state = ptl.split_advance([(f, op) for f, op, _ in ops], state, outer_dt,
                                             [(sc, pcfg)] * len(ops), outer_step=step,
                                             refresh={q: f for q, (f, op, _) in enumerate(ops) if op.kind == "aligned"})
+            reps = state.reports
             for rep in reps:
                 rep.write_csv(rpath, append=not first)
                 first = False

@@ -18,6 +18,8 @@
 #include <cstddef>
 #include <cstring>
 #include <string>
+#include <mutex>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/paracycle_b200.h"

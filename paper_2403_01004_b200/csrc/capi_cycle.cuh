@@ -132,16 +132,18 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
   if (!(outer_dt > 0.0)) return fail(PC_E_INVALID, "outer_dt must be > 0");
   if (max_cycles < 1 || !(eps_rel > 0.0)) return fail(PC_E_INVALID, "need max_cycles >= 1 and eps_rel > 0");
   if (scheme < PC_RKL2 || scheme > PC_EULER) return fail(PC_E_INVALID, "unknown scheme");
+  op_deps(op);
   TRY(need_frozen(op));
   if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
-  const double dtE = dt_euler > 0.0 ? dt_euler : op->dt_euler;
-  const double floor_dt = floor_mode == PC_FLOOR_EULER ? dtE : floor_fraction * dtE;
+  if (use_ptl < 0 || use_ptl > 2) return fail(PC_E_INVALID, "use_ptl: 0 off, 1 dynamic, 2 static");
+  double dtE = dt_euler > 0.0 ? dt_euler : op->dt_euler;
+  double floor_dt = floor_mode == PC_FLOOR_EULER ? dtE : floor_fraction * dtE;
   double remaining = outer_dt;
   int64_t cyc = 0;
   *n_rec = 0;
-  if ((scheme == PC_RKL2 || scheme == PC_RKG2) && !check_all && persist_ok(op))
+  if ((scheme == PC_RKL2 || scheme == PC_RKG2) && !check_all && use_ptl != 2 && persist_ok(op))
     return cycle_persistent(op, u, outer_dt, scheme, make_odd, eps_rel, use_ptl, floor_dt, dtE, max_cycles, rec, rec_cap,
                             n_rec);
   Work y0;
@@ -170,6 +172,8 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
     }
   } gp;
   gp.on = getenv("PC_GAP_PROFILE") != nullptr;
+  double static_ptl = INFINITY;
+  int static_limited = 0;
   if (gp.on)
     for (auto& e : gp.cur) e = ev_new(c);
   while (remaining > 0.0) {
@@ -182,12 +186,25 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
       rc = fail(PC_E_CAP, "max_cycles reached (partial report returned)", cyc);
       break;
     }
+    if (op->refresh_cycle) {  // lagged T0 := u, coefficients and Gershgorin bound re-evaluated
+      rc = pc_op_freeze(op, u);
+      if (rc) break;
+      if (!(dt_euler > 0.0)) {
+        dtE = op->dt_euler;
+        floor_dt = floor_mode == PC_FLOOR_EULER ? dtE : floor_fraction * dtE;
+      }
+    }
     if (gp.on) cudaEventRecord(gp.cur[0], c->s);
     rc = halo_field(u);
     if (rc) break;
-    rc = apply_any(op, cfld(u), y0.f(), true);
-    if (rc) break;
-    if (use_ptl) {
+    // static first-PTL cycling (use_ptl 2): the PTL of the first
+    // cycle is reused by every later cycle; F is still formed (it is y0)
+    const bool eval_ptl = use_ptl == 1 || (use_ptl == 2 && cyc == 0);
+    if (scheme != PC_BE || eval_ptl) {
+      rc = apply_any(op, cfld(u), y0.f(), true);
+      if (rc) break;
+    }
+    if (eval_ptl) {
       double* yb[3] = {y0.b[0], y0.b[1], y0.b[2]};
       rc = ptl_device(g, op->ncomp, cfld(u), y0.cf(), yb, eps_rel, check_all);
       if (rc) break;
@@ -195,10 +212,22 @@ int pc_cycle(pc_op* op, pc_field* u, double outer_dt, int scheme, int make_odd, 
     double ptl;
     int limited;
     if (gp.on) cudaEventRecord(gp.cur[1], c->s);
-    rc = ptl_read(c, check_all, use_ptl, &ptl, &limited, nullptr);
-    if (rc) break;
-    rc = check_pending_bad(c);  // ptl_read synchronised the stream
-    if (rc) break;
+    if (eval_ptl || use_ptl == 0) {
+      rc = ptl_read(c, check_all, use_ptl != 0, &ptl, &limited, nullptr);
+      if (rc) break;
+      rc = check_pending_bad(c);  // ptl_read synchronised the stream
+      if (rc) break;
+      static_ptl = ptl;
+      static_limited = limited;
+    } else {
+      ptl = static_ptl;
+      limited = static_limited;
+      if (c->bad_pending) {  // the previous cycle's non-finite flag, before the next step reuses it
+        CUDA_TRY(cudaStreamSynchronize(c->s));
+        rc = check_pending_bad(c);
+        if (rc) break;
+      }
+    }
     double dt;
     if (!limited) {
       dt = remaining;

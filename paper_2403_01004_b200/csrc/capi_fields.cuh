@@ -106,6 +106,10 @@ int pc_ctx_destroy(pc_ctx* c) {
     nccl::Api* A = nccl::api();
     if (A) A->commDestroy(c->comm);
   }
+  cudaFree(c->pslot[0]);
+  cudaFree(c->pslot[1]);
+  cudaFree(c->pvec);
+  cudaFree(c->pvec_all);
   cudaFree(c->red_v);
   cudaFree(c->red_v2);
   cudaFree(c->red_i);
@@ -310,12 +314,14 @@ int pc_field_create(pc_grid* g, int ncomp, pc_field** out) {
     }
     cudaMemsetAsync(f->buf[q], 0, g->comp_elems * sizeof(double), g->ctx->s);
   }
+  live_add(f);
   *out = f;
   return PC_OK;
 }
 
 int pc_field_destroy(pc_field* f) {
   if (!f) return PC_OK;
+  live_del(f);
   if (f->copied) cudaEventSynchronize(f->ready);  // the host side of an in-flight copy may go away next
   f->pending = false;
   if (f->ready) cudaEventDestroy(f->ready);
@@ -449,8 +455,8 @@ int pc_field_wait(pc_field* f) {
 }
 
 int pc_field_set_ghost(pc_field* f, int side, const double* host) {
-  field_dep(f);
   if (!f || !host || (side != 0 && side != 1)) return fail(PC_E_INVALID, "bad ghost-plane arguments");
+  field_dep(f);
   pc_grid* g = f->grid;
   const size_t pl = (size_t)g->g.plane;
   const int64_t plane = side == 0 ? -1 : g->g.n0;
@@ -462,8 +468,8 @@ int pc_field_set_ghost(pc_field* f, int side, const double* host) {
 }
 
 int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* host) {
-  field_dep(f);
   if (!f || !host) return fail(PC_E_INVALID, "null argument");
+  field_dep(f);
   pc_grid* g = f->grid;
   if (i0 < 0 || n < 0 || i0 + n > g->g.n0) return fail(PC_E_INVALID, "plane window out of range");
   const size_t pl = (size_t)g->g.plane;
@@ -475,10 +481,10 @@ int pc_field_download_planes(const pc_field* f, int64_t i0, int64_t n, double* h
 }
 
 int pc_field_copy(pc_field* dst, const pc_field* src) {
-  field_dep(dst);
-  field_dep(src);
   if (!dst || !src || dst->ncomp != src->ncomp || dst->grid->comp_elems != src->grid->comp_elems)
     return fail(PC_E_INVALID, "field copy: shape mismatch");
+  field_dep(dst);
+  field_dep(src);
   for (int q = 0; q < dst->ncomp; ++q)
     CUDA_TRY(cudaMemcpyAsync(dst->buf[q], src->buf[q], dst->grid->comp_elems * sizeof(double),
                              cudaMemcpyDeviceToDevice, dst->grid->ctx->s));
@@ -486,6 +492,7 @@ int pc_field_copy(pc_field* dst, const pc_field* src) {
 }
 
 int pc_field_fill(pc_field* f, double v) {
+  if (!f) return fail(PC_E_INVALID, "null field");
   field_dep(f);
   pc_ctx* c = f->grid->ctx;
   for (int q = 0; q < f->ncomp; ++q) {
@@ -497,13 +504,14 @@ int pc_field_fill(pc_field* f, double v) {
 }
 
 int pc_field_exchange_halo(pc_field* f) {
+  if (!f) return fail(PC_E_INVALID, "null field");
   field_dep(f);
   return halo_field(f);
 }
 
 int pc_field_count(const pc_field* f, int test, int64_t* count) {
-  field_dep(f);
   if (!f || !count || test < 0 || test > 2) return fail(PC_E_INVALID, "bad pc_field_count arguments");
+  field_dep(f);
   pc_grid* g = f->grid;
   pc_ctx* c = g->ctx;
   CUDA_TRY(cudaMemsetAsync(c->maxout, 0, sizeof(double), c->s));

@@ -77,6 +77,14 @@ struct pc_ctx {
   unsigned long long* minbits = nullptr;
   double* maxout = nullptr;
   double* gath = nullptr;  // per-rank (|F| max, index) pairs
+  // GPU-count-invariant PCG reductions (kernels.cuh PlaneRed): slot partials
+  // of up to two sums, the per-plane vector [2][n0g] (entries of other
+  // ranks' planes stay 0) and its allreduced copy
+  double* pslot[2] = {nullptr, nullptr};
+  size_t pslot_cap = 0;
+  double* pvec = nullptr;
+  double* pvec_all = nullptr;
+  int pvec_n0g = 0, pvec_i0g = -1, pvec_n = 0;
   // pinned host mirrors
   ArgRes* h_res = nullptr;
   PcgDev* h_pcg = nullptr;
@@ -151,6 +159,14 @@ struct pc_op {
   double* lbuf = nullptr;   // r-line preconditioner: -J_{i,i-1}, -J_{i,i+1} (2 component-sized buffers)
   double* rho_r = nullptr;  // aligned: rho(i) per interior plane when the density field is radial
   bool line_valid = false;
+  // the caller's coefficient fields the kernels read in place (D, rho, b-hat):
+  // every launching entry point waits for their in-flight asynchronous
+  // uploads (op_deps), not only the constructor
+  const pc_field* deps[3] = {nullptr, nullptr, nullptr};
+  // aligned: re-freeze T0 := u at the start of every cycle of pc_cycle
+  // ("per-cycle refresh available via config"; default: once per
+  // outer step, by the caller)
+  bool refresh_cycle = false;
 };
 
 // ------------------------------------------------------------------ helpers
@@ -257,12 +273,32 @@ static void swap_storage(pc_field* f, Work& w) {
   for (int q = 0; q < f->ncomp; ++q) std::swap(f->buf[q], w.b[q]);
 }
 
+// live fields: an operator keeps pointers to its coefficient fields, which
+// the caller may destroy first; op_deps only touches fields still alive
+static std::mutex g_live_mu;
+static std::unordered_set<const pc_field*> g_live;
+static void live_add(const pc_field* f) {
+  std::lock_guard<std::mutex> l(g_live_mu);
+  g_live.insert(f);
+}
+static void live_del(const pc_field* f) {
+  std::lock_guard<std::mutex> l(g_live_mu);
+  g_live.erase(f);
+}
+
 // the compute stream waits for a field's in-flight asynchronous copy
 static void field_dep(const pc_field* f) {
   if (f && f->pending) {
     cudaStreamWaitEvent(f->grid->ctx->s, f->ready, 0);
     f->pending = false;
   }
+}
+// ... and for every coefficient field an operator reads in place
+static void op_deps(const pc_op* op) {
+  if (!op) return;
+  std::lock_guard<std::mutex> l(g_live_mu);
+  for (const pc_field* f : op->deps)
+    if (f && g_live.count(f)) field_dep(f);
 }
 
 static int check_launch(const char* what) {
@@ -325,6 +361,12 @@ static int allreduce_d(pc_ctx* c, double* dptr, size_t n, int op) {
   if (!c->comm) return PC_OK;
   nccl::Api* A = nccl::api();
   if (!A || A->allReduce(dptr, dptr, n, nccl::kDouble, op, c->comm, c->s) != 0)
+    return fail(PC_E_NCCL, "ncclAllReduce");
+  return PC_OK;
+}
+static int allreduce_d2(pc_ctx* c, const double* src, double* dst, size_t n, int op) {
+  nccl::Api* A = nccl::api();
+  if (!c->comm || !A || A->allReduce(src, dst, n, nccl::kDouble, op, c->comm, c->s) != 0)
     return fail(PC_E_NCCL, "ncclAllReduce");
   return PC_OK;
 }

@@ -23,6 +23,8 @@ int pc_op_create_scalar(pc_grid* g, int ncomp, int vector_metric, double D_const
   op->so.rho = rho ? rho->base(0) : nullptr;
   op->so.ncomp = ncomp;
   op->so.vector = (vector_metric && g->g.spherical) ? 1 : 0;
+  op->deps[0] = D;
+  op->deps[1] = rho;
   *out = op;
   return PC_OK;
 }
@@ -47,6 +49,8 @@ int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, 
   op->kind = K_ALIGNED;
   op->ncomp = 1;
   for (int q = 0; q < 3; ++q) op->bsrc[q] = bhat->base(q);
+  op->deps[0] = bhat;
+  op->deps[1] = rho;
   op->ao.rho = rho ? rho->base(0) : nullptr;
   op->ao.pref = pref;
   op->ao.ncomp = 1;
@@ -75,6 +79,13 @@ int pc_op_set_preconditioner(pc_op* op, int pc) {
   if (pc == PC_PC_LINE_R && op->grid->ctx->nranks > 1)
     return fail(PC_E_INVALID, "the r-line preconditioner needs the whole r line on one rank");
   op->pc = pc;
+  return PC_OK;
+}
+
+int pc_op_set_refresh(pc_op* op, int per_cycle) {
+  if (!op) return fail(PC_E_INVALID, "null operator");
+  if (per_cycle && op->kind != K_ALIGNED) return fail(PC_E_INVALID, "per-cycle T0 refresh needs an aligned operator");
+  op->refresh_cycle = per_cycle != 0;
   return PC_OK;
 }
 
@@ -133,6 +144,7 @@ static int detect_radial_rho(pc_op* op) {
 int pc_op_freeze(pc_op* op, const pc_field* T0) {
   field_dep(T0);
   if (!op) return fail(PC_E_INVALID, "null operator");
+  op_deps(op);
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   if (op->kind == K_ALIGNED) {
@@ -216,6 +228,7 @@ int pc_op_euler_dt(pc_op* op, double* dt) {
 int pc_op_diagonal(pc_op* op, pc_field* out) {
   field_dep(out);
   if (!op || !out || out->ncomp != 1) return fail(PC_E_INVALID, "diagonal output must be a scalar field");
+  op_deps(op);
   if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
   TRY(ensure_diag(op));
   CUDA_TRY(cudaMemcpyAsync(out->buf[0], op->dbuf, op->grid->comp_elems * sizeof(double),
@@ -489,6 +502,7 @@ static int need_frozen(pc_op* op) {
 int pc_op_apply(pc_op* op, const pc_field* u, pc_field* F) {
   field_dep(u); field_dep(F);
   if (!op || !u || !F || u->ncomp != op->ncomp || F->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  op_deps(op);
   TRY(need_frozen(op));
   TRY(halo_field(const_cast<pc_field*>(u)));
   TRY(apply_any(op, cfld(u), fld(F), false));

@@ -6,11 +6,56 @@
 #pragma once
 
 // ------------------------------------------------------------------ PCG
-// r-slabs: finish a PCG reduction after the allreduce of the local sums
-static int pcg_split_fin(pc_ctx* c, bool split, int mode, int nred, double tol, int it) {
+// the plane-ordered reduction scratch of a solve with S slots per plane
+// (kernels.cuh PlaneRed: the sums are independent of the r-slab split)
+static int plane_red(pc_grid* g, int S, PlaneRed& pr) {
+  pc_ctx* c = g->ctx;
+  const size_t need = (size_t)S * (size_t)g->g.n0;
+  if (need > c->pslot_cap) {
+    cudaFree(c->pslot[0]);
+    cudaFree(c->pslot[1]);
+    c->pslot[0] = c->pslot[1] = nullptr;
+    c->pslot_cap = 0;
+    CUDA_TRY(cudaMalloc(&c->pslot[0], need * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&c->pslot[1], need * sizeof(double)));
+    c->pslot_cap = need;
+  }
+  const int n0g = g->g.n0g;
+  if (n0g > c->pvec_n) {
+    cudaFree(c->pvec);
+    cudaFree(c->pvec_all);
+    c->pvec = c->pvec_all = nullptr;
+    c->pvec_n = 0;
+    CUDA_TRY(cudaMalloc(&c->pvec, 2 * (size_t)n0g * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&c->pvec_all, 2 * (size_t)n0g * sizeof(double)));
+    c->pvec_n = n0g;
+    c->pvec_n0g = -1;
+  }
+  if (c->pvec_n0g != n0g || c->pvec_i0g != g->g.i0g) {  // other ranks' entries must be exactly 0
+    CUDA_TRY(cudaMemsetAsync(c->pvec, 0, 2 * (size_t)n0g * sizeof(double), c->s));
+    c->pvec_n0g = n0g;
+    c->pvec_i0g = g->g.i0g;
+  }
+  pr.slot[0] = c->pslot[0];
+  pr.slot[1] = c->pslot[1];
+  pr.S = S;
+  pr.vec = c->pvec;
+  pr.n0g = n0g;
+  pr.i0g = g->g.i0g;
+  return PC_OK;
+}
+// stages 2 and 3 of a PCG reduction: per-plane sums, then (one rank) the
+// fixed-order sum over the planes and the scalar recurrence in the last
+// block, or (r-slabs) an allreduce of the per-plane vector and the same
+// finish in k_pcg_fin -- bitwise the one-rank result
+static int plane_sums(pc_grid* g, const PlaneRed& pr, int nsum, int mode, int keep, bool split, double tol, int it) {
+  pc_ctx* c = g->ctx;
+  k_plane_sums<<<g->g.n0, kThreads, 0, c->s>>>(pr, nsum, mode, split ? 0 : 1, keep, tol, it, c->counter, c->pcg);
+  c->st.launches++;
+  TRY(check_launch("k_plane_sums"));
   if (!split) return PC_OK;
-  TRY(allreduce_d(c, c->pcg->red, (size_t)nred, nccl::kSum));
-  k_pcg_fin<<<1, 1, 0, c->s>>>(c->pcg, mode, tol, it);
+  TRY(allreduce_d2(c, c->pvec, c->pvec_all, 2 * (size_t)pr.n0g, nccl::kSum));
+  k_pcg_fin<<<1, kThreads, 0, c->s>>>(c->pcg, c->pvec_all, pr.n0g, mode, keep, tol, it);
   c->st.launches++;
   return check_launch("k_pcg_fin");
 }
@@ -66,34 +111,39 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
     TRY(work_get(g, 2, Lf));
   }
   int rc = halo_field(x);
-  // split reductions: the kernels stop at the local sums, NCCL adds them up
-  // (the r-line preconditioner is single-rank and finishes its own reductions)
+  // split reductions: the kernels stop at the per-plane sums, NCCL gathers
+  // them (the r-line preconditioner is single-rank)
   const bool split = c->comm != nullptr && !line;
-  if (rc == PC_OK && cudaMemsetAsync(&c->pcg->split, split ? 1 : 0, sizeof(int), c->s) != cudaSuccess)
-    rc = fail(PC_E_CUDA, "PCG state");
+  // slots per plane: the marching kernels (aligned matvec / init) write one
+  // partial per warp and tile, the row kernels one per theta row
+  const dim3 mg = march_grid(g, 1);
+  const int Sm = std::is_same<Op, AlignedOp>::value ? (int)(mg.x * mg.y) * (MNT / 32) : g->g.n1;
+  PlaneRed prm{}, prr{};  // (one scratch, consumed by each reduction before the next one writes)
+  if (rc == PC_OK) rc = plane_red(g, std::max(Sm, g->g.n1), prm);
+  prr = prm;
+  prm.S = Sm;
+  prr.S = g->g.n1;
   if (rc == PC_OK) {
     if constexpr (std::is_same<Op, AlignedOp>::value) {
       // r = b - A x0 through the marching kernel (x0 staged like any T)
       if (adiag) {
-        EpiPcgInitT<true> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg,
-                            line};
+        EpiPcgInitT<true> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, prm.slot[0], prm.slot[1]};
         rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
       } else {
-        EpiPcgInitT<false> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, c->red_v, c->red_v2, c->counter, c->pcg,
-                             line};
+        EpiPcgInitT<false> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, prm.slot[0], prm.slot[1]};
         rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
       }
+      if (rc == PC_OK) rc = plane_sums(g, prm, 2, PR_INIT, line ? 1 : 0, split, tol, 0);
       if (rc == PC_OK && line) {  // z0 = M^{-1} r0, (r0, z0) -> fin_init
         rc = line_prepare(op, dt, adiag, Lf);
         if (rc == PC_OK) rc = line_apply(op, r.base(0), Lf, dt, z.base(0), 0);
       }
     } else {
-      k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, c->red_v, c->red_v2,
-                                            c->counter, c->pcg);
+      k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, prr, c->pcg);
       c->st.launches++;
       rc = check_launch("k_pcg_init");
+      if (rc == PC_OK) rc = plane_sums(g, prr, 2, PR_INIT, 0, split, tol, 0);
     }
-    if (rc == PC_OK) rc = pcg_split_fin(c, split, 0, 2, tol, 0);
   }
   Work* pold = &p0;
   Work* pnew = &p1;
@@ -134,22 +184,22 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         if (rc) break;
         const int* done = reinterpret_cast<const int*>(reinterpret_cast<const char*>(c->pcg) + offsetof(PcgDev, done));
         if (adiag) {
-          EpiMatvecT<true> e{adiag, Ap.base(0), dt, c->red_v, c->counter, c->pcg};
+          EpiMatvecT<true> e{adiag, Ap.base(0), dt, prm.slot[0]};
           rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
         } else {
-          EpiMatvecT<false> e{adiag, Ap.base(0), dt, c->red_v, c->counter, c->pcg};
+          EpiMatvecT<false> e{adiag, Ap.base(0), dt, prm.slot[0]};
           rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
         }
-        if (rc == PC_OK) rc = pcg_split_fin(c, split, 1, 1, tol, it);
+        if (rc == PC_OK) rc = plane_sums(g, prm, 1, PR_MATVEC, 0, split, tol, it);
         if (rc) break;
       } else {
         rc = halo_work(g, r);
         if (rc == PC_OK) rc = halo_work(g, *pold);
         if (rc) break;
         k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
-                                                c->red_v, c->counter, c->pcg);
+                                                prr, c->pcg);
         rc = check_launch("k_pcg_matvec");
-        if (rc == PC_OK) rc = pcg_split_fin(c, split, 1, 1, tol, it);
+        if (rc == PC_OK) rc = plane_sums(g, prr, 1, PR_MATVEC, 0, split, tol, it);
         if (rc) break;
       }
       if constexpr (std::is_same<Op, AlignedOp>::value) {
@@ -164,15 +214,15 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
                               : (o.rho ? (adiag ? k_pcg_update1<true, true> : k_pcg_update1<true, false>)
                                        : (adiag ? k_pcg_update1<false, true> : k_pcg_update1<false, false>)));
         upd<<<nb, kThreads, 0, c->s>>>(g->g, x->base(0), r.base(0), pnew->base(0), Ap.base(0), dg, adiag, o.rho, dt,
-                                       tol, it, c->red_v, c->red_v2, c->counter, c->pcg);
+                                       tol, it, prr, c->pcg);
       } else {
-        k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, tol, it,
-                                                c->red_v, c->red_v2, c->counter, c->pcg);
+        k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, prr,
+                                                c->pcg);
       }
       c->st.launches += std::is_same<Op, AlignedOp>::value ? 1 : 2;  // (march counted at launch)
       c->st.stage_launches += std::is_same<Op, AlignedOp>::value ? 3 : 2;
       rc = check_launch("k_pcg");
-      if (rc == PC_OK) rc = pcg_split_fin(c, split, 2, 2, tol, it);
+      if (rc == PC_OK) rc = plane_sums(g, prr, line ? 1 : 2, line ? PR_UPDATE_RR : PR_UPDATE, 0, split, tol, it);
       if (rc == PC_OK && line) rc = line_apply(op, r.base(0), Lf, dt, z.base(0), 1);
       std::swap(pold, pnew);
     }
@@ -224,6 +274,7 @@ int pc_pcg_solve(pc_op* op, double dt, const pc_field* diag_a, const pc_field* b
   field_dep(diag_a); field_dep(b); field_dep(x);
   if (!op || !b || !x || !iters || !relres || !converged) return fail(PC_E_INVALID, "null argument");
   if (b->ncomp != op->ncomp || x->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  op_deps(op);
   if (!(tol > 0.0 && tol < 1.0) || max_iter < 1) return fail(PC_E_INVALID, "need 0 < tol < 1 and max_iter >= 1");
   TRY(need_frozen(op));
   if (!op->frozen) TRY(pc_op_freeze(op, nullptr));
@@ -250,6 +301,7 @@ int pc_step_be(pc_op* op, pc_field* u, double dt, double tol, int max_iter, int*
                int* converged) {
   field_dep(u);
   if (!op || !u || u->ncomp != op->ncomp || !iters || !relres || !converged) return fail(PC_E_INVALID, "bad arguments");
+  op_deps(op);
   if (!(tol > 0.0 && tol < 1.0) || max_iter < 1) return fail(PC_E_INVALID, "need 0 < tol < 1 and max_iter >= 1");
   TRY(need_frozen(op));
   if (!op->frozen) TRY(pc_op_freeze(op, nullptr));

@@ -255,6 +255,7 @@ int pc_step_sts(pc_op* op, pc_field* u, double dt, int kind, int s, const pc_fie
   field_dep(u); field_dep(y0in);
   if (!op || !u || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
   if (kind != PC_RKL2 && kind != PC_RKG2) return fail(PC_E_INVALID, "unknown STS kind");
+  op_deps(op);
   TRY(need_frozen(op));
   pc_grid* g = op->grid;
   std::vector<double> tab(5 * (size_t)s);
@@ -279,6 +280,7 @@ int pc_step_sts(pc_op* op, pc_field* u, double dt, int kind, int s, const pc_fie
 int pc_step_euler(pc_op* op, pc_field* u, double dt) {
   field_dep(u);
   if (!op || !u || u->ncomp != op->ncomp) return fail(PC_E_INVALID, "shape mismatch");
+  op_deps(op);
   TRY(need_frozen(op));
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;

@@ -348,6 +348,75 @@ __device__ __forceinline__ void pcg_alpha(PcgDev* st, double pAp) {
   }
 }
 
+// ---- GPU-count-invariant PCG reductions
+// Every PCG inner product is summed in three fixed stages: (1) per slot --
+// one (r, theta) row for the row-per-warp kernels, one warp of one
+// (theta, phi) tile for the marching kernels (lane sums in a fixed shuffle
+// tree); (2) per axis-0 plane over its slots in a fixed order
+// (k_plane_sums); (3) over the GLOBAL planes 0 .. n0g-1 in a fixed order
+// (plane_finish).  No stage depends on how the planes are split into
+// r-slabs, so 1, 2, ..., 8 GPUs form bitwise the same sums and the same PCG
+// iteration counts.  On several ranks stage 3 runs after an allreduce of the
+// per-plane vector, whose every entry has exactly one non-zero contribution
+// (its owner's), so the allreduce is exact.
+struct PlaneRed {
+  double* slot[2];  // [n0_local][S] slot partials of the (up to two) sums
+  int S;            // slots per plane
+  double* vec;      // [2][n0g] per-plane sums; entries of other ranks' planes stay 0
+  int n0g, i0g;
+};
+__device__ __forceinline__ void slot_flush(double s, double* part, int64_t slot) {
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[slot] = s;
+}
+// fixed-order sum of n values by one block of kThreads (valid in thread 0)
+__device__ __forceinline__ double sum_fixed(const double* v, int n, double* sh) {
+  double a = 0.0;
+  for (int q = threadIdx.x; q < n; q += kThreads) a += v[q];
+  return block_sum<kThreads>(a, sh);
+}
+enum { PR_INIT = 0, PR_MATVEC = 1, PR_UPDATE = 2, PR_UPDATE_RR = 3 };
+// stage 3 + the PCG scalar recurrences: mode PR_INIT (r, z)_W, (b, b)_W
+// (keep: leave both in st->red for the r-line solve), PR_MATVEC (p, Ap)_W,
+// PR_UPDATE (r, r)_W, (r, z)_W, PR_UPDATE_RR (r, r)_W only (r-line)
+__device__ __forceinline__ void plane_finish(PcgDev* st, const double* vec, int n0g, int mode, int keep,
+                                             double tol, int it, double* sh) {
+  const double a = sum_fixed(vec, n0g, sh);
+  const double b = (mode == PR_INIT || mode == PR_UPDATE) ? sum_fixed(vec + n0g, n0g, sh) : 0.0;
+  if (threadIdx.x == 0) {
+    if (mode == PR_INIT) {
+      if (keep) {
+        st->red[0] = a;
+        st->red[1] = b;
+      } else {
+        pcg_fin_init(st, a, b);
+      }
+    } else if (mode == PR_MATVEC) {
+      pcg_alpha(st, a);
+    } else if (mode == PR_UPDATE) {
+      pcg_fin_update(st, a, b, tol, it);
+    } else {
+      pcg_fin_rr(st, a, tol, it);
+    }
+  }
+}
+// stage 2 (one block per local plane) and, on one rank, stage 3 in the last block
+__global__ void __launch_bounds__(kThreads) k_plane_sums(PlaneRed pr, int nsum, int mode, int finish, int keep,
+                                                         double tol, int it, unsigned int* counter, PcgDev* st) {
+  __shared__ double sh[kThreads / 32];
+  if (mode != PR_INIT && st->done) return;
+  const int i = blockIdx.x;
+  for (int q = 0; q < nsum; ++q) {
+    const double a = sum_fixed(pr.slot[q] + (int64_t)i * pr.S, pr.S, sh);
+    if (threadIdx.x == 0) pr.vec[(int64_t)q * pr.n0g + pr.i0g + i] = a;
+  }
+  if (!finish) return;
+  if (last_block(counter)) {
+    plane_finish(st, pr.vec, pr.n0g, mode, keep, tol, it, sh);
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+}
+
 // p = z + beta p_old, z = r / (a + dt dg): the search-direction update of the
 // aligned PCG, ahead of the marching matvec (which then stages p like any T)
 __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const double* r, const double* pold,
@@ -412,18 +481,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
                                                           const double* __restrict__ dg,
                                                           const double* __restrict__ adiag,
                                                           const double* __restrict__ rho, double dt, double tol,
-                                                          int it, double* p1, double* p2, unsigned int* counter,
-                                                          PcgDev* st) {
-  __shared__ double sh[kThreads / 32];
+                                                          int it, PlaneRed pr, PcgDev* st) {
   if (st->done) return;
   const double alpha = st->alpha;
   const int lane = threadIdx.x & 31;
-  double s1 = 0.0, s2 = 0.0;
   const int nrows = g.n0 * g.n1;
   for (int row = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < nrows; row += gridDim.x * (kThreads / 32)) {
     const int i = row / g.n1, j = row - i * g.n1;
     const double V2 = __ldg(g.Val2 + row2(g, i, j));
     const int64_t base = (int64_t)i * g.plane + (int64_t)j * g.n2;
+    double s1 = 0.0, s2 = 0.0;
     for (int k0 = lane; k0 < g.n2; k0 += 128) {
       double xv[4], pv[4], rv[4], av[4], dv[4], wv[4], mv[4];
 #pragma unroll
@@ -458,32 +525,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
         }
       }
     }
-  }
-  s1 = block_sum<kThreads>(s1, sh);
-  s2 = block_sum<kThreads>(s2, sh);
-  if (threadIdx.x == 0) {
-    p1[blockIdx.x] = s1;
-    p2[blockIdx.x] = s2;
-  }
-  if (last_block(counter)) {
-    double a = 0.0, b = 0.0;
-    for (int t = threadIdx.x; t < (int)gridDim.x; t += kThreads) {
-      a += p1[t];
-      b += p2[t];
-    }
-    const double rr = block_sum<kThreads>(a, sh);
-    const double rzn = block_sum<kThreads>(b, sh);
-    if (threadIdx.x == 0) {
-      if (LINE) {
-        pcg_fin_rr(st, rr, tol, it);
-      } else if (st->split) {
-        st->red[0] = rr;
-        st->red[1] = rzn;
-      } else {
-        pcg_fin_update(st, rr, rzn, tol, it);
-      }
-      *counter = 0u;
-    }
+    slot_flush(s1, pr.slot[0], row);
+    if (!LINE) slot_flush(s2, pr.slot[1], row);
   }
 }
 
@@ -497,18 +540,16 @@ __global__ void __launch_bounds__(kThreads, U == 1 ? 4 : 2) k_pcg_update1v(GridD
                                                            const double* __restrict__ dg,
                                                            const double* __restrict__ adiag,
                                                            const double* __restrict__ rho, double dt, double tol,
-                                                           int it, double* p1, double* p2, unsigned int* counter,
-                                                           PcgDev* st) {
-  __shared__ double sh[kThreads / 32];
+                                                           int it, PlaneRed pr, PcgDev* st) {
   if (st->done) return;
   const double alpha = st->alpha;
   const int lane = threadIdx.x & 31;
-  double s1 = 0.0, s2 = 0.0;
   const int nrows = g.n0 * g.n1;
   for (int row = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < nrows; row += gridDim.x * (kThreads / 32)) {
     const int i = row / g.n1, j = row - i * g.n1;
     const double V2 = __ldg(g.Val2 + row2(g, i, j));
     const int64_t base = (int64_t)i * g.plane + (int64_t)j * g.n2;
+    double s1 = 0.0, s2 = 0.0;
     for (int k0 = 2 * lane; k0 < g.n2; k0 += 64 * U) {
       double2 xv[U], pv[U], rv[U], av[U], dv[U], mv[U], rh[U];
       double wv[U][2];
@@ -553,32 +594,8 @@ __global__ void __launch_bounds__(kThreads, U == 1 ? 4 : 2) k_pcg_update1v(GridD
         }
       }
     }
-  }
-  s1 = block_sum<kThreads>(s1, sh);
-  s2 = block_sum<kThreads>(s2, sh);
-  if (threadIdx.x == 0) {
-    p1[blockIdx.x] = s1;
-    p2[blockIdx.x] = s2;
-  }
-  if (last_block(counter)) {
-    double a = 0.0, b = 0.0;
-    for (int t = threadIdx.x; t < (int)gridDim.x; t += kThreads) {
-      a += p1[t];
-      b += p2[t];
-    }
-    const double rr = block_sum<kThreads>(a, sh);
-    const double rzn = block_sum<kThreads>(b, sh);
-    if (threadIdx.x == 0) {
-      if (LINE) {
-        pcg_fin_rr(st, rr, tol, it);
-      } else if (st->split) {
-        st->red[0] = rr;
-        st->red[1] = rzn;
-      } else {
-        pcg_fin_update(st, rr, rzn, tol, it);
-      }
-      *counter = 0u;
-    }
+    slot_flush(s1, pr.slot[0], row);
+    if (!LINE) slot_flush(s2, pr.slot[1], row);
   }
 }
 
@@ -674,12 +691,13 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate_z(GridDev g, const dou
   }
 }
 
-// multi-rank finish of a PCG reduction after the allreduce of red[]
-__global__ void k_pcg_fin(PcgDev* st, int mode, double tol, int it) {
-  if (mode == 0) pcg_fin_init(st, st->red[0], st->red[1]);
-  else if (st->done) return;
-  else if (mode == 1) pcg_alpha(st, st->red[0]);
-  else pcg_fin_update(st, st->red[0], st->red[1], tol, it);
+// multi-rank finish of a PCG reduction: stage 3 over the allreduced
+// per-plane vector (the same plane_finish as one rank's k_plane_sums)
+__global__ void __launch_bounds__(kThreads) k_pcg_fin(PcgDev* st, const double* vec, int n0g, int mode, int keep,
+                                                      double tol, int it) {
+  __shared__ double sh[kThreads / 32];
+  if (mode != PR_INIT && st->done) return;
+  plane_finish(st, vec, n0g, mode, keep, tol, it, sh);
 }
 
 // global |F| argmax from the per-rank (value, index) pairs (lowest index on ties)
@@ -710,15 +728,20 @@ struct PVal {
 };
 
 // init: r = b - A x, z = r/d, p_old = 0; partials (r,z)_W and (b,b)_W
+// (row-per-warp loops with one slot partial per (r, theta) row: the
+// GPU-count-invariant reduction order, see PlaneRed)
+#define PC_FOR_ROWS(g, row, i, j)                                                                          \
+  for (int row = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), i = 0, j = 0;                        \
+       row < (g).n0 * (g).n1 && ((i = row / (g).n1), (j = row - i * (g).n1), true);                      \
+       row += gridDim.x * (kThreads / 32))
 template <class Op>
 __global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b, CFld x, Fld r, Fld pold,
                                                        const double* dg, const double* adiag, double dt,
-                                                       double* p1, double* p2, unsigned int* counter,
-                                                       PcgDev* st) {
-  __shared__ double sh[kThreads / 32];
+                                                       PlaneRed pr, PcgDev* st) {
   PlainVal val{{x.p[0], x.p[1], x.p[2]}};
+  PC_FOR_ROWS(g, row, i, j) {
   double s1 = 0.0, s2 = 0.0;
-  PC_FOR_NODES(g, i, j, k) {
+  for (int k = threadIdx.x & 31; k < g.n2; k += 32) {
     double Fx[3];
     op.F(g, val, i, j, k, Fx);
     const int64_t o = off3(g, i, j, k);
@@ -736,24 +759,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b,
       s2 += (W * bv) * bv;
     }
   }
-  s1 = block_sum<kThreads>(s1, sh);
-  s2 = block_sum<kThreads>(s2, sh);
-  if (threadIdx.x == 0) {
-    p1[blockIdx.x] = s1;
-    p2[blockIdx.x] = s2;
-  }
-  if (last_block(counter)) {
-    if (threadIdx.x == 0) {
-      double a = 0.0, bb = 0.0;
-      for (int t = 0; t < (int)gridDim.x; ++t) { a += p1[t]; bb += p2[t]; }
-      if (st->split) {
-        st->red[0] = a;
-        st->red[1] = bb;
-      } else {
-        pcg_fin_init(st, a, bb);
-      }
-      *counter = 0u;
-    }
+  slot_flush(s1, pr.slot[0], row);
+  slot_flush(s2, pr.slot[1], row);
   }
 }
 
@@ -761,12 +768,12 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b,
 template <class Op>
 __global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld r, CFld pold, Fld pnew, Fld Ap,
                                                          const double* dg, const double* adiag, double dt,
-                                                         double* p1, unsigned int* counter, PcgDev* st) {
-  __shared__ double sh[kThreads / 32];
+                                                         PlaneRed pr, PcgDev* st) {
   if (st->done) return;
   PVal val{{r.p[0], r.p[1], r.p[2]}, {pold.p[0], pold.p[1], pold.p[2]}, dg, adiag, dt, st->beta};
+  PC_FOR_ROWS(g, row, i, j) {
   double s1 = 0.0;
-  PC_FOR_NODES(g, i, j, k) {
+  for (int k = threadIdx.x & 31; k < g.n2; k += 32) {
     double Fp[3];
     op.F(g, val, i, j, k, Fp);
     const int64_t o = off3(g, i, j, k);
@@ -779,16 +786,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld 
       s1 += (W * pv) * ap;
     }
   }
-  s1 = block_sum<kThreads>(s1, sh);
-  if (threadIdx.x == 0) p1[blockIdx.x] = s1;
-  if (last_block(counter)) {
-    if (threadIdx.x == 0) {
-      double a = 0.0;
-      for (int t = 0; t < (int)gridDim.x; ++t) a += p1[t];
-      if (st->split) st->red[0] = a;
-      else pcg_alpha(st, a);
-      *counter = 0u;
-    }
+  slot_flush(s1, pr.slot[0], row);
   }
 }
 
@@ -796,13 +794,12 @@ __global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld 
 template <class Op>
 __global__ void __launch_bounds__(kThreads) k_pcg_update(GridDev g, Op op, Fld x, Fld r, CFld p, CFld Ap,
                                                          const double* dg, const double* adiag, double dt,
-                                                         double tol, int it, double* p1, double* p2,
-                                                         unsigned int* counter, PcgDev* st) {
-  __shared__ double sh[kThreads / 32];
+                                                         PlaneRed pr, PcgDev* st) {
   if (st->done) return;
   const double alpha = st->alpha;
+  PC_FOR_ROWS(g, row, i, j) {
   double s1 = 0.0, s2 = 0.0;
-  PC_FOR_NODES(g, i, j, k) {
+  for (int k = threadIdx.x & 31; k < g.n2; k += 32) {
     const int64_t o = off3(g, i, j, k);
     const double W = op.weight(g, i, j, k);
     const double dvec = (adiag ? adiag[o] : 1.0) + dt * dg[o];
@@ -814,24 +811,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(GridDev g, Op op, Fld x
       s2 += (W * rv) * (rv / dvec);
     }
   }
-  s1 = block_sum<kThreads>(s1, sh);
-  s2 = block_sum<kThreads>(s2, sh);
-  if (threadIdx.x == 0) {
-    p1[blockIdx.x] = s1;
-    p2[blockIdx.x] = s2;
-  }
-  if (last_block(counter)) {
-    if (threadIdx.x == 0) {
-      double rr = 0.0, rzn = 0.0;
-      for (int t = 0; t < (int)gridDim.x; ++t) { rr += p1[t]; rzn += p2[t]; }
-      if (st->split) {
-        st->red[0] = rr;
-        st->red[1] = rzn;
-      } else {
-        pcg_fin_update(st, rr, rzn, tol, it);
-      }
-      *counter = 0u;
-    }
+  slot_flush(s1, pr.slot[0], row);
+  slot_flush(s2, pr.slot[1], row);
   }
 }
 

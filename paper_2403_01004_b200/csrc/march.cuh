@@ -228,6 +228,20 @@ __device__ __forceinline__ void node_E_rows(double Tv, const double (&Tn)[3][2],
   node_E_core<ONLY_A, ONLY_S>(Tv, Tn, bv, il2, w01, il1, w2, E);
 }
 
+// Slot of the plane partial of one warp of a marching block: warp w of tile
+// (blockIdx.y, blockIdx.x) on local plane tf; S = tiles x warps per plane
+// (the GPU-count-invariant reduction order, kernels.cuh PlaneRed).
+__device__ __forceinline__ int64_t march_slot(int tf) {
+  const int w = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+  return (((int64_t)tf * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * (MNT / 32) + w;
+}
+// epilogues with a plane_end(tf) member get it called by every thread after
+// plane tf is finalised (block-uniform)
+template <class E, class = void>
+struct has_plane_end : std::false_type {};
+template <class E>
+struct has_plane_end<E, std::void_t<decltype(&E::plane_end)>> : std::true_type {};
+
 // Epilogue contract (per tile node n of the thread):
 //   Epi::NOPS, epi.opnd(q)                 nodal operand arrays the kernel stages
 //                                          through cp.async one plane ahead
@@ -235,6 +249,7 @@ __device__ __forceinline__ void node_E_rows(double Tv, const double (&Tn)[3][2],
 //                                          ov[q] = staged operands, W = the
 //                                          node's inner-product weight rho V
 //                                          (formed only if Epi::NEEDS_W)
+//   epi.plane_end(tf)                      optional: after plane tf is finalised
 //   epi.finish(g)                          block reduction, if any
 template <class Epi>
 __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp op, const double* __restrict__ Tin,
@@ -484,6 +499,9 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
         Tc[n] = Tp;
       }
     }
+    if constexpr (has_plane_end<Epi>::value) {
+      if (t > i0) epi.plane_end(tf);
+    }
     // ---- halo ring of plane t: one flux component per ring node
     if (!LAST && ra >= 0) {
       const double Tcr = S.T[sc][rh];
@@ -686,9 +704,7 @@ struct EpiMatvecT {
   const double* adiag;
   double* Ap;
   double dt;
-  double* p1;
-  unsigned int* counter;
-  PcgDev* st;
+  double* part;  // PlaneRed slot array of (p, Ap)_W
   double acc = 0.0;
   __host__ __device__ __forceinline__ const double* opnd(int) const { return adiag; }
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double pv, bool,
@@ -697,22 +713,11 @@ struct EpiMatvecT {
     Ap[o] = ap;
     acc += (W * pv) * ap;
   }
-  __device__ __forceinline__ void finish(const GridDev&) {
-    __shared__ double sh[kMaxWarps];
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const int nblk = gridDim.x * gridDim.y * gridDim.z;
-    const double v = block_sum2d(acc, sh);
-    if (tid == 0) p1[bid] = v;
-    if (last_block3(counter, nblk)) {
-      const double a = sum_partials(p1, nblk, sh);
-      if (tid == 0) {
-        if (st->split) st->red[0] = a;
-        else pcg_alpha(st, a);
-        *counter = 0u;
-      }
-    }
+  __device__ __forceinline__ void plane_end(int tf) {
+    slot_flush(acc, part, march_slot(tf));
+    acc = 0.0;
   }
+  __device__ __forceinline__ void finish(const GridDev&) {}
 };
 
 // PCG start (the marching form of k_pcg_init): r = b - (a x - dt F(x)),
@@ -728,11 +733,8 @@ struct EpiPcgInitT {
   double* r;
   double* pold;
   double dt;
-  double* p1;
-  double* p2;
-  unsigned int* counter;
-  PcgDev* st;
-  bool line = false;  // r-line preconditioner: keep ||b||^2 in st->red[1]; (r, z) follows from the line solve
+  double* part1;  // PlaneRed slot arrays of (r, z)_W and (b, b)_W
+  double* part2;
   double s1 = 0.0, s2 = 0.0;
   __host__ __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? b : (q == 1 ? dg : adiag); }
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double xv, bool,
@@ -747,31 +749,14 @@ struct EpiPcgInitT {
     s1 += (W * rv) * z;
     s2 += (W * bv) * bv;
   }
-  __device__ __forceinline__ void finish(const GridDev&) {
-    __shared__ double sh[kMaxWarps];
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const int nblk = gridDim.x * gridDim.y * gridDim.z;
-    const double v1 = block_sum2d(s1, sh);
-    const double v2 = block_sum2d(s2, sh);
-    if (tid == 0) {
-      p1[bid] = v1;
-      p2[bid] = v2;
-    }
-    if (last_block3(counter, nblk)) {
-      const double a = sum_partials(p1, nblk, sh);
-      const double bb = sum_partials(p2, nblk, sh);
-      if (tid == 0) {
-        if (st->split || line) {
-          st->red[0] = a;
-          st->red[1] = bb;
-        } else {
-          pcg_fin_init(st, a, bb);
-        }
-        *counter = 0u;
-      }
-    }
+  __device__ __forceinline__ void plane_end(int tf) {
+    const int64_t q = march_slot(tf);
+    slot_flush(s1, part1, q);
+    slot_flush(s2, part2, q);
+    s1 = 0.0;
+    s2 = 0.0;
   }
+  __device__ __forceinline__ void finish(const GridDev&) {}
 };
 
 }  // namespace pc

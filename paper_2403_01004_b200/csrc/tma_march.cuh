@@ -378,6 +378,9 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           Tc[n] = Tp;
         }
       }
+      if constexpr (has_plane_end<Epi>::value) {
+        if (!FIRST) epi.plane_end(tf);
+      }
       // ---- halo ring of plane t (warp-uniform variant)
       if (!LAST && ra >= 0) {
         const double Tcr = sT[ro_c];

@@ -269,6 +269,37 @@ def _embed3(values: np.ndarray, dims: int) -> np.ndarray:
     return v
 
 
+def require_gather_group():
+    """Host-Field results on more than one rank are gathered with
+    torch.distributed: raise before any work when no process group exists."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        raise ValueError("host Fields on a multi-rank context need an initialised torch.distributed process group "
+                         "(the slabs are gathered back to a global Field); pass DeviceFields instead")
+
+
+def gather_slabs(dgrid: DeviceGrid, local: np.ndarray) -> np.ndarray:
+    """All-gather the axis-0 slabs (n0_local, n1, n2, ncomp) of every rank
+    into the global (n0, n1, n2, ncomp) array (geometry.slab_bounds order)."""
+    import torch
+    import torch.distributed as dist
+    require_gather_group()
+    P = dgrid.ctx.nranks
+    n0 = dgrid.global_shape[0]
+    bounds = [geometry.slab_bounds(n0, P, r) for r in range(P)]
+    nmax = max(n for _, n in bounds)
+    tail = local.shape[1:]
+    dev = torch.device("cuda", dgrid.ctx.device) if dist.get_backend() == "nccl" else torch.device("cpu")
+    buf = torch.zeros((nmax,) + tuple(tail), dtype=torch.float64, device=dev)
+    buf[:local.shape[0]] = torch.from_numpy(np.ascontiguousarray(local)).to(dev)
+    parts = [torch.empty_like(buf) for _ in range(P)]
+    dist.all_gather(parts, buf)
+    out = np.empty((n0,) + tuple(tail))
+    for (i0, n), p in zip(bounds, parts):
+        out[i0:i0 + n] = p[:n].cpu().numpy()
+    return out
+
+
 class DeviceField:
     def __init__(self, dgrid: DeviceGrid, ncomp: int = 1):
         self.dgrid = dgrid
@@ -353,8 +384,14 @@ class DeviceField:
         return self
 
     def to_field(self) -> mesh.Field:
+        """The GLOBAL reference Field: on one rank a download; on an r-slab
+        decomposition every rank's slab is all-gathered (torch.distributed,
+        the process group the ranks were launched with) into the global array
+        on every rank."""
         grid = self.dgrid.grid
         vals = self.download()
+        if self.dgrid.ctx.nranks > 1:
+            vals = gather_slabs(self.dgrid, vals)
         return mesh.Field(grid, vals.reshape(tuple(grid.shape) + (self.ncomp,)))
 
     @classmethod

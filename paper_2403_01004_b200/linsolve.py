@@ -53,7 +53,9 @@ class Preconditioner:
 
 def build_jacobi(A: LinearOperatorAction, grid=None, ncomp: int = 1) -> Preconditioner:
     """Point-Jacobi (PC1): stored inverse diagonal of A."""
-    grid = grid or A.op.frozen_state.grid if getattr(A.op, "frozen_state", None) is not None else grid
+    fs = getattr(A.op, "frozen_state", None)
+    if grid is None and fs is not None:
+        grid = fs.dgrid.grid if hasattr(fs, "dgrid") else fs.grid
     if grid is None:
         raise ValueError("build_jacobi needs the grid of the system")
     dop = A.op.device_op(grid, ncomp)

@@ -45,6 +45,14 @@ class PtlConfig:
     max_cycles: int = 10**6
     check_all_points: bool = False
     enabled: bool = True  # False: one cycle of the whole outer step (no PTL)
+    # "dynamic": the PTL is re-evaluated every cycle;
+    # "static": first-PTL cycling, the first cycle's PTL is reused by every
+    # cycle (the comparison mode of SPEC.md:362 and acceptance 6)
+    reevaluate: str = "dynamic"
+    # lagged T0 of aligned operators: "outer" = refreshed once per outer step
+    # (SPEC default); "cycle" = re-frozen at T0 := u at the start
+    # of every cycle ("per-cycle refresh available via config")
+    refresh_T0: str = "outer"
 
     def __post_init__(self):
         if not self.eps_rel > 0:
@@ -53,6 +61,15 @@ class PtlConfig:
             raise ValueError("max_cycles must be >= 1")
         if self.dt_floor_mode not in ("clamp-to-euler", "clamp-to-fraction"):
             raise ValueError(f"unknown dt_floor_mode {self.dt_floor_mode!r}")
+        if self.reevaluate not in ("dynamic", "static"):
+            raise ValueError(f"unknown reevaluate mode {self.reevaluate!r}")
+        if self.refresh_T0 not in ("outer", "cycle"):
+            raise ValueError(f"unknown refresh_T0 cadence {self.refresh_T0!r}")
+
+    @property
+    def ptl_mode(self) -> int:
+        """pc_cycle's use_ptl: 0 off, 1 dynamic, 2 static."""
+        return 0 if not self.enabled else (2 if self.reevaluate == "static" else 1)
 
 
 @dataclass
@@ -162,6 +179,8 @@ def cycle_operator(op, scheme, u, outer_dt: float, cfg: PtlConfig | None = None,
         host = False
     else:
         dop = op.device_op(u.grid, u.n_components, ctx)
+        if dop.ctx.nranks > 1:
+            device.require_gather_group()  # the result is gathered back to a global Field
         du = device.DeviceField.from_values(dop.dgrid, u.values)
         host = True
     recs = _record_buffer(record_cap)
@@ -170,16 +189,43 @@ def cycle_operator(op, scheme, u, outer_dt: float, cfg: PtlConfig | None = None,
     dtE = float(dt_euler) if dt_euler is not None else -1.0
     if scheme.kind == "backward_euler":
         _lib.check(_lib.lib().pc_op_set_preconditioner(dop.handle, scheme.pc_code), "preconditioner")
+    if cfg.refresh_T0 == "cycle" and op.kind != "aligned":
+        raise ValueError("refresh_T0='cycle' applies to aligned (lagged-T0) operators only")
+    if op.kind == "aligned":
+        _lib.check(_lib.lib().pc_op_set_refresh(dop.handle, int(cfg.refresh_T0 == "cycle")), "refresh_T0")
     rc = _lib.lib().pc_cycle(dop.handle, du.handle, float(outer_dt), scheme.code, int(scheme.make_odd),
                              float(scheme.tol), int(scheme.max_iter), float(cfg.eps_rel), int(cfg.check_all_points),
-                             int(cfg.enabled), floor_mode, float(cfg.floor_fraction), int(cfg.max_cycles), dtE,
+                             cfg.ptl_mode, floor_mode, float(cfg.floor_fraction), int(cfg.max_cycles), dtE,
                              recs, record_cap, byref(n))
     rep = _report(recs, min(n.value, record_cap), dop.dt_euler if dt_euler is None else float(dt_euler), outer_step)
     _lib.check(rc, "cycle_operator", report=rep)
     return (du.to_field() if host else du), rep
 
 
-def split_advance(ops, state: dict, outer_dt: float, cfgs, *, outer_step: int = 0, refresh=None):
+def _check_host_state(state, ops):
+    """Host Fields on a multi-rank context are gathered back to global
+    Fields at the end (device.DeviceField.to_field): that needs an
+    initialised torch.distributed process group -- fail before any work."""
+    if any(not isinstance(v, device.DeviceField) for n, v in state.items() if any(n == m for m, _ in ops)):
+        ctx = device.default_context()
+        if ctx.nranks > 1:
+            device.require_gather_group()
+
+
+class FieldSet(dict):
+    """The state returned by ``split_advance``: a dict name -> Field /
+    DeviceField (the SPEC's ``Field set``) that also carries the
+    per-operator ``CycleReport`` list as ``.reports``."""
+
+    reports: list
+
+    def __init__(self, *a, reports=None, **k):
+        super().__init__(*a, **k)
+        self.reports = list(reports or [])
+
+
+def split_advance(ops, state: dict, outer_dt: float, cfgs, *, outer_step: int = 0, refresh=None,
+                  out_reports: list | None = None) -> FieldSet:
     """First-order (Lie) splitting over ``outer_dt`` in list order.
 
     ops:   list of (field_name, DiffusionOperator)
@@ -187,10 +233,14 @@ def split_advance(ops, state: dict, outer_dt: float, cfgs, *, outer_step: int = 
     cfgs:  list of (SchemeConfig, PtlConfig) per operator
     refresh: optional {op_index: state_name}; aligned operators are re-frozen
              at the named state once per outer step before cycling begins
-             (lagged T0).
-    Returns (state, [CycleReport per operator]).
+             (lagged T0; PtlConfig.refresh_T0 = "cycle" re-freezes
+             every cycle instead).
+    out_reports: optional list that receives the CycleReport of every operator.
+    Returns the advanced state (SPEC.md:363 ``-> Field set``), a FieldSet whose
+    ``.reports`` holds the same CycleReports.
     """
     refresh = refresh or {}
+    _check_host_state(state, ops)
     # host Fields go to the device once per outer step and come back once at
     # the end.  The first operator's state and coefficients go first; the
     # other operators' states then move on the copy stream while the first
@@ -230,4 +280,6 @@ def split_advance(ops, state: dict, outer_dt: float, cfgs, *, outer_step: int = 
             out[name] = mesh.Field(grid, pending[name].reshape(tuple(grid.shape) + (dev[name].ncomp,)))
         else:
             out[name] = dev[name].to_field()
-    return out, reports
+    if out_reports is not None:
+        out_reports.extend(reports)
+    return FieldSet(out, reports=reports)

@@ -129,7 +129,6 @@ def rkl2_coefficients(s: int) -> StsCoefficients:
 
 def _bind(op, u):
     if isinstance(u, device.DeviceField):
-        dop = op._dev_for(u) if hasattr(op, "_dev_for") else None
         raise TypeError("pass a mesh.Field, or use ptl.cycle_operator for device-resident fields")
     dop = op.device_op(u.grid, u.n_components)
     du = device.DeviceField.from_values(dop.dgrid, u.values)

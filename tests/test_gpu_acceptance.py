@@ -1,0 +1,115 @@
+"""SPEC acceptance criteria 4, 5, 6 and 9 through the
+PRODUCT path (public API -> C ABI -> sm_100a kernels), each run also checked
+against the CPU oracle on the same inputs (cycle counts equal, STS fields
+bitwise, BE fields within the PCG contract)."""
+import numpy as np
+import pytest
+
+from acceptance_cases import (RATIO, STEP_CASES, coords, neighbours, oracle_geom, random_fields, sign_changes,
+                              step_values)
+from helpers import oracle_scalar, soa
+from oracle import ptl as optl
+from paper_2403_01004_b200 import configs, mesh, operators, ptl, schemes
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(dim, n):
+    g = mesh.build_grid([n] * dim, coords=coords(dim, n))
+    bc = mesh.BoundaryCondition.neumann(dim)
+    op = operators.DiffusionOperator.scalar(operators.ScalarDiffusionConfig(nu=1.0, bc=bc), 1)
+    return g, bc, op
+
+
+def _run(dim, n, kind, use_ptl, static=False):
+    g, bc, op = _setup(dim, n)
+    dtE = op.device_op(g, 1).dt_euler
+    u0 = step_values(dim, n)
+    cfg = ptl.PtlConfig(enabled=use_ptl, reevaluate="static" if static else "dynamic")
+    out, rep = ptl.cycle_operator(op, schemes.SchemeConfig(kind, tol=1e-10), mesh.Field(g, u0[..., None]),
+                                  RATIO * dtE, cfg)
+    # the oracle on the same input
+    og = oracle_geom(dim, n)
+    oop = optl.OracleOperator(og, "scalar", 1, 1.0, None, False)
+    assert oop.euler_dt() == dtE
+    uo, repo = optl.cycle_operator(oop, optl.OracleScheme(kind, tol=1e-10), u0.reshape(og.shape)[None],
+                                   RATIO * dtE, use_ptl=use_ptl, static=static)
+    assert [e.iters for e in rep.entries] == [r.iters for r in repo]
+    assert [e.dt for e in rep.entries] == [r.dt for r in repo]
+    a, b = out.values[..., 0], uo[0].reshape((n,) * dim)
+    if kind == "backward_euler":
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+    else:
+        assert np.array_equal(a, b)
+    return a, rep
+
+
+@pytest.mark.parametrize("dim,n", STEP_CASES)
+def test_acceptance4_on_gpu(gpu_ctx, dim, n):
+    init = sign_changes(step_values(dim, n))
+    u_free, _ = _run(dim, n, "rkg2", False)
+    u_ptl, _ = _run(dim, n, "rkg2", True)
+    assert sign_changes(u_free) > init
+    assert sign_changes(u_ptl) <= init
+    b_free, _ = _run(dim, n, "backward_euler", False)
+    b_ptl, _ = _run(dim, n, "backward_euler", True)
+    assert sign_changes(b_ptl) <= sign_changes(b_free)
+
+
+@pytest.mark.parametrize("dim,n", STEP_CASES)
+@pytest.mark.parametrize("kind", ["rkg2", "rkl2", "backward_euler"])
+def test_acceptance6_static_vs_dynamic_on_gpu(gpu_ctx, dim, n, kind):
+    _, dyn = _run(dim, n, kind, True)
+    _, sta = _run(dim, n, kind, True, static=True)
+    assert dyn.n_cycles <= sta.n_cycles
+    if dim == 2:
+        assert dyn.n_cycles < sta.n_cycles
+    assert len({e.dt for e in sta.entries[:-1]}) == 1
+    assert all(e.ptl_raw == sta.entries[0].ptl_raw for e in sta.entries)
+
+
+def test_acceptance5_on_gpu(gpu_ctx):
+    """Eq. 3 after a GPU explicit Euler step at the GPU's limited PTL, at
+    every pair adjacent to the |F| maximum, 1000 seeded random fields."""
+    limited = 0
+    for u in random_fields(1000):
+        dim = u.ndim
+        g = mesh.build_grid(list(u.shape), coords=[np.linspace(0.0, 1.0, m) for m in u.shape])
+        bc = mesh.BoundaryCondition.neumann(dim)
+        cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=bc)
+        op = operators.DiffusionOperator.scalar(cfg, 1)
+        U = mesh.Field(g, u[..., None])
+        F = op.apply(U)
+        p = ptl.compute_ptl(U, F, g, ptl.PtlConfig(), bc=bc)
+        if p is ptl.UNLIMITED:
+            continue
+        limited += 1
+        u1 = schemes.step_euler(op, U, p).values[..., 0]
+        absF = np.abs(F.values[..., 0])
+        k = np.unravel_index(int(np.argmax(absF)), u.shape)
+        scale = float(np.max(np.abs(u))) ** 2
+        for nb in neighbours(u.shape, k):
+            assert (u1[k] - u1[nb]) * (u[k] - u[nb]) >= -1e-14 * scale
+    assert limited >= 900
+
+
+@pytest.mark.parametrize("kind,ratio", [("euler", 0.5), ("rkl2", 20.0), ("rkg2", 20.0), ("backward_euler", 20.0)])
+@pytest.mark.parametrize("use_ptl", [False, True])
+def test_acceptance9_conservation_on_gpu(gpu_ctx, kind, ratio, use_ptl):
+    """Neumann (zero-flux) diffusion conserves sum(rho V u) to 1e-12 relative
+    over 100 outer steps, for the Cartesian 2-D case of the oracle test and a
+    spherical shell (Neumann r-ends, axis, periodic phi)."""
+    x = np.linspace(0.0, 1.0, 24)
+    cases = [(mesh.build_grid([24, 24], coords=[x, x]), mesh.BoundaryCondition.neumann(2)),
+             (mesh.build_spherical_grid(np.linspace(1.0, 2.0, 10), 8, 16), configs.spherical_bc("neumann"))]
+    for g, bc in cases:
+        op = operators.DiffusionOperator.scalar(operators.ScalarDiffusionConfig(nu=1.0, bc=bc), 1)
+        W = oracle_scalar(g, bc).weights()[0].reshape(tuple(g.shape))
+        u0 = np.random.default_rng(9).random(tuple(g.shape))
+        dt = ratio * op.device_op(g, 1).dt_euler
+        u = mesh.Field(g, u0[..., None])
+        for _ in range(100):
+            u, _ = ptl.cycle_operator(op, schemes.SchemeConfig(kind, tol=1e-10), u, dt,
+                                      ptl.PtlConfig(enabled=use_ptl))
+        s0, s1 = float(np.sum(W * u0)), float(np.sum(W * u.values[..., 0]))
+        assert abs(s1 - s0) <= 1e-12 * abs(s0), (g.metric, s0, s1)

@@ -94,3 +94,39 @@ def test_periodic_self_exchange_through_nccl(gpu_ctx, nccl_ctx, kind):
     assert res[0][0] == res[1][0]
     assert res[0][1] == res[1][1]
     assert np.array_equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("name", ["aligned", "scalar", "viscous"])
+def test_pcg_split_reduction_bitwise_equals_single_rank(gpu_ctx, nccl_ctx, name):
+    """The r-slab PCG reduction (per-plane sums -> ncclAllReduce of the
+    per-plane vector -> k_pcg_fin's fixed-order sum over the global planes)
+    is bitwise the single-rank reduction: same iteration counts, same field
+    bits -- the GPU-count invariance of SURVEY.md §8e on the device."""
+    if name == "aligned":
+        w = configs.c4(n=(24, 40, 64))
+        cfg = operators.AlignedConductionConfig(b_hat=w.fields["b"], m_p=3.0, k_B=1.0, bc=w.bc)
+        u = operators.Field(w.grid, w.fields["T"])
+        make = lambda: operators.DiffusionOperator.aligned(cfg, u)  # noqa: E731
+        nc = 1
+    elif name == "scalar":
+        w = configs.c1(n=(20, 16, 32))
+        cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc)
+        u = operators.Field(w.grid, w.fields["u"][..., None])
+        make = lambda: operators.DiffusionOperator.scalar(cfg, 1)  # noqa: E731
+        nc = 1
+    else:
+        w = configs.c2(n=(20, 16, 32))
+        cfg = operators.ScalarDiffusionConfig(nu=1.0, bc=w.bc, vector_metric=True)
+        u = operators.Field(w.grid, w.fields["v"])
+        make = lambda: operators.DiffusionOperator.scalar(cfg, 3)  # noqa: E731
+        nc = 3
+    res = []
+    for ctx in (gpu_ctx, nccl_ctx):
+        op = make()
+        dtE = op.device_op(w.grid, nc, ctx).dt_euler
+        out, rep = ptl.cycle_operator(op, schemes.SchemeConfig("backward_euler", tol=1e-9), u, 500 * dtE, ctx=ctx)
+        res.append(([e.iters for e in rep.entries], [e.relres for e in rep.entries], out.values.copy()))
+    assert sum(res[0][0]) > 10
+    assert res[0][0] == res[1][0]
+    assert res[0][1] == res[1][1]
+    assert np.array_equal(res[0][2], res[1][2])

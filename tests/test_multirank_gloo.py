@@ -1,9 +1,10 @@
 """The N > 1 path on CPU: two gloo ranks run the slab-decomposed cycle
 (oracle/distributed.py -- the algorithm of the r-slab CUDA path: ghost-plane
 exchange, allgathered argmax + owner pair tests + allreduced PTL minimum,
-allreduced PCG dots) and must reproduce the single-domain oracle: identical
+plane-ordered PCG dots) and must reproduce the single-domain oracle: identical
 cycle and stage counts and bitwise-equal fields for RKL2, identical PCG
-iteration counts and fields to 1e-10 for BE.  Also pins the product's
+iteration counts and fields to 1e-10 for BE; and BE+PCG is bitwise the same
+for 1, 2, 3 and 8 slabs (GPU-count-invariant reductions).  Also pins the product's
 host-side slab logic (geometry.slab_bounds / pack / flags) used by the CUDA
 path."""
 import multiprocessing as mp
@@ -93,6 +94,51 @@ def test_two_rank_be_pcg_matches_single_domain():
         assert [x[1] for x in rep] == [r.iters for r in repo]
         ref = uo[:, i0:i0 + out.shape[1]]
         assert np.linalg.norm(out - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def _worker_c4(rank, world, port, kind, q):
+    import torch.distributed as dist
+    from oracle import distributed as od
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        w = configs.c4(n=(16, 10, 16))
+        op = oracle_aligned(w.grid, w.bc, w.fields["b"], w.fields["T"])
+        u = soa(w.fields["T"][..., None])
+        slab = od.Slab(op.geom, rank, world)
+        sop = od.SlabOperator(op, slab)
+        dtE = sop.euler_dt()
+        u_int = u[:, slab.i0:slab.i0 + slab.n].copy()
+        out, rep = od.slab_cycle_operator(sop, kind, u_int, 1e3 * dtE, dtE, tol=1e-9)
+        q.put((rank, slab.i0, out, [(r.dt, r.iters) for r in rep], dtE))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_be_pcg_bitwise_invariant_to_slab_count():
+    """C4 recipe (BE + Jacobi PCG, PTL cycling): 1, 2, 3 and 8 slabs give the
+    same iteration counts per cycle and bitwise the same field -- the PCG
+    inner products are summed per plane and then over the global planes in
+    order, whatever the split."""
+    ctx = mp.get_context("fork")
+    results = {}
+    for world in (1, 2, 3, 8):
+        q = ctx.Queue()
+        port = _free_port()
+        ps = [ctx.Process(target=_worker_c4, args=(r, world, port, "backward_euler", q)) for r in range(world)]
+        for p in ps:
+            p.start()
+        res = sorted(q.get(timeout=300) for _ in range(world))
+        for p in ps:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        assert all(r[3] == res[0][3] for r in res)
+        results[world] = (np.concatenate([r[2] for r in res], axis=1), res[0][3])
+    f1, rep1 = results[1]
+    assert sum(it for _, it in rep1) > 20
+    for world in (2, 3, 8):
+        f, rep = results[world]
+        assert rep == rep1, world
+        assert np.array_equal(f, f1), world
 
 
 @pytest.mark.parametrize("nranks", [2, 3, 8])
