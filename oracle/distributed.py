@@ -218,8 +218,10 @@ def slab_compute_ptl(sop, u_ext, F_int, eps_rel=1e-12):
     return None if math.isinf(best) else best
 
 
-def slab_cycle_operator(sop, kind, u_int, outer_dt, dt_euler, eps_rel=1e-12, tol=1e-10, max_iter=10000):
-    """oracle.ptl.cycle_operator over slabs (RKL2/RKG2 or BE+PCG)."""
+def slab_cycle_operator(sop, kind, u_int, outer_dt, dt_euler, eps_rel=1e-12, tol=1e-10, max_iter=10000,
+                        max_cycles=None):
+    """oracle.ptl.cycle_operator over slabs (RKL2/RKG2 or BE+PCG);
+    ``max_cycles``: stop after that many cycles (partial step)."""
     slab = sop.slab
     pinned = slab.interior(slab.geom.pinned[None])[0]
     report = []
@@ -227,7 +229,7 @@ def slab_cycle_operator(sop, kind, u_int, outer_dt, dt_euler, eps_rel=1e-12, tol
     u = u_int.copy()
     cyc = 0
     scheme = type("S", (), {"kind": kind, "make_odd": False})()
-    while remaining > 0.0:
+    while remaining > 0.0 and (max_cycles is None or cyc < max_cycles):
         u_ext = slab.extend(u)
         F = sop.apply_ext(u_ext)
         ptl = slab_compute_ptl(sop, u_ext, F, eps_rel)

@@ -13,6 +13,16 @@ from paper_2403_01004_b200 import configs, operators, ptl, schemes
 pytestmark = pytest.mark.gpu
 
 
+def _same_dts(a, b, kind):
+    """STS fields are bitwise the oracle's, so every PTL (and cycle dt) is
+    too; a BE field agrees to the PCG contract (~1e-10), so the PTL of the
+    next cycle agrees to about that (the cycle counts stay identical)."""
+    if kind == "backward_euler":
+        assert len(a) == len(b) and np.allclose(a, b, rtol=1e-8, atol=0.0)
+    else:
+        assert a == b
+
+
 @pytest.fixture(scope="module", params=[(24, 24, 48), (20, 40, 64)], ids=["cpasync", "tma"])
 def c3s(request):
     return configs.c3(n=request.param)
@@ -29,19 +39,19 @@ def test_static_ptl_aligned_parity(gpu_ctx, c3s, kind):
     dtE = op.device_op(c3s.grid, 1).dt_euler
     T = operators.Field(c3s.grid, c3s.fields["T"])
     sc = schemes.SchemeConfig(kind, tol=1e-9)
-    out, rep = ptl.cycle_operator(op, sc, T, 2e3 * dtE, ptl.PtlConfig(reevaluate="static"))
+    out, rep = ptl.cycle_operator(op, sc, T, 300 * dtE, ptl.PtlConfig(reevaluate="static"))
     oop = oracle_aligned(c3s.grid, c3s.bc, c3s.fields["b"], c3s.fields["T"])
     uo, repo = optl.cycle_operator(oop, optl.OracleScheme(kind, tol=1e-9), soa(c3s.fields["T"][..., None]),
-                                   2e3 * dtE, dt_euler=dtE, static=True)
+                                   300 * dtE, dt_euler=dtE, static=True)
     assert [e.iters for e in rep.entries] == [r.iters for r in repo]
-    assert [e.dt for e in rep.entries] == [r.dt for r in repo]
+    _same_dts([e.dt for e in rep.entries], [r.dt for r in repo], kind)
     a, b = out.values[..., 0], uo[0]
     if kind == "backward_euler":
         assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
     else:
         assert np.array_equal(a, b)
     # dynamic re-evaluation never needs more cycles
-    _, dyn = ptl.cycle_operator(op, sc, T, 2e3 * dtE)
+    _, dyn = ptl.cycle_operator(op, sc, T, 300 * dtE)
     assert dyn.n_cycles <= rep.n_cycles
 
 
@@ -54,23 +64,25 @@ def test_per_cycle_T0_refresh_parity(gpu_ctx, c3s, kind):
     dtE0 = op.device_op(c3s.grid, 1).dt_euler
     T = operators.Field(c3s.grid, c3s.fields["T"])
     sc = schemes.SchemeConfig(kind, tol=1e-9)
-    out, rep = ptl.cycle_operator(op, sc, T, 1e4 * dtE0, ptl.PtlConfig(refresh_T0="cycle"))
+    # (ratio 100: longer steps undershoot T below 0 on these coarse grids,
+    # which a per-cycle refresh rightly reports as a domain error)
+    out, rep = ptl.cycle_operator(op, sc, T, 100 * dtE0, ptl.PtlConfig(refresh_T0="cycle"))
     oop = oracle_aligned(c3s.grid, c3s.bc, c3s.fields["b"], c3s.fields["T"])
 
     def refresh(o, u):
         o.c = oops.aligned_coefficient(u[0], 1.0, None, 1e-10)
 
     uo, repo = optl.cycle_operator(oop, optl.OracleScheme(kind, tol=1e-9), soa(c3s.fields["T"][..., None]),
-                                   1e4 * dtE0, refresh_cycle=refresh)
+                                   100 * dtE0, refresh_cycle=refresh)
     assert [e.iters for e in rep.entries] == [r.iters for r in repo]
-    assert [e.dt for e in rep.entries] == [r.dt for r in repo]
+    _same_dts([e.dt for e in rep.entries], [r.dt for r in repo], kind)
     a, b = out.values[..., 0], uo[0]
     if kind == "backward_euler":
         assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
     else:
         assert np.array_equal(a, b)
     # the default (once per outer step) is a different advance
-    out2, rep2 = ptl.cycle_operator(op.freeze(T), sc, T, 1e4 * dtE0)
+    out2, rep2 = ptl.cycle_operator(op.freeze(T), sc, T, 100 * dtE0)
     assert not np.array_equal(out2.values, out.values)
 
 
