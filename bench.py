@@ -372,23 +372,14 @@ def run_ours(args, rank, world, local_rank):
             "dtype": "f64",
             "data": "synthetic (seeded recipes, configs.py; generated in HBM bit-identically to the host recipe; "
                     "no public dataset exists)",
-            "config": {
-                "workload": CONFIG_MODEL[name],
-                "config": name.upper(),
-                "grid": list(prob.dg.global_shape),
-                "cells": cells_global,
-                "fields": {f: nc for f, _, nc in ops_info},
-                "scheme": sc.kind + ("(" + sc.preconditioner + ")" if sc.kind == "backward_euler" else "") + "+PTL",
-                "outer_dt_over_dtE": prob.w.ratio,
-                "operators": [{"field": f, "kind": kd, "cycles": r.n_cycles,
-                               "stages_or_iters": r.total_iters} for (f, kd, _), r in zip(ops_info, rep0)],
-                "cell_updates_per_step": total_cu // max(args.steps, 1),
-                "decomposition": f"r-slabs x{world}" if world > 1 else "single GPU",
-                "l2": "inputs larger than L2 (each field %.0f MB > 126 MB)" % (cells_global * 8 / 1e6)
-                if cells_global * 8 > 126e6 else "fields L2-resident (smaller than 126 MB)",
-                "parallelism": f"slab{world}",
-                "setup_s": round(setup_s, 2),
-            },
+            "config": workload_config(
+                name, world, prob.dg.global_shape, {f: nc for f, _, nc in ops_info},
+                sc.kind + ("(" + sc.preconditioner + ")" if sc.kind == "backward_euler" else "") + "+PTL",
+                prob.w.ratio,
+                [{"field": f, "kind": kd, "cycles": r.n_cycles, "stages_or_iters": r.total_iters}
+                 for (f, kd, _), r in zip(ops_info, rep0)],
+                total_cu // max(args.steps, 1)),
+            "setup_s": round(setup_s, 2),
             "roofline": None if dom is None else {
                 "bound": "hbm",
                 "kernel": dom["kernel"],
@@ -411,7 +402,7 @@ def run_ours(args, rank, world, local_rank):
         if e2e is not None:
             line["e2e"] = e2e
         if args.cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(name, args.cpu_sample_s)
+            line["cpu_baseline"] = cpu_baseline(name, procs=1)
     if dist:
         dist.barrier()
     prob.free()
@@ -519,17 +510,32 @@ def run_e2e(args, prob, sc, pcfg, ctx, dist):
 
 
 # ---------------------------------------------------------------- CPU oracle
+# The reference CPU path is the oracle (the reference repository ships no
+# implementation of this path).  A full C3-C5 step of it takes
+# hours, so it is timed on bounded r-chunk samples of the same workload and
+# EXTRAPOLATED to the step with the step's exact work mix:
+#   T_step = sum_ops [ t_setup + cycles * (t_F+argmax+PTL + t_stage1) + (stages - cycles) * t_stage ]
+# (BE: stages = PCG iterations, t_stage = one PCG iteration, t_stage1 = the
+# PCG start r0 = b - A x0), each t_* per cell measured on the sample and
+# scaled by the step's cells.  The per-operator cycle / stage counts are the
+# config's own (identical on the oracle and the GPU: full-size parity,
+# profiles/r02_full_parity_*.json, BENCH_r01.json for C5).
+STEP_COUNTS = {  # config -> [(field, kind, ncomp, cycles, stages or PCG iterations)]
+    "c1": [("u", "scalar", 1, 477, 962)],
+    "c2": [("v", "vector", 3, 327, 803)],
+    "c3": [("T", "aligned", 1, 11, 466)],
+    "c4": [("T", "aligned", 1, 6, 576)],
+    "c5": [("T", "aligned_rho", 1, 45, 1406), ("v", "vector_rho", 3, 1, 2)],
+}
 
-def _oracle_chunk(job):
-    """Run `stages` oracle RKL2 stages of each operator of the config on an
-    r-chunk (its own sub-domain); returns (cell-updates, seconds)."""
-    name, lo, nplanes, stages = job
+
+def _chunk_ops(name, lo, nplanes):
+    """The config's oracle operators on the r-chunk [lo, lo + nplanes) (its
+    own sub-domain with pinned ends) and their initial states."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from helpers import oracle_aligned, oracle_scalar, soa
-    from oracle import schemes as osch
     from paper_2403_01004_b200 import configs, mesh
-    n = {"c1": (48, 48, 96), "c2": (128, 128, 256), "c3": (256, 256, 512), "c4": (512, 512, 1024),
-         "c5": (768, 768, 1536)}[name]
+    n = CONFIG_SHAPE[name]
     if name in ("c3", "c4", "c5"):
         full = mesh.build_spherical_grid(configs.r_stretched_c3(n[0]), n[1], n[2])
     elif name == "c2":
@@ -539,63 +545,150 @@ def _oracle_chunk(job):
     bc = configs.spherical_bc("dirichlet")
     sub = mesh.Grid((full.coords[0][lo:lo + nplanes], full.coords[1], full.coords[2]), full.metric)
     seed = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}[name]
-    work = []  # (oracle operator, u0)
+    work = []
     if name in ("c3", "c4", "c5"):
         T = configs.temperature(full, seed, i0=lo, n0=nplanes)
         b = configs.dipole_bhat(full, seed, i0=lo, n0=nplanes)
         rho = None
         if name == "c5":
             rho = np.exp(-10.0 * (full.coords[0][lo:lo + nplanes] - 1.0))[:, None, None] * np.ones(sub.shape)
-        work.append((oracle_aligned(sub, bc, b, T, rho=rho), T[None].copy()))
+        work.append(("T", (sub, bc, b, T, rho), T[None].copy(), oracle_aligned))
         if name == "c5":
-            work.append((oracle_scalar(sub, bc, nu=1.0, rho=rho, ncomp=3, vector_metric=True),
-                         soa(configs.harmonic_velocity(full, seed, i0=lo, n0=nplanes))))
+            work.append(("v", (sub, bc, 1.0, rho, 3, True),
+                         soa(configs.harmonic_velocity(full, seed, i0=lo, n0=nplanes)), oracle_scalar))
     elif name == "c2":
-        work.append((oracle_scalar(sub, bc, ncomp=3, vector_metric=True),
-                     soa(configs.harmonic_velocity(full, 2, i0=lo, n0=nplanes))))
+        work.append(("v", (sub, bc, 1.0, None, 3, True), soa(configs.harmonic_velocity(full, 2, i0=lo, n0=nplanes)),
+                     oracle_scalar))
     else:
-        work.append((oracle_scalar(sub, bc), configs.c1().fields["u"][lo:lo + nplanes][None].copy()))
-    cu, secs = 0, 0.0
-    for op, u0 in work:
-        dtE = op.euler_dt()
-        y0 = op.apply(u0)
+        work.append(("u", (sub, bc), configs.c1().fields["u"][lo:lo + nplanes][None].copy(), oracle_scalar))
+    return work
+
+
+def _oracle_chunk(job):
+    """Per-cell times of every piece of the step on one r-chunk sample:
+    setup (coefficients + Gershgorin), F + argmax + PTL pairs, stage 1 and a
+    stage k >= 2 (RKL2) or the PCG start and one PCG iteration (BE)."""
+    name, lo, nplanes = job
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle import ptl as optl
+    from oracle import schemes as osch
+    be = name == "c4"
+    out = {}
+    for field, args, u0, make in _chunk_ops(name, lo, nplanes):
         t = time.perf_counter()
-        osch.sts_step(op.apply, u0, y0, 10 * dtE, stages, "rkl2", op.geom.pinned)
-        secs += time.perf_counter() - t
-        cu += int(np.prod(op.geom.shape)) * (stages - 1)  # stages 2..s each one full pass
-    return cu, secs
+        if make.__name__ == "oracle_aligned":
+            sub, bc, b, T, rho = args
+            op = make(sub, bc, b, T, rho=rho)  # c = f(T0): the coefficient setup
+        else:
+            op = make(*args[:2], **dict(zip(("nu", "rho", "ncomp", "vector_metric"), args[2:])))
+        lam, diag = op.bound_and_diag()
+        dtE = optl.ops.euler_dt(lam)
+        t_setup = time.perf_counter() - t
+        t = time.perf_counter()
+        F = op.apply(u0)
+        optl.compute_ptl(u0, F, op.geom)
+        t_F = time.perf_counter() - t
+        cells = int(np.prod(op.geom.shape))
+        if be:
+            W = op.weights()
+            times = []
+            for it in (1, 2):  # PCG start + it iterations (tol unreachable)
+                t = time.perf_counter()
+                osch.backward_euler_step(op.apply, diag, W, u0, 100 * dtE, 1e-300, it, op.geom.pinned)
+                times.append(time.perf_counter() - t)
+            t_stage = times[1] - times[0]
+            t_stage1 = max(times[0] - t_stage, 0.0)
+        else:
+            times = []
+            for s in (2, 3):
+                t = time.perf_counter()
+                osch.sts_step(op.apply, u0, F, 10 * dtE, s, "rkl2", op.geom.pinned)
+                times.append(time.perf_counter() - t)
+            t_stage = times[1] - times[0]
+            t_stage1 = max(times[0] - t_stage, 0.0)
+        out[field] = {"cells": cells, "setup": t_setup / cells, "F": t_F / cells, "stage1": t_stage1 / cells,
+                      "stage": t_stage / cells}
+    return out
 
 
-def cpu_baseline(name, budget_s=20.0, procs=1):
-    """Oracle (numpy, single thread) on an r-chunk sample."""
-    n0 = {"c1": 48, "c2": 128, "c3": 256, "c4": 512, "c5": 768}[name]
-    planes = {"c1": 48, "c2": 16, "c3": 8, "c4": 4, "c5": 3}[name]
-    stages = 4
+def cpu_baseline(name, procs=1, planes=None):
+    """The oracle on ``procs`` host processes (one r-chunk each, run
+    concurrently), extrapolated to one full step of the config."""
+    n = CONFIG_SHAPE[name]
+    planes = planes or {"c1": 48, "c2": 16, "c3": 8, "c4": 3, "c5": 3}[name]
     t0 = time.perf_counter()
-    jobs = [(name, (k * planes) % max(1, n0 - planes + 1), planes, stages) for k in range(procs)]
+    jobs = [(name, (k * planes) % max(1, n[0] - planes + 1), planes) for k in range(procs)]
     if procs == 1:
         res = [_oracle_chunk(jobs[0])]
     else:
         import multiprocessing as mp
         with mp.get_context("fork").Pool(procs) as pool:
             res = pool.map(_oracle_chunk, jobs)
-    cells = sum(r[0] for r in res)
-    secs = max(r[1] for r in res)
-    return {"value": cells / secs, "unit": "cell-updates/s", "cores": procs, "kind": "port",
-            "sample": f"{procs} x r-chunk of {planes} planes of {name.upper()}, {stages - 1} fused RKL2 stages each "
-                      f"(numpy oracle, oracle/operators.py); wall {time.perf_counter() - t0:.1f} s"}
+    wall = time.perf_counter() - t0
+    cells = int(np.prod(n))
+    t_step = 0.0
+    parts = {}
+    cu = 0
+    for field, kind, nc, cycles, stages in STEP_COUNTS[name]:
+        # concurrent chunks: per-cell time of the whole machine = the slowest
+        # process's per-cell time / procs (perfect r-slab scaling assumed)
+        per = {k: max(r[field][k] for r in res) / procs for k in ("setup", "F", "stage1", "stage")}
+        t_op = cells * (per["setup"] + cycles * (per["F"] + per["stage1"]) + (stages - cycles) * per["stage"])
+        parts[field] = {"cycles": cycles, "stages_or_iters": stages, "t_op_s": round(t_op, 1),
+                        "ns_per_cell": {k: round(v * 1e9, 2) for k, v in per.items()}}
+        t_step += t_op
+        cu += cells * stages
+    return {"value": cu / t_step, "unit": "cell-updates/s", "cores": procs, "kind": "port",
+            "extrapolated": True, "ms_per_step_extrapolated": 1e3 * t_step,
+            "sample": f"{procs} concurrent process(es), each an r-chunk of {planes} planes of {name.upper()} "
+                      f"(numpy oracle, oracle/): coefficient setup + Gershgorin, F + argmax + PTL, stage 1 and "
+                      f"stage-k (RKL2) / PCG-start and PCG-iteration times per cell, extrapolated with the step's "
+                      f"exact cycle and stage counts; sample wall {wall:.1f} s",
+            "parts": parts}
+
+
+def workload_config(name, world, grid, fields, scheme, ratio, operators, cu_per_step):
+    """The `config` dict of both arms (the driver compares them)."""
+    cells = int(np.prod(grid))
+    return {
+        "workload": CONFIG_MODEL[name],
+        "config": name.upper(),
+        "grid": list(grid),
+        "cells": cells,
+        "fields": fields,
+        "scheme": scheme,
+        "outer_dt_over_dtE": ratio,
+        "operators": operators,
+        "cell_updates_per_step": cu_per_step,
+        "decomposition": f"r-slabs x{world}" if world > 1 else "single GPU",
+        "l2": "inputs larger than L2 (each field %.0f MB > 126 MB)" % (cells * 8 / 1e6)
+        if cells * 8 > 126e6 else "fields L2-resident (smaller than 126 MB)",
+        "parallelism": f"slab{world}",
+    }
+
+
+def reference_config(name, world):
+    ops = STEP_COUNTS[name]
+    cells = int(np.prod(CONFIG_SHAPE[name]))
+    kind = "backward_euler(jacobi)+PTL" if name == "c4" else "rkl2+PTL"
+    return workload_config(name, world, CONFIG_SHAPE[name], {f: nc for f, _, nc, _, _ in ops}, kind,
+                           {"c1": 500.0, "c2": 2000.0, "c3": 1e4, "c4": 1e4, "c5": 5e4}[name],
+                           [{"field": f, "kind": "aligned" if k.startswith("aligned") else "scalar", "cycles": c,
+                             "stages_or_iters": st} for f, k, _, c, st in ops],
+                           sum(cells * st for _, _, _, _, st in ops))
 
 
 def run_reference(args, rank, world):
+    """The reference CPU path (the oracle port) on all host cores: each step
+    is one bounded concurrent sample extrapolated to the full step; the
+    line's value is the median step, its ms_per_step the extrapolated step
+    time of the reference on this host."""
     if rank != 0:
         return None
     procs = os.cpu_count() or 1
-    vals = []
-    for _ in range(args.warmup):
+    for _ in range(min(args.warmup, 1)):  # (one warm-up sample: page-in and imports; keeps the run to minutes)
         cpu_baseline(args.config, procs=procs)
-    t_all = time.perf_counter()
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(args.config, procs=procs))
+    vals = [cpu_baseline(args.config, procs=procs) for _ in range(args.steps)]
     v = statistics.median(x["value"] for x in vals)
     cb = dict(vals[-1])
     cb["value"] = v
@@ -607,15 +700,16 @@ def run_reference(args, rank, world):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1e3 * (time.perf_counter() - t_all) / max(args.steps, 1),
+        "ms_per_step": statistics.median(x["ms_per_step_extrapolated"] for x in vals),
+        "ms_per_step_kind": "extrapolated full step of the reference CPU path (see cpu_baseline.sample)",
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded recipe, configs.py)",
-        "config": {"workload": CONFIG_MODEL[args.config], "config": args.config.upper(),
-                   "note": "the reference repo ships no implementation of this path; its CPU algorithm is "
-                           "the numpy oracle (oracle/), run on all host cores over r-chunks"},
+        "data": "synthetic (seeded recipes, configs.py; no public dataset exists)",
+        "config": reference_config(args.config, world),
+        "note": "the reference repo ships no implementation of this path; its CPU algorithm is the numpy oracle "
+                "(oracle/, the SPEC restatement), run on all host cores over r-chunks and extrapolated",
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -669,7 +763,6 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
-    ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--dry-run", action="store_true",
                     help="start the N ranks, check the process group, print one line (no GPU work)")
     args = ap.parse_args()
