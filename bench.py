@@ -72,9 +72,11 @@ CONFIG_MODEL = {
     "c5": "C5 coupled Spitzer conduction + vector viscosity (rho field) 768x768x1536 spherical, "
           "one split MAS step of 5e4 dtE",
 }
+CONFIG_MODEL["c5v"] = ("C5 viscosity operator alone (3-component vector viscosity with metric terms, rho field) "
+                       "768x768x1536 spherical, one step of 5e4 dtE(viscosity) -- the C5 vector kernel at full weight")
 DEFAULT_CONFIG = "c5"
 CONFIG_SHAPE = {"c1": (48, 48, 96), "c2": (128, 128, 256), "c3": (256, 256, 512), "c4": (512, 512, 1024),
-                "c5": (768, 768, 1536)}
+                "c5": (768, 768, 1536), "c5v": (768, 768, 1536)}
 
 
 def _peaks():
@@ -172,6 +174,8 @@ class Problem:
         kw = {} if n is None else {"n": n}
         if name in ("c3", "c4", "c5"):
             w = getattr(configs, name)(host=False, **kw)
+        elif name == "c5v":
+            w = configs.c5(host=False, **kw)
         else:
             w = getattr(configs, name)(**kw)
         self.w = w
@@ -190,6 +194,12 @@ class Problem:
                 self.fields["v"] = device.DeviceField(dg, 3)
                 vcfg = operators.ScalarDiffusionConfig(nu=1.0, rho=rho, bc=w.bc, vector_metric=True)
                 self.ops.append(("v", operators.DiffusionOperator.scalar(vcfg, 3), 3, "vector_rho"))
+        elif name == "c5v":
+            rho = configs.gen_radial(device.DeviceField(dg, 1), w.meta["rho_r"])
+            self.rho = rho
+            self.fields["v"] = device.DeviceField(dg, 3)
+            vcfg = operators.ScalarDiffusionConfig(nu=1.0, rho=rho, bc=w.bc, vector_metric=True)
+            self.ops.append(("v", operators.DiffusionOperator.scalar(vcfg, 3), 3, "vector_rho"))
         elif name == "c2":
             self.v0 = device.DeviceField.from_values(dg, w.fields["v"])
             self.fields["v"] = device.DeviceField(dg, 3)
@@ -215,7 +225,7 @@ class Problem:
         w = self.w
         if "T" in self.fields:
             configs.gen_temperature(self.fields["T"], w.grid, w.seed)
-        if self.name == "c5":
+        if self.name in ("c5", "c5v"):
             configs.gen_harmonic(self.fields["v"], w.grid, w.seed)
         elif self.name == "c2":
             self.fields["v"].copy_from(self.v0)
@@ -226,9 +236,8 @@ class Problem:
         from paper_2403_01004_b200 import ptl
         self.reset()
         st = ptl.split_advance([(f, op) for f, op, _, _ in self.ops], self.fields, self.outer_dt,
-                                     [(sc, pcfg)] * len(self.ops))
-        reps = st.reports
-        return reps
+                               [(sc, pcfg)] * len(self.ops))
+        return st.reports
 
     def host_inputs(self):
         """Pinned-host copies of every input of a step (for the e2e leg)."""
@@ -239,11 +248,10 @@ class Problem:
             out[k] = np.ascontiguousarray(f.download())
         if self.name in ("c1", "c2"):  # the initial state (fields may have been advanced)
             out[self.ops[0][0]] = np.ascontiguousarray((self.u0 if self.name == "c1" else self.v0).download())
-        elif "T" in self.fields:
+        else:
             self.reset()
-            out["T"] = np.ascontiguousarray(self.fields["T"].download())
-            if self.name == "c5":
-                out["v"] = np.ascontiguousarray(self.fields["v"].download())
+            for k in self.fields:
+                out[k] = np.ascontiguousarray(self.fields[k].download())
         return out
 
     def free(self):
@@ -280,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
         n_over = (base[0] * world, base[1], base[2])
     prob = Problem(name, ctx, n_over)
     sc = scheme_for(name, args)
-    pcfg = ptl.PtlConfig()
+    pcfg = ptl.PtlConfig(enabled=not args.no_ptl)
     setup_s = time.perf_counter() - t_setup
 
     for _ in range(args.warmup):
@@ -374,7 +382,8 @@ def run_ours(args, rank, world, local_rank):
                     "no public dataset exists)",
             "config": workload_config(
                 name, world, prob.dg.global_shape, {f: nc for f, _, nc in ops_info},
-                sc.kind + ("(" + sc.preconditioner + ")" if sc.kind == "backward_euler" else "") + "+PTL",
+                sc.kind + ("(" + sc.preconditioner + ")" if sc.kind == "backward_euler" else "") +
+                ("" if args.no_ptl else "+PTL"),
                 prob.w.ratio,
                 [{"field": f, "kind": kd, "cycles": r.n_cycles, "stages_or_iters": r.total_iters}
                  for (f, kd, _), r in zip(ops_info, rep0)],
@@ -526,6 +535,7 @@ STEP_COUNTS = {  # config -> [(field, kind, ncomp, cycles, stages or PCG iterati
     "c3": [("T", "aligned", 1, 11, 466)],
     "c4": [("T", "aligned", 1, 6, 576)],
     "c5": [("T", "aligned_rho", 1, 45, 1406), ("v", "vector_rho", 3, 1, 2)],
+    "c5v": [("v", "vector_rho", 3, 1, 447)],  # (placeholder until the first GPU run: see profiles/)
 }
 
 
@@ -536,7 +546,7 @@ def _chunk_ops(name, lo, nplanes):
     from helpers import oracle_aligned, oracle_scalar, soa
     from paper_2403_01004_b200 import configs, mesh
     n = CONFIG_SHAPE[name]
-    if name in ("c3", "c4", "c5"):
+    if name in ("c3", "c4", "c5", "c5v"):
         full = mesh.build_spherical_grid(configs.r_stretched_c3(n[0]), n[1], n[2])
     elif name == "c2":
         full = mesh.build_spherical_grid(configs.r_geometric_ratio(n[0], 1.0, 2.5, 1.01), n[1], n[2])
@@ -544,9 +554,13 @@ def _chunk_ops(name, lo, nplanes):
         full = mesh.build_spherical_grid(configs.r_uniform(n[0], 1.0, 2.5), n[1], n[2])
     bc = configs.spherical_bc("dirichlet")
     sub = mesh.Grid((full.coords[0][lo:lo + nplanes], full.coords[1], full.coords[2]), full.metric)
-    seed = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}[name]
+    seed = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5, "c5v": 5}[name]
     work = []
-    if name in ("c3", "c4", "c5"):
+    if name == "c5v":
+        rho = np.exp(-10.0 * (full.coords[0][lo:lo + nplanes] - 1.0))[:, None, None] * np.ones(sub.shape)
+        work.append(("v", (sub, bc, 1.0, rho, 3, True),
+                     soa(configs.harmonic_velocity(full, seed, i0=lo, n0=nplanes)), oracle_scalar))
+    elif name in ("c3", "c4", "c5"):
         T = configs.temperature(full, seed, i0=lo, n0=nplanes)
         b = configs.dipole_bhat(full, seed, i0=lo, n0=nplanes)
         rho = None
@@ -615,7 +629,7 @@ def cpu_baseline(name, procs=1, planes=None):
     """The oracle on ``procs`` host processes (one r-chunk each, run
     concurrently), extrapolated to one full step of the config."""
     n = CONFIG_SHAPE[name]
-    planes = planes or {"c1": 48, "c2": 16, "c3": 8, "c4": 3, "c5": 3}[name]
+    planes = planes or {"c1": 48, "c2": 16, "c3": 8, "c4": 3, "c5": 3, "c5v": 3}[name]
     t0 = time.perf_counter()
     jobs = [(name, (k * planes) % max(1, n[0] - planes + 1), planes) for k in range(procs)]
     if procs == 1:
@@ -672,7 +686,7 @@ def reference_config(name, world):
     cells = int(np.prod(CONFIG_SHAPE[name]))
     kind = "backward_euler(jacobi)+PTL" if name == "c4" else "rkl2+PTL"
     return workload_config(name, world, CONFIG_SHAPE[name], {f: nc for f, _, nc, _, _ in ops}, kind,
-                           {"c1": 500.0, "c2": 2000.0, "c3": 1e4, "c4": 1e4, "c5": 5e4}[name],
+                           {"c1": 500.0, "c2": 2000.0, "c3": 1e4, "c4": 1e4, "c5": 5e4, "c5v": 5e4}[name],
                            [{"field": f, "kind": "aligned" if k.startswith("aligned") else "scalar", "cycles": c,
                              "stages_or_iters": st} for f, k, _, c, st in ops],
                            sum(cells * st for _, _, _, _, st in ops))
@@ -752,7 +766,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c1", "c2", "c3", "c4", "c5", "c5v"])
     ap.add_argument("--scheme", default=None, choices=[None, "rkl2", "rkg2", "be"])
     ap.add_argument("--pc", default="jacobi", choices=["jacobi", "line-r"],
                     help="BE+PCG preconditioner (default: point Jacobi, the SPEC's PC1)")
@@ -763,6 +777,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-ptl", action="store_true",
+                    help="one cycle of the whole outer step (no PTL cycling; time-to-solution comparisons)")
     ap.add_argument("--dry-run", action="store_true",
                     help="start the N ranks, check the process group, print one line (no GPU work)")
     args = ap.parse_args()

@@ -91,17 +91,24 @@ int pc_ctx_destroy(pc_ctx* ctx);
    exchange) and the caller sets the axis-0 ghost planes with
    pc_field_set_ghost; used to check the slab kernels on one GPU */
 int pc_ctx_create_detached(int device, int nranks, int rank, pc_ctx** out);
+/* slab decomposition axis of a multi-rank context: 0 = r-slabs (default,
+   axis-0 ghost planes), 2 = phi-slabs (BASELINE C4's split: each rank owns
+   phi columns [k0, k0 + n) of every plane and keeps one ghost column on each
+   side, exchanged over a periodic NCCL ring).  Set before creating grids. */
+int pc_ctx_set_decomposition(pc_ctx* ctx, int axis);
 int pc_ctx_sync(pc_ctx* ctx);
 int pc_nccl_unique_id(void* out128); /* fills a fresh ncclUniqueId */
 
 /* ---- grid.  shape = LOCAL (n0, n1, n2).  iflags (PC_GRID_NFLAGS ints):
  *  [0..2] periodic per axis, [3..8] pinned lo/hi per axis (Dirichlet),
  *  [9] ghost_lo0 (a lower axis-0 neighbour rank exists), [10] ghost_hi0,
- *  [11] global n0, [12] global axis-0 offset of this slab, [13] spherical.
+ *  [11] global n0, [12] global axis-0 offset of this slab, [13] spherical,
+ *  [14] phi-slab (local columns 0 and n2-1 are ghost columns: pinned, zero
+ *  weight), [15] global n2, [16] global phi offset of local column 1.
  * tables: pc_grid_table_size(shape) doubles in the order documented in
  * paper_2403_01004_b200/geometry.py (TABLE_ORDER); 2-D tables carry axis-0
  * ghost rows (n0 + 2 rows). */
-#define PC_GRID_NFLAGS 14
+#define PC_GRID_NFLAGS 17
 int64_t pc_grid_table_size(const int64_t shape[3]);
 int pc_grid_create(pc_ctx* ctx, const int64_t shape[3], const int32_t* iflags,
                    const double* tables, int64_t ntables, pc_grid** out);
@@ -137,6 +144,9 @@ int pc_field_count(const pc_field* f, int test, int64_t* count);
 /* write ghost plane -1 (side 0) or n0 (side 1) of every component from a host
    SoA plane [ncomp][n1][n2] */
 int pc_field_set_ghost(pc_field* f, int side, const double* host);
+/* phi-slab test hook: write both ghost columns of every component from host
+   [ncomp][2][n0 * n1] (side 0 = column 0, side 1 = column n2 - 1) */
+int pc_field_set_ghost_cols(pc_field* f, const double* host);
 /* pin / unpin a host buffer so uploads and downloads run at full PCIe speed */
 int pc_host_register(void* ptr, size_t bytes);
 int pc_host_unregister(void* ptr);

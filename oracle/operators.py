@@ -263,7 +263,7 @@ def aligned_E(geom, T, beta):
 
 
 def aligned_apply(geom, T, b, c, rho=None, pref=1.0):
-    """F(T) = -((G * iVal) * pref) / rho, G = dQ/dT (see module docstring).
+    """F(T) = (G * iVal) * (0 - pref / rho), G = dQ/dT (see module docstring).
 
     T: (n0, n1, n2); b: (3, n0, n1, n2); c: (n0, n1, n2) nodal conductivity.
     G is summed in the order an r-marching kernel produces it:
@@ -279,9 +279,10 @@ def aligned_apply(geom, T, b, c, rho=None, pref=1.0):
         shift_zero(E[(2, "+")], 2, -1, per[2]) - shift_zero(E[(2, "-")], 2, 1, per[2]))
     G = (shift_zero(E[(0, "+")], 0, -1, per[0]) - shift_zero(E[(0, "-")], 0, 1, per[0])) + (own + nbr)
     iv = _b2(geom.iVal2) * _b1(geom.iValg)
-    F = ((0.0 - G) * iv) * pref
-    if rho is not None:
-        F = F / rho
+    # prefactor and density as one scale 0 - pref / rho (SPEC.md:117 F = pref/rho div(...)):
+    # one product per node on the device, the division once per plane for a radial rho
+    nscale = (0.0 - pref) if rho is None else 0.0 - (pref / rho)
+    F = (G * iv) * nscale
     F = F.copy()
     F[geom.pinned] = 0.0
     return F

@@ -56,6 +56,8 @@ _SIGS = {
     "pc_op_set_preconditioner": (c_int, [c_void_p, c_int]),
     "pc_op_set_refresh": (c_int, [c_void_p, c_int]),
     "pc_field_set_ghost": (c_int, [c_void_p, c_int, POINTER(c_double)]),
+    "pc_field_set_ghost_cols": (c_int, [c_void_p, POINTER(c_double)]),
+    "pc_ctx_set_decomposition": (c_int, [c_void_p, c_int]),
     "pc_ctx_destroy": (c_int, [c_void_p]),
     "pc_ctx_sync": (c_int, [c_void_p]),
     "pc_nccl_unique_id": (c_int, [c_void_p]),

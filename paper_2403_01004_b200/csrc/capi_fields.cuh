@@ -78,6 +78,11 @@ int pc_ctx_create(int device, int nranks, int rank, const void* nccl_uid, pc_ctx
 int pc_ctx_create_detached(int device, int nranks, int rank, pc_ctx** out) {
   return ctx_create(device, nranks, rank, nullptr, true, out);
 }
+int pc_ctx_set_decomposition(pc_ctx* c, int axis) {
+  if (!c || (axis != 0 && axis != 2)) return fail(PC_E_INVALID, "decomposition axis must be 0 (r) or 2 (phi)");
+  c->axis = axis;
+  return PC_OK;
+}
 
 int pc_ctx_destroy(pc_ctx* c) {
   if (c) {
@@ -106,6 +111,7 @@ int pc_ctx_destroy(pc_ctx* c) {
     nccl::Api* A = nccl::api();
     if (A) A->commDestroy(c->comm);
   }
+  cudaFree(c->phibuf);
   cudaFree(c->pslot[0]);
   cudaFree(c->pslot[1]);
   cudaFree(c->pvec);
@@ -235,6 +241,19 @@ int pc_grid_create(pc_ctx* c, const int64_t shape[3], const int32_t* fl, const d
   d.n0g = fl[11];
   d.i0g = fl[12];
   d.spherical = fl[13];
+  d.phis = fl[14];
+  d.n2g = fl[15];
+  d.k0g = fl[16];
+  if (d.phis) {
+    if (c->axis != 2 || !d.per2 || !d.pin_lo2 || !d.pin_hi2 || d.n2 < 3 || d.ghost_lo0 || d.ghost_hi0 ||
+        d.k0g < 0 || d.k0g + d.n2 - 2 > d.n2g) {
+      delete g;
+      return fail(PC_E_INVALID, "phi-slab grid: periodic phi, pinned ghost columns, a phi-decomposed context");
+    }
+  } else {
+    d.n2g = d.n2;
+    d.k0g = 0;
+  }
   g->comp_elems = (size_t)(shape[0] + 2) * (size_t)d.plane;
   {  // the marching kernels rely on unit axis-0/1 column factors iL1 (geometry.py)
     int64_t A, K, J;
@@ -347,10 +366,34 @@ static int ensure_staging(pc_ctx* c, size_t bytes) {
 
 // host -> field on stream st (AoS components go through st's staging buffer
 // in 256 MB plane chunks and are transposed on the device)
+// host plane of a field: n1 x the owned columns (phi-slabs: without the ghost columns)
+static size_t host_plane(const pc_grid* g) { return (size_t)g->g.n1 * (size_t)(g->g.n2 - 2 * g->g.phis); }
 static int upload_on(pc_field* f, const double* host, int layout, cudaStream_t st, double*& stg, size_t& stg_bytes) {
   pc_grid* g = f->grid;
   pc_ctx* c = g->ctx;
   const size_t pl = (size_t)g->g.plane, n0 = (size_t)g->g.n0;
+  if (g->g.phis) {  // owned columns only: strided rows (SoA) or the chunked transposition (AoS)
+    const size_t hn2 = (size_t)g->g.n2 - 2, hpl = host_plane(g);
+    if (layout == PC_LAYOUT_SOA || f->ncomp == 1) {
+      for (int q = 0; q < f->ncomp; ++q)
+        CUDA_TRY(cudaMemcpy2DAsync(f->base(q) + 1, (size_t)g->g.n2 * sizeof(double), host + (size_t)q * n0 * hpl,
+                                   hn2 * sizeof(double), hn2 * sizeof(double), n0 * (size_t)g->g.n1,
+                                   cudaMemcpyHostToDevice, st));
+      return PC_OK;
+    }
+    const size_t chunk_planes = std::max<size_t>(1, std::min<size_t>(n0, (256u << 20) / (hpl * f->ncomp * 8)));
+    TRY(ensure_staging_on(st, stg, stg_bytes, chunk_planes * hpl * f->ncomp * sizeof(double)));
+    for (size_t p0 = 0; p0 < n0; p0 += chunk_planes) {
+      size_t np = std::min(chunk_planes, n0 - p0);
+      CUDA_TRY(cudaMemcpyAsync(stg, host + p0 * hpl * f->ncomp, np * hpl * f->ncomp * sizeof(double),
+                               cudaMemcpyHostToDevice, st));
+      k_aos_to_soa<<<grid_blocks(c, (int64_t)(np * hpl)), kThreads, 0, st>>>(g->g, f->ncomp, stg, fld(f), (int)p0,
+                                                                              (int)np);
+      c->st.launches++;
+      TRY(check_launch("k_aos_to_soa"));
+    }
+    return PC_OK;
+  }
   if (layout == PC_LAYOUT_SOA || f->ncomp == 1) {
     for (int q = 0; q < f->ncomp; ++q)
       CUDA_TRY(cudaMemcpyAsync(f->base(q), host + (size_t)q * n0 * pl, n0 * pl * sizeof(double),
@@ -375,6 +418,28 @@ static int download_on(const pc_field* f, double* host, int layout, cudaStream_t
   pc_grid* g = f->grid;
   pc_ctx* c = g->ctx;
   const size_t pl = (size_t)g->g.plane, n0 = (size_t)g->g.n0;
+  if (g->g.phis) {
+    const size_t hn2 = (size_t)g->g.n2 - 2, hpl = host_plane(g);
+    if (layout == PC_LAYOUT_SOA || f->ncomp == 1) {
+      for (int q = 0; q < f->ncomp; ++q)
+        CUDA_TRY(cudaMemcpy2DAsync(host + (size_t)q * n0 * hpl, hn2 * sizeof(double), f->base(q) + 1,
+                                   (size_t)g->g.n2 * sizeof(double), hn2 * sizeof(double), n0 * (size_t)g->g.n1,
+                                   cudaMemcpyDeviceToHost, st));
+      return PC_OK;
+    }
+    const size_t chunk_planes = std::max<size_t>(1, std::min<size_t>(n0, (256u << 20) / (hpl * f->ncomp * 8)));
+    TRY(ensure_staging_on(st, stg, stg_bytes, chunk_planes * hpl * f->ncomp * sizeof(double)));
+    for (size_t p0 = 0; p0 < n0; p0 += chunk_planes) {
+      size_t np = std::min(chunk_planes, n0 - p0);
+      k_soa_to_aos<<<grid_blocks(c, (int64_t)(np * hpl)), kThreads, 0, st>>>(g->g, f->ncomp, cfld(f), stg, (int)p0,
+                                                                              (int)np);
+      c->st.launches++;
+      TRY(check_launch("k_soa_to_aos"));
+      CUDA_TRY(cudaMemcpyAsync(host + p0 * hpl * f->ncomp, stg, np * hpl * f->ncomp * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
+    }
+    return PC_OK;
+  }
   if (layout == PC_LAYOUT_SOA || f->ncomp == 1) {
     for (int q = 0; q < f->ncomp; ++q)
       CUDA_TRY(cudaMemcpyAsync(host + (size_t)q * n0 * pl, f->base(q), n0 * pl * sizeof(double),
@@ -464,6 +529,21 @@ int pc_field_set_ghost(pc_field* f, int side, const double* host) {
     CUDA_TRY(cudaMemcpyAsync(f->base(q) + plane * (int64_t)pl, host + (size_t)q * pl, pl * sizeof(double),
                              cudaMemcpyHostToDevice, g->ctx->s));
   CUDA_TRY(cudaStreamSynchronize(g->ctx->s));
+  return PC_OK;
+}
+
+int pc_field_set_ghost_cols(pc_field* f, const double* host) {
+  if (!f || !host || !f->grid->g.phis) return fail(PC_E_INVALID, "ghost columns need a phi-slab field");
+  field_dep(f);
+  pc_grid* g = f->grid;
+  pc_ctx* c = g->ctx;
+  const size_t rows = (size_t)g->g.n0 * g->g.n1;
+  TRY(ensure_staging(c, 2 * rows * f->ncomp * sizeof(double)));
+  CUDA_TRY(cudaMemcpyAsync(c->staging, host, 2 * rows * f->ncomp * sizeof(double), cudaMemcpyHostToDevice, c->s));
+  k_phi_unpack<<<grid_blocks(c, (int64_t)rows), kThreads, 0, c->s>>>(g->g, f->ncomp, c->staging, fld(f));
+  c->st.launches++;
+  TRY(check_launch("k_phi_unpack"));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
   return PC_OK;
 }
 

@@ -84,6 +84,9 @@ struct pc_ctx {
   size_t pslot_cap = 0;
   double* pvec = nullptr;
   double* pvec_all = nullptr;
+  int axis = 0;                 // slab decomposition axis: 0 = r (planes), 2 = phi (columns, ghost columns)
+  double* phibuf = nullptr;     // phi-slab exchange: packed send [ncomp][2][rows] + receive halves
+  size_t phibuf_cap = 0;
   int pvec_n0g = 0, pvec_i0g = -1, pvec_n = 0;
   // pinned host mirrors
   ArgRes* h_res = nullptr;
@@ -308,9 +311,11 @@ static int check_launch(const char* what) {
 }
 
 // ------------------------------------------------------------------ NCCL
+static int phi_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp, cudaStream_t st);
 static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp, cudaStream_t st = nullptr) {
   if (!c->comm) return PC_OK;  // one rank, or a detached test rank (ghosts set by the caller)
   if (!st) st = c->s;
+  if (g->g.phis) return phi_exchange(c, g, bufs, ncomp, st);
   nccl::Api* A = nccl::api();
   if (!A) return fail(PC_E_NCCL, "NCCL not available");
   const size_t pl = (size_t)g->g.plane;
@@ -331,6 +336,47 @@ static int halo_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp, 
   }
   if (A->groupEnd() != 0) return fail(PC_E_NCCL, "ncclGroupEnd");
   return PC_OK;
+}
+// phi-slabs: the owned edge columns of every (plane, row) packed, swapped
+// with the ring neighbours (rank - 1, rank + 1 mod P; the same pairing order
+// as the planes, so a one- or two-rank ring pairs right) and unpacked into
+// the ghost columns
+static int phi_exchange(pc_ctx* c, pc_grid* g, double* const* bufs, int ncomp, cudaStream_t st) {
+  nccl::Api* A = nccl::api();
+  if (!A) return fail(PC_E_NCCL, "NCCL not available");
+  const size_t rows = (size_t)g->g.n0 * g->g.n1;
+  const size_t need = 4 * rows * (size_t)ncomp;
+  if (need > c->phibuf_cap) {
+    cudaStreamSynchronize(st);
+    cudaFree(c->phibuf);
+    c->phibuf = nullptr;
+    c->phibuf_cap = 0;
+    CUDA_TRY(cudaMalloc(&c->phibuf, need * sizeof(double)));
+    c->phibuf_cap = need;
+  }
+  double* snd = c->phibuf;
+  double* rcv = c->phibuf + 2 * rows * (size_t)ncomp;
+  CFld src{{bufs[0] + g->g.plane, ncomp > 1 ? bufs[1] + g->g.plane : nullptr, ncomp > 2 ? bufs[2] + g->g.plane : nullptr}};
+  Fld dst{{bufs[0] + g->g.plane, ncomp > 1 ? bufs[1] + g->g.plane : nullptr, ncomp > 2 ? bufs[2] + g->g.plane : nullptr}};
+  k_phi_pack<<<grid_blocks(c, (int64_t)rows), kThreads, 0, st>>>(g->g, ncomp, src, snd);
+  c->st.launches++;
+  TRY(check_launch("k_phi_pack"));
+  const int lo = (c->rank - 1 + c->nranks) % c->nranks, hi = (c->rank + 1) % c->nranks;
+  if (A->groupStart() != 0) return fail(PC_E_NCCL, "ncclGroupStart");
+  for (int q = 0; q < ncomp; ++q) {
+    double* s_lo = snd + (2 * q) * rows;      // column 1 -> lower neighbour (its upper ghost)
+    double* s_hi = snd + (2 * q + 1) * rows;  // column n2-2 -> upper neighbour (its lower ghost)
+    double* r_lo = rcv + (2 * q) * rows;      // lower ghost <- lower neighbour's column n2-2
+    double* r_hi = rcv + (2 * q + 1) * rows;  // upper ghost <- upper neighbour's column 1
+    A->send(s_hi, rows, nccl::kDouble, hi, c->comm, st);
+    A->recv(r_lo, rows, nccl::kDouble, lo, c->comm, st);
+    A->send(s_lo, rows, nccl::kDouble, lo, c->comm, st);
+    A->recv(r_hi, rows, nccl::kDouble, hi, c->comm, st);
+  }
+  if (A->groupEnd() != 0) return fail(PC_E_NCCL, "ncclGroupEnd");
+  k_phi_unpack<<<grid_blocks(c, (int64_t)rows), kThreads, 0, st>>>(g->g, ncomp, rcv, dst);
+  c->st.launches++;
+  return check_launch("k_phi_unpack");
 }
 static int halo_field(pc_field* f) {
   double* b[3] = {f->buf[0], f->buf[1], f->buf[2]};

@@ -53,6 +53,7 @@ int pc_op_create_aligned(pc_grid* g, const pc_field* bhat, const pc_field* rho, 
   op->deps[1] = rho;
   op->ao.rho = rho ? rho->base(0) : nullptr;
   op->ao.pref = pref;
+  op->ao.npref = 0.0 - pref;
   op->ao.ncomp = 1;
   op->Tfloor = T_floor;
   const int rows = g->g.n0 + 2;
@@ -126,6 +127,7 @@ static int detect_radial_rho(pc_op* op) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   op->ao.rho_r = nullptr;
+  op->ao.nsc_r = nullptr;
   if (!op->ao.rho || getenv("PC_NO_RADIAL_RHO")) return PC_OK;
   CUDA_TRY(cudaMemsetAsync(c->bad, 0, sizeof(int), c->s));
   k_radial_check<<<node_blocks(c, g->g), kThreads, 0, c->s>>>(g->g, op->ao.rho, c->bad);
@@ -134,10 +136,16 @@ static int detect_radial_rho(pc_op* op) {
   CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
   CUDA_TRY(cudaStreamSynchronize(c->s));
   if (*c->h_bad != 0) return PC_OK;  // not radial
-  if (!op->rho_r) CUDA_TRY(cudaMalloc(&op->rho_r, sizeof(double) * (size_t)g->g.n0));
+  if (!op->rho_r) CUDA_TRY(cudaMalloc(&op->rho_r, 2 * sizeof(double) * (size_t)g->g.n0));
   CUDA_TRY(cudaMemcpy2DAsync(op->rho_r, sizeof(double), op->ao.rho, (size_t)g->g.plane * sizeof(double), sizeof(double),
                              (size_t)g->g.n0, cudaMemcpyDeviceToDevice, c->s));
+  // the per-plane scale 0 - pref / rho(i) (the node path divides per node: same value)
+  k_neg_scale<<<(g->g.n0 + kThreads - 1) / kThreads, kThreads, 0, c->s>>>(op->rho_r, g->g.n0, op->ao.pref,
+                                                                          op->rho_r + g->g.n0);
+  c->st.launches++;
+  TRY(check_launch("k_neg_scale"));
   op->ao.rho_r = op->rho_r;
+  op->ao.nsc_r = op->rho_r + g->g.n0;
   return PC_OK;
 }
 
@@ -335,7 +343,9 @@ static int make_rows_map(pc_grid* g) {
 }
 static bool tma_ok(const pc_grid* g) {
   const GridDev& d = g->g;
-  return d.per2 && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && tma_encoder() != nullptr &&
+  // (phi-slabs: the periodic phi strips of the TMA boxes would wrap across
+  // the ghost columns -- the cp.async march reads them as ordinary columns)
+  return d.per2 && !d.phis && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && tma_encoder() != nullptr &&
          getenv("PC_NO_TMA") == nullptr;
 }
 template <class Epi, int RHO>

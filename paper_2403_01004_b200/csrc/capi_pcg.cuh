@@ -242,7 +242,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   if (rc == PC_OK) {
     CUDA_TRY(cudaMemcpyAsync(c->h_pcg, c->pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, c->s));
     c->st.kind_launches[pkind] += (int64_t)c->h_pcg->it * (std::is_same<Op, AlignedOp>::value ? 3 : 2);
-    c->st.kind_units[pkind] += (int64_t)c->h_pcg->it * g->g.N;
+    c->st.kind_units[pkind] += (int64_t)c->h_pcg->it * owned_cells(g->g);
     CUDA_TRY(cudaStreamSynchronize(c->s));
     const PcgDev& st = *c->h_pcg;
     *iters = st.it;

@@ -107,11 +107,12 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
   const bool marching = std::is_same<Op, AlignedOp>::value || smarch_ok(op);
   const int Rz = std::is_same<Op, AlignedOp>::value ? march_R(g) : smarch_R(g, op->ncomp);
   const int nz = (g->g.n0 + Rz - 1) / Rz;
-  const bool overlap = marching && nz >= 3 && (c->comm != nullptr || force_split);
+  // (phi-slabs exchange ghost COLUMNS: every r-chunk reads them, no overlap split)
+  const bool overlap = marching && nz >= 3 && !g->g.phis && (c->comm != nullptr || force_split);
   // 7-point march, one rank without ghost planes: stages 1 and 2 in one pass
   // (SEpiStage12: u1 formed in shared memory from u0 and y0; PC_NO_FUSE12 off)
   const bool fuse12 = !std::is_same<Op, AlignedOp>::value && smarch_ok(op) && !overlap && !g->g.ghost_lo0 &&
-                      !g->g.ghost_hi0 && getenv("PC_NO_FUSE12") == nullptr;
+                      !g->g.ghost_hi0 && !g->g.phis && getenv("PC_NO_FUSE12") == nullptr;
   CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
   if (fuse12) {
     const double* r = tab + 5;
@@ -140,7 +141,7 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
       c->ev.push_back({f0, f1, kind});
     }
     c->st.kind_launches[kind] += 1;
-    c->st.kind_units[kind] += 2 * g->g.N;
+    c->st.kind_units[kind] += 2 * owned_cells(g->g);
     c->st.stage_launches++;
     // rotate as after stage 2 below: u1 (A) -> u_{k-2}, u2 (B) -> u_{k-1}
     um2w = &A;
@@ -216,7 +217,7 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     }
     const int nst = s - (fuse12 ? 2 : 1);
     c->st.kind_launches[kind] += nst;
-    c->st.kind_units[kind] += (int64_t)nst * g->g.N;
+    c->st.kind_units[kind] += (int64_t)nst * owned_cells(g->g);
   }
   if (rc == PC_OK && deferred) {
     // pc_cycle: no host sync per step -- the flag travels with the stream and

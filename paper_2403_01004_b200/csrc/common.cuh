@@ -29,6 +29,12 @@ struct GridDev {
   int pin_lo0, pin_hi0, pin_lo1, pin_hi1, pin_lo2, pin_hi2;
   int ghost_lo0, ghost_hi0;  // neighbour slab exists (read the ghost plane)
   int spherical;
+  // phi-slab rank (phis = 1): local columns 1 .. n2-2 are the global columns
+  // k0g .. k0g + n2 - 3; columns 0 and n2-1 are ghost copies of the
+  // neighbour ranks' edge columns (pinned, zero weight: they are read as
+  // neighbours and never advanced or summed); phi stays periodic
+  int phis;
+  int n2g, k0g;            // global n2, global phi offset of the owned columns
   // scalar finite-volume tables
   const double* W2[3];
   const double* g1[3];
@@ -51,6 +57,16 @@ struct GridDev {
   const double* Valg;
 };
 
+// global phi index / extent of a local column (phi-slabs: ghost columns map
+// to the neighbours' columns, periodically)
+__device__ __forceinline__ int kglob(const GridDev& g, int k) {
+  return g.phis ? (k - 1 + g.k0g + g.n2g) % g.n2g : k;
+}
+__device__ __forceinline__ int n2glob(const GridDev& g) { return g.phis ? g.n2g : g.n2; }
+// cells this rank owns (phi-slabs: without the ghost columns)
+__host__ __device__ __forceinline__ int64_t owned_cells(const GridDev& g) {
+  return (int64_t)g.n0 * g.n1 * (g.n2 - 2 * g.phis);
+}
 __device__ __forceinline__ int64_t off3(const GridDev& g, int i, int j, int k) {
   return (int64_t)i * g.plane + (int64_t)j * g.n2 + k;
 }

@@ -31,7 +31,7 @@ __host__ __device__ __forceinline__ unsigned long long stream_key(unsigned long 
   return ((seed & 0xFFFFFFFFULL) << 32) | ((unsigned long long)(stream & 0xFFFF) << 16);
 }
 __device__ __forceinline__ unsigned long long global_index(const GridDev& g, int i, int j, int k) {
-  return ((unsigned long long)(i + g.i0g) * g.n1 + j) * g.n2 + k;
+  return ((unsigned long long)(i + g.i0g) * g.n1 + j) * n2glob(g) + kglob(g, k);
 }
 
 // T = prof(r) * (1 + sigma * N)                       (configs.temperature)
@@ -69,9 +69,10 @@ __global__ void __launch_bounds__(kThreads) k_gen_dipole(GridDev g, Fld b, unsig
 __global__ void __launch_bounds__(kThreads) k_gen_harmonic(GridDev g, Fld v, int ncomp, const double* acc,
                                                            double checker) {
   PC_FOR_NODES(g, i, j, k) {
-    const double cb = ((i + g.i0g + j + k) % 2 == 0) ? checker : -checker;
+    const int kg = kglob(g, k);  // (phi-slab ghost columns hold the neighbours' values)
+    const double cb = ((i + g.i0g + j + kg) % 2 == 0) ? checker : -checker;
     const int64_t o = off3(g, i, j, k);
-    for (int c = 0; c < ncomp; ++c) v.p[c][o] = acc[((int64_t)c * g.n1 + j) * g.n2 + k] + cb;
+    for (int c = 0; c < ncomp; ++c) v.p[c][o] = acc[((int64_t)c * g.n1 + j) * n2glob(g) + kg] + cb;
   }
 }
 

@@ -29,7 +29,7 @@ struct ArgRes {  // device result of the F-argmax reduction and the PTL
 };
 
 __device__ __forceinline__ long long aos_index(const GridDev& g, int i, int j, int k, int c, int ncomp) {
-  return (((long long)(i + g.i0g) * g.n1 + j) * g.n2 + k) * ncomp + c;
+  return (((long long)(i + g.i0g) * g.n1 + j) * n2glob(g) + kglob(g, k)) * ncomp + c;
 }
 
 template <class Op>
@@ -148,13 +148,16 @@ __global__ void k_ptl_pairs(GridDev g, int ncomp, CFld u, CFld F, double eps_rel
   const long long kid = res->kidx;
   const double thr = eps_rel * res->fmax;
   const long long pt = kid / ncomp;
-  const int kk = (int)(pt % g.n2);
-  const long long t2 = pt / g.n2;
+  const int n2x = n2glob(g);
+  const int kgl = (int)(pt % n2x);
+  const int kk = g.phis ? kgl - g.k0g + 1 : kgl;  // local column (phi-slabs)
+  const long long t2 = pt / n2x;
   const int kj = (int)(t2 % g.n1);
   const int ki = (int)(t2 / g.n1) - g.i0g;
   double best = INFINITY;
   const int t = threadIdx.x;
-  const bool owner = ki >= 0 && ki < g.n0;  // r-slabs: only the owner of k evaluates the pairs
+  // slabs: only the owner of k evaluates the pairs
+  const bool owner = ki >= 0 && ki < g.n0 && (!g.phis || (kk >= 1 && kk <= g.n2 - 2));
   if (owner && t < 6 * ncomp) {
     const int dirn = t / ncomp, q = t % ncomp;
     const int a = dirn / 2, d = (dirn & 1) ? 1 : -1;
@@ -183,6 +186,7 @@ __global__ void __launch_bounds__(kThreads) k_ptl_all(GridDev g, int ncomp, CFld
   const double thr = eps_rel * res->fmax;
   double best = INFINITY;
   PC_FOR_NODES(g, i, j, k) {
+    if (g.phis && (k == 0 || k == g.n2 - 1)) continue;  // pairs start at owned nodes (each pair once)
     const int64_t o = off3(g, i, j, k);
     const int co[3] = {i, j, k};
     for (int a = 0; a < 3; ++a) {
@@ -346,6 +350,12 @@ __device__ __forceinline__ void pcg_alpha(PcgDev* st, double pAp) {
   } else {
     st->alpha = 0.0;
   }
+}
+
+// out[i] = 0 - pref / rho[i] (aligned operator: the per-plane scale of a radial density)
+__global__ void k_neg_scale(const double* rho, int n, double pref, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = 0.0 - (pref / rho[i]);
 }
 
 // ---- GPU-count-invariant PCG reductions
@@ -818,20 +828,50 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(GridDev g, Op op, Fld x
 
 // ---------------------------------------------------------------- layout
 // host AoS chunk [planes][n1][n2][ncomp] -> SoA field planes [p0, p0+np)
+// host node c of the chunk (host rows: the owned columns only) -> field offset
+__device__ __forceinline__ int64_t host_node_off(const GridDev& g, int p0, int64_t c) {
+  if (!g.phis) return (int64_t)p0 * g.plane + c;
+  const int hn2 = g.n2 - 2;
+  const int64_t row = c / hn2;
+  return (int64_t)p0 * g.plane + row * g.n2 + (c - row * hn2) + 1;
+}
 __global__ void __launch_bounds__(kThreads) k_aos_to_soa(GridDev g, int ncomp, const double* src, Fld dst,
                                                          int p0, int np) {
-  const int64_t n = (int64_t)np * g.plane;
+  const int64_t n = (int64_t)np * g.n1 * (g.n2 - 2 * g.phis);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = (int64_t)p0 * g.plane + c;
+    const int64_t o = host_node_off(g, p0, c);
     for (int q = 0; q < ncomp; ++q) dst.p[q][o] = src[c * ncomp + q];
   }
 }
 __global__ void __launch_bounds__(kThreads) k_soa_to_aos(GridDev g, int ncomp, CFld src, double* dst,
                                                          int p0, int np) {
-  const int64_t n = (int64_t)np * g.plane;
+  const int64_t n = (int64_t)np * g.n1 * (g.n2 - 2 * g.phis);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = (int64_t)p0 * g.plane + c;
+    const int64_t o = host_node_off(g, p0, c);
     for (int q = 0; q < ncomp; ++q) dst[c * ncomp + q] = src.p[q][o];
+  }
+}
+// phi-slab ghost columns: pack the owned edge columns 1 (to the lower
+// neighbour) and n2-2 (to the upper) of every (plane, row) into
+// buf[q][side][n0 x n1], and unpack the received ones into columns 0 / n2-1
+__global__ void __launch_bounds__(kThreads) k_phi_pack(GridDev g, int ncomp, CFld f, double* buf) {
+  const int64_t rows = (int64_t)g.n0 * g.n1;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = r * g.n2;
+    for (int q = 0; q < ncomp; ++q) {
+      buf[(2 * q) * rows + r] = f.p[q][o + 1];
+      buf[(2 * q + 1) * rows + r] = f.p[q][o + g.n2 - 2];
+    }
+  }
+}
+__global__ void __launch_bounds__(kThreads) k_phi_unpack(GridDev g, int ncomp, const double* buf, Fld f) {
+  const int64_t rows = (int64_t)g.n0 * g.n1;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = r * g.n2;
+    for (int q = 0; q < ncomp; ++q) {
+      f.p[q][o] = buf[(2 * q) * rows + r];                 // from the lower neighbour's column n2-2
+      f.p[q][o + g.n2 - 1] = buf[(2 * q + 1) * rows + r];  // from the upper neighbour's column 1
+    }
   }
 }
 

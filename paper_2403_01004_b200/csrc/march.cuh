@@ -480,8 +480,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
         const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
         const double iv = S.rowt[rslm][10][jr] * col.ivg;
         const int64_t of = pbase - g.plane + onode(n);
-        double f = ((0.0 - G) * iv) * op.pref;
-        if (op.rho) f = f / __ldg(op.rho + of);
+        double f = (G * iv) * op.nscale(of);
         const bool pin = pin_i || pin_j[n] || pin_k;
         if (pin) f = 0.0;
         double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];

@@ -159,7 +159,15 @@ struct AlignedOp {
   const double* beta[3];
   const double* rho;  // nullptr -> 1
   const double* rho_r = nullptr;  // rho(i) per interior plane when rho is radial (TMA march reads it per plane)
+  const double* nsc_r = nullptr;  // with rho_r: the per-plane scale 0 - pref / rho(i)
   double pref;
+  double npref;  // 0 - pref: the scale when there is no density
+  // F = (G iv) * (0 - pref / rho): one product per node for the prefactor and
+  // the density (oracle/operators.py aligned_apply; the division only where rho
+  // varies per node)
+  __device__ __forceinline__ double nscale(int64_t o) const {
+    return rho ? 0.0 - (pref / __ldg(rho + o)) : npref;
+  }
   int ncomp;  // always 1
   int tma_split = 2;  // TMA march: per-plane copies issued by 1 + tma_split warps (PC_TMA_SPLIT overrides)
 
@@ -247,8 +255,7 @@ struct AlignedOp {
     const double G = (Em[0] - Ep[0]) + (own + nbr);
     const int64_t o = off3(g, i, j, k);
     const double iv = __ldg(g.iVal2 + row2(g, i, j)) * __ldg(g.iValg + k);
-    double f = ((0.0 - G) * iv) * pref;
-    if (rho) f = f / __ldg(rho + o);
+    const double f = (G * iv) * nscale(o);
     out[0] = pinned(g, i, j, k) ? 0.0 : f;
   }
 

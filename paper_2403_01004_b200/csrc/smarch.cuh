@@ -43,7 +43,8 @@ struct SMarchSmem {
   double V[3][NC + 1][SHP];          // planes t, t+1, t+2 (in flight); slot NC = D / rho source
   double rowt[3][SROWT][SHJ];        // row tables of planes t-1 (r- face), t, t+1 (in flight)
   double EO[2][F1 ? 1 : SEO][SNT];   // epilogue operands of planes t (read) and t+1 (landing)
-  double M[4][SMJ][9];               // frame rotations t+, t-, p+, p- of the tile rows
+  double2 M[4][SMJ][5];              // frame rotations t+, t-, p+, p- of the tile rows (16-B pairs,
+                                     // theta faces reordered m00 m01 m10 m11 first: two LDS.128)
   double Y[F1 ? 3 : 1][F1 ? NC : 1][F1 ? SHP : 1];  // y0 ring (F1 only; V then holds u0)
   double U[F1 ? 3 : 1][F1 ? NC : 1][F1 ? SHP : 1];  // u1 ring formed from V and Y (F1 only)
 };
@@ -97,10 +98,13 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
 
   // rotation table of the tile rows (loaded once; rows beyond n1 clamp)
   if (VEC) {
-    for (int e = tid; e < 4 * SMJ * 9; e += SNT) {
-      const int f = e / (SMJ * 9), r = (e / 9) % SMJ, q = e % 9;
+    for (int e = tid; e < 4 * SMJ * 10; e += SNT) {
+      const int f = e / (SMJ * 10), r = (e / 10) % SMJ, q = e % 10;
       const int jr = min(j0 + r, g.n1 - 1);
-      S.M[f][r][q] = __ldg(g.M[f] + (int64_t)jr * 9 + q);
+      // theta faces: slots 0..3 = M[0], M[1], M[3], M[4]; phi faces: M[0..8]; slot 9 unused
+      const int th = q < 2 ? q : (q < 4 ? q + 1 : (q == 4 ? 2 : (q < 9 ? q : 8)));  // 0 1 3 4 2 5 6 7 8 8
+      const int src = f < 2 ? th : (q < 9 ? q : 8);
+      reinterpret_cast<double*>(&S.M[f][r][0])[q] = __ldg(g.M[f] + (int64_t)jr * 9 + src);
     }
   }
 
@@ -122,13 +126,10 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
   const int h = (ty + 1) * MHK + (tx + 1);
   const int onode = jg * g.n2 + kg;
 
-  auto vslot = [&](int p) { return (p - i0 + 1) % 3; };
-  auto rslot = [&](int p) { return (p - i0 + 1) % 3; };
   auto eslot = [&](int p) { return (p - i0) & 1; };
-  auto issue_V = [&](int p) {
+  auto issue_V = [&](int p, int sl) {
     const PlaneMap pm = plane_map(g, p);
     const int64_t base = (int64_t)pm.mem * g.plane;
-    const int sl = vslot(p);
 #pragma unroll
     for (int q = 0; q < SNFILL; ++q)
       if (foff[q] >= 0) {
@@ -145,12 +146,11 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
   // F1: u1 = pin ? u0 : u0 + mt1 y0 (k_stage1's expression) over the elements
   // this thread staged for plane p, after its own cp.async group completed
   // (the block barrier that follows publishes them)
-  auto form_u1 = [&](int p) {
+  auto form_u1 = [&](int p, int sl) {
     if constexpr (F1) {
       const PlaneMap pm = plane_map(g, p);
       const int ig = pm.mem + g.i0g;
       const bool ppin = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
-      const int sl = vslot(p);
 #pragma unroll
       for (int q = 0; q < SNFILL; ++q)
         if (foff[q] >= 0) {
@@ -164,10 +164,10 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
         }
     }
   };
-  auto issue_rows = [&](int p) {
+  auto issue_rows = [&](int p, int sl) {
     if (rton) {
       const PlaneMap pm = plane_map(g, p);
-      cp_async8(&S.rowt[rslot(p)][rtab][rhj], rbase + row2(g, pm.row, rjj));
+      cp_async8(&S.rowt[sl][rtab][rhj], rbase + row2(g, pm.row, rjj));
     }
   };
   // stencil input of component c at ring slot sl, element e
@@ -184,23 +184,26 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
     }
   };
 
+  // ring slots of planes t-1, t, t+1 (vslot / rslot (p - i0 + 1) % 3, rotated
+  // once per plane instead of a modulo per use); t+2 reuses the t-1 slot
+  int s_m = 0, s_c = 1, s_p = 2;
   // ---- prologue: V(i0-1..i0+1), rows(i0-1, i0), operands(i0)
-  issue_V(i0 - 1);
-  issue_V(i0);
-  if (i0 + 1 <= iend) issue_V(i0 + 1);
-  issue_rows(i0 - 1);
-  issue_rows(i0);
+  issue_V(i0 - 1, s_m);
+  issue_V(i0, s_c);
+  if (i0 + 1 <= iend) issue_V(i0 + 1, s_p);
+  issue_rows(i0 - 1, s_m);
+  issue_rows(i0, s_c);
   issue_ops(i0);
   cp_async_commit();
   cp_async_wait<0>();
-  form_u1(i0 - 1);
-  form_u1(i0);
-  if (i0 + 1 <= iend) form_u1(i0 + 1);
+  form_u1(i0 - 1, s_m);
+  form_u1(i0, s_c);
+  if (i0 + 1 <= iend) form_u1(i0 + 1, s_p);
   __syncthreads();
 
   double vm[NC], vc[NC], dm = 0.0, dc = 0.0;
   {
-    const int s0 = vslot(i0 - 1), s1 = vslot(i0);
+    const int s0 = s_m, s1 = s_c;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       vm[c] = uat(s0, c, h);
@@ -218,12 +221,12 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
 
 #pragma unroll 1
   for (int t = i0; t < iend; ++t) {
-    if (t + 2 <= iend) issue_V(t + 2);
-    if (t + 1 <= iend) issue_rows(t + 1);
+    if (t + 2 <= iend) issue_V(t + 2, s_m);
+    if (t + 1 <= iend) issue_rows(t + 1, s_p);
     if (t + 1 < iend) issue_ops(t + 1);
     cp_async_commit();
 
-    const int sc = vslot(t), sp = vslot(t + 1), rs = rslot(t), rm = rslot(t - 1), es = eslot(t);
+    const int sc = s_c, sp = s_p, rs = s_c, rm = s_m, es = eslot(t);
     const PlaneMap pmm = plane_map(g, t - 1);
     const bool okim = pmm.exists;  // r- neighbour exists
     double vp[NC], dp = 0.0;
@@ -275,17 +278,25 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
           }
           const bool first = (a == 0 && tt == 0);
           if (VEC && a > 0) {
-            const double* M = S.M[(a == 1 ? 0 : 2) + (tt == 1 ? 0 : 1)][ty];
+            const double2* M2 = S.M[(a == 1 ? 0 : 2) + (tt == 1 ? 0 : 1)][ty];
             const double v0 = nv[a][tt][0], v1 = nv[a][tt][NC > 1 ? 1 : 0], v2 = nv[a][tt][NC > 2 ? 2 : 0];
             double rv[NC];
             if (a == 1) {
               // theta faces rotate about e_phi: M = [[m00 m01 0] [m10 m11 0] [0 0 1]]
               // with exact zeros and one (geometry._rotation_tables), so the
               // dense row sums reduce to these bits (up to the sign of a zero)
-              rv[0] = (M[0] * v0) + (M[1] * v1);
-              if (NC > 1) rv[NC > 1 ? 1 : 0] = (M[3] * v0) + (M[4] * v1);
+              const double2 r0 = M2[0], r1 = M2[1];  // (m00, m01), (m10, m11)
+              rv[0] = (r0.x * v0) + (r0.y * v1);
+              if (NC > 1) rv[NC > 1 ? 1 : 0] = (r1.x * v0) + (r1.y * v1);
               if (NC > 2) rv[NC > 2 ? 2 : 0] = v2;
             } else {
+              double M[10];
+#pragma unroll
+              for (int q = 0; q < 5; ++q) {
+                const double2 w = M2[q];
+                M[2 * q] = w.x;
+                M[2 * q + 1] = w.y;
+              }
 #pragma unroll
               for (int c = 0; c < NC; ++c) rv[c] = ((M[3 * c] * v0) + (M[3 * c + 1] * v1)) + (M[3 * c + 2] * v2);
             }
@@ -335,8 +346,14 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       dc = dp;
     }
     cp_async_wait<0>();
-    if (t + 2 <= iend) form_u1(t + 2);
+    if (t + 2 <= iend) form_u1(t + 2, s_m);
     __syncthreads();
+    {  // rotate the slot roles: t-1 <- t, t <- t+1, t+1 <- t+2 (the old t-1 slot)
+      const int o = s_m;
+      s_m = s_c;
+      s_c = s_p;
+      s_p = o;
+    }
   }
   epi.finish(g);
 }
@@ -367,6 +384,7 @@ struct SEpiStage {
   StageCoef sc;
   int stage;
   int* bad;
+  int fl = 0x7fffffff;  // this thread saw a non-finite value (the stage), reported in finish()
   __host__ __device__ __forceinline__ const double* opnd(int q) const {
     const int c = q / 3, w = q % 3;
     return w == 0 ? u0[c] : (w == 1 ? um2[c] : y0[c]);
@@ -381,10 +399,12 @@ struct SEpiStage {
                  (sc.gtdt * ov[3 * c + 2]);
       v = pin ? a0 : v;
       out[c][o] = v;
-      if (!isfinite(v)) atomicMin(bad, stage);
+      fl = isfinite(v) ? fl : stage;  // (one stage per launch)
     }
   }
-  __device__ __forceinline__ void finish(const GridDev&) {}
+  __device__ __forceinline__ void finish(const GridDev&) {
+    if (fl != 0x7fffffff) atomicMin(bad, fl);  // one atomic per flagged thread, not a branch per node
+  }
 };
 // one-component variant (only 3 operand slots are staged)
 struct SEpiStage1 : SEpiStage {
@@ -407,6 +427,7 @@ struct SEpiStage12 {
   double mt1;
   StageCoef sc;
   int* bad;
+  int fl = 0x7fffffff;  // lowest stage this thread saw non-finite (1: u1, 2: u2), reported in finish()
   __host__ __device__ __forceinline__ const double* opnd(int q) const { return (q & 1) ? y0[q >> 1] : u0[q >> 1]; }
   template <int NC>
   __device__ __forceinline__ void apply(const GridDev&, int, int, int, int64_t o, const double (&f)[NC],
@@ -415,14 +436,16 @@ struct SEpiStage12 {
     for (int c = 0; c < NC; ++c) {
       const double a0 = ov[2 * c];
       if (u1out[0]) u1out[c][o] = u1[c];
-      if (!isfinite(u1[c])) atomicMin(bad, 1);
       double v = ((((sc.mu * u1[c]) + (sc.nu * a0)) + (sc.kap * a0)) + (sc.mtdt * f[c])) + (sc.gtdt * ov[2 * c + 1]);
       v = pin ? a0 : v;
       out[c][o] = v;
-      if (!isfinite(v)) atomicMin(bad, 2);
+      fl = isfinite(v) ? fl : min(fl, 2);
+      fl = isfinite(u1[c]) ? fl : 1;
     }
   }
-  __device__ __forceinline__ void finish(const GridDev&) {}
+  __device__ __forceinline__ void finish(const GridDev&) {
+    if (fl != 0x7fffffff) atomicMin(bad, fl);
+  }
 };
 
 struct SEpiArgmax {  // y0 = F(u0) with the |F| argmax over points x components (PTL)

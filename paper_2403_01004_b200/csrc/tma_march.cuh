@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       const bool exists = LAST ? plane_map(g, t).exists : true;
       const int tf = t - 1;
       const double rpl = (RHO == 2 && !FIRST) ? __ldg(op.rho_r + tf) : 1.0;  // radial density of plane tf
+      const double nsp = (RHO == 2 && !FIRST) ? __ldg(op.nsc_r + tf) : op.npref;  // its scale 0 - pref / rho
       const int ig = tf + g.i0g;
       const bool pin_i = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
 #pragma unroll
@@ -351,9 +352,9 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
           const double iv = rM[jr * RW + 10] * col.ivg;
           const int64_t of = pofs + n * nstride;
-          double f = ((0.0 - G) * iv) * op.pref;
-          if constexpr (RHO == 1) f = f / rr[n];
-          if constexpr (RHO == 2) f = f / rpl;
+          double f;
+          if constexpr (RHO == 1) f = (G * iv) * (0.0 - (op.pref / rr[n]));
+          else f = (G * iv) * nsp;
           const bool pin = pin_i || pin_j[n] || pin_k;
           if (pin) f = 0.0;
           double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];

@@ -18,9 +18,11 @@ from . import _lib, geometry, mesh
 
 class Context:
     def __init__(self, device: int = 0, nranks: int = 1, rank: int = 0, nccl_uid: bytes | None = None,
-                 detached: bool = False):
-        """``detached``: test hook -- an r-slab rank with no communicator
-        (collectives skipped; ghost planes set with DeviceField.set_ghost)."""
+                 detached: bool = False, axis: int = 0):
+        """``detached``: test hook -- a slab rank with no communicator
+        (collectives skipped; ghost planes / columns set with
+        DeviceField.set_ghost / set_ghost_cols).  ``axis``: the slab
+        decomposition, 0 = r-slabs, 2 = phi-slabs (BASELINE C4's split)."""
         L = _lib.lib()
         h = c_void_p()
         if detached:
@@ -35,6 +37,9 @@ class Context:
         self.device = device
         self.nranks = nranks
         self.rank = rank
+        self.axis = int(axis)
+        if self.axis != 0:
+            _lib.check(L.pc_ctx_set_decomposition(h, self.axis), "pc_ctx_set_decomposition")
         self._grids = {}
         self._pinned = []
 
@@ -199,9 +204,10 @@ class DeviceGrid:
     the slab geometry."""
 
     def __init__(self, grid, bc, ctx: Context | None = None, force_ghosts: bool = False):
-        """``force_ghosts`` (test hook): a single rank of a periodic axis 0
-        reads its axis-0 neighbours from ghost planes filled by the (self)
-        NCCL exchange instead of wrapping in-kernel."""
+        """``force_ghosts`` (test hook): a single rank reads its neighbours
+        from ghost planes (r-slabs, periodic axis 0) or ghost columns
+        (phi-slabs) filled by the (self) NCCL exchange instead of wrapping
+        in-kernel."""
         ctx = ctx or default_context()
         self.ctx = ctx
         self.grid = grid
@@ -212,15 +218,30 @@ class DeviceGrid:
         P, r = ctx.nranks, ctx.rank
         if P > n0:
             raise ValueError(f"{P} ranks but only {n0} axis-0 planes")
-        i0, n0l = geometry.slab_bounds(n0, P, r)
-        per0 = gt.periodic[0]
-        self.ghost_lo = (P > 1 and (r > 0 or per0)) or (force_ghosts and per0)
-        self.ghost_hi = (P > 1 and (r < P - 1 or per0)) or (force_ghosts and per0)
-        self.i0, self.n0_local = i0, n0l
         self.global_shape = gt.shape
-        self.shape = (n0l, gt.shape[1], gt.shape[2])
-        tab = geometry.pack(gt, i0, n0l, self.ghost_lo, self.ghost_hi)
-        fl = geometry.flags(gt, i0, n0l, self.ghost_lo, self.ghost_hi)
+        self.phi = None  # (k0, n) of a phi-slab rank
+        if ctx.axis == 2 and (P > 1 or force_ghosts):
+            n2 = gt.shape[2]
+            if P > n2:
+                raise ValueError(f"{P} ranks but only {n2} phi columns")
+            self.phi = geometry.slab_bounds(n2, P, r)
+            i0, n0l = 0, n0
+            self.ghost_lo = self.ghost_hi = False
+            self.i0, self.n0_local = i0, n0l
+            self.shape = (n0, gt.shape[1], self.phi[1] + 2)  # + ghost columns
+            self.host_shape = (n0, gt.shape[1], self.phi[1])
+            tab = geometry.pack(gt, phi=self.phi)
+            fl = geometry.flags(gt, phi=self.phi)
+        else:
+            i0, n0l = geometry.slab_bounds(n0, P, r)
+            per0 = gt.periodic[0]
+            self.ghost_lo = (P > 1 and (r > 0 or per0)) or (force_ghosts and per0)
+            self.ghost_hi = (P > 1 and (r < P - 1 or per0)) or (force_ghosts and per0)
+            self.i0, self.n0_local = i0, n0l
+            self.shape = (n0l, gt.shape[1], gt.shape[2])
+            self.host_shape = self.shape
+            tab = geometry.pack(gt, i0, n0l, self.ghost_lo, self.ghost_hi)
+            fl = geometry.flags(gt, i0, n0l, self.ghost_lo, self.ghost_hi)
         shp = (c_int64 * 3)(*self.shape)
         L = _lib.lib()
         if L.pc_grid_table_size(shp) != tab.size:
@@ -233,10 +254,14 @@ class DeviceGrid:
 
     @property
     def ncells(self) -> int:
-        return int(np.prod(self.shape))
+        """Cells this rank owns (phi-slabs: without the ghost columns)."""
+        return int(np.prod(self.host_shape))
 
     def local_slice(self, values: np.ndarray) -> np.ndarray:
-        """This rank's axis-0 slab of a global grid-shaped array."""
+        """This rank's slab of a global grid-shaped array."""
+        if self.phi is not None:
+            k0, n = self.phi
+            return values[:, :, k0:k0 + n]
         if self.ctx.nranks == 1:
             return values
         return values[self.i0:self.i0 + self.n0_local]
@@ -285,19 +310,21 @@ def gather_slabs(dgrid: DeviceGrid, local: np.ndarray) -> np.ndarray:
     import torch.distributed as dist
     require_gather_group()
     P = dgrid.ctx.nranks
-    n0 = dgrid.global_shape[0]
-    bounds = [geometry.slab_bounds(n0, P, r) for r in range(P)]
+    ax = 2 if dgrid.phi is not None else 0
+    nax = dgrid.global_shape[ax]
+    bounds = [geometry.slab_bounds(nax, P, r) for r in range(P)]
     nmax = max(n for _, n in bounds)
-    tail = local.shape[1:]
+    loc = np.moveaxis(np.asarray(local), ax, 0)
+    tail = loc.shape[1:]
     dev = torch.device("cuda", dgrid.ctx.device) if dist.get_backend() == "nccl" else torch.device("cpu")
     buf = torch.zeros((nmax,) + tuple(tail), dtype=torch.float64, device=dev)
-    buf[:local.shape[0]] = torch.from_numpy(np.ascontiguousarray(local)).to(dev)
+    buf[:loc.shape[0]] = torch.from_numpy(np.ascontiguousarray(loc)).to(dev)
     parts = [torch.empty_like(buf) for _ in range(P)]
     dist.all_gather(parts, buf)
-    out = np.empty((n0,) + tuple(tail))
+    out = np.empty((nax,) + tuple(tail))
     for (i0, n), p in zip(bounds, parts):
         out[i0:i0 + n] = p[:n].cpu().numpy()
-    return out
+    return np.ascontiguousarray(np.moveaxis(out, 0, ax))
 
 
 class DeviceField:
@@ -312,6 +339,10 @@ class DeviceField:
     @property
     def shape(self):
         return self.dgrid.shape
+
+    def _host_shape(self, layout):
+        hs = tuple(self.dgrid.host_shape)
+        return hs + (self.ncomp,) if layout == _lib.LAYOUT_AOS else (self.ncomp,) + hs
 
     def upload(self, values: np.ndarray, layout: int = _lib.LAYOUT_AOS, async_: bool = False):
         """values: local slab, (n0, n1, n2, ncomp) AoS (or (ncomp, n0, n1, n2) SoA).
@@ -331,7 +362,7 @@ class DeviceField:
 
     def download_async(self, layout: int = _lib.LAYOUT_AOS) -> np.ndarray:
         """Start a download into a page-locked array; valid after ``wait()``."""
-        shape = tuple(self.dgrid.shape) + (self.ncomp,) if layout == _lib.LAYOUT_AOS else (self.ncomp,) + tuple(self.dgrid.shape)
+        shape = self._host_shape(layout)
         out = pinned_empty(shape)
         _lib.check(_lib.lib().pc_field_download_async(self.handle, _lib.dptr(out), layout), "download_async")
         self._holds.append(out)
@@ -344,13 +375,19 @@ class DeviceField:
         return self
 
     def download(self, out: np.ndarray | None = None, layout: int = _lib.LAYOUT_AOS) -> np.ndarray:
-        shape = tuple(self.dgrid.shape) + (self.ncomp,) if layout == _lib.LAYOUT_AOS else (self.ncomp,) + tuple(self.dgrid.shape)
+        shape = self._host_shape(layout)
         if out is None:
             out = pinned_empty(shape)
         elif not (out.flags.c_contiguous and out.dtype == np.float64 and out.size == int(np.prod(shape))):
             raise ValueError("download target must be a contiguous float64 array of the field size")
         _lib.check(_lib.lib().pc_field_download(self.handle, _lib.dptr(out), layout), "download")
         return out.reshape(shape)
+
+    def set_ghost_cols(self, cols: np.ndarray):
+        """phi-slab ghost columns from (ncomp, 2, n0, n1): side 0 = the column
+        below the slab, side 1 = the column above it (test hook)."""
+        a = np.ascontiguousarray(cols, dtype=np.float64)
+        _lib.check(_lib.lib().pc_field_set_ghost_cols(self.handle, _lib.dptr(a)), "set_ghost_cols")
 
     def set_ghost(self, side: int, plane_soa: np.ndarray):
         """Ghost plane -1 (side 0) or n0 (side 1) from (ncomp, n1, n2)."""

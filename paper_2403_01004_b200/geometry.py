@@ -33,7 +33,7 @@ from . import mesh
 
 FACES = ("t+", "t-", "p+", "p-")
 SIGNS = ("+", "-")
-NFLAGS = 14
+NFLAGS = 17
 
 
 def _isin(kind):
@@ -286,12 +286,20 @@ TWO_ORDER_1 = ["W0", "W1", "W2"]
 ONE_ORDER_1 = ["g0", "g1", "g2"]
 
 
-def pack(gt: GlobalTables, i0: int = 0, n0_local: int | None = None, ghost_lo=False, ghost_hi=False):
+def pack(gt: GlobalTables, i0: int = 0, n0_local: int | None = None, ghost_lo=False, ghost_hi=False, phi=None):
     """Flat table array for the axis-0 slab [i0, i0 + n0_local), ghost rows
-    filled from the global tables when the neighbour slab exists."""
+    filled from the global tables when the neighbour slab exists.
+    ``phi = (k0, n)``: a phi-slab -- the columns [k0, k0 + n) plus one ghost
+    column on each side (the neighbours' columns, periodically); the ghost
+    columns carry zero inner-product weight (gv = Valg = 0: never summed) and
+    are pinned by flags() (never advanced)."""
     n0, n1, n2 = gt.shape
     if n0_local is None:
         n0_local = n0
+    cols = None
+    if phi is not None:
+        k0, nl = phi
+        cols = np.array([(k0 - 1 + c) % n2 for c in range(nl + 2)])
 
     def two(name):
         t = gt.two[name]
@@ -304,7 +312,14 @@ def pack(gt: GlobalTables, i0: int = 0, n0_local: int | None = None, ghost_lo=Fa
         return out.ravel()
 
     def one(name):
-        return np.asarray(gt.one[name], float).ravel()
+        t = np.asarray(gt.one[name], float).ravel()
+        if cols is None:
+            return t
+        t = t[cols].copy()
+        if name in ("gv", "Valg"):  # ghost columns: zero weight
+            t[0] = 0.0
+            t[-1] = 0.0
+        return t
 
     parts = [two(n) for n in TWO_ORDER_1] + [one(n) for n in ONE_ORDER_1]
     parts += [two("iV2"), one("igv")]
@@ -319,7 +334,7 @@ def pack(gt: GlobalTables, i0: int = 0, n0_local: int | None = None, ghost_lo=Fa
     return np.ascontiguousarray(np.concatenate(parts))
 
 
-def flags(gt: GlobalTables, i0=0, n0_local=None, ghost_lo=False, ghost_hi=False):
+def flags(gt: GlobalTables, i0=0, n0_local=None, ghost_lo=False, ghost_hi=False, phi=None):
     n0 = gt.shape[0]
     if n0_local is None:
         n0_local = n0
@@ -332,6 +347,15 @@ def flags(gt: GlobalTables, i0=0, n0_local=None, ghost_lo=False, ghost_hi=False)
     f[11] = n0
     f[12] = i0
     f[13] = int(gt.spherical)
+    f[15] = gt.shape[2]
+    if phi is not None:  # phi-slab: periodic phi, ghost columns 0 and n + 1 pinned
+        if not gt.periodic[2]:
+            raise ValueError("phi-slabs need a periodic axis 2")
+        f[2] = 1
+        f[7] = 1
+        f[8] = 1
+        f[14] = 1
+        f[16] = phi[0]
     return f
 
 
