@@ -278,14 +278,15 @@ def run_ours(args, rank, world, local_rank):
         obj = [device.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    ctx = device.Context(local_rank, world, rank, uid)
+    decomp = args.decomp or ("phi" if args.config == "c4" else "r")
+    ctx = device.Context(local_rank, world, rank, uid, axis=2 if decomp == "phi" else 0)
     device.set_default_context(ctx)
     name = args.config
     t_setup = time.perf_counter()
     n_over = None if args.n is None else tuple(int(x) for x in args.n.split(","))
-    if args.weak and world > 1:  # weak scaling: the config's grid per rank, stacked in r
+    if args.weak and world > 1:  # weak scaling: the config's grid per rank, stacked along the slab axis
         base = n_over or CONFIG_SHAPE[name]
-        n_over = (base[0] * world, base[1], base[2])
+        n_over = (base[0], base[1], base[2] * world) if decomp == "phi" else (base[0] * world, base[1], base[2])
     prob = Problem(name, ctx, n_over)
     sc = scheme_for(name, args)
     pcfg = ptl.PtlConfig(enabled=not args.no_ptl)
@@ -387,7 +388,7 @@ def run_ours(args, rank, world, local_rank):
                 prob.w.ratio,
                 [{"field": f, "kind": kd, "cycles": r.n_cycles, "stages_or_iters": r.total_iters}
                  for (f, kd, _), r in zip(ops_info, rep0)],
-                total_cu // max(args.steps, 1)),
+                total_cu // max(args.steps, 1), decomp),
             "setup_s": round(setup_s, 2),
             "roofline": None if dom is None else {
                 "bound": "hbm",
@@ -661,7 +662,7 @@ def cpu_baseline(name, procs=1, planes=None):
             "parts": parts}
 
 
-def workload_config(name, world, grid, fields, scheme, ratio, operators, cu_per_step):
+def workload_config(name, world, grid, fields, scheme, ratio, operators, cu_per_step, decomp="r"):
     """The `config` dict of both arms (the driver compares them)."""
     cells = int(np.prod(grid))
     return {
@@ -674,14 +675,14 @@ def workload_config(name, world, grid, fields, scheme, ratio, operators, cu_per_
         "outer_dt_over_dtE": ratio,
         "operators": operators,
         "cell_updates_per_step": cu_per_step,
-        "decomposition": f"r-slabs x{world}" if world > 1 else "single GPU",
+        "decomposition": f"{decomp}-slabs x{world}" if world > 1 else "single GPU",
         "l2": "inputs larger than L2 (each field %.0f MB > 126 MB)" % (cells * 8 / 1e6)
         if cells * 8 > 126e6 else "fields L2-resident (smaller than 126 MB)",
         "parallelism": f"slab{world}",
     }
 
 
-def reference_config(name, world):
+def reference_config(name, world, decomp=None):
     ops = STEP_COUNTS[name]
     cells = int(np.prod(CONFIG_SHAPE[name]))
     kind = "backward_euler(jacobi)+PTL" if name == "c4" else "rkl2+PTL"
@@ -689,7 +690,7 @@ def reference_config(name, world):
                            {"c1": 500.0, "c2": 2000.0, "c3": 1e4, "c4": 1e4, "c5": 5e4, "c5v": 5e4}[name],
                            [{"field": f, "kind": "aligned" if k.startswith("aligned") else "scalar", "cycles": c,
                              "stages_or_iters": st} for f, k, _, c, st in ops],
-                           sum(cells * st for _, _, _, _, st in ops))
+                           sum(cells * st for _, _, _, _, st in ops), decomp or ("phi" if name == "c4" else "r"))
 
 
 def run_reference(args, rank, world):
@@ -721,7 +722,7 @@ def run_reference(args, rank, world):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded recipes, configs.py; no public dataset exists)",
-        "config": reference_config(args.config, world),
+        "config": reference_config(args.config, world, args.decomp),
         "note": "the reference repo ships no implementation of this path; its CPU algorithm is the numpy oracle "
                 "(oracle/, the SPEC restatement), run on all host cores over r-chunks and extrapolated",
         "cpu_baseline": cb,
@@ -777,6 +778,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--decomp", default=None, choices=["r", "phi"],
+                    help="N > 1: slab axis (default: phi-slabs for C4, as BASELINE.json names them; r-slabs otherwise)")
     ap.add_argument("--no-ptl", action="store_true",
                     help="one cycle of the whole outer step (no PTL cycling; time-to-solution comparisons)")
     ap.add_argument("--dry-run", action="store_true",

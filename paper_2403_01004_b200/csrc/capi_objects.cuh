@@ -198,11 +198,20 @@ static int node_blocks(pc_ctx* c, const GridDev& g) {
   return (int)std::min<int64_t>(b, c->max_blocks);
 }
 
+// PC_POISON (test switch, the initcheck substitute: compute-sanitizer is
+// not available on the GPU pool): every buffer the pool hands out is filled
+// with NaN bytes, so a kernel that reads workspace it did not write poisons
+// its result and the parity checks fail (fields are still created zeroed)
+static bool pool_poison() {
+  static const bool on = getenv("PC_POISON") != nullptr;
+  return on;
+}
 static double* pool_get(pc_ctx* c, size_t elems) {
   for (size_t q = 0; q < c->pool.size(); ++q) {
     if (c->pool[q].first == elems) {
       double* p = c->pool[q].second;
       c->pool.erase(c->pool.begin() + q);
+      if (pool_poison()) cudaMemsetAsync(p, 0xFF, elems * sizeof(double), c->s);
       return p;
     }
   }
@@ -218,7 +227,7 @@ static double* pool_get(pc_ctx* c, size_t elems) {
       return nullptr;
     }
   }
-  cudaMemsetAsync(p, 0, elems * sizeof(double), c->s);
+  cudaMemsetAsync(p, pool_poison() ? 0xFF : 0, elems * sizeof(double), c->s);
   return p;
 }
 static void pool_put(pc_ctx* c, size_t elems, double* p) {

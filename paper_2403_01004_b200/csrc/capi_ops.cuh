@@ -137,7 +137,7 @@ static int detect_radial_rho(pc_op* op) {
   CUDA_TRY(cudaStreamSynchronize(c->s));
   if (*c->h_bad != 0) return PC_OK;  // not radial
   if (!op->rho_r) CUDA_TRY(cudaMalloc(&op->rho_r, 2 * sizeof(double) * (size_t)g->g.n0));
-  CUDA_TRY(cudaMemcpy2DAsync(op->rho_r, sizeof(double), op->ao.rho, (size_t)g->g.plane * sizeof(double), sizeof(double),
+  CUDA_TRY(cudaMemcpy2DAsync(op->rho_r, sizeof(double), op->ao.rho + g->g.phis, (size_t)g->g.plane * sizeof(double), sizeof(double),
                              (size_t)g->g.n0, cudaMemcpyDeviceToDevice, c->s));
   // the per-plane scale 0 - pref / rho(i) (the node path divides per node: same value)
   k_neg_scale<<<(g->g.n0 + kThreads - 1) / kThreads, kThreads, 0, c->s>>>(op->rho_r, g->g.n0, op->ao.pref,

@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(kThreads) k_bound(GridDev g, Op op, double* di
 // flag = 1 if some rho(i, j, k) != rho(i, 0, 0) (the density is not radial)
 __global__ void __launch_bounds__(kThreads) k_radial_check(GridDev g, const double* rho, int* flag) {
   PC_FOR_NODES(g, i, j, k) {
-    const double a = __ldg(rho + off3(g, i, j, k)), b = __ldg(rho + (int64_t)i * g.plane);
+    if (g.phis && (k == 0 || k == g.n2 - 1)) continue;  // (ghost columns may not be exchanged yet)
+    const double a = __ldg(rho + off3(g, i, j, k)), b = __ldg(rho + (int64_t)i * g.plane + g.phis);
     if (!(a == b)) atomicExch(flag, 1);
   }
 }
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(kThreads) k_radial_check(GridDev g, const doub
 __global__ void __launch_bounds__(kThreads) k_count_fail(GridDev g, CFld f, int ncomp, int test, double* count) {
   double n = 0.0;
   PC_FOR_NODES(g, i, j, k) {
+    if (g.phis && (k == 0 || k == g.n2 - 1)) continue;  // owned nodes only (ghost columns: the neighbours')
     const int64_t o = off3(g, i, j, k);
     for (int q = 0; q < ncomp; ++q) {
       const double x = __ldg(f.p[q] + o);

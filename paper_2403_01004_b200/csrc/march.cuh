@@ -635,16 +635,28 @@ struct EpiArgmax {  // y0 = F(u0) with the |F| argmax (PTL)
   unsigned int* counter;
   ArgRes* res;
   ArgMax best;
-  __device__ __forceinline__ void operator()(int, const GridDev& g, int i, int j, int k, int64_t o, double f, double,
+  // this thread's maximum so far: a thread visits its nodes in increasing AoS
+  // index (planes in order, row ty before ty + 8), so a strict > keeps the
+  // lowest index among equal maxima without forming indices per node; the
+  // index is formed once, in finish()
+  int bi = 0, bj = 0, bk = 0;
+  __device__ __forceinline__ void operator()(int, const GridDev&, int i, int j, int k, int64_t o, double f, double,
                                              bool, const double*, double) {
     F[o] = f;
-    best = am_better(best, ArgMax{fabs(f), aos_index(g, i, j, k, 0, 1)});
+    const double a = fabs(f);
+    if (a > best.v) {
+      best.v = a;
+      bi = i;
+      bj = j;
+      bk = k;
+    }
   }
-  __device__ __forceinline__ void finish(const GridDev&) {
+  __device__ __forceinline__ void finish(const GridDev& g) {
     __shared__ double shv[kMaxWarps];
     __shared__ long long shi[kMaxWarps];
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblk = gridDim.x * gridDim.y * gridDim.z;
+    if (best.v >= 0.0) best.i = aos_index(g, bi, bj, bk, 0, 1);
     ArgMax b = block_argmax2d(best, shv, shi);
     if (threadIdx.x == 0 && threadIdx.y == 0) {
       pv[bid] = b.v;

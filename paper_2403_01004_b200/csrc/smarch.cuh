@@ -458,21 +458,33 @@ struct SEpiArgmax {  // y0 = F(u0) with the |F| argmax over points x components 
   ArgRes* res;
   ArgMax best;
   int ncomp;
+  // this thread's maximum so far (nodes visited in increasing AoS index --
+  // planes in order, components in order -- so a strict > keeps the lowest
+  // index among equal maxima); the index is formed once, in finish()
+  int bi = 0, bc = 0, bj = 0, bk = 0;
   template <int NC>
-  __device__ __forceinline__ void apply(const GridDev& g, int i, int j, int k, int64_t o, const double (&f)[NC],
+  __device__ __forceinline__ void apply(const GridDev&, int i, int j, int k, int64_t o, const double (&f)[NC],
                                         const double (&)[NC], bool, const double*) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       F[c][o] = f[c];
-      best = am_better(best, ArgMax{fabs(f[c]), aos_index(g, i, j, k, c, NC)});
+      const double a = fabs(f[c]);
+      if (a > best.v) {
+        best.v = a;
+        bi = i;
+        bc = c;
+        bj = j;
+        bk = k;
+      }
     }
   }
-  __device__ __forceinline__ void finish(const GridDev&) {
+  __device__ __forceinline__ void finish(const GridDev& g) {
     __shared__ double shv[SNT / 32];
     __shared__ long long shi[SNT / 32];
     const int tid = threadIdx.x;
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nblk = gridDim.x * gridDim.y * gridDim.z;
+    if (best.v >= 0.0) best.i = aos_index(g, bi, bj, bk, bc, ncomp);
     ArgMax b = block_argmax<SNT>(best, shv, shi);
     if (tid == 0) {
       pv[bid] = b.v;
