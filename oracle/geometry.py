@@ -276,8 +276,12 @@ def _spherical(g, coords, sp):
     tm[0] = 0.0
     St = _mcos(tm) - _mcos(tp)
     dth = th[1:] - th[:-1]
-    hp2, hm2, hasp2, hasm2 = sp[2]
-    wphi = _dual_widths(ph, True)
+    # phi: the exact uniform spacing 2 pi / n2 (DESIGN.md §2 D1: constant phi
+    # metric factors; the coordinate differences wander in the last bit)
+    h2 = 2.0 * math.pi / n2
+    hp2, hm2 = np.full(n2, h2), np.full(n2, h2)
+    hasp2, hasm2 = np.ones(n2, bool), np.ones(n2, bool)
+    wphi = np.full(n2, h2)
     h0p, h0m, has0p, has0m = sp[0]
     ih0p = _safe_inv(h0p, has0p)
     W0 = ((rp * rp)[:, None] * St[None, :]) * ih0p[:, None]

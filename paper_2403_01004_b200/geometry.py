@@ -209,8 +209,16 @@ def _spherical_tables(coords, kinds, periodic, info, two, one, wo):
     St = _cos(tm) - _cos(tp)
     dth = th[1:] - th[:-1]
     hp0, hm0, okp0, okm0 = info[0]
-    hp2, hm2, okp2, okm2 = info[2]
-    wphi = _dual(ph, True)
+    # phi: the exact uniform spacing 2 pi / n2 (the
+    # differences of the coordinates 2 pi k / n2 wander in the last bit), so
+    # every phi metric factor is one constant -- the TMA march folds them into
+    # its per-(r, theta) row records (oracle/geometry.py does the same)
+    h2 = 2.0 * math.pi / n2
+    hp2 = np.full(n2, h2)
+    hm2 = np.full(n2, h2)
+    okp2 = np.ones(n2, bool)
+    okm2 = np.ones(n2, bool)
+    wphi = np.full(n2, h2)
     W0 = ((rp * rp)[:, None] * St[None, :]) * _inv_where(hp0, okp0)[:, None]
     W0[-1, :] = 0.0
     W1 = np.zeros((n0, n1))

@@ -65,3 +65,43 @@ def neighbours(shape, k):
             if 0 <= q[a] < shape[a]:
                 out.append(tuple(q))
     return out
+
+
+# ---- criterion 8: smooth 2-D anisotropic conduction (b at 30 degrees to x,
+# periodic unit square, c = 1), one outer time T = dt_E, every scheme at
+# T/16 .. T/128 against a fine explicit Euler (T / 2^16)
+ANISO_N = 24
+ANISO_STEPS = (16, 32, 64, 128)
+ANISO_FINE = 1 << 16
+
+
+def aniso_problem():
+    import math
+    x = np.arange(ANISO_N) / ANISO_N
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u0 = 0.1 * np.sin(2 * np.pi * X) * np.cos(2 * np.pi * Y) + 0.05 * np.cos(2 * np.pi * (X + Y))
+    b = np.zeros((ANISO_N, ANISO_N, 3))
+    b[..., 0] = math.cos(math.pi / 6)
+    b[..., 1] = math.sin(math.pi / 6)
+    return x, u0, b
+
+
+_FINE = {}
+
+
+def aniso_reference():
+    """Fine explicit Euler (oracle) of the criterion-8 problem: (dt_E, u(T))."""
+    if "ref" not in _FINE:
+        from oracle import operators as oops
+        from oracle import ptl as optl
+        from oracle import schemes as osch
+        x, u0, b = aniso_problem()
+        g = build_geometry([x, x], [("periodic", "periodic")] * 2)
+        op = optl.OracleOperator(g, "aligned", 1, None, None, False, np.moveaxis(b, -1, 0)[..., None],
+                                 oops.aligned_coefficient(np.ones(g.shape)), 1.0)
+        dtE = op.euler_dt()
+        u = u0.reshape((1,) + g.shape)
+        for _ in range(ANISO_FINE):
+            u = osch.euler_step(op.apply, u, dtE / ANISO_FINE, g.pinned)
+        _FINE["ref"] = (dtE, u.reshape(u0.shape), op)
+    return _FINE["ref"]

@@ -134,3 +134,38 @@ def test_acceptance9_conservation_on_gpu(gpu_ctx, kind, ratio, use_ptl):
                                       ptl.PtlConfig(enabled=use_ptl))
         s0, s1 = float(np.sum(W * u0)), float(np.sum(W * u.values[..., 0]))
         assert abs(s1 - s0) <= 1e-12 * abs(s0), (g.metric, s0, s1)
+
+
+@pytest.mark.parametrize("kind", ["euler", "backward_euler", "rkl2", "rkg2"])
+def test_acceptance8_on_gpu(gpu_ctx, kind):
+    """Criterion 8 through the GPU path (aligned operator on a 2-D periodic
+    Cartesian grid): every dt's final field equals the oracle's (bitwise,
+    BE to 1e-10) and the errors against the fine-Euler oracle decrease
+    monotonically to below 1e-6."""
+    from acceptance_cases import ANISO_STEPS, aniso_problem, aniso_reference
+    from oracle import ptl as optl
+    dtE_o, ref, oop = aniso_reference()
+    x, u0, b = aniso_problem()
+    g = mesh.build_grid([len(x), len(x)], coords=[x, x])
+    per = mesh.FaceBC("periodic")
+    bc = mesh.BoundaryCondition(((per, per), (per, per)))
+    cfg = operators.AlignedConductionConfig(b_hat=b, m_p=3.0, k_B=1.0, bc=bc)
+    op = operators.DiffusionOperator.aligned(cfg, mesh.Field(g, np.ones(u0.shape + (1,))))
+    dtE = op.device_op(g, 1).dt_euler
+    assert dtE == dtE_o
+    errs = []
+    for m in ANISO_STEPS:
+        u = mesh.Field(g, u0[..., None])
+        uo = u0.reshape((1,) + oop.geom.shape)
+        for _ in range(m):
+            u, _ = ptl.cycle_operator(op, schemes.SchemeConfig(kind, tol=1e-13), u, dtE / m,
+                                      ptl.PtlConfig(enabled=False))
+            uo, _ = optl.cycle_operator(oop, optl.OracleScheme(kind, tol=1e-13), uo, dtE / m, use_ptl=False)
+        a, o = u.values[..., 0], uo.reshape(u0.shape)
+        if kind == "backward_euler":
+            assert np.linalg.norm(a - o) <= 1e-10 * np.linalg.norm(o)
+        else:
+            assert np.array_equal(a, o)
+        errs.append(float(np.max(np.abs(a - ref))))
+    assert all(q < p for p, q in zip(errs, errs[1:])), errs
+    assert errs[-1] < 1e-6, errs

@@ -98,3 +98,22 @@ def test_acceptance9_conservation(kind, ratio, use_ptl):
             # (BE iterates conserve only to the PCG tolerance: solve below the 1e-12 bar)
             u, _ = optl.cycle_operator(op, optl.OracleScheme(kind, tol=1e-13), u, dt, use_ptl=use_ptl)
         assert abs(float(np.sum(W * u)) - s0) <= 1e-12 * abs(s0)
+
+
+@pytest.mark.parametrize("kind", ["euler", "backward_euler", "rkl2", "rkg2"])
+def test_acceptance8_schemes_converge_to_fine_euler(kind):
+    """Criterion 8: on a smooth 2-D anisotropic-conduction
+    problem every scheme converges to the fine-Euler oracle as dt -> 0: the
+    final max-norm error decreases monotonically over 3 halvings and is
+    below 1e-6 at the finest dt."""
+    from acceptance_cases import ANISO_STEPS, aniso_problem, aniso_reference
+    dtE, ref, op = aniso_reference()
+    _, u0, _ = aniso_problem()
+    errs = []
+    for m in ANISO_STEPS:
+        u = u0.reshape((1,) + op.geom.shape)
+        for _ in range(m):
+            u, _ = optl.cycle_operator(op, optl.OracleScheme(kind, tol=1e-13), u, dtE / m, use_ptl=False)
+        errs.append(float(np.max(np.abs(u.reshape(ref.shape) - ref))))
+    assert all(b < a for a, b in zip(errs, errs[1:])), errs
+    assert errs[-1] < 1e-6, errs
