@@ -13,6 +13,9 @@ from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libparacycle_b200.so")
+# experiment switch (same-box A/B of two builds): load another in-tree build
+if os.environ.get("PC_LIB_PATH"):
+    LIB_PATH = os.path.join(_HERE, "_lib", os.path.basename(os.environ["PC_LIB_PATH"]))
 
 PC_OK = 0
 PC_E_INVALID, PC_E_INDEFINITE, PC_E_DIVERGED, PC_E_BLOWUP, PC_E_CAP = 1, 2, 3, 4, 5

@@ -288,35 +288,18 @@ int pc_grid_create(pc_ctx* c, const int64_t shape[3], const int32_t* fl, const d
   d.gv = takeK();
   d.Val2 = takeA();
   d.Valg = takeK();
-  {  // folded row records of the TMA march from the host copy of the tables:
-     // with uniform phi every column factor is one constant, and the record
-     // holds the products the general path forms per node (same operands,
-     // same IEEE products: -ffp-contract=off), so the march is bitwise
+  {  // interleaved row records from the host copy of the tables (same bits)
     const double* h = tables + 3 * A + 3 * K + A + K;  // iL2[0]
-    const double* hl1 = h + 6 * A;                      // iL1[0]
     const double* hw = h + 6 * A + 6 * K;               // wo01[0]
-    const double* hw2 = hw + 4 * A;                     // wo2[0]
     const double* hv = hw + 4 * A + 2 * K;              // iVal2
-    const double* hvg = hv + A;                         // iValg
     const double* hV = hv + A + K + 48 * J + A + K;     // Val2 (after iValg, M, Rabs, V2, gv)
-    const double* hVg = hV + A;                         // Valg
-    bool uni = true;
-    for (int64_t k = 1; k < K && uni; ++k)
-      uni = hl1[4 * K + k] == hl1[4 * K] && hl1[5 * K + k] == hl1[5 * K] && hw2[k] == hw2[0] &&
-            hw2[K + k] == hw2[K] && hvg[k] == hvg[0] && hVg[k] == hVg[0];
-    g->phi_uniform = uni;
     std::vector<double> rec((size_t)A * RW, 0.0);
     for (int64_t q = 0; q < A; ++q) {
       double* r = rec.data() + q * RW;
-      for (int t = 0; t < 4; ++t) r[t] = h[t * A + q];
-      r[4] = h[4 * A + q] * hl1[4 * K];  // il2(2, +) * il1(2, +)
-      r[5] = h[5 * A + q] * hl1[5 * K];  // il2(2, -) * il1(2, -)
-      for (int c = 0; c < 8; ++c) {      // om(s0 s1 s2) = wo01(s0 s1) * wo2(s2), c = s0*4 + s1*2 + s2
-        const int s01 = c >> 1, s2 = c & 1;
-        r[6 + c] = hw[s01 * A + q] * hw2[s2 * K];
-      }
-      r[14] = hv[q] * hvg[0];
-      r[15] = hV[q] * hVg[0];
+      for (int t = 0; t < 6; ++t) r[t] = h[t * A + q];
+      for (int t = 0; t < 4; ++t) r[6 + t] = hw[t * A + q];
+      r[10] = hv[q];
+      r[11] = hV[q];
     }
     CUDA_TRY(cudaMalloc(&g->rowrec, sizeof(double) * rec.size()));
     CUDA_TRY(cudaMemcpy(g->rowrec, rec.data(), sizeof(double) * rec.size(), cudaMemcpyHostToDevice));

@@ -122,7 +122,6 @@ struct pc_grid {
   double* rowrec = nullptr;  // [n0+2][n1][RW] interleaved row records (TMA march)
   CUtensorMap rowmap;
   bool rowmap_ok = false;
-  bool phi_uniform = false;  // every phi column factor is one constant (the TMA march's folded records)
   int64_t shape[3];
   size_t comp_elems;  // (n0 + 2) * plane
 };

@@ -345,8 +345,7 @@ static bool tma_ok(const pc_grid* g) {
   const GridDev& d = g->g;
   // (phi-slabs: the periodic phi strips of the TMA boxes would wrap across
   // the ghost columns -- the cp.async march reads them as ordinary columns)
-  return d.per2 && !d.phis && g->phi_uniform && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 &&
-         tma_encoder() != nullptr &&
+  return d.per2 && !d.phis && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && tma_encoder() != nullptr &&
          getenv("PC_NO_TMA") == nullptr;
 }
 template <class Epi, int RHO>

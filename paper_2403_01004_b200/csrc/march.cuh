@@ -228,75 +228,6 @@ __device__ __forceinline__ void node_E_rows(double Tv, const double (&Tn)[3][2],
   node_E_core<ONLY_A, ONLY_S>(Tv, Tn, bv, il2, w01, il1, w2, E);
 }
 
-// The same fluxes from FOLDED metric values (uniform phi: the column factors
-// are one constant each, pre-multiplied on the host with the very products the
-// general path forms per node): il2f[x][t] (x = 2 already times iL1_2t),
-// om[q] = wo01(s0 s1) * wo2(s2), q = s0*4 + s1*2 + s2.  Bitwise node_E_core.
-template <int ONLY_A, int ONLY_S>
-__device__ __forceinline__ void node_E_core_f(double Tv, const double (&Tn)[3][2], const double (&bv)[3],
-                                              const double (&il2f)[3][2], const double (&om)[8], double (&E)[3][2]) {
-  double bil[3][2], p[3][2];
-#pragma unroll
-  for (int x = 0; x < 3; ++x) {
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const bool need_p = !(ONLY_A >= 0 && x == ONLY_A && t != ONLY_S);
-      const bool need_bil = need_p || (ONLY_A < 0) || (x == ONLY_A && t == ONLY_S);
-      if (need_bil) bil[x][t] = bv[x] * il2f[x][t];
-      if (need_p) p[x][t] = bil[x][t] * (t == 0 ? (Tn[x][0] - Tv) : (Tv - Tn[x][1]));
-      else p[x][t] = 0.0;
-    }
-  }
-  double f[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int s0 = (q >> 2) & 1, s1 = (q >> 1) & 1, s2 = q & 1;
-    if (ONLY_A >= 0) {
-      const int sa = ONLY_A == 0 ? s0 : (ONLY_A == 1 ? s1 : s2);
-      if (sa != ONLY_S) { f[q] = 0.0; continue; }
-    }
-    const double sv = (p[0][s0] + p[1][s1]) + p[2][s2];
-    f[q] = om[q] * sv;
-  }
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (ONLY_A >= 0 && (a != ONLY_A || s != ONLY_S)) { E[a][s] = 0.0; continue; }
-      double acc = 0.0;
-      bool first = true;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int sa = a == 0 ? (q >> 2) & 1 : (a == 1 ? (q >> 1) & 1 : q & 1);
-        if (sa != s) continue;
-        acc = first ? f[q] : acc + f[q];
-        first = false;
-      }
-      E[a][s] = bil[a][s] * acc;
-    }
-  }
-}
-// folded row record [16] (16-byte aligned): il2f pairs, om pairs, iv, W
-template <int ONLY_A, int ONLY_S>
-__device__ __forceinline__ void node_E_rows_f(double Tv, const double (&Tn)[3][2], const double (&bv)[3],
-                                              const double* rw, double (&E)[3][2]) {
-  const double2* r2 = reinterpret_cast<const double2*>(rw);
-  double il2f[3][2], om[8];
-#pragma unroll
-  for (int x = 0; x < 3; ++x) {
-    const double2 v = r2[x];
-    il2f[x][0] = v.x;
-    il2f[x][1] = v.y;
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const double2 v = r2[3 + q];
-    om[2 * q] = v.x;
-    om[2 * q + 1] = v.y;
-  }
-  node_E_core_f<ONLY_A, ONLY_S>(Tv, Tn, bv, il2f, om, E);
-}
-
 // Slot of the plane partial of one warp of a marching block: warp w of tile
 // (blockIdx.y, blockIdx.x) on local plane tf; S = tiles x warps per plane
 // (the GPU-count-invariant reduction order, kernels.cuh PlaneRed).

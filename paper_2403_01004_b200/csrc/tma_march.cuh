@@ -42,14 +42,11 @@ struct TmaMaps {
   CUtensorMap B[3];  // beta, box {32, 18, 1}
   CUtensorMap BS[3]; // beta strips
   CUtensorMap O[3];  // epilogue operands, box {32, 16, 1}
-  CUtensorMap RW;    // row records [n0+2][n1][16], box {16, 18, 1}
+  CUtensorMap RW;    // row records [n0+2][n1][12], box {12, 18, 1}
 };
 
-// folded metric row record (uniform phi, pc_grid_create): iL2[6] with the phi
-// pair times iL1_2, om[8] = wo01(s0 s1) * wo2(s2), iVal2 * iValg, Val2 * Valg
-// (16-byte aligned pairs; 128 bytes per row)
-constexpr int RW = 16;
-constexpr int RSLOT = MHJ * RW;  // one plane of row records (18 x 16 = 288 doubles, a 128-byte multiple)
+constexpr int RW = 12;  // metric row record: iL2[6], wo01[4], iVal2, pad (16-byte aligned pairs)
+constexpr int RSLOT = 224;  // one plane of row records (18 x 12) padded to a 128-byte multiple
 constexpr unsigned kRowBytes = (unsigned)(MHJ * RW) * 8u;
 struct TmaSmem {
   double T[TSL][XA];
@@ -57,6 +54,7 @@ struct TmaSmem {
   double EO[2][3][XO];
   FluxX E[2];
   double rowt[RSL][RSLOT];
+  double ringcol[2][9];
   unsigned long long bar;
 };
 
@@ -110,9 +108,22 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   const int kL = k0 == 0 ? g.n2 - 2 : k0 - 2;     // strip of columns k0-2, k0-1
   const int kR = k0 + MTK == g.n2 ? 0 : k0 + MTK;  // strip of columns k0+32, k0+33
 
-  // (uniform phi: every column factor is folded into the row records, so
-  // the march carries no per-column metric state; tma_ok checks it)
+  ColT col;
+  load_col(g, kg, col);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) col.il1[q] = launder(col.il1[q]);
+  col.w2[0] = launder(col.w2[0]);
+  col.w2[1] = launder(col.w2[1]);
+  col.ivg = launder(col.ivg);
   const bool pin_k = (g.pin_lo2 && kg == 0) || (g.pin_hi2 && kg == g.n2 - 1);
+  const double valg = Epi::NEEDS_W ? launder(__ldg(g.Valg + kg)) : 0.0;
+  if (tid < 18) {  // phi-ring column tables
+    const int side = tid / 9, q = tid % 9;
+    bool okr;
+    const int kr = map_k(g, side == 0 ? k0 - 1 : k0 + MTK, okr);
+    const double* src = q < 6 ? g.iL1[q] : (q < 8 ? g.wo2[q - 6] : g.iValg);
+    S.ringcol[side][q] = __ldg(src + kr);
+  }
   if (tid == 0) {
     mbar_init(&S.bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -261,7 +272,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
                                    {sTm1[opp[n]], sTm1[opm[n]]}};
           const double bv[3] = {sBn[oc[n]], sBn[XA + oc[n]], sBn[2 * XA + oc[n]]};
           double E[3][2];
-          node_E_rows_f<0, 0>(Tm[n], Tn, bv, rM + (ty + n * MTY + 1) * RW, E);
+          node_E_rows<0, 0>(Tm[n], Tn, bv, rM + (ty + n * MTY + 1) * RW, col.il1, col.w2, E);
           qb[n] = E[0][0];
         }
       }
@@ -324,8 +335,8 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
         if ((FULL && !LAST) || (exists && inside[n])) {
           const double Tn[3][2] = {{Tp, Tm[n]}, {sT[oc[n] + MTK], sT[oc[n] - MTK]}, {sT[opp[n]], sT[opm[n]]}};
           const double bv[3] = {sB[oc[n]], sB[XA + oc[n]], sB[2 * XA + oc[n]]};
-          if (!LAST) node_E_rows_f<-1, 0>(Tc[n], Tn, bv, rC + jr * RW, E);
-          else node_E_rows_f<0, 1>(Tc[n], Tn, bv, rC + jr * RW, E);
+          if (!LAST) node_E_rows<-1, 0>(Tc[n], Tn, bv, rC + jr * RW, col.il1, col.w2, E);
+          else node_E_rows<0, 1>(Tc[n], Tn, bv, rC + jr * RW, col.il1, col.w2, E);
         } else {
 #pragma unroll
           for (int a = 0; a < 3; ++a) E[a][0] = E[a][1] = 0.0;
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
         if (!FIRST && inside[n]) {
           const double nbr = (Er->e1p[r][tx] - Er->e1m[r + 1][tx]) + (Er->e2p[r][tx] - Er->e2m[r][tx + 1]);
           const double G = (qa[n] - E[0][1]) + (ownp[n] + nbr);
-          const double iv = rM[jr * RW + 14];  // iVal2 * iValg
+          const double iv = rM[jr * RW + 10] * col.ivg;
           const int64_t of = pofs + n * nstride;
           double f;
           if constexpr (RHO == 1) f = (G * iv) * (0.0 - (op.pref / rr[n]));
@@ -351,7 +362,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           for (int q = 0; q < Epi::NOPS; ++q) ov[q] = eR[q * XO + r * MTK + tx];
           double W = 0.0;  // inner-product weight rho V = rho * (Val2(row) * Valg(k)) (record slot 11)
           if constexpr (Epi::NEEDS_W) {
-            W = rM[jr * RW + 15];  // Val2 * Valg
+            W = rM[jr * RW + 11] * valg;
             if constexpr (RHO == 1) W = rr[n] * W;
             if constexpr (RHO == 2) W = rpl * W;
           }
@@ -383,18 +394,21 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           const double* rw = rC + rhj_ * RW;
           if (ra == 1) {
             if (rs == 0) {
-              node_E_rows_f<1, 0>(Tcr, Tn, bv, rw, E);
+              node_E_rows<1, 0>(Tcr, Tn, bv, rw, col.il1, col.w2, E);
               Ev = E[1][0];
             } else {
-              node_E_rows_f<1, 1>(Tcr, Tn, bv, rw, E);
+              node_E_rows<1, 1>(Tcr, Tn, bv, rw, col.il1, col.w2, E);
               Ev = E[1][1];
             }
           } else {
+            const double* cs = S.ringcol[rs];
+            const double il1[2] = {cs[4], cs[5]};
+            const double w2[2] = {cs[6], cs[7]};
             if (rs == 0) {
-              node_E_rows_f<2, 0>(Tcr, Tn, bv, rw, E);
+              node_E_rows<2, 0>(Tcr, Tn, bv, rw, il1, w2, E);
               Ev = E[2][0];
             } else {
-              node_E_rows_f<2, 1>(Tcr, Tn, bv, rw, E);
+              node_E_rows<2, 1>(Tcr, Tn, bv, rw, il1, w2, E);
               Ev = E[2][1];
             }
           }
