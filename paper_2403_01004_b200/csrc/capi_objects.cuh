@@ -122,6 +122,14 @@ struct pc_grid {
   double* rowrec = nullptr;  // [n0+2][n1][RW] interleaved row records (TMA march)
   CUtensorMap rowmap;
   bool rowmap_ok = false;
+  // TMA maps of field buffers by (base, box): the pooled buffers recur, so a
+  // stage launch re-encodes nothing after the first cycle
+  struct MapEntry {
+    const double* base;
+    unsigned b0, b1;
+    CUtensorMap m;
+  };
+  std::vector<MapEntry> mapcache;
   int64_t shape[3];
   size_t comp_elems;  // (n0 + 2) * plane
 };

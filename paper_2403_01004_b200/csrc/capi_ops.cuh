@@ -341,6 +341,18 @@ static int make_rows_map(pc_grid* g) {
   g->rowmap_ok = true;
   return PC_OK;
 }
+// a tensor map of a field buffer from the grid's cache (encoded on a miss)
+static int cached_map(pc_grid* g, CUtensorMap* out, const double* base, unsigned box0, unsigned box1) {
+  for (const auto& e : g->mapcache)
+    if (e.base == base && e.b0 == box0 && e.b1 == box1) {
+      *out = e.m;
+      return PC_OK;
+    }
+  TRY(make_field_map(out, base, g->g, box0, box1));
+  if (g->mapcache.size() >= 96) g->mapcache.erase(g->mapcache.begin());
+  g->mapcache.push_back({base, box0, box1, *out});
+  return PC_OK;
+}
 static bool tma_ok(const pc_grid* g) {
   const GridDev& d = g->g;
   // (phi-slabs: the periodic phi strips of the TMA boxes would wrap across
@@ -432,6 +444,22 @@ static int smarch_R(const pc_grid* g, int ncomp) {
   return R;
 }
 static bool smarch_ok(const pc_op* op) { return op->ncomp == 1 || op->ncomp == 3; }
+// TMA staging for the 7-point march (opt-in: PC_SMARCH_TMA=1): phi periodic
+// with whole 32-column tiles, theta not periodic, not a phi-slab.  Measured
+// against the cp.async staging on the same box it is no faster (C2 -2..-10 %,
+// C5v +2 % on the fused stage 1+2, -3 % on the plain stage;
+// profiles/r02_smarch_tma_ab.txt): the per-thread cp.async issue it removes is
+// not what bounds the 3-component stencil, so cp.async stays the default
+static bool smarch_tma_ok(const pc_grid* g) {
+  const GridDev& d = g->g;
+  static const bool on = getenv("PC_SMARCH_TMA") != nullptr && getenv("PC_SMARCH_TMA")[0] == '1';
+  return on && d.per2 && !d.phis && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && tma_encoder() != nullptr;
+}
+template <class E, class = void>
+struct has_y0 : std::false_type {};
+template <class E>
+struct has_y0<E, std::void_t<decltype(&E::y0)>> : std::true_type {};
+
 template <int NC, bool VEC, int DM, class Epi>
 static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, const char* what) {
   pc_grid* g = op->grid;
@@ -439,15 +467,49 @@ static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, c
   const int R = smarch_R(g, NC);
   dim3 grid((g->g.n2 + MTK - 1) / MTK, (g->g.n1 + SMJ - 1) / SMJ, (g->g.n0 + R - 1) / R);
   if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_scalar_march<NC, VEC, DM, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(SMarchSmem<NC, fuse1_of<Epi>::value>)));
-    attr = true;
-  }
+  constexpr bool F1 = fuse1_of<Epi>::value;
   const int zsel = zsplit(c, grid);
-  k_scalar_march<NC, VEC, DM, Epi><<<grid, SNT, sizeof(SMarchSmem<NC, fuse1_of<Epi>::value>), c->s>>>(g->g, op->so, u.p[0], u.p[1], u.p[2],
-                                                                                epi, R, zsel, skip);
+  SMaps maps;
+  if (smarch_tma_ok(g)) {
+    const int smem = (int)sizeof(SMarchSmem<NC, F1, true>) + 128;  // (+ the 128-byte alignment of the boxes)
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(k_scalar_march<NC, VEC, DM, Epi, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    for (int q = 0; q < NC; ++q) {
+      TRY(cached_map(g, &maps.V[q], u.p[q], MTK, SHJ));
+      TRY(cached_map(g, &maps.VS[q], u.p[q], 2, SHJ));
+    }
+    if (DM != 0) {
+      const double* d = DM == 1 ? op->so.D : op->so.rho;
+      TRY(cached_map(g, &maps.D, d, MTK, SHJ));
+      TRY(cached_map(g, &maps.DS, d, 2, SHJ));
+    }
+    if constexpr (F1) {
+      if constexpr (has_y0<Epi>::value) {
+        for (int q = 0; q < NC; ++q) {
+          TRY(cached_map(g, &maps.Y[q], epi.y0[q], MTK, SHJ));
+          TRY(cached_map(g, &maps.YS[q], epi.y0[q], 2, SHJ));
+        }
+      }
+    } else {
+      for (int q = 0; q < Epi::NOPS; ++q) TRY(cached_map(g, &maps.O[q], epi.opnd(q), MTK, SMJ));
+    }
+    k_scalar_march<NC, VEC, DM, Epi, true><<<grid, SNT, smem, c->s>>>(g->g, op->so, u.p[0], u.p[1], u.p[2], epi, R,
+                                                                       zsel, skip, maps);
+  } else {
+    const int smem = (int)sizeof(SMarchSmem<NC, F1, false>);
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(k_scalar_march<NC, VEC, DM, Epi, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    k_scalar_march<NC, VEC, DM, Epi, false><<<grid, SNT, smem, c->s>>>(g->g, op->so, u.p[0], u.p[1], u.p[2], epi,
+                                                                        R, zsel, skip, maps);
+  }
   c->st.launches++;
   return check_launch(what);
 }

@@ -14,7 +14,7 @@
 // forms it (same operands, same order), so the result is bitwise the generic
 // kernel's -- and the oracle's (oracle/operators.py scalar_apply).
 #pragma once
-#include "march.cuh"
+#include "tma_march.cuh"
 
 namespace pc {
 
@@ -35,11 +35,36 @@ constexpr int SEO = 9;               // epilogue operands staged per node (max: 
 #define SMARCH_BLOCKS(NC) ((NC) == 3 ? 2 : 3)
 #endif
 
+// TMA staging (TM, spherical-type grids: phi periodic with n2 % 32 == 0, theta
+// not periodic): per staged array and plane a 32 x 10 main box (columns
+// k0 .. k0+31, rows j0-1 .. j0+8; rows outside theta are zero-filled and only
+// meet a zero face coefficient) and two 2 x 10 strips whose phi coordinates
+// wrap across the periodic seam (columns k0-2, k0-1 and k0+32, k0+33), issued
+// by one lane and completed on one mbarrier per plane; the epilogue operands
+// as 32 x 8 boxes.  Otherwise per-thread cp.async into the 10 x 34 halo tile.
+constexpr int SXM = MTK * SHJ;      // TMA main box 32 x 10
+constexpr int SXS = 32;             // strip 2 x 10, padded to 256 B (128-B aligned boxes)
+constexpr int SXA = SXM + 2 * SXS;  // one staged array-plane in the TMA layout
+constexpr int SPL = SXA > SHP ? SXA : SHP;  // slot size covering both layouts
+constexpr int SNREAL = SXM + 2 * 2 * SHJ;   // real elements of the TMA layout (main + strips)
+constexpr int SNFILL_T = (SNREAL + SNT - 1) / SNT;
+constexpr int kSIss = SNT - 32;     // TMA issuer: lane 0 of the last warp
+constexpr unsigned kSArrBytes = (unsigned)(SXM + 2 * 2 * SHJ) * 8u;  // bytes of one staged array-plane
+constexpr unsigned kSOpBytes = (unsigned)(MTK * SMJ) * 8u;
+
+struct SMaps {                // tensor maps of the TMA-staged 7-point march
+  CUtensorMap V[3], VS[3];    // stencil input components: main box, strips
+  CUtensorMap D, DS;          // D / rho source
+  CUtensorMap Y[3], YS[3];    // F1: y0 components
+  CUtensorMap O[9];           // epilogue operands, box 32 x 8
+};
+
 // F1 (fused stages 1 + 2, Epi::FUSE1): the stencil input is u1 = u0 + mt1 y0,
 // formed into U from a u0 ring (V) and a y0 ring (Y) when each plane lands;
-// the epilogue takes u0 and y0 at the node from V and Y (no operand staging)
+// the epilogue takes u0 and y0 at the node from V and Y (no operand staging).
+// cp.async staging: the 10 x 34 halo tile per array-plane
 template <int NC, bool F1 = false>
-struct SMarchSmem {
+struct SMarchSmemC {
   double V[3][NC + 1][SHP];          // planes t, t+1, t+2 (in flight); slot NC = D / rho source
   double rowt[3][SROWT][SHJ];        // row tables of planes t-1 (r- face), t, t+1 (in flight)
   double EO[2][F1 ? 1 : SEO][SNT];   // epilogue operands of planes t (read) and t+1 (landing)
@@ -47,7 +72,22 @@ struct SMarchSmem {
                                      // theta faces reordered m00 m01 m10 m11 first: two LDS.128)
   double Y[F1 ? 3 : 1][F1 ? NC : 1][F1 ? SHP : 1];  // y0 ring (F1 only; V then holds u0)
   double U[F1 ? 3 : 1][F1 ? NC : 1][F1 ? SHP : 1];  // u1 ring formed from V and Y (F1 only)
+  unsigned long long bar;            // (TMA variant only)
 };
+// TMA staging: the same members in the box layout, ordered so that every
+// TMA destination is 128-byte aligned
+template <int NC, bool F1 = false>
+struct SMarchSmemT {
+  double V[3][NC + 1][SPL];
+  double Y[F1 ? 3 : 1][F1 ? NC : 1][F1 ? SPL : 16];
+  double U[F1 ? 3 : 1][F1 ? NC : 1][F1 ? SPL : 16];
+  double EO[2][F1 ? 1 : SEO][SNT];
+  double2 M[4][SMJ][5];
+  double rowt[3][SROWT][SHJ];
+  unsigned long long bar;            // TMA completion barrier
+};
+template <int NC, bool F1, bool TM>
+using SMarchSmem = std::conditional_t<TM, SMarchSmemT<NC, F1>, SMarchSmemC<NC, F1>>;
 
 template <class E, class = void>
 struct fuse1_of {
@@ -58,15 +98,18 @@ struct fuse1_of<E, std::void_t<decltype(E::FUSE1)>> {
   static constexpr bool value = E::FUSE1;
 };
 
-// DM: 0 = D constant Dc, 1 = D nodal field, 2 = D = Dc * rho (viscosity)
-template <int NC, bool VEC, int DM, class Epi>
+// DM: 0 = D constant Dc, 1 = D nodal field, 2 = D = Dc * rho (viscosity);
+// TM: TMA staging (see SMaps), else cp.async
+template <int NC, bool VEC, int DM, class Epi, bool TM = false>
 __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev g, ScalarOp op, const double* __restrict__ u0p,
                                                          const double* __restrict__ u1p,
                                                          const double* __restrict__ u2p, Epi epi, int R, int zsel,
-                                                         const int* skip) {
+                                                         const int* skip, const __grid_constant__ SMaps maps) {
   constexpr bool F1 = fuse1_of<Epi>::value;
-  extern __shared__ __align__(16) unsigned char smarch_smem[];
-  SMarchSmem<NC, F1>& S = *reinterpret_cast<SMarchSmem<NC, F1>*>(smarch_smem);
+  extern __shared__ __align__(128) unsigned char smarch_smem[];
+  // TMA destinations must be 128-byte aligned: align the dynamic base (the launch adds 128 bytes)
+  SMarchSmem<NC, F1, TM>& S = *reinterpret_cast<SMarchSmem<NC, F1, TM>*>(
+      smarch_smem + (TM ? ((128u - (smem_u32(smarch_smem) & 127u)) & 127u) : 0u));
   if (skip && *skip) return;
   constexpr bool HASD = DM != 0;
   const double* uin[3] = {u0p, u1p, u2p};
@@ -77,19 +120,47 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
   const int iend = min(i0 + R, g.n0);
   const int kg = k0 + tx, jg = j0 + ty;
 
-  int foff[SNFILL];
+  // fill elements of this thread: cp.async staging (halo tile 10 x 34: the
+  // source offset) or, with TMA, the layout slots F1 forms u1 over
+  constexpr int NF = TM ? SNFILL_T : SNFILL;
+  int foff[NF];
   unsigned pinfill = 0;  // F1: fill element q sits on a theta/phi Dirichlet node (u1 = u0 there)
 #pragma unroll
-  for (int q = 0; q < SNFILL; ++q) {
+  for (int q = 0; q < NF; ++q) {
     const int e = tid + q * SNT;
-    const int hj = e / MHK, hk = e - hj * MHK;
+    int hj, kk0;
+    if (TM) {  // main rows of 32, then the left (k0-2, k0-1) and right (k0+32, k0+33) strips
+      if (e < SXM) {
+        hj = e / MTK;
+        kk0 = k0 + (e - hj * MTK);
+      } else {
+        const int r = e - SXM, side = r / (2 * SHJ), w = r - side * 2 * SHJ;
+        hj = w >> 1;
+        kk0 = (side == 0 ? k0 - 2 : k0 + MTK) + (w & 1);
+      }
+    } else {
+      hj = e / MHK;
+      kk0 = k0 - 1 + (e - hj * MHK);
+    }
     bool oj, ok;
-    const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, k0 - 1 + hk, ok);
-    foff[q] = e < SHP ? jj * g.n2 + kk : -1;
+    const int jj = map_j(g, j0 - 1 + hj, oj), kk = map_k(g, kk0, ok);
+    if (TM) {
+      const int r = e - SXM;
+      foff[q] = e >= SNREAL ? -1 : (e < SXM ? e : SXM + (r / (2 * SHJ)) * SXS + (r % (2 * SHJ)));
+    } else {
+      foff[q] = e < SHP ? jj * g.n2 + kk : -1;
+    }
     if ((g.pin_lo1 && jj == 0) || (g.pin_hi1 && jj == g.n1 - 1) || (g.pin_lo2 && kk == 0) ||
         (g.pin_hi2 && kk == g.n2 - 1))
       pinfill |= 1u << q;
   }
+  const int kL = k0 == 0 ? g.n2 - 2 : k0 - 2;     // TMA strips (phi wraps across the seam)
+  const int kR = k0 + MTK == g.n2 ? 0 : k0 + MTK;
+  if (TM && tid == 0) {
+    mbar_init(&S.bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned phase = 0;
   const bool rton = tid < SROWT * SHJ;
   const int rtab = tid / SHJ, rhj = tid - (tid / SHJ) * SHJ;
   bool rok;
@@ -123,12 +194,35 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
   nb1(g, jg < g.n1 ? jg : g.n1 - 1, -1, okjm);
   const bool pin_jk = (g.pin_lo1 && jg == 0) || (g.pin_hi1 && jg == g.n1 - 1) || (g.pin_lo2 && kg == 0) ||
                       (g.pin_hi2 && kg == g.n2 - 1);
-  const int h = (ty + 1) * MHK + (tx + 1);
+  // staged-tile offsets of the own node and its theta / phi neighbours
+  const int h = TM ? (ty + 1) * MTK + tx : (ty + 1) * MHK + (tx + 1);
+  const int htm = TM ? h - MTK : h - MHK, htp = TM ? h + MTK : h + MHK;
+  const int hpm = TM ? (tx > 0 ? h - 1 : SXM + (ty + 1) * 2 + 1) : h - 1;
+  const int hpp = TM ? (tx < MTK - 1 ? h + 1 : SXM + SXS + (ty + 1) * 2) : h + 1;
   const int onode = jg * g.n2 + kg;
+  // (TMA issue, lane 0 of the last warp: all boxes of one plane complete on S.bar)
+  auto tma_arr = [&](double* dst, const CUtensorMap* mm, const CUtensorMap* ms, int z) {
+    tma3(dst, mm, k0, j0 - 1, z, &S.bar);
+    tma3(dst + SXM, ms, kL, j0 - 1, z, &S.bar);
+    tma3(dst + SXM + SXS, ms, kR, j0 - 1, z, &S.bar);
+  };
 
   auto eslot = [&](int p) { return (p - i0) & 1; };
   auto issue_V = [&](int p, int sl) {
     const PlaneMap pm = plane_map(g, p);
+    if constexpr (TM) {
+      if (tid == kSIss) {
+        const int z = pm.mem + 1;  // (the tensors start at ghost plane -1)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) tma_arr(&S.V[sl][c][0], &maps.V[c], &maps.VS[c], z);
+        if (HASD) tma_arr(&S.V[sl][NC][0], &maps.D, &maps.DS, z);
+        if constexpr (F1) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) tma_arr(&S.Y[sl][c][0], &maps.Y[c], &maps.YS[c], z);
+        }
+      }
+      return;
+    }
     const int64_t base = (int64_t)pm.mem * g.plane;
 #pragma unroll
     for (int q = 0; q < SNFILL; ++q)
@@ -152,9 +246,9 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       const int ig = pm.mem + g.i0g;
       const bool ppin = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
 #pragma unroll
-      for (int q = 0; q < SNFILL; ++q)
+      for (int q = 0; q < NF; ++q)
         if (foff[q] >= 0) {
-          const int e = tid + q * SNT;
+          const int e = TM ? foff[q] : tid + q * SNT;
           const bool pn = ppin || ((pinfill >> q) & 1u);
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
@@ -176,6 +270,14 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
     else return S.V[sl][c][e];
   };
   auto issue_ops = [&](int p) {
+    if constexpr (TM) {
+      if (!F1 && Epi::NOPS > 0 && tid == kSIss) {
+        const int es = eslot(p);
+#pragma unroll
+        for (int q = 0; q < Epi::NOPS; ++q) tma3(&S.EO[es][q][0], &maps.O[q], k0, j0, p + 1, &S.bar);
+      }
+      return;
+    }
     if (!F1 && Epi::NOPS > 0 && inside) {
       const int64_t o = (int64_t)p * g.plane + onode;
       const int es = eslot(p);
@@ -187,7 +289,14 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
   // ring slots of planes t-1, t, t+1 (vslot / rslot (p - i0 + 1) % 3, rotated
   // once per plane instead of a modulo per use); t+2 reuses the t-1 slot
   int s_m = 0, s_c = 1, s_p = 2;
+  // bytes of one plane's boxes (TMA): staged arrays (+ D, + y0) and operands
+  constexpr unsigned kVB = (unsigned)(NC + (HASD ? 1 : 0) + (F1 ? NC : 0)) * kSArrBytes;
+  constexpr unsigned kOB = F1 ? 0u : (unsigned)Epi::NOPS * kSOpBytes;
   // ---- prologue: V(i0-1..i0+1), rows(i0-1, i0), operands(i0)
+  if (TM) {
+    __syncthreads();  // barrier initialised
+    if (tid == kSIss) mbar_expect_tx(&S.bar, (i0 + 1 <= iend ? 3u : 2u) * kVB + kOB);
+  }
   issue_V(i0 - 1, s_m);
   issue_V(i0, s_c);
   if (i0 + 1 <= iend) issue_V(i0 + 1, s_p);
@@ -196,6 +305,10 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
   issue_ops(i0);
   cp_async_commit();
   cp_async_wait<0>();
+  if (TM) {
+    mbar_wait(&S.bar, phase);
+    phase ^= 1u;
+  }
   form_u1(i0 - 1, s_m);
   form_u1(i0, s_c);
   if (i0 + 1 <= iend) form_u1(i0 + 1, s_p);
@@ -221,6 +334,10 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
 
 #pragma unroll 1
   for (int t = i0; t < iend; ++t) {
+    if (TM && tid == kSIss) {  // one phase per plane: arm it with all of this plane's boxes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&S.bar, (t + 2 <= iend ? kVB : 0u) + (t + 1 < iend ? kOB : 0u));
+    }
     if (t + 2 <= iend) issue_V(t + 2, s_m);
     if (t + 1 <= iend) issue_rows(t + 1, s_p);
     if (t + 1 < iend) issue_ops(t + 1);
@@ -251,18 +368,18 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       for (int c = 0; c < NC; ++c) {
         nv[0][0][c] = vm[c];
         nv[0][1][c] = vp[c];
-        nv[1][0][c] = uat(sc, c, h - MHK);
-        nv[1][1][c] = uat(sc, c, h + MHK);
-        nv[2][0][c] = uat(sc, c, h - 1);
-        nv[2][1][c] = uat(sc, c, h + 1);
+        nv[1][0][c] = uat(sc, c, htm);
+        nv[1][1][c] = uat(sc, c, htp);
+        nv[2][0][c] = uat(sc, c, hpm);
+        nv[2][1][c] = uat(sc, c, hpp);
       }
       if (HASD) {
         nd[0][0] = dm;
         nd[0][1] = dp;
-        nd[1][0] = S.V[sc][NC][h - MHK];
-        nd[1][1] = S.V[sc][NC][h + MHK];
-        nd[2][0] = S.V[sc][NC][h - 1];
-        nd[2][1] = S.V[sc][NC][h + 1];
+        nd[1][0] = S.V[sc][NC][htm];
+        nd[1][1] = S.V[sc][NC][htp];
+        nd[2][0] = S.V[sc][NC][hpm];
+        nd[2][1] = S.V[sc][NC][hpp];
       }
       double Sx[NC];
 #pragma unroll
@@ -346,6 +463,10 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       dc = dp;
     }
     cp_async_wait<0>();
+    if (TM) {
+      mbar_wait(&S.bar, phase);
+      phase ^= 1u;
+    }
     if (t + 2 <= iend) form_u1(t + 2, s_m);
     __syncthreads();
     {  // rotate the slot roles: t-1 <- t, t <- t+1, t+1 <- t+2 (the old t-1 slot)

@@ -28,3 +28,12 @@ def test_kernel_families_poisoned_and_repeated(poison):
                        capture_output=True, text=True, env=env, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "all cases ok" in r.stdout
+
+
+def test_smarch_tma_staging_opt_in():
+    """The opt-in TMA staging of the 7-point march (PC_SMARCH_TMA=1) is
+    bitwise the cp.async staging and the oracle (smarch and persist cases)."""
+    env = dict(os.environ, PC_SMARCH_TMA="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "sanitize_cases.py"), "smarch", "pcg"],
+                       capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
