@@ -2,29 +2,34 @@
 """Benchmark of the PTL-cycled parabolic advance (BASELINE.json metric:
 cell-updates/s per full parabolic step, fp64, with the HBM roofline fraction).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+                    [--decomp r|phi] [--weak] [--scheme rkl2|rkg2|be] [--pc jacobi|line-r] [--no-ptl]
 
 A "step" is one full MAS parabolic step of the chosen config: refresh the
 lagged T0 (coefficients + Gershgorin bound) and advance the outer step with
 PTL cycling (RKL2 stages or BE+PCG iterations).  Every step starts from the
 same seeded initial state (restored by a device copy inside the step), so each
 timed step is the same workload.  One cell-update = one cell advanced by one
-RKL2 stage or one PCG iteration.
+RKL2 stage or one PCG iteration.  ``--gpus N`` without a
+launcher starts the N ranks itself (one per GPU, rendezvous on 127.0.0.1).
 
   value        = cells x (sum of stages / PCG iterations) / device time of the
                  K steps (CUDA events on the library stream, max over ranks)
   e2e          = the same metric through the public API (ptl.split_advance on
                  host Fields): pinned host -> device copies of the step inputs
-                 (T, b) and the device -> host copy of the result are inside
-  roofline     = algorithmic bytes of the fused stage kernels / their device
-                 time (CUDA events around the stage launches), vs the measured
-                 HBM copy bandwidth in MEASURED_PEAKS.json
-  cpu_baseline = the numpy oracle (oracle/, "port" of the reference algorithm)
-                 on a bounded r-chunk sample, 1 host thread
+                 (T, b, rho, v) and the device -> host copy of the result inside
+  roofline     = algorithmic bytes of the dominant hot loop / its device time
+                 (CUDA events around its launches), vs the measured HBM copy
+                 bandwidth in MEASURED_PEAKS.json; traffic from the committed
+                 ncu capture (profiles/ncu_summary.json)
+  cpu_baseline = the numpy oracle (oracle/, the "port" of the reference
+                 algorithm), 1 host process: per-piece timings of bounded
+                 r-chunk samples EXTRAPOLATED to the full step with its exact
+                 cycle / stage mix (see STEP_COUNTS)
 
-``--impl reference`` times the oracle (the reference CPU algorithm; the
-reference repository ships no implementation of this path) on all host cores
-(one process per core over r-chunks) and prints the same metric.
+``--impl reference`` times the same extrapolated oracle on all host cores
+(one process per core over r-chunks; the reference repository ships no
+implementation of this path) and prints the same metric and config.
 """
 from __future__ import annotations
 
