@@ -53,6 +53,9 @@ BYTES = {
     ("aligned", "rkl2"): 64,   # reads u_{k-1}, beta(3), u_{k-2}, u0, y0; writes u_k
     ("aligned_rho", "rkl2"): 64,   # + rho, radial (C5: rho(r), read once per plane, not per node)
     ("aligned", "be"): 128,    # Kp: r, p_old, d -> p; K7: p, beta(3) -> Ap; K8: x, r, p, Ap, d -> x, r
+    # one rank, point Jacobi: the p-update fused into the matvec march (EpiMatvecP)
+    # r, p_old, d, beta(3) -> p, Ap; K8: x, r, p, Ap, d -> x, r
+    ("aligned", "be-fused"): 120,
     # r-line preconditioner: z, p_old -> p; p, beta(3) -> Ap; x, r, p, Ap -> x, r;
     # line solve r, jl, inv -> z' and z', cp, r -> z
     ("aligned", "be-line"): 176,
@@ -332,20 +335,23 @@ def run_ours(args, rank, world, local_rank):
     kind = "be" if sc.kind == "backward_euler" else "rkl2"
     if kind == "be" and sc.preconditioner == "line-r":
         kind = "be-line"
+    fusedp = kind == "be" and world == 1 and os.environ.get("PC_PCG_NO_FUSEP") is None
     # roofline: the hot loop with the largest device time, its algorithmic bytes
     rows = []
     for fname, op, nc, bkey in prob.ops:
         kk = ("pcg_" if kind.startswith("be") else "sts_") + ("aligned" if op.kind == "aligned" else "scalar")
         d = kinds[kk]
         if d["ms"] > 0:
-            bpc = BYTES[(bkey, kind)]
+            bpc = BYTES[(bkey, "be-fused")] if (fusedp and op.kind == "aligned") else BYTES[(bkey, kind)]
             rows.append({"kernel": {"sts_aligned": "k_aligned_tma<EpiStage> (TMA march)",
                                     "sts_scalar": ("k_cycle_small<%d> (persistent cycle loop: F, argmax, stages)" % nc
                                                    if prob.dg.ncells * nc <= (1 << 21) else
                                                    "k_scalar_march<" + str(nc) + " comp, SEpiStage>"),
                                     "pcg_aligned": ("k_pcg_pupdate_z + k_aligned_tma<EpiMatvecT> + k_pcg_update1 + "
                                                     "k_line_solve") if kind == "be-line" else
-                                                   "k_pcg_pupdate + k_aligned_tma<EpiMatvecT> + k_pcg_update1",
+                                                   ("k_aligned_tma<EpiMatvecP> (p-update fused) + k_pcg_update1"
+                                                    if fusedp else
+                                                    "k_pcg_pupdate + k_aligned_tma<EpiMatvecT> + k_pcg_update1"),
                                     "pcg_scalar": "k_pcg_matvec + k_pcg_update"}[kk],
                          "ms": d["ms"], "bytes_per_cell_update": bpc,
                          "achieved": bpc * d["cell_updates"] / (d["ms"] / 1e3) / 1e9,

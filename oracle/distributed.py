@@ -249,7 +249,8 @@ def slab_cycle_operator(sop, kind, u_int, outer_dt, dt_euler, eps_rel=1e-12, tol
             W = slab.interior(sop.op.weights())
             wdot = lambda x, y: slab.plane_sum((W * x) * y)  # noqa: E731
             A = lambda x: x - dt * sop.apply_ext(slab.extend(x))  # noqa: E731
-            u, iters = _pcg(A, u, lambda r: r / dvec, u, wdot, tol, max_iter)
+            inv = 1.0 / dvec  # the stored inverse diagonal
+            u, iters = _pcg(A, u, lambda r: r * inv, u, wdot, tol, max_iter)
         cyc += 1
         report.append(CycleRecord(cyc, dt, ptl, ptl is not None, iters))
         remaining = 0.0 if dt == remaining else remaining - dt

@@ -192,13 +192,14 @@ def backward_euler_step(apply, diag, W, u, dt, tol, max_iter, pinned, line=None)
     ``line`` = (jl, ju): the r-line preconditioner (-J_{i,i-1}, -J_{i,i+1},
     single component) instead of point Jacobi."""
     dvec = 1.0 + dt * diag
+    inv = 1.0 / dvec  # the stored inverse diagonal (SPEC.md:192-200), once per solve
 
     def A(x):
         return x - dt * apply(x)
 
     if line is None:
         def dinv(r):
-            return r / dvec
+            return r * inv
     else:
         from .operators import line_factor, line_solve
         jl, ju = line

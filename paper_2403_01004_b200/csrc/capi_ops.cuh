@@ -403,6 +403,12 @@ static int launch_tma(pc_op* op, const double* Tin, const Epi& epi, const int* s
   TRY(make_field_map(&maps.T, Tin, g->g, MTK, MHJ));
   TRY(make_field_map(&maps.TS, Tin, g->g, 2, MHJ));
   for (int q = 0; q < Epi::NOPS; ++q) TRY(make_field_map(&maps.O[q], epi.opnd(q), g->g, MTK, MTJ));
+  if constexpr (fusep_of<Epi>::value) {  // fused PCG matvec: p_old and d boxes beside r (= Tin)
+    TRY(make_field_map(&maps.P[0], epi.pold, g->g, MTK, MHJ));
+    TRY(make_field_map(&maps.PS[0], epi.pold, g->g, 2, MHJ));
+    TRY(make_field_map(&maps.P[1], epi.dinv, g->g, MTK, MHJ));
+    TRY(make_field_map(&maps.PS[1], epi.dinv, g->g, 2, MHJ));
+  }
   if (op->ao.rho && op->ao.rho_r) return launch_tma_t<Epi, 2>(op, maps, epi, skip, what);
   if (op->ao.rho) return launch_tma_t<Epi, 1>(op, maps, epi, skip, what);
   return launch_tma_t<Epi, 0>(op, maps, epi, skip, what);

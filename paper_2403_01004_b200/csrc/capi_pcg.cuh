@@ -111,6 +111,16 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
     TRY(work_get(g, 2, Lf));
   }
   int rc = halo_field(x);
+  // the stored inverse Jacobi diagonal of this solve, dinv = 1 / (a + dt d)
+  // (SPEC.md:192-200): every z = r dinv below multiplies by it
+  Work dvw;
+  if (rc == PC_OK) rc = work_get(g, 1, dvw);
+  if (rc == PC_OK) {
+    k_pcg_dinv<<<nb, kThreads, 0, c->s>>>(g->g, dg, adiag, dt, dvw.base(0));
+    c->st.launches++;
+    rc = check_launch("k_pcg_dinv");
+  }
+  const double* dinv = dvw.b[0] ? dvw.base(0) : nullptr;
   // split reductions: the kernels stop at the per-plane sums, NCCL gathers
   // them (the r-line preconditioner is single-rank)
   const bool split = c->comm != nullptr && !line;
@@ -127,10 +137,10 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
     if constexpr (std::is_same<Op, AlignedOp>::value) {
       // r = b - A x0 through the marching kernel (x0 staged like any T)
       if (adiag) {
-        EpiPcgInitT<true> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, prm.slot[0], prm.slot[1]};
+        EpiPcgInitT<true> e{b.p[0], dinv, adiag, r.base(0), p0.base(0), dt, prm.slot[0], prm.slot[1]};
         rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
       } else {
-        EpiPcgInitT<false> e{b.p[0], dg, adiag, r.base(0), p0.base(0), dt, prm.slot[0], prm.slot[1]};
+        EpiPcgInitT<false> e{b.p[0], dinv, adiag, r.base(0), p0.base(0), dt, prm.slot[0], prm.slot[1]};
         rc = launch_march(op, cfld(x).p[0], e, nullptr, "k_aligned_march<pcg init>");
       }
       if (rc == PC_OK) rc = plane_sums(g, prm, 2, PR_INIT, line ? 1 : 0, split, tol, 0);
@@ -139,7 +149,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         if (rc == PC_OK) rc = line_apply(op, r.base(0), Lf, dt, z.base(0), 0);
       }
     } else {
-      k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dg, adiag, dt, prr, c->pcg);
+      k_pcg_init<<<nb, kThreads, 0, c->s>>>(g->g, o, b, cfld(x), r.f(), p0.f(), dinv, adiag, dt, prr, c->pcg);
       c->st.launches++;
       rc = check_launch("k_pcg_init");
       if (rc == PC_OK) rc = plane_sums(g, prr, 2, PR_INIT, 0, split, tol, 0);
@@ -161,10 +171,24 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   // C4 update 2.72 -> 2.03 ms (profiles/r01_c4_pcg_vec.txt).  PC_PCG_SCALAR_IO
   // keeps the 64-bit kernels (tests compare the two)
   const bool vio = g->g.n2 % 2 == 0 && getenv("PC_PCG_SCALAR_IO") == nullptr;
+  // the p-update fused into the matvec march (EpiMatvecP: r, p_old, d staged,
+  // p formed on the fly): TMA march, point Jacobi, no mass diagonal, and no
+  // ghost planes / columns (their p would need r, p_old, d exchanged instead
+  // of p); PC_PCG_NO_FUSEP keeps the separate p-update kernel (tests compare)
+  const bool fusep = std::is_same<Op, AlignedOp>::value && !line && !adiag && tma_ok(g) && !g->g.ghost_lo0 &&
+                     !g->g.ghost_hi0 && !g->g.phis && getenv("PC_PCG_NO_FUSEP") == nullptr;
   while (rc == PC_OK && !stop && it < max_iter) {
     for (int q = 0; q < batch && it < max_iter && rc == PC_OK; ++q) {
       ++it;
       if constexpr (std::is_same<Op, AlignedOp>::value) {
+        const int* done = reinterpret_cast<const int*>(reinterpret_cast<const char*>(c->pcg) + offsetof(PcgDev, done));
+        if (fusep) {  // p-update + matvec in one march
+          EpiMatvecP e{pold->base(0), dinv, pnew->base(0), Ap.base(0), dt, prm.slot[0], c->pcg};
+          rc = launch_march(op, r.base(0), e, done, "k_aligned_march<matvec + p-update>");
+          if (rc == PC_OK) rc = plane_sums(g, prm, 1, PR_MATVEC, 0, split, tol, it);
+          if (rc) break;
+          goto matvec_done;
+        }
         // p = z + beta p_old (beta from the device-side PCG state), then the
         // marching matvec stages p like any other field
         if (line) {
@@ -172,17 +196,15 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         } else if (vio) {
           // four phi pairs per lane at 2 blocks/SM: 1.21 ms at C4 (7.1 TB/s) against 1.32 (two pairs,
           // 4 blocks, spills) and 1.54 (two pairs, 85 registers) -- profiles/r01_c4_pcg_vec.txt
-          k_pcg_pupdatev<4, 2><<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag,
-                                                          dt, c->pcg);
+          k_pcg_pupdatev<4, 2><<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dinv,
+                                                          c->pcg);
         } else {
-          k_pcg_pupdate<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dg, adiag, dt,
-                                                   c->pcg);
+          k_pcg_pupdate<<<nb, kThreads, 0, c->s>>>(g->g, r.base(0), pold->base(0), pnew->base(0), dinv, c->pcg);
         }
         c->st.launches++;
         rc = check_launch("k_pcg_pupdate");
         if (rc == PC_OK) rc = halo_work(g, *pnew);
         if (rc) break;
-        const int* done = reinterpret_cast<const int*>(reinterpret_cast<const char*>(c->pcg) + offsetof(PcgDev, done));
         if (adiag) {
           EpiMatvecT<true> e{adiag, Ap.base(0), dt, prm.slot[0]};
           rc = launch_march(op, pnew->base(0), e, done, "k_aligned_march<matvec>");
@@ -192,11 +214,12 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
         }
         if (rc == PC_OK) rc = plane_sums(g, prm, 1, PR_MATVEC, 0, split, tol, it);
         if (rc) break;
+      matvec_done:;
       } else {
         rc = halo_work(g, r);
         if (rc == PC_OK) rc = halo_work(g, *pold);
         if (rc) break;
-        k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dg, adiag, dt,
+        k_pcg_matvec<<<nb, kThreads, 0, c->s>>>(g->g, o, r.cf(), pold->cf(), pnew->f(), Ap.f(), dinv, adiag, dt,
                                                 prr, c->pcg);
         rc = check_launch("k_pcg_matvec");
         if (rc == PC_OK) rc = plane_sums(g, prr, 1, PR_MATVEC, 0, split, tol, it);
@@ -213,10 +236,10 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
                                        : (adiag ? k_pcg_update1<false, true, true> : k_pcg_update1<false, false, true>))
                               : (o.rho ? (adiag ? k_pcg_update1<true, true> : k_pcg_update1<true, false>)
                                        : (adiag ? k_pcg_update1<false, true> : k_pcg_update1<false, false>)));
-        upd<<<nb, kThreads, 0, c->s>>>(g->g, x->base(0), r.base(0), pnew->base(0), Ap.base(0), dg, adiag, o.rho, dt,
+        upd<<<nb, kThreads, 0, c->s>>>(g->g, x->base(0), r.base(0), pnew->base(0), Ap.base(0), dinv, adiag, o.rho, dt,
                                        tol, it, prr, c->pcg);
       } else {
-        k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dg, adiag, dt, prr,
+        k_pcg_update<<<nb, kThreads, 0, c->s>>>(g->g, o, fld(x), r.f(), pnew->cf(), Ap.cf(), dinv, adiag, dt, prr,
                                                 c->pcg);
       }
       c->st.launches += std::is_same<Op, AlignedOp>::value ? 1 : 2;  // (march counted at launch)
@@ -241,7 +264,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   }
   if (rc == PC_OK) {
     CUDA_TRY(cudaMemcpyAsync(c->h_pcg, c->pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, c->s));
-    c->st.kind_launches[pkind] += (int64_t)c->h_pcg->it * (std::is_same<Op, AlignedOp>::value ? 3 : 2);
+    c->st.kind_launches[pkind] += (int64_t)c->h_pcg->it * (std::is_same<Op, AlignedOp>::value ? (fusep ? 2 : 3) : 2);
     c->st.kind_units[pkind] += (int64_t)c->h_pcg->it * owned_cells(g->g);
     CUDA_TRY(cudaStreamSynchronize(c->s));
     const PcgDev& st = *c->h_pcg;
@@ -255,6 +278,7 @@ static int pcg_run(pc_op* op, const Op& o, double dt, const double* adiag, CFld 
   work_put(p0);
   work_put(p1);
   work_put(Ap);
+  if (dvw.b[0]) work_put(dvw);
   if (line) {
     work_put(z);
     work_put(Lf);

@@ -429,17 +429,25 @@ __global__ void __launch_bounds__(kThreads) k_plane_sums(PlaneRed pr, int nsum, 
   }
 }
 
-// p = z + beta p_old, z = r / (a + dt dg): the search-direction update of the
-// aligned PCG, ahead of the marching matvec (which then stages p like any T)
+// the stored inverse Jacobi diagonal of a solve ("stored
+// inverse diagonal"): dinv = 1 / (a + dt d), once per PCG solve
+__global__ void __launch_bounds__(kThreads) k_pcg_dinv(GridDev g, const double* dg, const double* adiag, double dt,
+                                                       double* dinv) {
+  PC_FOR_NODES(g, i, j, k) {
+    const int64_t o = off3(g, i, j, k);
+    dinv[o] = 1.0 / ((adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o));
+  }
+}
+
+// p = z + beta p_old, z = r dinv: the search-direction update of the aligned
+// PCG, ahead of the marching matvec (which then stages p like any T)
 __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const double* r, const double* pold,
-                                                          double* pnew, const double* dg, const double* adiag,
-                                                          double dt, const PcgDev* st) {
+                                                          double* pnew, const double* dinv, const PcgDev* st) {
   if (st->done) return;
   const double beta = st->beta;
   PC_FOR_NODES(g, i, j, k) {
     const int64_t o = off3(g, i, j, k);
-    const double dvec = (adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o);
-    const double z = __ldg(r + o) / dvec;
+    const double z = __ldg(r + o) * __ldg(dinv + o);
     pnew[o] = z + beta * __ldg(pold + o);
   }
 }
@@ -448,9 +456,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(GridDev g, const doubl
 template <int U = 4, int MINB = 2>
 __global__ void __launch_bounds__(kThreads, MINB) k_pcg_pupdatev(GridDev g, const double* __restrict__ r,
                                                            const double* __restrict__ pold, double* __restrict__ pnew,
-                                                           const double* __restrict__ dg,
-                                                           const double* __restrict__ adiag, double dt,
-                                                           const PcgDev* st) {
+                                                           const double* __restrict__ dinv, const PcgDev* st) {
   if (st->done) return;
   const double beta = st->beta;
   const int lane = threadIdx.x & 31;
@@ -458,22 +464,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_pcg_pupdatev(GridDev g, cons
   for (int row = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < nrows; row += gridDim.x * (kThreads / 32)) {
     const int64_t base = (int64_t)(row / g.n1) * g.plane + (int64_t)(row % g.n1) * g.n2;
     for (int k0 = 2 * lane; k0 < g.n2; k0 += 64 * U) {
-      double2 rv[U], pv[U], dv[U], mv[U];
+      double2 rv[U], pv[U], dv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t o = base + k0 + 64 * u;
         if (k0 + 64 * u < g.n2) {
           rv[u] = __ldg(reinterpret_cast<const double2*>(r + o));
           pv[u] = __ldg(reinterpret_cast<const double2*>(pold + o));
-          dv[u] = __ldg(reinterpret_cast<const double2*>(dg + o));
-          mv[u] = adiag ? __ldg(reinterpret_cast<const double2*>(adiag + o)) : make_double2(1.0, 1.0);
+          dv[u] = __ldg(reinterpret_cast<const double2*>(dinv + o));
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t o = base + k0 + 64 * u;
         if (k0 + 64 * u < g.n2) {
-          const double z0 = rv[u].x / (mv[u].x + dt * dv[u].x), z1 = rv[u].y / (mv[u].y + dt * dv[u].y);
+          const double z0 = rv[u].x * dv[u].x, z1 = rv[u].y * dv[u].y;
           *reinterpret_cast<double2*>(pnew + o) = make_double2(z0 + beta * pv[u].x, z1 + beta * pv[u].y);
         }
       }
@@ -490,7 +495,7 @@ template <bool RHO, bool ADIAG, bool LINE = false>
 __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* __restrict__ x, double* __restrict__ r,
                                                           const double* __restrict__ p,
                                                           const double* __restrict__ Ap,
-                                                          const double* __restrict__ dg,
+                                                          const double* __restrict__ dinv,  // the stored inverse Jacobi diagonal
                                                           const double* __restrict__ adiag,
                                                           const double* __restrict__ rho, double dt, double tol,
                                                           int it, PlaneRed pr, PcgDev* st) {
@@ -514,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
           pv[u] = __ldg(p + o);
           rv[u] = r[o];
           av[u] = __ldg(Ap + o);
-          dv[u] = LINE ? 0.0 : __ldg(dg + o);
+          dv[u] = LINE ? 0.0 : __ldg(dinv + o);
           wv[u] = __ldg(g.Valg + k);
           mv[u] = ADIAG ? __ldg(adiag + o) : 1.0;
           if (RHO) wv[u] = __ldg(rho + o) * (V2 * wv[u]);
@@ -530,10 +535,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_pcg_update1(GridDev g, double* 
           const double rn = rv[u] - alpha * av[u];
           r[o] = rn;
           s1 += (wv[u] * rn) * rn;
-          if (!LINE) {
-            const double dvec = mv[u] + dt * dv[u];
-            s2 += (wv[u] * rn) * (rn / dvec);
-          }
+          if (!LINE) s2 += (wv[u] * rn) * (rn * dv[u]);  // dv = the stored inverse diagonal
         }
       }
     }
@@ -549,7 +551,7 @@ template <bool RHO, bool ADIAG, bool LINE = false, int U = 2>
 __global__ void __launch_bounds__(kThreads, U == 1 ? 4 : 2) k_pcg_update1v(GridDev g, double* __restrict__ x, double* __restrict__ r,
                                                            const double* __restrict__ p,
                                                            const double* __restrict__ Ap,
-                                                           const double* __restrict__ dg,
+                                                           const double* __restrict__ dinv,  // the stored inverse Jacobi diagonal
                                                            const double* __restrict__ adiag,
                                                            const double* __restrict__ rho, double dt, double tol,
                                                            int it, PlaneRed pr, PcgDev* st) {
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, U == 1 ? 4 : 2) k_pcg_update1v(GridD
           pv[u] = __ldg(reinterpret_cast<const double2*>(p + o));
           rv[u] = *reinterpret_cast<const double2*>(r + o);
           av[u] = __ldg(reinterpret_cast<const double2*>(Ap + o));
-          dv[u] = LINE ? make_double2(0.0, 0.0) : __ldg(reinterpret_cast<const double2*>(dg + o));
+          dv[u] = LINE ? make_double2(0.0, 0.0) : __ldg(reinterpret_cast<const double2*>(dinv + o));
           mv[u] = ADIAG ? __ldg(reinterpret_cast<const double2*>(adiag + o)) : make_double2(1.0, 1.0);
           rh[u] = RHO ? __ldg(reinterpret_cast<const double2*>(rho + o)) : make_double2(1.0, 1.0);
           wv[u][0] = __ldg(g.Valg + k);
@@ -596,10 +598,7 @@ __global__ void __launch_bounds__(kThreads, U == 1 ? 4 : 2) k_pcg_update1v(GridD
             xn[e] = xa[e] + alpha * pa[e];
             rn[e] = ra[e] - alpha * aa[e];
             s1 += (w * rn[e]) * rn[e];
-            if (!LINE) {
-              const double dvec = ma[e] + dt * da[e];
-              s2 += (w * rn[e]) * (rn[e] / dvec);
-            }
+            if (!LINE) s2 += (w * rn[e]) * (rn[e] * da[e]);  // da = the stored inverse diagonal
           }
           *reinterpret_cast<double2*>(x + o) = make_double2(xn[0], xn[1]);
           *reinterpret_cast<double2*>(r + o) = make_double2(rn[0], rn[1]);
@@ -729,12 +728,10 @@ __global__ void k_argmax_combine(const double* gath, int nranks, ArgRes* res) {
 struct PVal {
   const double* r[3];
   const double* pold[3];
-  const double* dg;
-  const double* adiag;
-  double dt, beta;
+  const double* dinv;  // the stored inverse Jacobi diagonal
+  double beta;
   __device__ __forceinline__ double operator()(int c, int64_t o, int, int, int) const {
-    double dvec = (adiag ? __ldg(adiag + o) : 1.0) + dt * __ldg(dg + o);
-    double z = __ldg(r[c] + o) / dvec;
+    double z = __ldg(r[c] + o) * __ldg(dinv + o);
     return z + beta * __ldg(pold[c] + o);
   }
 };
@@ -748,7 +745,7 @@ struct PVal {
        row += gridDim.x * (kThreads / 32))
 template <class Op>
 __global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b, CFld x, Fld r, Fld pold,
-                                                       const double* dg, const double* adiag, double dt,
+                                                       const double* dinv, const double* adiag, double dt,
                                                        PlaneRed pr, PcgDev* st) {
   PlainVal val{{x.p[0], x.p[1], x.p[2]}};
   PC_FOR_ROWS(g, row, i, j) {
@@ -758,14 +755,14 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b,
     op.F(g, val, i, j, k, Fx);
     const int64_t o = off3(g, i, j, k);
     const double W = op.weight(g, i, j, k);
-    const double dvec = (adiag ? adiag[o] : 1.0) + dt * dg[o];
+    const double di = dinv[o];
     for (int q = 0; q < op.ncomp; ++q) {
       double xv = x.p[q][o];
       double Ax = (adiag ? adiag[o] * xv : xv) - dt * Fx[q];
       double rv = b.p[q][o] - Ax;
       r.p[q][o] = rv;
       pold.p[q][o] = 0.0;
-      double z = rv / dvec;
+      double z = rv * di;
       s1 += (W * rv) * z;
       double bv = b.p[q][o];
       s2 += (W * bv) * bv;
@@ -779,10 +776,10 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(GridDev g, Op op, CFld b,
 // K7: p_new = z + beta p_old; Ap = a p_new - dt F(p_new); partial (p, Ap)_W
 template <class Op>
 __global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld r, CFld pold, Fld pnew, Fld Ap,
-                                                         const double* dg, const double* adiag, double dt,
+                                                         const double* dinv, const double* adiag, double dt,
                                                          PlaneRed pr, PcgDev* st) {
   if (st->done) return;
-  PVal val{{r.p[0], r.p[1], r.p[2]}, {pold.p[0], pold.p[1], pold.p[2]}, dg, adiag, dt, st->beta};
+  PVal val{{r.p[0], r.p[1], r.p[2]}, {pold.p[0], pold.p[1], pold.p[2]}, dinv, st->beta};
   PC_FOR_ROWS(g, row, i, j) {
   double s1 = 0.0;
   for (int k = threadIdx.x & 31; k < g.n2; k += 32) {
@@ -805,7 +802,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_matvec(GridDev g, Op op, CFld 
 // K8: x += alpha p; r -= alpha Ap; partials (r,r)_W and (r,z)_W
 template <class Op>
 __global__ void __launch_bounds__(kThreads) k_pcg_update(GridDev g, Op op, Fld x, Fld r, CFld p, CFld Ap,
-                                                         const double* dg, const double* adiag, double dt,
+                                                         const double* dinv, const double* adiag, double dt,
                                                          PlaneRed pr, PcgDev* st) {
   if (st->done) return;
   const double alpha = st->alpha;
@@ -814,13 +811,13 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(GridDev g, Op op, Fld x
   for (int k = threadIdx.x & 31; k < g.n2; k += 32) {
     const int64_t o = off3(g, i, j, k);
     const double W = op.weight(g, i, j, k);
-    const double dvec = (adiag ? adiag[o] : 1.0) + dt * dg[o];
+    const double di = dinv[o];
     for (int q = 0; q < op.ncomp; ++q) {
       x.p[q][o] = x.p[q][o] + alpha * p.p[q][o];
       double rv = r.p[q][o] - alpha * Ap.p[q][o];
       r.p[q][o] = rv;
       s1 += (W * rv) * rv;
-      s2 += (W * rv) * (rv / dvec);
+      s2 += (W * rv) * (rv * di);
     }
   }
   slot_flush(s1, pr.slot[0], row);

@@ -731,9 +731,41 @@ struct EpiMatvecT {
   __device__ __forceinline__ void finish(const GridDev&) {}
 };
 
+// PCG K7 with the search-direction update fused in (TMA march, one rank, no
+// mass diagonal, point Jacobi): the march stages r, p_old, dinv and forms
+// p = r dinv + beta p_old in shared memory (tma_march.cuh form_p, the
+// p-update kernel's expression), so the iteration skips k_pcg_pupdatev and the
+// p re-read: Ap = p - dt F(p), p written at the node, partial (W p, Ap)
+struct EpiMatvecP {
+  static constexpr int NOPS = 0;
+  static constexpr bool NEEDS_W = true;
+  static constexpr bool FUSEP = true;
+  const double* pold;  // (TMA maps only)
+  const double* dinv;
+  double* P;
+  double* Ap;
+  double dt;
+  double* part;
+  const PcgDev* st;
+  double acc = 0.0;
+  __host__ __device__ __forceinline__ const double* opnd(int) const { return nullptr; }
+  __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double pv, bool,
+                                             const double*, double W) {
+    const double ap = pv - dt * f;
+    P[o] = pv;
+    Ap[o] = ap;
+    acc += (W * pv) * ap;
+  }
+  __device__ __forceinline__ void plane_end(int tf) {
+    slot_flush(acc, part, march_slot(tf));
+    acc = 0.0;
+  }
+  __device__ __forceinline__ void finish(const GridDev&) {}
+};
+
 // PCG start (the marching form of k_pcg_init): r = b - (a x - dt F(x)),
-// p_old = 0, partial (W r, z) and (W b, b), z = r / (a + dt d).
-// Operands: b, d (Jacobi diagonal), [a].
+// p_old = 0, partial (W r, z) and (W b, b), z = r dinv.
+// Operands: b, dinv (the stored inverse Jacobi diagonal), [a].
 template <bool ADIAG>
 struct EpiPcgInitT {
   static constexpr int NOPS = ADIAG ? 3 : 2;
@@ -751,12 +783,11 @@ struct EpiPcgInitT {
   __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double xv, bool,
                                              const double* ov, double W) {
     const double bv = ov[0];
-    const double dvec = (ADIAG ? ov[2] : 1.0) + dt * ov[1];
     const double Ax = (ADIAG ? ov[2] * xv : xv) - dt * f;
     const double rv = bv - Ax;
     r[o] = rv;
     pold[o] = 0.0;
-    const double z = rv / dvec;
+    const double z = rv * ov[1];  // ov[1] = the stored inverse Jacobi diagonal
     s1 += (W * rv) * z;
     s2 += (W * bv) * bv;
   }

@@ -43,7 +43,18 @@ struct TmaMaps {
   CUtensorMap BS[3]; // beta strips
   CUtensorMap O[3];  // epilogue operands, box {32, 16, 1}
   CUtensorMap RW;    // row records [n0+2][n1][12], box {12, 18, 1}
+  CUtensorMap P[2], PS[2];  // fused PCG matvec: p_old and the Jacobi diagonal d (T = the residual r)
 };
+
+// Epilogues with FUSEP: the march stages r, p_old and d instead of its input
+// and forms the PCG search direction p = r / (1 + dt d) + beta p_old (the
+// Jacobi preconditioner applied on the fly, k_pcg_pupdatev's expression) into
+// the input slot as each plane lands; the epilogue gets p as the node value
+// (d here is the stored inverse diagonal dinv = 1 / (1 + dt d): p = r dinv + beta p_old)
+template <class E, class = void>
+struct fusep_of : std::false_type {};
+template <class E>
+struct fusep_of<E, std::void_t<decltype(E::FUSEP)>> : std::integral_constant<bool, E::FUSEP> {};
 
 constexpr int RW = 12;  // metric row record: iL2[6], wo01[4], iVal2, pad (16-byte aligned pairs)
 constexpr int RSLOT = 224;  // one plane of row records (18 x 12) padded to a 128-byte multiple
@@ -208,6 +219,34 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
     tma3(dst + XM, ms, kL, j0 - 1, z, &S.bar);
     tma3(dst + XM + XS, ms, kR, j0 - 1, z, &S.bar);
   };
+  // the stage input of plane p into its slot: a TMA box, or (FUSEP) the raw
+  // r, p_old, d boxes into the staging area the unused epilogue-operand slots
+  // provide; form_p turns them into p after the plane's barrier phase
+  constexpr bool FP = fusep_of<Epi>::value;
+  static_assert(!FP || (Epi::NOPS == 0 && 3 * XA <= 2 * 3 * XO), "FUSEP stages r, p_old, d in the operand slots");
+  double* raw = &S.EO[0][0][0];
+  auto issue_T = [&](double* dst, int p) {
+    if constexpr (FP) {
+      tma_arr(raw, &maps.T, &maps.TS, p);
+      tma_arr(raw + XA, &maps.P[0], &maps.PS[0], p);
+      tma_arr(raw + 2 * XA, &maps.P[1], &maps.PS[1], p);
+    } else {
+      tma_arr(dst, &maps.T, &maps.TS, p);
+    }
+  };
+  constexpr unsigned kTBytes = (FP ? 3u : 1u) * kArrBytes;
+  auto form_p = [&](double* dst) {
+    if constexpr (FP) {
+      const double beta = epi.st->beta;
+      for (int e = tid; e < XA; e += MNT) {
+        const bool real = e < XM || (e - XM) % XS < MHJ * 2;  // (strip padding slots stay unread)
+        if (real) {
+          const double z = raw[e] * raw[2 * XA + e];  // r dinv
+          dst[e] = z + beta * raw[XA + e];
+        }
+      }
+    }
+  };
   auto issue_B = [&](double* dst, int p) {
 #pragma unroll
     for (int q = 0; q < 3; ++q) tma_arr(dst + q * XA, &maps.B[q], &maps.BS[q], p);
@@ -220,20 +259,42 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
 
   // ---- prologue: T(i0-1..i0+1), beta and row records of (i0-1, i0)
   __syncthreads();  // barrier initialised
-  if (tid == kIssuer) {
-    mbar_expect_tx(&S.bar, 9u * kArrBytes + 2u * kRowBytes);
-    tma_arr(sTm1, &maps.T, &maps.TS, i0 - 1);
-    tma_arr(sT, &maps.T, &maps.TS, i0);
-    tma_arr(sTp, &maps.T, &maps.TS, i0 + 1);  // iend >= i0 + 1
-    issue_B(sBn, i0 - 1);
-    issue_B(sB, i0);
-    issue_rows(rM, i0 - 1);
-    issue_rows(rC, i0);
-  }
   unsigned phase = 0;
-  mbar_wait(&S.bar, phase);
-  phase ^= 1u;
-  __syncthreads();
+  if constexpr (FP) {  // one staging area: the three input planes one after the other
+    double* slots[3] = {sTm1, sT, sTp};
+#pragma unroll 1
+    for (int q = 0; q < 3; ++q) {
+      if (tid == kIssuer) {
+        if (q > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&S.bar, kTBytes + (q == 0 ? 6u * kArrBytes + 2u * kRowBytes : 0u));
+        issue_T(slots[q], i0 - 1 + q);
+        if (q == 0) {
+          issue_B(sBn, i0 - 1);
+          issue_B(sB, i0);
+          issue_rows(rM, i0 - 1);
+          issue_rows(rC, i0);
+        }
+      }
+      mbar_wait(&S.bar, phase);
+      phase ^= 1u;
+      form_p(slots[q]);
+      __syncthreads();
+    }
+  } else {
+    if (tid == kIssuer) {
+      mbar_expect_tx(&S.bar, 9u * kArrBytes + 2u * kRowBytes);
+      tma_arr(sTm1, &maps.T, &maps.TS, i0 - 1);
+      tma_arr(sT, &maps.T, &maps.TS, i0);
+      tma_arr(sTp, &maps.T, &maps.TS, i0 + 1);  // iend >= i0 + 1
+      issue_B(sBn, i0 - 1);
+      issue_B(sB, i0);
+      issue_rows(rM, i0 - 1);
+      issue_rows(rC, i0);
+    }
+    mbar_wait(&S.bar, phase);
+    phase ^= 1u;
+    __syncthreads();
+  }
 
   auto run = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
@@ -293,9 +354,9 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
         if (tid == kIssuer) {
           const bool t2 = t + 2 <= iend;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_expect_tx(&S.bar, (t2 ? kArrBytes : 0u) + 3u * kArrBytes + (unsigned)Epi::NOPS * kOpBytes +
+          mbar_expect_tx(&S.bar, (t2 ? kTBytes : 0u) + 3u * kArrBytes + (unsigned)Epi::NOPS * kOpBytes +
                                      kRowBytes);
-          if (t2) tma_arr(sTm1, &maps.T, &maps.TS, t + 2);
+          if (t2) issue_T(sTm1, t + 2);
           if (op.tma_split < 2) issue_B(sBn, t + 1);
           if (op.tma_split == 0) {
             issue_ops(eW, t);
@@ -419,6 +480,9 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       if (!LAST) {
         mbar_wait(&S.bar, phase);
         phase ^= 1u;
+        if constexpr (FP) {
+          if (t + 2 <= iend) form_p(sTm1);  // plane t+2 into the slot that becomes sTp
+        }
         __syncthreads();
         pofs += g.plane;
         // advance the slot roles by one plane

@@ -165,3 +165,24 @@ def test_split_stage_launches_bitwise(gpu_ctx, monkeypatch, kind, n, no_tma):
         out.append((o.values.copy(), [e.iters for e in rep.entries]))
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+def test_fused_pupdate_matvec_bitwise(gpu_ctx, monkeypatch):
+    """EpiMatvecP (the p-update fused into the TMA matvec march: r, p_old, d
+    staged, p formed in shared memory) is bitwise the separate p-update
+    kernel + matvec: same iteration counts, residuals and field bits."""
+    w = configs.c4(n=(24, 40, 64))
+    T = operators.Field(w.grid, w.fields["T"])
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("PC_PCG_NO_FUSEP", env)
+        else:
+            monkeypatch.delenv("PC_PCG_NO_FUSEP", raising=False)
+        op = _aligned(w)
+        dtE = op.device_op(w.grid, 1).dt_euler
+        out, rep = ptl.cycle_operator(op, schemes.SchemeConfig("backward_euler", tol=1e-9), T, 1e4 * dtE)
+        outs.append(([e.iters for e in rep.entries], [e.relres for e in rep.entries], out.values.copy()))
+    assert sum(outs[0][0]) > 20
+    assert outs[0][0] == outs[1][0] and outs[0][1] == outs[1][1]
+    assert np.array_equal(outs[0][2], outs[1][2])
