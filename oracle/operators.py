@@ -98,12 +98,13 @@ def scalar_apply(geom, u, D=None, rho=None, vector_metric=False):
 
     u: (ncomp, n0, n1, n2).  D = nu*rho nodal (None == 1), rho nodal or None.
     Face term: t = (Dface * (W*g)) * (u_nb - u_c); sum order
-    ((((t0m + t0p) + t1m) + t1p) + t2m) + t2p; F = (S * iv) / rho.
+    ((((t0m + t0p) + t1m) + t1p) + t2m) + t2p; F = (S * iv) * (1 / rho).
     """
     ncomp = u.shape[0]
     per = geom.periodic
     coefs = face_coefs(geom)
     iv = _b2(geom.iV2) * _b1(geom.igv)
+    irho = None if rho is None else 1.0 / rho  # (1/rho) div(...), SPEC.md:108: one reciprocal per node
     rot = vector_metric and geom.metric == "spherical" and ncomp == 3
     F = np.empty_like(u)
     nbs = {}
@@ -133,8 +134,8 @@ def scalar_apply(geom, u, D=None, rho=None, vector_metric=False):
                     t = (Df * coef) * du
                 S = t if S is None else S + t
         Fc = S * iv
-        if rho is not None:
-            Fc = Fc / rho
+        if irho is not None:
+            Fc = Fc * irho
         F[c] = Fc
     F[:, geom.pinned] = 0.0
     return F

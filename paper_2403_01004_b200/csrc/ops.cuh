@@ -102,9 +102,10 @@ struct ScalarOp {
     }
     const bool pin = pinned(g, i, j, k);
     const double iv = __ldg(g.iV2 + row2(g, i, j)) * __ldg(g.igv + k);
+    const double irho = rho ? 1.0 / __ldg(rho + o) : 1.0;  // (1/rho) div(...): one reciprocal per node
     for (int c = 0; c < ncomp; ++c) {
       double f = S[c] * iv;
-      if (rho) f = f / __ldg(rho + o);
+      if (rho) f = f * irho;
       out[c] = pin ? 0.0 : f;
     }
   }

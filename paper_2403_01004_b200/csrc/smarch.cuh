@@ -434,10 +434,12 @@ __global__ void __launch_bounds__(SNT, SMARCH_BLOCKS(NC)) k_scalar_march(GridDev
       const double iv = S.rowt[rs][3][jr] * igv;
       const int64_t o = (int64_t)t * g.plane + onode;
       double f[NC];
+      // (1/rho) div(nu rho grad v): one reciprocal per node, not a division per component
+      const double irho = op.rho ? 1.0 / (DM == 2 ? dc : __ldg(op.rho + o)) : 1.0;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         double x = Sx[c] * iv;
-        if (op.rho) x = x / (DM == 2 ? dc : __ldg(op.rho + o));
+        if (op.rho) x = x * irho;
         f[c] = pin ? 0.0 : x;
       }
       double ov[Epi::NOPS > 0 ? Epi::NOPS : 1];
