@@ -547,7 +547,7 @@ STEP_COUNTS = {  # config -> [(field, kind, ncomp, cycles, stages or PCG iterati
     "c3": [("T", "aligned", 1, 11, 466)],
     "c4": [("T", "aligned", 1, 6, 576)],
     "c5": [("T", "aligned_rho", 1, 45, 1406), ("v", "vector_rho", 3, 1, 2)],
-    "c5v": [("v", "vector_rho", 3, 1601, 4220)],
+    "c5v": [("v", "vector_rho", 3, 1601, 4202)],
 }
 
 
