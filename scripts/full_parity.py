@@ -66,7 +66,7 @@ def _workload(name, n):
 
 
 # ------------------------------------------------------------------ GPU leg
-def run_gpu(case, out, max_cycles=None):
+def run_gpu(case, out, max_cycles=None, from_cycle=None):
     import bench
     from paper_2403_01004_b200 import device, ptl
     name, n = CASES[case]
@@ -81,26 +81,39 @@ def run_gpu(case, out, max_cycles=None):
     dts = {f: op.device_op(prob.w.grid, nc, ctx).dt_euler for f, op, nc, _ in prob.ops}
     ctx.sync()
     t1 = time.perf_counter()
-    if max_cycles is None:
+    remaining = None
+    if max_cycles is None and from_cycle is None:
         reps = prob.step(sc, ptl.PtlConfig())
-    else:  # a partial step: the first max_cycles cycles (the field is advanced in place)
+    else:  # a partial step (the field is advanced in place): cycles [from_cycle, from_cycle + max_cycles)
         from paper_2403_01004_b200 import errors
         prob.reset()
         reps = []
         for f, op, nc, _ in prob.ops:
             if op.kind == "aligned":
                 op.freeze(prob.fields[f])
-        for f, op, nc, _ in prob.ops:
+
+        def cycles(f, op, outer, k):
             try:
-                ptl.cycle_operator(op, sc, prob.fields[f], prob.outer_dt, ptl.PtlConfig(max_cycles=max_cycles))
+                ptl.cycle_operator(op, sc, prob.fields[f], outer, ptl.PtlConfig(max_cycles=k))
                 raise RuntimeError("the step finished within max_cycles")
             except errors.CycleCapError as e:
-                reps.append(e.report)
+                return e.report
+
+        for f, op, nc, _ in prob.ops:
+            outer = prob.outer_dt
+            if from_cycle:  # run the first cycles, keep their end state, continue from it
+                first = cycles(f, op, outer, from_cycle)
+                for e in first.entries:  # the C loop's own bookkeeping
+                    outer = 0.0 if e.dt == outer else outer - e.dt
+                remaining = outer
+                np.save(os.path.join(out, f"{case}_{f}_start.npy"), prob.fields[f].download(layout=_lib.LAYOUT_SOA))
+            reps.append(cycles(f, op, outer, max_cycles or 1))
     ctx.sync()
     t2 = time.perf_counter()
     rec = {"case": case, "config": name, "grid": list(prob.dg.global_shape), "outer_dt": prob.outer_dt,
            "dt_euler_min": prob.dtE, "dt_euler": dts, "scheme": sc.kind, "tol": sc.tol,
-           "step_s": t2 - t1, "setup_s": t1 - t0, "max_cycles": max_cycles, "ops": []}
+           "step_s": t2 - t1, "setup_s": t1 - t0, "max_cycles": max_cycles, "from_cycle": from_cycle,
+           "remaining_dt": remaining, "ops": []}
     for (f, op, nc, _), rep in zip(prob.ops, reps):
         np.save(os.path.join(out, f"{case}_{f}_final.npy"), prob.fields[f].download(layout=_lib.LAYOUT_SOA))
         rec["ops"].append({"field": f, "kind": op.kind, "ncomp": nc,
@@ -208,8 +221,14 @@ def _oracle_rank(rank, world, port, case, out, gpu_rec, max_cycles=None):
             u = slab.interior(ext).copy()
             g0 = np.load(os.path.join(out, f"{case}_{f}_init.npy"), mmap_mode="r")[:, slab.i0:slab.i0 + slab.n]
             res["inputs_bitwise"] &= bool(np.array_equal(u, g0))
-            u, rep = od.slab_cycle_operator(sop, kind, u, outer, dts[f], tol=tol, max_iter=100000,
-                                            max_cycles=gpu_rec.get("max_cycles"))
+            outer_f = outer
+            if gpu_rec.get("from_cycle"):  # continue from the GPU's state after the first cycles
+                u = np.array(np.load(os.path.join(out, f"{case}_{f}_start.npy"),
+                                     mmap_mode="r")[:, slab.i0:slab.i0 + slab.n])
+                outer_f = gpu_rec["remaining_dt"]
+            u, rep = od.slab_cycle_operator(sop, kind, u, outer_f, dts[f], tol=tol, max_iter=100000,
+                                            max_cycles=gpu_rec.get("max_cycles") or
+                                            (1 if gpu_rec.get("from_cycle") else None))
             g1 = np.load(os.path.join(out, f"{case}_{f}_final.npy"), mmap_mode="r")[:, slab.i0:slab.i0 + slab.n]
             d = np.asarray(g1) - u
             sums = torch.tensor([float(np.sum(d * d)), float(np.sum(u * u)), float(np.max(np.abs(d)))],
@@ -261,6 +280,7 @@ def compare(case, gpu, orc, ranks, wall):
                "outer_dt_over_dtE": gpu["outer_dt"] / gpu["dt_euler_min"], "oracle_ranks": ranks,
                "oracle_wall_s": round(wall, 1), "gpu_step_s": round(gpu["step_s"], 3),
                "inputs_bitwise": orc["inputs_bitwise"], "max_cycles": gpu.get("max_cycles"),
+               "from_cycle": gpu.get("from_cycle"),
                "dt_euler_equal": all(gpu["dt_euler"][f] == orc["dt_euler"][f] for f in gpu["dt_euler"]),
                "ops": []}
     ok = summary["inputs_bitwise"] and summary["dt_euler_equal"]
@@ -291,11 +311,14 @@ def main():
     ap.add_argument("--out", default="/tmp/full_parity")
     ap.add_argument("--ranks", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--max-cycles", type=int, default=None, help="partial step: the first K cycles")
+    ap.add_argument("--from-cycle", type=int, default=None,
+                    help="partial step: run the first K cycles on the GPU, then compare the next --max-cycles "
+                         "(default 1) cycles, the oracle starting from the GPU's state after cycle K")
     ap.add_argument("--json", default=None, help="summary output (default gpurun_out/full_parity_<case>.json)")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     if a.leg in ("gpu", "both"):
-        run_gpu(a.case, a.out, a.max_cycles)
+        run_gpu(a.case, a.out, a.max_cycles, a.from_cycle)
     if a.leg == "fake":
         run_fake(a.case, a.out)
     if a.leg in ("oracle", "both", "fake"):
