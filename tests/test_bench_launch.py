@@ -31,3 +31,22 @@ def test_mismatched_world_size_is_refused():
     r = _run(["--gpus", "4", "--dry-run"], env={"WORLD_SIZE": "2", "RANK": "0"})
     assert r.returncode == 2
     assert "refusing" in r.stderr
+
+
+def test_reference_arm_line_contract():
+    """The reference arm on CPU (C1, one bounded sample): the contract keys,
+    an extrapolated full-step time, and the same config dict our arm emits
+    (bench.workload_config) so the driver can compare like with like."""
+    r = _run(["--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "0"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["metric"].startswith("cell-updates/sec")
+    assert d["cpu_baseline"]["extrapolated"] is True and d["cpu_baseline"]["kind"] == "port"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    cfg = d["config"]
+    for k in ("workload", "config", "grid", "cells", "fields", "scheme", "outer_dt_over_dtE", "operators",
+              "cell_updates_per_step", "decomposition", "l2", "parallelism"):
+        assert k in cfg, k
+    assert cfg["grid"] == [48, 48, 96] and cfg["operators"][0]["stages_or_iters"] == 962
+    # the extrapolated step time is the step's cell-updates over the line's rate
+    assert abs(d["ms_per_step"] / 1e3 - cfg["cell_updates_per_step"] / d["value"]) <= 1e-6 * d["ms_per_step"] / 1e3
