@@ -241,10 +241,6 @@ template <class E, class = void>
 struct has_plane_end : std::false_type {};
 template <class E>
 struct has_plane_end<E, std::void_t<decltype(&E::plane_end)>> : std::true_type {};
-template <class E, class = void>
-struct has_plane_begin : std::false_type {};
-template <class E>
-struct has_plane_begin<E, std::void_t<decltype(&E::plane_begin)>> : std::true_type {};
 
 // Epilogue contract (per tile node n of the thread):
 //   Epi::NOPS, epi.opnd(q)                 nodal operand arrays the kernel stages
@@ -438,7 +434,6 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_march(GridDev g, AlignedOp o
   // finalises iend-1.
   auto step = [&](int t, auto last_tag) {
     constexpr bool LAST = decltype(last_tag)::value;
-    if constexpr (has_plane_begin<Epi>::value) epi.plane_begin();  // the previous plane's warp flush
     // ---- async prefetch, one group per plane (lands before this plane's barrier):
     // T(t+2), beta/rows(t+1), epilogue operands of plane t
     if (!LAST) {
@@ -729,20 +724,11 @@ struct EpiMatvecT {
     Ap[o] = ap;
     acc += (W * pv) * ap;
   }
-  // plane_end keeps the finished plane's partial; the warp flush (a shuffle
-  // chain) runs at the next plane's start, where the flux arithmetic hides it
-  double pend = 0.0;
-  int pend_tf = -1;
   __device__ __forceinline__ void plane_end(int tf) {
-    pend = acc;
-    pend_tf = tf;
+    slot_flush(acc, part, march_slot(tf));
     acc = 0.0;
   }
-  __device__ __forceinline__ void plane_begin() {
-    if (pend_tf >= 0) slot_flush(pend, part, march_slot(pend_tf));
-    pend_tf = -1;
-  }
-  __device__ __forceinline__ void finish(const GridDev&) { plane_begin(); }
+  __device__ __forceinline__ void finish(const GridDev&) {}
 };
 
 // PCG K7 with the search-direction update fused in (TMA march, one rank, no
@@ -770,20 +756,11 @@ struct EpiMatvecP {
     Ap[o] = ap;
     acc += (W * pv) * ap;
   }
-  // plane_end keeps the finished plane's partial; the warp flush (a shuffle
-  // chain) runs at the next plane's start, where the flux arithmetic hides it
-  double pend = 0.0;
-  int pend_tf = -1;
   __device__ __forceinline__ void plane_end(int tf) {
-    pend = acc;
-    pend_tf = tf;
+    slot_flush(acc, part, march_slot(tf));
     acc = 0.0;
   }
-  __device__ __forceinline__ void plane_begin() {
-    if (pend_tf >= 0) slot_flush(pend, part, march_slot(pend_tf));
-    pend_tf = -1;
-  }
-  __device__ __forceinline__ void finish(const GridDev&) { plane_begin(); }
+  __device__ __forceinline__ void finish(const GridDev&) {}
 };
 
 // PCG start (the marching form of k_pcg_init): r = b - (a x - dt F(x)),

@@ -380,7 +380,6 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
           issue_B(sBn, t + 1);
         }
       }
-      if constexpr (has_plane_begin<Epi>::value) epi.plane_begin();  // the previous plane's warp flush
       const bool exists = LAST ? plane_map(g, t).exists : true;
       const int tf = t - 1;
       const double rpl = (RHO == 2 && !FIRST) ? __ldg(op.rho_r + tf) : 1.0;  // radial density of plane tf
