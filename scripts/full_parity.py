@@ -93,9 +93,8 @@ def run_gpu(case, out, max_cycles=None, from_cycle=None):
                 op.freeze(prob.fields[f])
 
         def cycles(f, op, outer, k):
-            try:
-                ptl.cycle_operator(op, sc, prob.fields[f], outer, ptl.PtlConfig(max_cycles=k))
-                raise RuntimeError("the step finished within max_cycles")
+            try:  # the step may also end within these k cycles (the last one)
+                return ptl.cycle_operator(op, sc, prob.fields[f], outer, ptl.PtlConfig(max_cycles=k))[1]
             except errors.CycleCapError as e:
                 return e.report
 
