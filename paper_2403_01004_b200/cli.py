@@ -20,7 +20,8 @@ The config is a sectioned key/value document:
     [initial]     <field> = step | gaussian | sinusoid | random | transition, with
                   <field>.<param> = value  (amp, width, centre, lo, hi, k, sigma, offset)
     [scheme]      kind = rkl2 | rkg2 | backward_euler | euler ; tol ; max_iter ; make_odd
-    [ptl]         enabled ; eps_rel ; max_cycles ; check_all_points ; floor = euler | fraction:<f>
+    [ptl]         enabled ; eps_rel ; max_cycles ; check_all_points ; floor = euler | fraction:<f> ;
+                  reevaluate = dynamic | static ; refresh_T0 = outer | cycle
     [run]         outer_dt = <float> | dt_over_dt_euler = <float> ; n_outer_steps ; seed ;
                   out_prefix (field CSVs <prefix>_<field>.csv + <prefix>_coords.csv) ;
                   out_report (CycleReport CSV, all operators and outer steps)
@@ -45,7 +46,7 @@ KNOWN = {
     "grid": {"metric", "sizes", "extents", "r_spacing", "bc"},
     "initial": None,
     "scheme": {"kind", "tol", "max_iter", "make_odd"},
-    "ptl": {"enabled", "eps_rel", "max_cycles", "check_all_points", "floor"},
+    "ptl": {"enabled", "eps_rel", "max_cycles", "check_all_points", "floor", "reevaluate", "refresh_T0"},
     "run": {"outer_dt", "dt_over_dt_euler", "n_outer_steps", "seed", "out_prefix", "out_report"},
 }
 OP_KEYS = {"kind", "field", "nu", "rho", "vector", "ncomp", "b", "kappa0", "m_p", "k_B", "gamma", "T_floor"}
@@ -281,7 +282,9 @@ def cmd_run(path: str) -> int:
     pcfg = ptl.PtlConfig(eps_rel=c.get("ptl", "eps_rel", float, default=1e-12), dt_floor_mode=fmode,
                          floor_fraction=frac, max_cycles=c.get("ptl", "max_cycles", int, default=10**6),
                          check_all_points=c.get("ptl", "check_all_points", _bool, default=False),
-                         enabled=c.get("ptl", "enabled", _bool, default=True))
+                         enabled=c.get("ptl", "enabled", _bool, default=True),
+                         reevaluate=c.get("ptl", "reevaluate", default="dynamic"),
+                         refresh_T0=c.get("ptl", "refresh_T0", default="outer"))
     nsteps = c.get("run", "n_outer_steps", int, default=1)
     outer_dt = c.get("run", "outer_dt", float, default=None)
     ratio = c.get("run", "dt_over_dt_euler", float, default=None)
@@ -298,8 +301,10 @@ def cmd_run(path: str) -> int:
     first = True
     for step in range(nsteps):
         if ops:
-            state = ptl.split_advance([(f, op) for f, op, _ in ops], state, outer_dt,
-                                            [(sc, pcfg)] * len(ops), outer_step=step,
+            import dataclasses  # (the per-cycle T0 refresh applies to the aligned operators only)
+            cfgs = [(sc, pcfg if op.kind == "aligned" else dataclasses.replace(pcfg, refresh_T0="outer"))
+                    for _, op, _ in ops]
+            state = ptl.split_advance([(f, op) for f, op, _ in ops], state, outer_dt, cfgs, outer_step=step,
                                             refresh={q: f for q, (f, op, _) in enumerate(ops) if op.kind == "aligned"})
             reps = state.reports
             for rep in reps:
