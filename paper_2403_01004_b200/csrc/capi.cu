@@ -26,6 +26,7 @@
 #include "gen.cuh"
 #include "march.cuh"
 #include "smarch.cuh"
+#include "vmarch.cuh"
 #include "tma_march.cuh"
 #include "sts.cuh"
 #include "persist.cuh"

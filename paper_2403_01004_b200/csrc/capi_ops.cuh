@@ -466,6 +466,50 @@ struct has_y0 : std::false_type {};
 template <class E>
 struct has_y0<E, std::void_t<decltype(&E::y0)>> : std::true_type {};
 
+// the vector march (k_vec_march, vmarch.cuh) for y0 = F(u0) + argmax and the
+// fused stages 1 + 2 of the 3-component spherical operator: phi periodic in
+// whole 32-column tiles, theta not periodic, no theta / phi pinning, not a
+// phi-slab (PC_NO_VMARCH=1 keeps k_scalar_march; bitwise the same)
+static bool vmarch_ok(const pc_grid* g) {
+  const GridDev& d = g->g;
+  const char* e = getenv("PC_NO_VMARCH");
+  const bool off = e != nullptr && e[0] == '1';
+  return !off && d.spherical && d.per2 && !d.phis && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && !d.pin_lo1 &&
+         !d.pin_hi1 && !d.pin_lo2 && !d.pin_hi2 && tma_encoder() != nullptr;
+}
+template <int DM, class Epi>
+static int launch_vmarch(pc_op* op, CFld u, const Epi& epi, const int* skip, dim3 grid, int R, int zsel,
+                         const char* what) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  constexpr bool F1 = fuse1_of<Epi>::value;
+  SMaps maps;
+  for (int q = 0; q < 3; ++q) {
+    TRY(cached_map(g, &maps.V[q], u.p[q], MTK, SHJ));
+    TRY(cached_map(g, &maps.VS[q], u.p[q], 2, SHJ));
+  }
+  if (DM != 0) {
+    const double* d = DM == 1 ? op->so.D : op->so.rho;
+    TRY(cached_map(g, &maps.D, d, MTK, SHJ));
+    TRY(cached_map(g, &maps.DS, d, 2, SHJ));
+  }
+  if constexpr (F1) {
+    for (int q = 0; q < 3; ++q) {
+      TRY(cached_map(g, &maps.Y[q], epi.y0[q], MTK, SHJ));
+      TRY(cached_map(g, &maps.YS[q], epi.y0[q], 2, SHJ));
+    }
+  }
+  const int smem = (int)sizeof(VMarchSmem<F1, DM>) + 128;  // (+ the 128-byte alignment of the boxes)
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_vec_march<DM, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_vec_march<DM, Epi><<<grid, SNT, smem, c->s>>>(g->g, op->so, epi, R, zsel, skip, maps);
+  c->st.launches++;
+  return check_launch(what);
+}
+
 template <int NC, bool VEC, int DM, class Epi>
 static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, const char* what) {
   pc_grid* g = op->grid;
@@ -475,6 +519,12 @@ static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, c
   if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
   constexpr bool F1 = fuse1_of<Epi>::value;
   const int zsel = zsplit(c, grid);
+  if constexpr (NC == 3 && VEC && (F1 || std::is_same<Epi, SEpiArgmax>::value)) {
+    if (vmarch_ok(g)) return launch_vmarch<DM>(op, u, epi, skip, grid, R, zsel, what);
+    const char* st = getenv("PC_VMARCH_STRICT");  // (tests: a vector launch that would fall back is an error)
+    if (st && st[0] == '1' && !(getenv("PC_NO_VMARCH") && getenv("PC_NO_VMARCH")[0] == '1'))
+      return fail(PC_E_INVALID, "k_vec_march not applicable to this grid (PC_VMARCH_STRICT)");
+  }
   SMaps maps;
   if (smarch_tma_ok(g)) {
     const int smem = (int)sizeof(SMarchSmem<NC, F1, true>) + 128;  // (+ the 128-byte alignment of the boxes)
