@@ -498,8 +498,10 @@ static int launch_vmarch(pc_op* op, CFld u, const Epi& epi, const int* skip, dim
       TRY(cached_map(g, &maps.Y[q], epi.y0[q], MTK, SHJ));
       TRY(cached_map(g, &maps.YS[q], epi.y0[q], 2, SHJ));
     }
+  } else {
+    for (int q = 0; q < Epi::NOPS; ++q) TRY(cached_map(g, &maps.O[q], epi.opnd(q), MTK, SMJ));
   }
-  const int smem = (int)sizeof(VMarchSmem<F1, DM>) + 128;  // (+ the 128-byte alignment of the boxes)
+  const int smem = (int)sizeof(VMarchSmem<F1, DM, F1 ? 0 : Epi::NOPS>) + 128;  // (+ the 128-byte alignment of the boxes)
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(cudaFuncSetAttribute(k_vec_march<DM, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -519,7 +521,7 @@ static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, c
   if ((int64_t)grid.x * grid.y * grid.z > c->max_red) return fail(PC_E_INVALID, "grid too large for the reduction scratch");
   constexpr bool F1 = fuse1_of<Epi>::value;
   const int zsel = zsplit(c, grid);
-  if constexpr (NC == 3 && VEC && (F1 || std::is_same<Epi, SEpiArgmax>::value)) {
+  if constexpr (NC == 3 && VEC && (F1 || std::is_same<Epi, SEpiArgmax>::value || std::is_same<Epi, SEpiStage>::value)) {
     if (vmarch_ok(g)) return launch_vmarch<DM>(op, u, epi, skip, grid, R, zsel, what);
     const char* st = getenv("PC_VMARCH_STRICT");  // (tests: a vector launch that would fall back is an error)
     if (st && st[0] == '1' && !(getenv("PC_NO_VMARCH") && getenv("PC_NO_VMARCH")[0] == '1'))

@@ -52,14 +52,18 @@ __device__ __forceinline__ void mbar_expect_tx_elect(unsigned long long* bar, un
 
 constexpr int VSL = 4;  // staged-plane slots: t (read), t+1 (formed this iteration), t+2, t+3 (in flight)
 
-template <bool F1, int DM>
+constexpr int VOSL = 3;  // epilogue-operand slots (plain stage): t (read), t+1, t+2 (in flight)
+
+template <bool F1, int DM, int NOP>
 struct VMarchSmem {
   static constexpr int NA = F1 ? 6 : 3;          // u0[3] (+ y0[3]) -- the staged stencil sources
   static constexpr int ND = DM != 0 ? 1 : 0;     // D / rho source
   double A[VSL][NA + ND][SXA];                   // TMA layout (main box + padded strips); F1: u0 -> u1 in place
+  double O[NOP ? VOSL : 1][NOP ? NOP : 1][NOP ? SNT : 16];  // plain stage: u0, u_{k-2}, y0 at the tile nodes
   double2 M[4][SMJ][5];                          // frame rotations of the tile rows (as k_scalar_march)
   double rowt[3][SROWT][SHJ];                    // row tables of planes t-1, t, t+1
   unsigned long long full[VSL];
+  unsigned long long ofull[VOSL];
 };
 
 template <int DM, class Epi>
@@ -67,7 +71,8 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
                                                       const int* skip, const __grid_constant__ SMaps maps) {
   constexpr bool F1 = fuse1_of<Epi>::value;
   constexpr bool HASD = DM != 0;
-  using Sm = VMarchSmem<F1, DM>;
+  constexpr int NOP = F1 ? 0 : Epi::NOPS;  // operand boxes of the plain stage (SEpiStage: 9)
+  using Sm = VMarchSmem<F1, DM, NOP>;
   constexpr int NA = Sm::NA;
   constexpr int DS = NA;  // slot of the D / rho source
   extern __shared__ __align__(128) unsigned char vmarch_smem[];
@@ -85,6 +90,8 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < VSL; ++s) mbar_init(&S.full[s], 1);
+#pragma unroll
+    for (int s = 0; s < VOSL; ++s) mbar_init(&S.ofull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // rotation table of the tile rows (loaded once; rows beyond n1 clamp)
@@ -128,6 +135,17 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
       }
     if constexpr (HASD) {
       if (warp == 4) arr(&S.A[sl][DS][0], &maps.D, &maps.DS);
+    }
+  };
+  // plain stage: the nine operand boxes (32 x 8, the tile nodes) of plane p
+  // into operand slot sl, completing on ofull[sl] (warp 7 arms it)
+  auto issue_ops = [&](int p, int sl) {
+    if constexpr (NOP > 0) {
+      unsigned long long* b = &S.ofull[sl];
+      if (warp == 7) mbar_expect_tx_elect(b, (unsigned)NOP * kSOpBytes);
+#pragma unroll
+      for (int q = 0; q < NOP; ++q)
+        if (warp == 4 + (q & 3)) tma3_elect(&S.O[sl][q][0], &maps.O[q], k0, j0, p + 1, b);
     }
   };
   const bool issuer = warp >= 4;
@@ -204,7 +222,11 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
     issue_plane(i0);
     issue_plane(i0 + 1);  // (iend >= i0 + 1)
     if (i0 + 2 <= iend) issue_plane(i0 + 2);
+    issue_ops(i0, 0);
+    if (i0 + 1 < iend) issue_ops(i0 + 1, 1);
   }
+  int o_c = 0, o_p = 1, o_n = 2;  // operand slots of planes t, t+1, t+2
+  unsigned oph = 0u;
   int r_m = 0, r_c = 1, r_p = 2;  // row-table slots of planes t-1, t, t+1
   issue_rows(i0 - 1, r_m);
   issue_rows(i0, r_c);
@@ -232,6 +254,10 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
     if (issuer && t + 3 <= iend) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue_plane(t + 3);  // (into plane t-1's slot)
+    }
+    if (NOP > 0 && issuer && t + 2 < iend) {
+      if (t + 3 > iend) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_ops(t + 2, o_n);  // (into plane t-1's operand slot)
     }
     if (t + 1 <= iend) issue_rows(t + 1, r_p);  // (its slot held plane t-2's rows)
     cp_async_commit();
@@ -324,13 +350,18 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
         if (op.rho) x = x * irho;
         f[c] = pin ? 0.0 : x;
       }
-      double ov[F1 ? 6 : 1];
+      double ov[F1 ? 6 : (NOP > 0 ? NOP : 1)];
       if constexpr (F1) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           ov[2 * c] = a0c[c];
           ov[2 * c + 1] = S.A[sc][3 + c][h];
         }
+      }
+      if constexpr (NOP > 0) {
+        mbar_wait(&S.ofull[o_c], (oph >> o_c) & 1u);
+#pragma unroll
+        for (int q = 0; q < NOP; ++q) ov[q] = S.O[o_c][q][tid];
       }
       epi.template apply<3>(g, t, jg, kg, o, f, vc, pin, ov);
     }
@@ -349,6 +380,13 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
       r_m = r_c;
       r_c = r_p;
       r_p = o;
+    }
+    if constexpr (NOP > 0) {  // operand slots: t <- t+1, t+1 <- t+2, t+2 <- the old t slot
+      oph ^= 1u << o_c;
+      const int o = o_c;
+      o_c = o_p;
+      o_p = o_n;
+      o_n = o;
     }
   }
   cp_async_wait<0>();
