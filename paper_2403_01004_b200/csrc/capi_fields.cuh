@@ -312,6 +312,7 @@ int pc_grid_destroy(pc_grid* g) {
   if (!g) return PC_OK;
   cudaFree(g->tables);
   cudaFree(g->rowrec);
+  cudaFree(g->srowrec);
   delete g;
   return PC_OK;
 }

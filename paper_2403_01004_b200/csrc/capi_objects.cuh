@@ -122,6 +122,9 @@ struct pc_grid {
   double* rowrec = nullptr;  // [n0+2][n1][RW] interleaved row records (TMA march)
   CUtensorMap rowmap;
   bool rowmap_ok = false;
+  double* srowrec = nullptr;  // [n0+2][n1][4] W2[0..2], iV2 records (vector march), built on first use
+  CUtensorMap srowmap;
+  bool srow_ok = false;
   // TMA maps of field buffers by (base, box): the pooled buffers recur, so a
   // stage launch re-encodes nothing after the first cycle
   struct MapEntry {

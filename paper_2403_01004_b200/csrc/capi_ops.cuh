@@ -477,12 +477,43 @@ static bool vmarch_ok(const pc_grid* g) {
   return !off && d.spherical && d.per2 && !d.phis && d.n2 % MTK == 0 && !d.per1 && d.n2 >= 2 && !d.pin_lo1 &&
          !d.pin_hi1 && !d.pin_lo2 && !d.pin_hi2 && tma_encoder() != nullptr;
 }
+// the vector march's per-(r, theta) records: W2[0], W2[1], W2[2], iV2 interleaved
+// over the table rows -1 .. n0 (the same bits), one 4 x 10 TMA box per plane
+__global__ void k_srow_pack(GridDev g, double* rec, int64_t nrows) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nrows; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = q - g.n1;  // (the tables start at ghost row -1)
+    rec[4 * q + 0] = g.W2[0][s];
+    rec[4 * q + 1] = g.W2[1][s];
+    rec[4 * q + 2] = g.W2[2][s];
+    rec[4 * q + 3] = g.iV2[s];
+  }
+}
+static int make_srow_map(pc_grid* g) {
+  auto enc = tma_encoder();
+  if (!enc) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const GridDev& d = g->g;
+  const int64_t nrows = (int64_t)(d.n0 + 2) * d.n1;
+  CUDA_TRY(cudaMalloc(&g->srowrec, sizeof(double) * 4 * nrows));
+  k_srow_pack<<<(int)std::min<int64_t>((nrows + 255) / 256, 4096), 256, 0, g->ctx->s>>>(d, g->srowrec, nrows);
+  TRY(check_launch("k_srow_pack"));
+  cuuint64_t dims[3] = {4, (cuuint64_t)d.n1, (cuuint64_t)d.n0 + 2};
+  cuuint64_t strides[2] = {4 * 8, (cuuint64_t)d.n1 * 4 * 8};
+  cuuint32_t box[3] = {4, (cuuint32_t)SHJ, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(&g->srowmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, g->srowrec, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled (vector row records) failed (" + std::to_string((int)r) + ")");
+  g->srow_ok = true;
+  return PC_OK;
+}
 template <int DM, class Epi>
 static int launch_vmarch(pc_op* op, CFld u, const Epi& epi, const int* skip, dim3 grid, int R, int zsel,
                          const char* what) {
   pc_grid* g = op->grid;
   pc_ctx* c = g->ctx;
   constexpr bool F1 = fuse1_of<Epi>::value;
+  if (!g->srow_ok) TRY(make_srow_map(g));
   SMaps maps;
   for (int q = 0; q < 3; ++q) {
     TRY(cached_map(g, &maps.V[q], u.p[q], MTK, SHJ));
@@ -507,7 +538,7 @@ static int launch_vmarch(pc_op* op, CFld u, const Epi& epi, const int* skip, dim
     CUDA_TRY(cudaFuncSetAttribute(k_vec_march<DM, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  k_vec_march<DM, Epi><<<grid, SNT, smem, c->s>>>(g->g, op->so, epi, R, zsel, skip, maps);
+  k_vec_march<DM, Epi><<<grid, SNT, smem, c->s>>>(g->g, op->so, epi, R, zsel, skip, maps, g->srowmap);
   c->st.launches++;
   return check_launch(what);
 }

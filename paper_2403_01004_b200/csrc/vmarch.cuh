@@ -16,8 +16,15 @@
 //    in place over the staged u0 -- the owner forms its node (kept in a
 //    register, its u0 carried for the epilogue), 80 threads form the tile's
 //    theta / phi halo;
-//  * one __syncthreads per plane; the refill of the slot freed by plane t-1
-//    is issued right after it.
+//  * no block-wide barrier in the plane loop: per slot a `full` mbarrier (the
+//    plane's boxes and its row records landed), a `formed` one (F1: every
+//    thread formed its elements of the plane; count 256) and an `empty` one
+//    (every warp is done with the plane; count 8), so a warp that finished
+//    early starts the next plane instead of idling at a __syncthreads, and
+//    the issuer warps refill the slot of plane t-1 once `empty` says so;
+//  * the per-(r, theta) metric rows (W2[0..2], iV2) arrive as one 4 x 10 box
+//    of an interleaved record table per plane; the r- face coefficient is the
+//    previous plane's r+ one (the same product), carried in a register.
 //
 // Every face term, the rotation products and the epilogue are formed exactly
 // as k_scalar_march forms them (same operands, same order), so the result is
@@ -50,9 +57,14 @@ __device__ __forceinline__ void mbar_expect_tx_elect(unsigned long long* bar, un
       : "memory");
 }
 
-constexpr int VSL = 4;  // staged-plane slots: t (read), t+1 (formed this iteration), t+2, t+3 (in flight)
+constexpr int VSL = 4;    // staged-plane slots: t (read), t+1 (formed this iteration), t+2, t+3 (in flight)
+constexpr int VOSL = 3;   // epilogue-operand slots (plain stage): t (read), t+1, t+2 (in flight)
+constexpr int VRW = 48;   // one plane's row records [10 rows][W2[0], W2[1], W2[2], iV2], padded to 384 B
+constexpr unsigned kVRowBytes = (unsigned)(SHJ * 4) * 8u;
 
-constexpr int VOSL = 3;  // epilogue-operand slots (plain stage): t (read), t+1, t+2 (in flight)
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
 template <bool F1, int DM, int NOP>
 struct VMarchSmem {
@@ -60,15 +72,15 @@ struct VMarchSmem {
   static constexpr int ND = DM != 0 ? 1 : 0;     // D / rho source
   double A[VSL][NA + ND][SXA];                   // TMA layout (main box + padded strips); F1: u0 -> u1 in place
   double O[NOP ? VOSL : 1][NOP ? NOP : 1][NOP ? SNT : 16];  // plain stage: u0, u_{k-2}, y0 at the tile nodes
+  double rowt[VSL][VRW];                         // row records of the staged planes
   double2 M[4][SMJ][5];                          // frame rotations of the tile rows (as k_scalar_march)
-  double rowt[3][SROWT][SHJ];                    // row tables of planes t-1, t, t+1
-  unsigned long long full[VSL];
-  unsigned long long ofull[VOSL];
+  unsigned long long full[VSL], formed[VSL], empty[VSL], ofull[VOSL];
 };
 
 template <int DM, class Epi>
 __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Epi epi, int R, int zsel,
-                                                      const int* skip, const __grid_constant__ SMaps maps) {
+                                                      const int* skip, const __grid_constant__ SMaps maps,
+                                                      const __grid_constant__ CUtensorMap rowmap) {
   constexpr bool F1 = fuse1_of<Epi>::value;
   constexpr bool HASD = DM != 0;
   constexpr int NOP = F1 ? 0 : Epi::NOPS;  // operand boxes of the plain stage (SEpiStage: 9)
@@ -85,11 +97,15 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
   const int kg = k0 + tx, jg = j0 + ty;
   const int kL = k0 == 0 ? g.n2 - 2 : k0 - 2;  // phi strips (wrap across the seam)
   const int kR = k0 + MTK == g.n2 ? 0 : k0 + MTK;
-  constexpr unsigned kPlaneBytes = (unsigned)(NA + Sm::ND) * kSArrBytes;
+  constexpr unsigned kPlaneBytes = (unsigned)(NA + Sm::ND) * kSArrBytes + kVRowBytes;
 
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < VSL; ++s) mbar_init(&S.full[s], 1);
+    for (int s = 0; s < VSL; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.formed[s], SNT);
+      mbar_init(&S.empty[s], SNT / 32);
+    }
 #pragma unroll
     for (int s = 0; s < VOSL; ++s) mbar_init(&S.ofull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -102,31 +118,29 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
     const int src = f < 2 ? th : (q < 9 ? q : 8);
     reinterpret_cast<double*>(&S.M[f][r][0])[q] = __ldg(g.M[f] + (int64_t)jr * 9 + src);
   }
-  // row tables: W2[0..2], iV2 per (plane, halo row), one cp.async each by 50 threads
-  const bool rton = tid < SROWT * SHJ;
-  const int rtab = tid / SHJ, rhj = tid - (tid / SHJ) * SHJ;
-  bool rok;
-  const int rjj = map_j(g, j0 - 1 + rhj, rok);
-  const double* rbase = !rton ? g.iV2 : (rtab < 3 ? g.W2[rtab] : g.iV2);
-  auto issue_rows = [&](int p, int sl) {
-    if (rton) cp_async8(&S.rowt[sl][rtab][rhj], rbase + row2(g, plane_map(g, p).row, rjj));
-  };
-  auto aslot = [&](int p) { return (p - i0 + 1) & (VSL - 1); };
+  // plane p's slot and the parity of that slot's barriers for p (every plane
+  // i0-1 .. iend uses each barrier of its slot exactly once)
+  auto slot = [&](int p) { return (p - i0 + 1) & (VSL - 1); };
+  auto par = [&](int p) { return (unsigned)((p - i0 + 1) >> 2) & 1u; };
   // TMA issue: warps 4..7 each run this whole (warp-uniform operands, one
   // elected lane issues): warp 7 arms the slot's barrier and stages component
-  // 0 of u0 / u (and of y0), warps 6 and 5 components 1 and 2, warp 4 the D /
-  // rho source -- the issue work is spread instead of serialising one warp
+  // 0 of u0 / u (and of y0) and the row records, warps 6 and 5 components 1
+  // and 2, warp 4 the D / rho source
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   auto issue_plane = [&](int p) {
-    const int z = plane_map(g, p).mem + 1;  // (the tensors start at ghost plane -1)
-    const int sl = aslot(p);
+    const PlaneMap pm = plane_map(g, p);
+    const int z = pm.mem + 1;  // (the tensors start at ghost plane -1)
+    const int sl = slot(p);
     unsigned long long* b = &S.full[sl];
     auto arr = [&](double* dst, const CUtensorMap* mm, const CUtensorMap* ms) {
       tma3_elect(dst, mm, k0, j0 - 1, z, b);
       tma3_elect(dst + SXM, ms, kL, j0 - 1, z, b);
       tma3_elect(dst + SXM + SXS, ms, kR, j0 - 1, z, b);
     };
-    if (warp == 7) mbar_expect_tx_elect(b, kPlaneBytes);
+    if (warp == 7) {
+      mbar_expect_tx_elect(b, kPlaneBytes);
+      tma3_elect(&S.rowt[sl][0], &rowmap, 0, j0 - 1, pm.row + 1, b);
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       if (warp == 7 - c) {
@@ -166,6 +180,7 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
   const int hpm = tx > 0 ? h - 1 : SXM + (ty + 1) * 2 + 1;
   const int hpp = tx < MTK - 1 ? h + 1 : SXM + SXS + (ty + 1) * 2;
   const int onode = jg * g.n2 + kg;
+  const int jr = ty + 1;  // row-record index of the own row (record row 0 = j0 - 1)
   // F1: the halo element this thread forms (threads 0..79): theta rows j0-1 and
   // j0+8 of the main box, then the phi strips' columns k0-1 and k0+32 of rows 1..8
   int hx = -1;
@@ -193,9 +208,11 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
     const int ig = plane_map(g, p).mem + g.i0g;
     return (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
   };
-  // own stencil input of plane p (F1: formed here, the halo too; else the staged u)
+  // plane p landed: this thread's stencil input of it (F1: formed here, the
+  // halo too, then announced on `formed`; else the staged u)
   auto own_in = [&](int p, double (&v)[3], double (&a0)[3]) {
-    const int sl = aslot(p);
+    const int sl = slot(p);
+    mbar_wait(&S.full[sl], par(p));
     if constexpr (F1) {
       const bool pn = plane_pin(p);
       if (hx >= 0) {
@@ -203,19 +220,18 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
         form(sl, hx, pn, w, w0);
       }
       form(sl, h, pn, v, a0);
+      mbar_arrive(&S.formed[sl]);
     } else {
 #pragma unroll
       for (int c = 0; c < 3; ++c) v[c] = S.A[sl][c][h];
     }
   };
-
-  unsigned ph = 0u;  // one phase bit per slot
-  auto wait_plane = [&](int p) {
-    const int sl = aslot(p);
-    mbar_wait(&S.full[sl], (ph >> sl) & 1u);
-    ph ^= 1u << sl;
+  auto release = [&](int p) {  // this warp is done with plane p's slot
+    __syncwarp();
+    if (tx == 0) mbar_arrive(&S.empty[slot(p)]);
   };
-  // ---- prologue: planes i0-1 .. i0+2 in flight, rows of i0-1 and i0
+
+  // ---- prologue: planes i0-1 .. i0+2 in flight (and the operands of i0, i0+1)
   __syncthreads();  // barriers initialised
   if (issuer) {
     issue_plane(i0 - 1);
@@ -227,54 +243,46 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
   }
   int o_c = 0, o_p = 1, o_n = 2;  // operand slots of planes t, t+1, t+2
   unsigned oph = 0u;
-  int r_m = 0, r_c = 1, r_p = 2;  // row-table slots of planes t-1, t, t+1
-  issue_rows(i0 - 1, r_m);
-  issue_rows(i0, r_c);
-  cp_async_commit();
   double vm[3], vc[3], vp[3], a0c[3], a0n[3], dm = 0.0, dc = 0.0, dp = 0.0;
-  wait_plane(i0 - 1);
   own_in(i0 - 1, vm, a0n);
-  wait_plane(i0);
+  if (HASD) dm = S.A[slot(i0 - 1)][DS][h];
+  double cr0 = S.rowt[slot(i0 - 1)][jr * 4] * g10;  // r+ face of plane i0-1 = r- face of plane i0
+  release(i0 - 1);
   own_in(i0, vc, a0c);
-  if (HASD) {
-    dm = S.A[aslot(i0 - 1)][DS][h];
-    dc = S.A[aslot(i0)][DS][h];
-  }
-  const int jr = ty + 1;  // row-table index of the own row (halo row 0 = j0 - 1)
+  if (HASD) dc = S.A[slot(i0)][DS][h];
 
 #pragma unroll 1
   for (int t = i0; t < iend; ++t) {
-    // plane t+1: landed (issued two iterations ago); its stencil input formed
-    wait_plane(t + 1);
-    own_in(t + 1, vp, a0n);
-    const int sc = aslot(t);
-    if (HASD) dp = S.A[aslot(t + 1)][DS][h];
-    cp_async_wait<0>();  // rows of plane t (issued one iteration ago)
-    __syncthreads();     // u1(t+1), rows(t) visible; every thread is done with plane t-1's slots
-    if (issuer && t + 3 <= iend) {
+    // refill plane t-1's slots once every warp is done with them
+    const bool more = t + 3 <= iend, mops = NOP > 0 && t + 2 < iend;
+    if (issuer && (more || mops)) {
+      mbar_wait(&S.empty[slot(t - 1)], par(t - 1));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_plane(t + 3);  // (into plane t-1's slot)
+      if (more) issue_plane(t + 3);
+      if (mops) issue_ops(t + 2, o_n);
     }
-    if (NOP > 0 && issuer && t + 2 < iend) {
-      if (t + 3 > iend) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_ops(t + 2, o_n);  // (into plane t-1's operand slot)
-    }
-    if (t + 1 <= iend) issue_rows(t + 1, r_p);  // (its slot held plane t-2's rows)
-    cp_async_commit();
+    // plane t+1: landed (issued two iterations ago); its stencil input formed
+    own_in(t + 1, vp, a0n);
+    const int sc = slot(t);
+    if (HASD) dp = S.A[slot(t + 1)][DS][h];
+    if constexpr (F1) mbar_wait(&S.formed[sc], par(t));  // every element of u1(t) formed
 
-    const int rs = r_c, rm = r_m;
+    const double2 rw01 = *reinterpret_cast<const double2*>(&S.rowt[sc][jr * 4]);      // W2[0], W2[1]
+    const double2 rw2v = *reinterpret_cast<const double2*>(&S.rowt[sc][jr * 4 + 2]);  // W2[2], iV2
+    const double w1m = S.rowt[sc][(jr - 1) * 4 + 1];                                  // W2[1] at j-1
+    const double cr1 = rw01.x * g10;
     if (inside) {
       const bool okim = plane_map(g, t - 1).exists;
       const int ig = t + g.i0g;
       const bool pin = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
       const double Dcen = DM == 0 ? op.Dc : (DM == 1 ? dc : op.Dc * dc);
       double coef[3][2];
-      coef[0][0] = okim ? S.rowt[rm][0][jr] * g10 : 0.0;
-      coef[0][1] = S.rowt[rs][0][jr] * g10;
-      coef[1][0] = okjm ? S.rowt[rs][1][jr - 1] * g11 : 0.0;
-      coef[1][1] = S.rowt[rs][1][jr] * g11;
-      coef[2][0] = okkm ? S.rowt[rs][2][jr] * g12m : 0.0;
-      coef[2][1] = S.rowt[rs][2][jr] * g12;
+      coef[0][0] = okim ? cr0 : 0.0;
+      coef[0][1] = cr1;
+      coef[1][0] = okjm ? w1m * g11 : 0.0;
+      coef[1][1] = rw01.y * g11;
+      coef[2][0] = okkm ? rw2v.x * g12m : 0.0;
+      coef[2][1] = rw2v.x * g12;
       double nv[3][2][3], nd[3][2];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
           }
         }
       }
-      const double iv = S.rowt[rs][3][jr] * igv;
+      const double iv = rw2v.y * igv;
       const int64_t o = (int64_t)t * g.plane + onode;
       double f[3];
       const double irho = op.rho ? 1.0 / (DM == 2 ? dc : __ldg(op.rho + o)) : 1.0;
@@ -365,6 +373,8 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
       }
       epi.template apply<3>(g, t, jg, kg, o, f, vc, pin, ov);
     }
+    release(t);
+    cr0 = cr1;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       vm[c] = vc[c];
@@ -375,12 +385,6 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
       dm = dc;
       dc = dp;
     }
-    {  // rotate the row-table slots: t-1 <- t, t <- t+1, t+1 <- the old t-1 slot
-      const int o = r_m;
-      r_m = r_c;
-      r_c = r_p;
-      r_p = o;
-    }
     if constexpr (NOP > 0) {  // operand slots: t <- t+1, t+1 <- t+2, t+2 <- the old t slot
       oph ^= 1u << o_c;
       const int o = o_c;
@@ -389,7 +393,6 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
       o_n = o;
     }
   }
-  cp_async_wait<0>();
   epi.finish(g);
 }
 
