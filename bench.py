@@ -87,6 +87,14 @@ CONFIG_SHAPE = {"c1": (48, 48, 96), "c2": (128, 128, 256), "c3": (256, 256, 512)
                 "c5": (768, 768, 1536), "c5v": (768, 768, 1536)}
 
 
+def _vmarch_applies(prob, args):
+    """k_vec_march's conditions (capi_ops.cuh vmarch_ok): a spherical grid (phi periodic, theta
+    not), phi in whole 32-column tiles, not phi-slabs, PC_NO_VMARCH unset."""
+    n2 = int(prob.dg.global_shape[2])
+    return (getattr(prob.w.grid, "metric", "") == "spherical" and n2 % 32 == 0
+            and getattr(args, "decomp", None) != "phi" and os.environ.get("PC_NO_VMARCH") != "1")
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -366,6 +374,9 @@ def run_ours(args, rank, world, local_rank):
                                  "ms": d["ms"], "bytes_per_cell_update": bpc, "stages_per_launch": 2,
                                  "achieved": bpc * d["cell_updates"] / (d["ms"] / 1e3) / 1e9,
                                  "launches": d["launches"], "field": fname})
+    for r in rows:  # the 3-component spherical launches run on the vector march (csrc/vmarch.cuh) when it applies
+        if r["kernel"].startswith("k_scalar_march<3 comp") and _vmarch_applies(prob, args):
+            r["kernel"] = r["kernel"].replace("k_scalar_march<3 comp, ", "k_vec_march<")
     dom = max(rows, key=lambda r: r["ms"]) if rows else None
     peak, peak_src = _peaks()
 
