@@ -149,6 +149,33 @@ static int detect_radial_rho(pc_op* op) {
   return PC_OK;
 }
 
+// the same for the 3-component viscosity (D = nu rho) on one rank: the vector
+// march reads rho(i) and 1 / rho(i) per plane instead of staging a rho stream
+static int detect_radial_rho_visc(pc_op* op) {
+  pc_grid* g = op->grid;
+  pc_ctx* c = g->ctx;
+  op->so.rho_r = nullptr;
+  const GridDev& d = g->g;
+  if (!op->so.drho || !op->so.rho || !op->so.vector || op->ncomp != 3 || d.ghost_lo0 || d.ghost_hi0 || d.phis ||
+      getenv("PC_NO_RADIAL_RHO"))
+    return PC_OK;
+  CUDA_TRY(cudaMemsetAsync(c->bad, 0, sizeof(int), c->s));
+  k_radial_check<<<node_blocks(c, d), kThreads, 0, c->s>>>(d, op->so.rho, c->bad);
+  c->st.launches++;
+  TRY(check_launch("k_radial_check"));
+  CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+  CUDA_TRY(cudaStreamSynchronize(c->s));
+  if (*c->h_bad != 0) return PC_OK;  // not radial
+  if (!op->rho_r) CUDA_TRY(cudaMalloc(&op->rho_r, 2 * sizeof(double) * (size_t)d.n0));
+  CUDA_TRY(cudaMemcpy2DAsync(op->rho_r, sizeof(double), op->so.rho, (size_t)d.plane * sizeof(double), sizeof(double),
+                             (size_t)d.n0, cudaMemcpyDeviceToDevice, c->s));
+  k_recip<<<(d.n0 + kThreads - 1) / kThreads, kThreads, 0, c->s>>>(op->rho_r, d.n0, op->rho_r + d.n0);
+  c->st.launches++;
+  TRY(check_launch("k_recip"));
+  op->so.rho_r = op->rho_r;
+  return PC_OK;
+}
+
 int pc_op_freeze(pc_op* op, const pc_field* T0) {
   field_dep(T0);
   if (!op) return fail(PC_E_INVALID, "null operator");
@@ -197,6 +224,7 @@ int pc_op_freeze(pc_op* op, const pc_field* T0) {
       TRY(halo_exchange(c, g, rb, 1));
     }
     TRY(run_bound(op, op->so));
+    TRY(detect_radial_rho_visc(op));
   }
   op->diag_valid = op->dbuf != nullptr;
   op->line_valid = false;
@@ -519,7 +547,7 @@ static int launch_vmarch(pc_op* op, CFld u, const Epi& epi, const int* skip, dim
     TRY(cached_map(g, &maps.V[q], u.p[q], MTK, SHJ));
     TRY(cached_map(g, &maps.VS[q], u.p[q], 2, SHJ));
   }
-  if (DM != 0) {
+  if (DM == 1 || DM == 2) {
     const double* d = DM == 1 ? op->so.D : op->so.rho;
     TRY(cached_map(g, &maps.D, d, MTK, SHJ));
     TRY(cached_map(g, &maps.DS, d, 2, SHJ));
@@ -553,7 +581,10 @@ static int launch_smarch_t(pc_op* op, CFld u, const Epi& epi, const int* skip, c
   constexpr bool F1 = fuse1_of<Epi>::value;
   const int zsel = zsplit(c, grid);
   if constexpr (NC == 3 && VEC && (F1 || std::is_same<Epi, SEpiArgmax>::value || std::is_same<Epi, SEpiStage>::value)) {
-    if (vmarch_ok(g)) return launch_vmarch<DM>(op, u, epi, skip, grid, R, zsel, what);
+    if (vmarch_ok(g)) {
+      if (DM == 2 && op->so.rho_r) return launch_vmarch<3>(op, u, epi, skip, grid, R, zsel, what);
+      return launch_vmarch<DM>(op, u, epi, skip, grid, R, zsel, what);
+    }
     const char* st = getenv("PC_VMARCH_STRICT");  // (tests: a vector launch that would fall back is an error)
     if (st && st[0] == '1' && !(getenv("PC_NO_VMARCH") && getenv("PC_NO_VMARCH")[0] == '1'))
       return fail(PC_E_INVALID, "k_vec_march not applicable to this grid (PC_VMARCH_STRICT)");

@@ -355,6 +355,11 @@ __device__ __forceinline__ void pcg_alpha(PcgDev* st, double pAp) {
 }
 
 // out[i] = 0 - pref / rho[i] (aligned operator: the per-plane scale of a radial density)
+// out[i] = 1 / rho[i] (the vector march's per-plane reciprocal of a radial density)
+__global__ void k_recip(const double* rho, int n, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = 1.0 / rho[i];
+}
 __global__ void k_neg_scale(const double* rho, int n, double pref, double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = 0.0 - (pref / rho[i]);

@@ -35,6 +35,10 @@ struct ScalarOp {
   const double* rho;  // nullptr -> 1
   int ncomp;
   int vector;  // rotate 3-component spherical vectors
+  // viscosity with a radial density (rho(i, j, k) == rho(i), detected at
+  // freeze, one rank): rho(i) for i < n0 and 1 / rho(i) at n0 + i -- the field's
+  // own values, read once per plane by the vector march (DM = 3)
+  const double* rho_r = nullptr;
 
   // face coefficient (Dface * (W * g)) for direction (a, dir) of node (i,j,k);
   // returns false if the neighbour does not exist (coefficient exactly 0).

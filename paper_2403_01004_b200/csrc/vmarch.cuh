@@ -69,7 +69,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
 template <bool F1, int DM, int NOP>
 struct VMarchSmem {
   static constexpr int NA = F1 ? 6 : 3;          // u0[3] (+ y0[3]) -- the staged stencil sources
-  static constexpr int ND = DM != 0 ? 1 : 0;     // D / rho source
+  static constexpr int ND = (DM == 1 || DM == 2) ? 1 : 0;  // staged D / rho source
   double A[VSL][NA + ND][SXA];                   // TMA layout (main box + padded strips); F1: u0 -> u1 in place
   double O[NOP ? VOSL : 1][NOP ? NOP : 1][NOP ? SNT : 16];  // plain stage: u0, u_{k-2}, y0 at the tile nodes
   double rowt[VSL][VRW];                         // row records of the staged planes
@@ -77,12 +77,15 @@ struct VMarchSmem {
   unsigned long long full[VSL], formed[VSL], empty[VSL], ofull[VOSL];
 };
 
+// DM: 0 = D constant Dc, 1 = D nodal field, 2 = D = Dc * rho (a rho field),
+// 3 = D = Dc * rho(i) with a radial rho read per plane from op.rho_r (not staged)
 template <int DM, class Epi>
 __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Epi epi, int R, int zsel,
                                                       const int* skip, const __grid_constant__ SMaps maps,
                                                       const __grid_constant__ CUtensorMap rowmap) {
   constexpr bool F1 = fuse1_of<Epi>::value;
-  constexpr bool HASD = DM != 0;
+  constexpr bool HASD = DM != 0;              // the face coefficients carry a D average
+  constexpr bool SD = DM == 1 || DM == 2;     // D / rho staged per node
   constexpr int NOP = F1 ? 0 : Epi::NOPS;  // operand boxes of the plain stage (SEpiStage: 9)
   using Sm = VMarchSmem<F1, DM, NOP>;
   constexpr int NA = Sm::NA;
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
         arr(&S.A[sl][c][0], &maps.V[c], &maps.VS[c]);
         if constexpr (F1) arr(&S.A[sl][3 + c][0], &maps.Y[c], &maps.YS[c]);
       }
-    if constexpr (HASD) {
+    if constexpr (SD) {
       if (warp == 4) arr(&S.A[sl][DS][0], &maps.D, &maps.DS);
     }
   };
@@ -244,12 +247,16 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
   int o_c = 0, o_p = 1, o_n = 2;  // operand slots of planes t, t+1, t+2
   unsigned oph = 0u;
   double vm[3], vc[3], vp[3], a0c[3], a0n[3], dm = 0.0, dc = 0.0, dp = 0.0;
+  // radial rho (DM 3): rho of plane p from the table, the same value every node of it holds
+  auto rho_r = [&](int p) { return __ldg(op.rho_r + plane_map(g, p).mem); };
   own_in(i0 - 1, vm, a0n);
-  if (HASD) dm = S.A[slot(i0 - 1)][DS][h];
+  if (SD) dm = S.A[slot(i0 - 1)][DS][h];
+  if (DM == 3) dm = rho_r(i0 - 1);
   double cr0 = S.rowt[slot(i0 - 1)][jr * 4] * g10;  // r+ face of plane i0-1 = r- face of plane i0
   release(i0 - 1);
   own_in(i0, vc, a0c);
-  if (HASD) dc = S.A[slot(i0)][DS][h];
+  if (SD) dc = S.A[slot(i0)][DS][h];
+  if (DM == 3) dc = rho_r(i0);
 
 #pragma unroll 1
   for (int t = i0; t < iend; ++t) {
@@ -264,7 +271,8 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
     // plane t+1: landed (issued two iterations ago); its stencil input formed
     own_in(t + 1, vp, a0n);
     const int sc = slot(t);
-    if (HASD) dp = S.A[slot(t + 1)][DS][h];
+    if (SD) dp = S.A[slot(t + 1)][DS][h];
+    if (DM == 3) dp = rho_r(t + 1);
     if constexpr (F1) mbar_wait(&S.formed[sc], par(t));  // every element of u1(t) formed
 
     const double2 rw01 = *reinterpret_cast<const double2*>(&S.rowt[sc][jr * 4]);      // W2[0], W2[1]
@@ -293,13 +301,18 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
         nv[2][0][c] = S.A[sc][c][hpm];
         nv[2][1][c] = S.A[sc][c][hpp];
       }
-      if (HASD) {
+      if (SD) {
         nd[0][0] = dm;
         nd[0][1] = dp;
         nd[1][0] = S.A[sc][DS][htm];
         nd[1][1] = S.A[sc][DS][htp];
         nd[2][0] = S.A[sc][DS][hpm];
         nd[2][1] = S.A[sc][DS][hpp];
+      }
+      if (DM == 3) {  // in-plane neighbours hold the plane's rho
+        nd[0][0] = dm;
+        nd[0][1] = dp;
+        nd[1][0] = nd[1][1] = nd[2][0] = nd[2][1] = dc;
       }
       double Sx[3];
 #pragma unroll
@@ -351,7 +364,8 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
       const double iv = rw2v.y * igv;
       const int64_t o = (int64_t)t * g.plane + onode;
       double f[3];
-      const double irho = op.rho ? 1.0 / (DM == 2 ? dc : __ldg(op.rho + o)) : 1.0;
+      const double irho = DM == 3 ? __ldg(op.rho_r + g.n0 + t)
+                                  : (op.rho ? 1.0 / (DM == 2 ? dc : __ldg(op.rho + o)) : 1.0);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         double x = Sx[c] * iv;

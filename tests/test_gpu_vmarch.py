@@ -6,7 +6,8 @@ silently fall back to k_scalar_march an error, so the default leg provably
 ran the new kernel.  Grids cover: several r-chunks with a partial last one
 (PC_SMARCH_R), theta extents that are not a multiple of the 8-row tile, one
 and several 32-column phi tiles (the periodic seam strips), Dirichlet r-ends,
-and the three D modes (constant nu, nu field, nu rho with a 3-D rho)."""
+and the four D modes (constant nu, nu field, nu rho with a 3-D rho, nu rho with
+a radial rho read once per plane)."""
 import numpy as np
 import pytest
 
@@ -32,7 +33,8 @@ def _op(w, kind):
                 oracle_scalar(w.grid, w.bc, nu=nu, ncomp=3, vector_metric=True), v)
     r = np.asarray(w.grid.coords[0])
     rho = np.broadcast_to(np.exp(-10.0 * (r - 1.0))[:, None, None], shape).copy()
-    rho *= 1.0 + 0.1 * np.random.default_rng(5).random(shape)
+    if kind != "rho_radial":  # (radial: C5's density, read per plane -- DM 3)
+        rho *= 1.0 + 0.1 * np.random.default_rng(5).random(shape)
     return (operators.DiffusionOperator.scalar(
                 operators.ScalarDiffusionConfig(nu=1.0, rho=rho, bc=w.bc, vector_metric=True), 3),
             oracle_scalar(w.grid, w.bc, rho=rho, ncomp=3, vector_metric=True), v)
@@ -52,7 +54,7 @@ def _run(monkeypatch, op, w, u, T, use_ptl, vm):
 
 
 CASES = [((20, 24, 32), "const", None), ((21, 20, 64), "rho", "8"), ((37, 12, 96), "nu_field", "8"),
-         ((18, 16, 32), "rho", "4")]
+         ((18, 16, 32), "rho", "4"), ((27, 20, 64), "rho_radial", "8")]
 
 
 @pytest.mark.parametrize("n,kind,R", CASES)
@@ -99,7 +101,29 @@ def test_vmarch_argmax_ties_and_index(gpu_ctx, monkeypatch):
     assert np.array_equal(np.moveaxis(a[0], -1, 0), uo)
 
 
-@pytest.mark.parametrize("kind", ["const", "rho"])
+def test_vmarch_radial_rho_equals_field_path(gpu_ctx, monkeypatch):
+    """A radial density read once per plane (DM 3) gives the bits of the
+    staged-rho path (PC_NO_RADIAL_RHO=1 at freeze) and the oracle."""
+    monkeypatch.setenv("PC_NO_PERSIST", "1")
+    monkeypatch.setenv("PC_SMARCH_R", "8")
+    w = configs.c2(n=(27, 20, 64))
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("PC_NO_RADIAL_RHO", env)
+        else:
+            monkeypatch.delenv("PC_NO_RADIAL_RHO", raising=False)
+        op, oop, u = _op(w, "rho_radial")  # (the detection runs when the operator freezes)
+        dtE = op.device_op(w.grid, 3).dt_euler
+        outs.append(_run(monkeypatch, op, w, u, 300 * dtE, True, True))
+    monkeypatch.delenv("PC_NO_RADIAL_RHO", raising=False)
+    assert outs[0][1] == outs[1][1] and np.array_equal(outs[0][0], outs[1][0])
+    uo, repo = optl.cycle_operator(oop, optl.OracleScheme("rkl2"), soa(u), 300 * dtE, dt_euler=dtE, use_ptl=True)
+    assert [it for it, _, _ in outs[0][1]] == [r.iters for r in repo]
+    assert np.array_equal(np.moveaxis(outs[0][0], -1, 0), uo)
+
+
+@pytest.mark.parametrize("kind", ["const", "rho", "rho_radial"])
 def test_vmarch_fused_step_sts(gpu_ctx, monkeypatch, kind):
     """schemes.step_rkl2 / step_rkg2 (s = 2..5, fused stage 1+2 on the new
     kernel) equal the oracle bit for bit."""
