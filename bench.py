@@ -62,7 +62,7 @@ BYTES = {
     ("scalar", "rkl2"): 40,    # reads u_{k-1}, u_{k-2}, u0, y0; writes u_k
     ("scalar", "be"): 96,      # K7: r, p, d -> p, Ap;  K8: x, r, p, Ap, d -> x, r
     ("vector", "rkl2"): 120,   # 3 components x 40
-    ("vector_rho", "rkl2"): 128,   # + rho (D = nu rho formed per node)
+    ("vector_rho", "rkl2"): 128,   # + rho (D = nu rho formed per node; a radial rho is read per plane: 120)
 }
 # the fused stage-1+2 launch of the 7-point march, per cell-update (two per
 # launch and cell): reads u0, y0 (+ rho); writes u2 (f12) and u1 (f12w)
@@ -347,6 +347,10 @@ def run_ours(args, rank, world, local_rank):
     # roofline: the hot loop with the largest device time, its algorithmic bytes
     rows = []
     for fname, op, nc, bkey in prob.ops:
+        if bkey == "vector_rho" and _vmarch_applies(prob, args) and world == 1 and \
+                os.environ.get("PC_NO_RADIAL_RHO") is None:
+            # C5 / C5v's rho(r) is radial: the vector march reads rho(i) once per plane (DM 3), no rho stream
+            bkey = "vector"
         kk = ("pcg_" if kind.startswith("be") else "sts_") + ("aligned" if op.kind == "aligned" else "scalar")
         d = kinds[kk]
         if d["ms"] > 0:
