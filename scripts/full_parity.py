@@ -43,13 +43,16 @@ CASES = {
     "c3": ("c3", None),
     "c4": ("c4", None),
     "c5r": ("c5", (128, 128, 256)),
+    # the C5v recipe (C5's viscosity alone at 5e4 dt_E(viscosity), radial rho) on the C5r grid
+    "c5vr": ("c5v", (128, 128, 256)),
     # tiny versions for the CPU self-check of this script (leg "fake")
     "c2t": ("c2", (12, 8, 16)),
     "c3t": ("c3", (14, 10, 32)),
     "c4t": ("c4", (14, 10, 32)),
     "c5t": ("c5", (14, 10, 32)),
+    "c5vt": ("c5v", (14, 10, 32)),
 }
-SEED = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
+SEED = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5, "c5v": 5}
 
 
 def _workload(name, n):
@@ -57,6 +60,8 @@ def _workload(name, n):
     kw = {} if n is None else {"n": n}
     if name in ("c3", "c4", "c5"):
         return getattr(configs, name)(host=False, **kw)
+    if name == "c5v":
+        return configs.c5(host=False, **kw)
     if name == "c2":  # grid only (the oracle ranks build their own slabs)
         from paper_2403_01004_b200 import mesh
         nn = n or (128, 128, 256)
@@ -137,12 +142,12 @@ def run_fake(case, out):
     seed = SEED[name]
     ops = []
     rho = None
-    if name == "c5":
+    if name in ("c5", "c5v"):
         rho = np.exp(-10.0 * (np.asarray(w.grid.coords[0]) - 1.0))[:, None, None] * np.ones(tuple(w.grid.shape))
     if name in ("c3", "c4", "c5"):
         T = configs.temperature(w.grid, seed)
         ops.append(("T", oracle_aligned(w.grid, w.bc, configs.dipole_bhat(w.grid, seed), T, rho=rho), T[None]))
-    if name in ("c2", "c5"):
+    if name in ("c2", "c5", "c5v"):
         ops.append(("v", oracle_scalar(w.grid, w.bc, nu=1.0, rho=rho, ncomp=3, vector_metric=True),
                     soa(configs.harmonic_velocity(w.grid, seed))))
     dts = {f: op.euler_dt() for f, op, _ in ops}
@@ -180,7 +185,7 @@ def _slab_ops(case, slab, grid, bc):
         return s
 
     rho = None
-    if name == "c5":
+    if name in ("c5", "c5v"):
         rho = np.exp(-10.0 * (np.asarray(grid.coords[0]) - 1.0))[lo:lo + ne][:, None, None] * np.ones(
             (ne,) + tuple(grid.shape[1:]))
     if name in ("c3", "c4", "c5"):
@@ -188,7 +193,7 @@ def _slab_ops(case, slab, grid, bc):
         b = soa(configs.dipole_bhat(grid, seed, i0=lo, n0=ne))
         c = oops.aligned_coefficient(T, 1.0, None, 1e-10)
         out.append(("T", sop_of(OracleOperator(slab.geom, "aligned", 1, None, rho, False, b, c, 1.0)), T[None]))
-    if name in ("c2", "c5"):
+    if name in ("c2", "c5", "c5v"):
         v = soa(configs.harmonic_velocity(grid, seed, i0=lo, n0=ne))
         D = 1.0 if rho is None else np.full(rho.shape, 1.0) * rho
         out.append(("v", sop_of(OracleOperator(slab.geom, "scalar", 3, D, rho, True)), v))

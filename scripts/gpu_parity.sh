@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 export OMP_NUM_THREADS=1 OPENBLAS_NUM_THREADS=1 MKL_NUM_THREADS=1
 for c in ${CASES:-c3 c2 c5r}; do
   echo "== $c"
-  python scripts/full_parity.py both $c --out /tmp/full_parity > gpurun_out/full_parity_$c.log 2>&1
+  timeout ${PT:-1800} python scripts/full_parity.py both $c --out /tmp/full_parity > gpurun_out/full_parity_$c.log 2>&1
   echo "rc=$?"; tail -4 gpurun_out/full_parity_$c.log
   rm -f /tmp/full_parity/${c}_*.npy
 done
