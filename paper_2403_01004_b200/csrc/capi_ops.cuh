@@ -466,10 +466,38 @@ static int launch_march(pc_op* op, const double* Tin, const Epi& epi, const int*
 // r-chunk length: the longest power of two (<= 32) that still gives ~12 blocks
 // per SM (3 resident, scalar) or ~6 (2 resident, 3-component); measured on C2:
 // R = 4 / 8 / 16 / 32 -> 2.49 / 2.77 / 2.92 / 2.83e10 cell-updates/s.
+static bool vmarch_ok(const pc_grid* g);
 static int smarch_R(const pc_grid* g, int ncomp) {
   if (const char* e = getenv("PC_SMARCH_R")) {
     const int r = atoi(e);
     if (r >= 1) return r;
+  }
+  if (ncomp == 3 && vmarch_ok(g)) {
+    // the vector march: a block marches R planes after a prologue of about two
+    // (four planes staged, two formed), so the device time is ~ ceil(blocks /
+    // resident slots) x (R + 2) plane-steps; take the R (4 .. 64) with the most
+    // useful plane-steps per slot-step among those that keep >= 3 blocks per
+    // slot (C2: R = 15 fills 3.9 waves where 16 left the fourth half empty)
+    const int64_t tiles = (int64_t)((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + SMJ - 1) / SMJ);
+    const int64_t slots = (int64_t)g->ctx->sms * 2;
+    const int n0 = g->g.n0;
+    const bool slab = g->g.ghost_lo0 || g->g.ghost_hi0;  // keep >= 3 chunks (interior / boundary overlap)
+    int best = 4;
+    double best_eff = -1.0;
+    for (int R = 4; R <= 64; ++R) {
+      if (slab && (n0 + R - 1) / R < 3 && R > 4) continue;
+      const int64_t blocks = tiles * ((n0 + R - 1) / R);
+      // (fewer than ~3 blocks per slot: the co-resident blocks speed up as the
+      // SM empties and the model's constant block time no longer holds)
+      if (blocks < 3 * slots && R > 4) continue;
+      const int64_t waves = (blocks + slots - 1) / slots;
+      const double eff = (double)n0 * tiles / ((double)waves * slots * (R + 2));
+      if (eff > best_eff + 1e-9) {
+        best_eff = eff;
+        best = R;
+      }
+    }
+    return best;
   }
   const int tiles = ((g->g.n2 + MTK - 1) / MTK) * ((g->g.n1 + SMJ - 1) / SMJ);
   const int64_t want = ncomp == 3 ? 148 * 6 : 148 * 12;
