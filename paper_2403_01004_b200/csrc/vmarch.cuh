@@ -258,6 +258,14 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
   if (SD) dc = S.A[slot(i0)][DS][h];
   if (DM == 3) dc = rho_r(i0);
 
+  const bool okim0 = plane_map(g, i0 - 1).exists;
+  constexpr bool AM = std::is_same<Epi, SEpiArgmax>::value;
+  // F+argmax: this thread's node is fixed, so only the plane and component of
+  // its running maximum vary (SEpiArgmax::apply's strict >, same visiting order)
+  double am_v = -1.0;
+  int am_t = 0, am_c = 0;
+  if constexpr (AM) am_v = epi.best.v;
+
 #pragma unroll 1
   for (int t = i0; t < iend; ++t) {
     // refill plane t-1's slots once every warp is done with them
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
     const double w1m = S.rowt[sc][(jr - 1) * 4 + 1];                                  // W2[1] at j-1
     const double cr1 = rw01.x * g10;
     if (inside) {
-      const bool okim = plane_map(g, t - 1).exists;
+      const bool okim = t > i0 || okim0;  // (plane t-1 exists: every plane after the chunk's first)
       const int ig = t + g.i0g;
       const bool pin = (g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1);
       const double Dcen = DM == 0 ? op.Dc : (DM == 1 ? dc : op.Dc * dc);
@@ -385,7 +393,20 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
 #pragma unroll
         for (int q = 0; q < NOP; ++q) ov[q] = S.O[o_c][q][tid];
       }
-      epi.template apply<3>(g, t, jg, kg, o, f, vc, pin, ov);
+      if constexpr (AM) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          epi.F[c][o] = f[c];
+          const double a = fabs(f[c]);
+          if (a > am_v) {
+            am_v = a;
+            am_t = t;
+            am_c = c;
+          }
+        }
+      } else {
+        epi.template apply<3>(g, t, jg, kg, o, f, vc, pin, ov);
+      }
     }
     release(t);
     cr0 = cr1;
@@ -405,6 +426,15 @@ __global__ void __launch_bounds__(SNT, 2) k_vec_march(GridDev g, ScalarOp op, Ep
       o_c = o_p;
       o_p = o_n;
       o_n = o;
+    }
+  }
+  if constexpr (AM) {
+    if (am_v > epi.best.v) {
+      epi.best.v = am_v;
+      epi.bi = am_t;
+      epi.bc = am_c;
+      epi.bj = jg;
+      epi.bk = kg;
     }
   }
   epi.finish(g);
