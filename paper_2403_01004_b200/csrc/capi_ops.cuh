@@ -549,8 +549,9 @@ static int make_srow_map(pc_grid* g) {
   if (!enc) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   const GridDev& d = g->g;
   const int64_t nrows = (int64_t)(d.n0 + 2) * d.n1;
-  CUDA_TRY(cudaMalloc(&g->srowrec, sizeof(double) * 4 * nrows));
+  if (!g->srowrec) CUDA_TRY(cudaMalloc(&g->srowrec, sizeof(double) * 4 * nrows));
   k_srow_pack<<<(int)std::min<int64_t>((nrows + 255) / 256, 4096), 256, 0, g->ctx->s>>>(d, g->srowrec, nrows);
+  g->ctx->st.launches++;
   TRY(check_launch("k_srow_pack"));
   cuuint64_t dims[3] = {4, (cuuint64_t)d.n1, (cuuint64_t)d.n0 + 2};
   cuuint64_t strides[2] = {4 * 8, (cuuint64_t)d.n1 * 4 * 8};
@@ -559,7 +560,11 @@ static int make_srow_map(pc_grid* g) {
   CUresult r = enc(&g->srowmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, g->srowrec, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(PC_E_CUDA, "cuTensorMapEncodeTiled (vector row records) failed (" + std::to_string((int)r) + ")");
+  if (r != CUDA_SUCCESS) {
+    cudaFree(g->srowrec);
+    g->srowrec = nullptr;
+    return fail(PC_E_CUDA, "cuTensorMapEncodeTiled (vector row records) failed (" + std::to_string((int)r) + ")");
+  }
   g->srow_ok = true;
   return PC_OK;
 }
