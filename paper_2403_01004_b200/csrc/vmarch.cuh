@@ -1,8 +1,8 @@
 // Vector-viscosity 7-point march (K2v of DESIGN.md §4): the 3-component
-// spherical operator (frame rotations on the theta / phi faces) for the two
-// launches every PTL cycle of C2 / C5v runs -- y0 = F(u0) + argmax, and the
-// fused stages 1 + 2 -- written around what bounds this stencil (issue and
-// latency at ~150 fp64 instructions per node), not around staging:
+// spherical operator (frame rotations on the theta / phi faces) for the
+// launches every PTL cycle of C2 / C5v runs -- y0 = F(u0) + argmax, the fused
+// stages 1 + 2 and (s >= 3) the plain stage -- written around what bounds
+// this stencil (issue and latency at ~150 fp64 instructions per node):
 //
 //  * the thread that owns node (j0 + ty, k0 + tx) keeps its stencil input
 //    in registers along r (planes t-1, t, t+1: the r-faces read no shared
@@ -24,7 +24,11 @@
 //    the issuer warps refill the slot of plane t-1 once `empty` says so;
 //  * the per-(r, theta) metric rows (W2[0..2], iV2) arrive as one 4 x 10 box
 //    of an interleaved record table per plane; the r- face coefficient is the
-//    previous plane's r+ one (the same product), carried in a register.
+//    previous plane's r+ one (the same product), carried in a register;
+//  * the plain stage's nine epilogue operands come as 32 x 8 boxes on a
+//    three-slot ring; a radial density (C5 / C5v) is read per plane (DM 3);
+//  * the F+argmax epilogue tracks only the plane and component of the
+//    thread's maximum (its node is fixed).
 //
 // Every face term, the rotation products and the epilogue are formed exactly
 // as k_scalar_march forms them (same operands, same order), so the result is
