@@ -50,3 +50,33 @@ def test_reference_arm_line_contract():
     assert cfg["grid"] == [48, 48, 96] and cfg["operators"][0]["stages_or_iters"] == 962
     # the extrapolated step time is the step's cell-updates over the line's rate
     assert abs(d["ms_per_step"] / 1e3 - cfg["cell_updates_per_step"] / d["value"]) <= 1e-6 * d["ms_per_step"] / 1e3
+
+
+def test_vector_march_label_and_radial_bytes():
+    """bench.py names the kernel that runs the 3-component launches
+    (k_vec_march under capi_ops.cuh vmarch_ok's grid conditions) and counts
+    no rho stream when C5 / C5v's radial density is read per plane."""
+    import types
+    sys.path.insert(0, ROOT)
+    import bench
+    sph = types.SimpleNamespace(w=types.SimpleNamespace(grid=types.SimpleNamespace(metric="spherical")),
+                                dg=types.SimpleNamespace(global_shape=(128, 128, 256)))
+    args = types.SimpleNamespace(decomp=None)
+    old = os.environ.pop("PC_NO_VMARCH", None)
+    try:
+        assert bench._vmarch_applies(sph, args)
+        assert not bench._vmarch_applies(sph, types.SimpleNamespace(decomp="phi"))
+        ragged = types.SimpleNamespace(w=sph.w, dg=types.SimpleNamespace(global_shape=(48, 48, 96 + 8)))
+        assert not bench._vmarch_applies(ragged, args)
+        cart = types.SimpleNamespace(w=types.SimpleNamespace(grid=types.SimpleNamespace(metric="cartesian")),
+                                     dg=sph.dg)
+        assert not bench._vmarch_applies(cart, args)
+        os.environ["PC_NO_VMARCH"] = "1"
+        assert not bench._vmarch_applies(sph, args)
+    finally:
+        os.environ.pop("PC_NO_VMARCH", None)
+        if old is not None:
+            os.environ["PC_NO_VMARCH"] = old
+    # the radial-rho stage / fused launch move the vector's bytes, the field path 8 B more
+    assert bench.BYTES[("vector_rho", "rkl2")] - bench.BYTES[("vector", "rkl2")] == 8
+    assert bench.BYTES_F12[("vector_rho", "f12")] - bench.BYTES_F12[("vector", "f12")] == 4
