@@ -19,7 +19,8 @@ in configs.py) over the same step and compares, rank by rank:
 
 Cases: c2, c3, c4 at their BASELINE sizes; c5r = the C5 recipe (coupled
 conduction + viscosity, rho field, 5e4 dt_E -- the bench's own ratio) on a
-reduced 128 x 128 x 256 grid.  Results: DIR/full_parity_<case>.json.
+reduced 128 x 128 x 256 grid; c5vr / c4r = the C5v / C4 recipes as one
+whole step on that grid.  Results: DIR/full_parity_<case>.json.
 This is test infrastructure (it executes oracle/), not part of the product.
 """
 from __future__ import annotations
@@ -45,6 +46,9 @@ CASES = {
     "c5r": ("c5", (128, 128, 256)),
     # the C5v recipe (C5's viscosity alone at 5e4 dt_E(viscosity), radial rho) on the C5r grid
     "c5vr": ("c5v", (128, 128, 256)),
+    # the C4 recipe (BE + Jacobi PCG under PTL at 1e4 dt_E) as one WHOLE step on the C5r grid: every PTL cycle
+    # and PCG solve of the step (the BASELINE-size C4 step is 576 iterations, hours of oracle time)
+    "c4r": ("c4", (128, 128, 256)),
     # tiny versions for the CPU self-check of this script (leg "fake")
     "c2t": ("c2", (12, 8, 16)),
     "c3t": ("c3", (14, 10, 32)),
