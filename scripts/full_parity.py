@@ -20,7 +20,7 @@ in configs.py) over the same step and compares, rank by rank:
 Cases: c2, c3, c4 at their BASELINE sizes; c5r = the C5 recipe (coupled
 conduction + viscosity, rho field, 5e4 dt_E -- the bench's own ratio) on a
 reduced 128 x 128 x 256 grid; c5vr / c4r = the C5v / C4 recipes as one
-whole step on that grid.  Results: DIR/full_parity_<case>.json.
+whole step on that grid; c3g = C3 advanced with RKG2.  Results: DIR/full_parity_<case>.json.
 This is test infrastructure (it executes oracle/), not part of the product.
 """
 from __future__ import annotations
@@ -49,13 +49,17 @@ CASES = {
     # the C4 recipe (BE + Jacobi PCG under PTL at 1e4 dt_E) as one WHOLE step on the C5r grid: every PTL cycle
     # and PCG solve of the step (the BASELINE-size C4 step is 576 iterations, hours of oracle time)
     "c4r": ("c4", (128, 128, 256)),
+    # C3 at BASELINE size advanced with RKG2 instead of RKL2 (the second STS family, whole step)
+    "c3g": ("c3", None),
     # tiny versions for the CPU self-check of this script (leg "fake")
     "c2t": ("c2", (12, 8, 16)),
     "c3t": ("c3", (14, 10, 32)),
+    "c3gt": ("c3", (14, 10, 32)),
     "c4t": ("c4", (14, 10, 32)),
     "c5t": ("c5", (14, 10, 32)),
     "c5vt": ("c5v", (14, 10, 32)),
 }
+SCHEME = {"c3g": "rkg2", "c3gt": "rkg2"}  # scheme overrides (default: the config's own, BE for C4, RKL2 otherwise)
 SEED = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5, "c5v": 5}
 
 
@@ -82,7 +86,7 @@ def run_gpu(case, out, max_cycles=None, from_cycle=None):
     ctx = device.default_context()
     t0 = time.perf_counter()
     prob = bench.Problem(name, ctx, n)
-    sc = bench.scheme_for(name, types.SimpleNamespace(scheme=None, pc="jacobi"))
+    sc = bench.scheme_for(name, types.SimpleNamespace(scheme=SCHEME.get(case), pc="jacobi"))
     prob.reset()
     from paper_2403_01004_b200 import _lib
     for f, _, _, _ in prob.ops:
@@ -156,7 +160,7 @@ def run_fake(case, out):
                     soa(configs.harmonic_velocity(w.grid, seed))))
     dts = {f: op.euler_dt() for f, op, _ in ops}
     dtE = min(dts.values())
-    kind = "backward_euler" if name == "c4" else "rkl2"
+    kind = SCHEME.get(case) or ("backward_euler" if name == "c4" else "rkl2")
     tol = 1e-9 if name in ("c3", "c4") else 1e-10
     rec = {"case": case, "config": name, "grid": list(w.grid.shape), "outer_dt": w.ratio * dtE, "dt_euler_min": dtE,
            "dt_euler": dts, "scheme": kind, "tol": tol, "step_s": 0.0, "setup_s": 0.0, "ops": []}
@@ -222,7 +226,7 @@ def _oracle_rank(rank, world, port, case, out, gpu_rec, max_cycles=None):
         dtE = min(dts.values())
         outer = w.ratio * dtE
         res["dt_euler"] = dts
-        kind = "backward_euler" if name == "c4" else "rkl2"
+        kind = SCHEME.get(case) or ("backward_euler" if name == "c4" else "rkl2")
         tol = 1e-9 if name in ("c3", "c4") else 1e-10
         t0 = time.perf_counter()
         for f, sop, ext in ops:
