@@ -70,6 +70,9 @@ BYTES_F12 = {
     ("scalar", "f12"): 12, ("scalar", "f12w"): 16,
     ("vector", "f12"): 36, ("vector", "f12w"): 48,
     ("vector_rho", "f12"): 40, ("vector_rho", "f12w"): 52,
+    # the aligned TMA march (EpiStageA12): reads u0, y0, beta(3); writes u2 (+ u1); rho radial (per plane)
+    ("aligned", "af12"): 24, ("aligned", "af12w"): 28,
+    ("aligned_rho", "af12"): 24, ("aligned_rho", "af12w"): 28,
 }
 
 CONFIG_MODEL = {
@@ -368,6 +371,16 @@ def run_ours(args, rank, world, local_rank):
                          "ms": d["ms"], "bytes_per_cell_update": bpc,
                          "achieved": bpc * d["cell_updates"] / (d["ms"] / 1e3) / 1e9,
                          "launches": d["launches"], "field": fname})
+        if op.kind == "aligned" and not kind.startswith("be"):
+            for fk in ("af12", "af12w"):
+                d = kinds["sts_" + fk]
+                if d["ms"] > 0:
+                    bpc = BYTES_F12[(bkey, fk)]
+                    rows.append({"kernel": "k_aligned_tma<EpiStageA12> (stages 1+2%s)"
+                                           % (", u1 written" if fk == "af12w" else ""),
+                                 "ms": d["ms"], "bytes_per_cell_update": bpc, "stages_per_launch": 2,
+                                 "achieved": bpc * d["cell_updates"] / (d["ms"] / 1e3) / 1e9,
+                                 "launches": d["launches"], "field": fname})
         if op.kind != "aligned" and not kind.startswith("be"):
             for fk in ("f12", "f12w"):
                 d = kinds["sts_" + fk]

@@ -234,8 +234,10 @@ int pc_gen_radial(pc_field* f, const double* tab);
 int pc_ctx_stats(pc_ctx* ctx, double* stage_ms, int64_t* stage_launches, int64_t* launches_total);
 int pc_ctx_reset_stats(pc_ctx* ctx);
 /* per hot-loop kind (0 scalar/vector STS stages k >= 2, 1 aligned STS stages,
- * 2 scalar PCG iterations, 3 aligned PCG iterations): device ms, launches and
- * cell-updates (local cells x stages / iterations) */
+ * 2 scalar PCG iterations, 3 aligned PCG iterations, 4/5 the fused stage-1+2
+ * launch of the 7-point march without/with the u1 write, 6/7 the same for the
+ * aligned TMA march): device ms, launches and cell-updates (local cells x
+ * stages / iterations; the fused launches count both stages) */
 int pc_ctx_stats_kind(pc_ctx* ctx, int kind, double* ms, int64_t* launches, int64_t* cell_updates);
 int pc_ctx_enable_timing(pc_ctx* ctx, int on);
 /* CUDA events on the context stream: record mark id (0..15); elapsed ms */

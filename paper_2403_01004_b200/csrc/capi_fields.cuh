@@ -181,7 +181,7 @@ static void flush_events(pc_ctx* c) {
   c->ev.clear();
 }
 int pc_ctx_stats_kind(pc_ctx* c, int kind, double* ms, int64_t* launches, int64_t* units) {
-  if (!c || kind < 0 || kind >= NKIND) return fail(PC_E_INVALID, "stats kind 0..5");
+  if (!c || kind < 0 || kind >= NKIND) return fail(PC_E_INVALID, "stats kind 0..7");
   cudaStreamSynchronize(c->s);
   flush_events(c);
   if (ms) *ms = c->st.kind_ms[kind];

@@ -39,7 +39,9 @@ enum {
   KIND_PCG_ALIGNED = 3,
   KIND_STS_F12 = 4,
   KIND_STS_F12W = 5,
-  NKIND = 6
+  KIND_STS_AF12 = 6,   // the aligned (TMA march) fused stage-1+2 launch, s == 2
+  KIND_STS_AF12W = 7,  // ... with the u1 write (s >= 3)
+  NKIND = 8
 };
 struct Stats {
   double stage_ms = 0.0;

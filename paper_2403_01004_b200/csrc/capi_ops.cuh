@@ -437,6 +437,10 @@ static int launch_tma(pc_op* op, const double* Tin, const Epi& epi, const int* s
     TRY(make_field_map(&maps.P[1], epi.dinv, g->g, MTK, MHJ));
     TRY(make_field_map(&maps.PS[1], epi.dinv, g->g, 2, MHJ));
   }
+  if constexpr (fuse1_of<Epi>::value) {  // fused STS stages 1 + 2: y0 boxes beside u0 (= Tin)
+    TRY(make_field_map(&maps.P[0], epi.y0, g->g, MTK, MHJ));
+    TRY(make_field_map(&maps.PS[0], epi.y0, g->g, 2, MHJ));
+  }
   if (op->ao.rho && op->ao.rho_r) return launch_tma_t<Epi, 2>(op, maps, epi, skip, what);
   if (op->ao.rho) return launch_tma_t<Epi, 1>(op, maps, epi, skip, what);
   return launch_tma_t<Epi, 0>(op, maps, epi, skip, what);

@@ -113,8 +113,37 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
   // (SEpiStage12: u1 formed in shared memory from u0 and y0; PC_NO_FUSE12 off)
   const bool fuse12 = !std::is_same<Op, AlignedOp>::value && smarch_ok(op) && !overlap && !g->g.ghost_lo0 &&
                       !g->g.ghost_hi0 && !g->g.phis && getenv("PC_NO_FUSE12") == nullptr;
+  // aligned TMA march, one rank without ghost planes: stages 1 and 2 in one
+  // pass as well (EpiStageA12: u1 formed in the input slot from u0 and y0;
+  // PC_NO_FUSE12A off)
+  const bool fuse12a = std::is_same<Op, AlignedOp>::value && s >= 2 && tma_ok(g) && !overlap && !g->g.ghost_lo0 &&
+                       !g->g.ghost_hi0 && !g->g.phis && getenv("PC_NO_FUSE12A") == nullptr;
   CUDA_TRY(cudaMemsetAsync(c->bad, 0x7f, sizeof(int), c->s));
-  if (fuse12) {
+  if (fuse12a) {
+    const double* r = tab + 5;
+    const StageCoef sc{r[0], r[1], r[2], r[3], r[4]};
+    const bool w1 = s >= 3;
+    const int kind = w1 ? KIND_STS_AF12W : KIND_STS_AF12;
+    cudaEvent_t f0 = nullptr, f1 = nullptr;
+    if (c->timing) {
+      f0 = ev_new(c);
+      f1 = ev_new(c);
+      cudaEventRecord(f0, c->s);
+    }
+    EpiStageA12 e{cfld(u).p[0], y0.base(0), B.base(0), w1 ? A.base(0) : nullptr, sc, tab[3], c->bad};
+    rc = launch_tma(op, cfld(u).p[0], e, nullptr, "k_aligned_tma<stage 1+2>");
+    if (c->timing) {
+      cudaEventRecord(f1, c->s);
+      c->ev.push_back({f0, f1, kind});
+    }
+    c->st.kind_launches[kind] += 1;
+    c->st.kind_units[kind] += 2 * owned_cells(g->g);
+    c->st.stage_launches++;
+    // rotate as after stage 2 below: u1 (A) -> u_{k-2}, u2 (B) -> u_{k-1}
+    um2w = &A;
+    um1 = &B;
+    out = &A;
+  } else if (fuse12) {
     const double* r = tab + 5;
     const StageCoef sc{r[0], r[1], r[2], r[3], r[4]};
     CFld u0f = cfld(u), y0f = y0.cf();
@@ -157,7 +186,7 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
     e1 = ev_new(c);
     cudaEventRecord(e0, c->s);
   }
-  for (int k = fuse12 ? 3 : 2; k <= s && rc == PC_OK; ++k) {
+  for (int k = (fuse12 || fuse12a) ? 3 : 2; k <= s && rc == PC_OK; ++k) {
     const double* r = tab + 5 * (k - 1);
     StageCoef sc{r[0], r[1], r[2], r[3], r[4]};
     CFld m2 = um2w ? um2w->cf() : cfld(u);
@@ -215,7 +244,7 @@ static int sts_stages(pc_op* op, const Op& o, pc_field* u, const double* tab, in
       cudaEventRecord(e1, c->s);
       c->ev.push_back({e0, e1, kind});
     }
-    const int nst = s - (fuse12 ? 2 : 1);
+    const int nst = s - ((fuse12 || fuse12a) ? 2 : 1);
     c->st.kind_launches[kind] += nst;
     c->st.kind_units[kind] += (int64_t)nst * owned_cells(g->g);
   }

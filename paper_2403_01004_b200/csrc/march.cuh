@@ -591,6 +591,40 @@ struct EpiStage {  // fused RKL2/RKG2 stage
   }
 };
 
+// stages 1 and 2 of the aligned STS in one TMA march (FUSE1): the march
+// stages u0 and y0 of each plane and forms u1 = u0 + mut1 dt y0 in the input
+// slot (k_stage1's expression, pinned nodes keep u0) as the plane lands; the
+// epilogue gets u1 as the node value and forms u2 exactly as EpiStage with
+// u_{k-2} = u0 (operand 0 serves both), and writes u1 when a stage 3 reads it
+struct EpiStageA12 {
+  static constexpr int NOPS = 2;
+  static constexpr bool NEEDS_W = false;
+  static constexpr bool FUSE1 = true;
+  const double* u0;
+  const double* y0;
+  double* out;   // u2
+  double* out1;  // u1 (nullptr: s == 2, nothing reads it)
+  StageCoef sc;  // stage 2
+  double mt1;    // mut1 dt of stage 1
+  int* bad;
+  bool nf1 = false, nf2 = false;
+  __host__ __device__ __forceinline__ const double* opnd(int q) const { return q == 0 ? u0 : y0; }
+  __device__ __forceinline__ void operator()(int, const GridDev&, int, int, int, int64_t o, double f, double um1,
+                                             bool pin, const double* ov, double) {
+    const double a0 = ov[0];
+    double v = ((((sc.mu * um1) + (sc.nu * a0)) + (sc.kap * a0)) + (sc.mtdt * f)) + (sc.gtdt * ov[1]);
+    v = pin ? a0 : v;
+    out[o] = v;
+    if (out1) out1[o] = um1;
+    nf1 |= (__double2hiint(um1) & 0x7ff00000) == 0x7ff00000;
+    nf2 |= (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
+  }
+  __device__ __forceinline__ void finish(const GridDev&) {
+    if (nf1) atomicMin(bad, 1);
+    if (nf2) atomicMin(bad, 2);
+  }
+};
+
 constexpr int kMaxWarps = 16;  // epilogue block reductions serve 256- and 512-thread marching kernels
 __device__ __forceinline__ int block_threads() { return blockDim.x * blockDim.y; }
 __device__ __forceinline__ ArgMax block_argmax2d(ArgMax a, double* shv, long long* shi) {

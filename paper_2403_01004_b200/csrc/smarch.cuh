@@ -89,14 +89,7 @@ struct SMarchSmemT {
 template <int NC, bool F1, bool TM>
 using SMarchSmem = std::conditional_t<TM, SMarchSmemT<NC, F1>, SMarchSmemC<NC, F1>>;
 
-template <class E, class = void>
-struct fuse1_of {
-  static constexpr bool value = false;
-};
-template <class E>
-struct fuse1_of<E, std::void_t<decltype(E::FUSE1)>> {
-  static constexpr bool value = E::FUSE1;
-};
+// (fuse1_of: tma_march.cuh)
 
 // DM: 0 = D constant Dc, 1 = D nodal field, 2 = D = Dc * rho (viscosity);
 // TM: TMA staging (see SMaps), else cp.async

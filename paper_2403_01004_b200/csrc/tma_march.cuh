@@ -55,6 +55,14 @@ template <class E, class = void>
 struct fusep_of : std::false_type {};
 template <class E>
 struct fusep_of<E, std::void_t<decltype(E::FUSEP)>> : std::integral_constant<bool, E::FUSEP> {};
+// Epilogues with FUSE1 (EpiStageA12 here, SEpiStage12 in the 7-point
+// marches): the march stages u0 into the input slot and y0 beside it, and
+// forms u1 = u0 + mut1 dt y0 in place (pinned nodes keep u0: k_stage1's
+// expression) as each plane lands
+template <class E, class = void>
+struct fuse1_of : std::false_type {};
+template <class E>
+struct fuse1_of<E, std::void_t<decltype(E::FUSE1)>> : std::integral_constant<bool, E::FUSE1> {};
 
 constexpr int RW = 12;  // metric row record: iL2[6], wo01[4], iVal2, pad (16-byte aligned pairs)
 constexpr int RSLOT = 224;  // one plane of row records (18 x 12) padded to a 128-byte multiple
@@ -207,8 +215,13 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   double* rM = S.rowt[0];   // metric rows of planes t-1, t, t+1
   double* rC = S.rowt[1];
   double* rN = S.rowt[2];
-  double* eW = S.EO[0][0];  // epilogue operands of plane t (landing), t-1 (read)
-  double* eR = S.EO[1][0];
+  constexpr bool FP1 = fuse1_of<Epi>::value;
+  // epilogue operands of plane t (landing), t-1 (read); FUSE1 (two operands)
+  // packs the two slots at a stride of two boxes and stages y0 behind them
+  static_assert(!FP1 || (Epi::NOPS == 2 && 4 * XO + XA <= 2 * 3 * XO), "FUSE1 stages y0 behind two operand slots");
+  double* eW = S.EO[0][0];
+  double* eR = FP1 ? S.EO[0][0] + 2 * XO : S.EO[1][0];
+  double* rawy = S.EO[0][0] + 4 * XO;
   FluxX* Ew = &S.E[0];      // flux exchange of plane t (write), t-1 (read)
   FluxX* Er = &S.E[1];
 
@@ -230,12 +243,51 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       tma_arr(raw, &maps.T, &maps.TS, p);
       tma_arr(raw + XA, &maps.P[0], &maps.PS[0], p);
       tma_arr(raw + 2 * XA, &maps.P[1], &maps.PS[1], p);
+    } else if constexpr (FP1) {
+      tma_arr(dst, &maps.T, &maps.TS, p);  // u0
+      tma_arr(rawy, &maps.P[0], &maps.PS[0], p);  // y0
     } else {
       tma_arr(dst, &maps.T, &maps.TS, p);
     }
   };
-  constexpr unsigned kTBytes = (FP ? 3u : 1u) * kArrBytes;
-  auto form_p = [&](double* dst) {
+  constexpr unsigned kTBytes = (FP ? 3u : (FP1 ? 2u : 1u)) * kArrBytes;
+  // FUSE1: this thread's staged elements e = tid + q MNT (q < 3) that get
+  // u1 = u0 + mut1 dt y0 -- real slots (strip padding stays unread) whose
+  // theta row and phi column are not pinned -- as a mask fixed per block
+  unsigned fmask = 0u;
+  if constexpr (FP1) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int e = tid + q * MNT;
+      if (e >= XA) continue;
+      int row, kc;
+      bool real = true;
+      if (e < XM) {
+        row = e / MTK;
+        kc = k0 + (e - row * MTK);
+      } else {
+        const int sx = (e - XM) / XS, ix = (e - XM) - sx * XS;
+        real = ix < MHJ * 2;
+        row = ix >> 1;
+        kc = (sx == 0 ? kL : kR) + (ix & 1);
+      }
+      const int jg = j0 - 1 + row;
+      const bool pin = (g.pin_lo1 && jg == 0) || (g.pin_hi1 && jg == g.n1 - 1) || (g.pin_lo2 && kc == 0) ||
+                       (g.pin_hi2 && kc == g.n2 - 1);
+      if (real && !pin) fmask |= 1u << q;
+    }
+  }
+  auto form_p = [&](double* dst, int p) {
+    if constexpr (FP1) {  // u1 = u0 + mut1 dt y0 of plane p, pinned nodes keep u0 (k_stage1)
+      const int ig = p + g.i0g;
+      if ((g.pin_lo0 && ig == 0) || (g.pin_hi0 && ig == g.n0g - 1)) return;
+      const double mt = epi.mt1;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int e = tid + q * MNT;
+        if (fmask & (1u << q)) dst[e] = dst[e] + mt * rawy[e];
+      }
+    }
     if constexpr (FP) {
       const double beta = epi.st->beta;
       for (int e = tid; e < XA; e += MNT) {
@@ -260,7 +312,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
   // ---- prologue: T(i0-1..i0+1), beta and row records of (i0-1, i0)
   __syncthreads();  // barrier initialised
   unsigned phase = 0;
-  if constexpr (FP) {  // one staging area: the three input planes one after the other
+  if constexpr (FP || FP1) {  // one staging area: the three input planes one after the other
     double* slots[3] = {sTm1, sT, sTp};
 #pragma unroll 1
     for (int q = 0; q < 3; ++q) {
@@ -277,7 +329,7 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       }
       mbar_wait(&S.bar, phase);
       phase ^= 1u;
-      form_p(slots[q]);
+      form_p(slots[q], i0 - 1 + q);
       __syncthreads();
     }
   } else {
@@ -480,8 +532,8 @@ __global__ void __launch_bounds__(MNT, 2) k_aligned_tma(GridDev g, AlignedOp op,
       if (!LAST) {
         mbar_wait(&S.bar, phase);
         phase ^= 1u;
-        if constexpr (FP) {
-          if (t + 2 <= iend) form_p(sTm1);  // plane t+2 into the slot that becomes sTp
+        if constexpr (FP || FP1) {
+          if (t + 2 <= iend) form_p(sTm1, t + 2);  // plane t+2 into the slot that becomes sTp
         }
         __syncthreads();
         pofs += g.plane;

@@ -79,7 +79,9 @@ class Context:
 
     # sts_f12 / sts_f12w: the fused stage-1+2 launch of the 7-point march
     # (without / with the u1 write); their cell-updates count both stages
-    KINDS = ("sts_scalar", "sts_aligned", "pcg_scalar", "pcg_aligned", "sts_f12", "sts_f12w")
+    # (sts_af12 / sts_af12w: the same for the aligned TMA march)
+    KINDS = ("sts_scalar", "sts_aligned", "pcg_scalar", "pcg_aligned", "sts_f12", "sts_f12w", "sts_af12",
+             "sts_af12w")
 
     def stats_by_kind(self):
         """{kind: {ms, launches, cell_updates}} of the timed hot loops."""
