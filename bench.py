@@ -443,7 +443,7 @@ def run_ours(args, rank, world, local_rank):
                 "frac_vs_nominal_8tbs": dom["achieved"] / 8000.0,  # B200 datasheet HBM3e figure
                 "peak_source": peak_src,
                 "kernel_ms_share": dom["ms"] / ms if ms > 0 else None,
-                "all_hot_loops": [{k: v for k, v in r.items() if k != "field"} for r in rows],
+                "all_hot_loops": [{k: v for k, v in r.items() if k != "field"} for r in rows if r.get("launches", 1)],
             },
             "gpu_launches": st["launches"],
             "clocks": clocks,
